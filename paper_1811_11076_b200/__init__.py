@@ -1,0 +1,18 @@
+"""tswarp_b200: a B200-native k-NN query engine for multi-dimensional time series.
+
+The hot path of arXiv 1811.11076's reference library (`tswarp`, proj/core) -- the k-NN linear
+scan under banded DTW with LB_Box pruning, and the dog-keeper (discrete Frechet) k-NN --
+re-built as hand-written sm_100a CUDA kernels behind a C ABI (include/tswarp_b200.h), with a
+C++ drop-in header (include/tswarp_b200.hpp) and this Python mirror (tswarp.py).
+"""
+from .tswarp import (  # noqa: F401
+    Dataset, Neighbor, Plan, SearchCounters, SearchReport, Store, TswError, ValidationError,
+    device_count, dist_all, envelope, epsnn_dk, knn, knn_dk, knn_dtw, lb_box_all, lib, synth,
+    synth_shape,
+)
+
+__all__ = [
+    "Dataset", "Neighbor", "Plan", "SearchCounters", "SearchReport", "Store", "TswError",
+    "ValidationError", "device_count", "dist_all", "envelope", "epsnn_dk", "knn", "knn_dk",
+    "knn_dtw", "lb_box_all", "lib", "synth", "synth_shape",
+]

@@ -1,0 +1,183 @@
+// C++ drop-in API (include/tswarp_b200.hpp) implemented over the C ABI (include/tswarp_b200.h).
+// Validation and error messages follow the reference: timeseries.cpp:7-47 (ValidationError)
+// and search.cpp:99-115,127,172,217 (std::invalid_argument).
+#include "tswarp_b200.hpp"
+
+#include <chrono>
+#include <mutex>
+
+#include "tswarp_b200.h"
+
+namespace tswarp {
+
+namespace detail {
+
+struct DeviceStore {
+    tsw_store* h = nullptr;
+    std::mutex mu;
+    ~DeviceStore() { tsw_store_destroy(h); }
+};
+
+[[noreturn]] void rethrow(int rc) {
+    const std::string msg = tsw_last_error();
+    switch (rc) {
+        case TSW_EINVAL: throw std::invalid_argument(msg);
+        case TSW_EVALIDATION: throw ValidationError(msg);
+        default: throw std::runtime_error("tswarp_b200: " + msg);
+    }
+}
+
+}  // namespace detail
+
+TimeSeries::TimeSeries(std::vector<double> values, std::size_t dim, std::optional<std::string> label)
+    : values_(std::move(values)), dim_(dim), label_(std::move(label)) {
+    if (dim_ == 0) throw ValidationError("time series dimensionality must be >= 1");
+    if (values_.empty() || values_.size() % dim_ != 0) {
+        throw ValidationError("time series values must hold n >= 1 complete " +
+                              std::to_string(dim_) + "-dimensional points, got " +
+                              std::to_string(values_.size()) + " components");
+    }
+    for (std::size_t i = 0; i < values_.size(); ++i) {
+        if (!std::isfinite(values_[i])) {
+            throw ValidationError("non-finite component at point " + std::to_string(i / dim_) +
+                                  ", dimension " + std::to_string(i % dim_));
+        }
+    }
+}
+
+Dataset::Dataset(std::vector<TimeSeries> series, std::map<std::string, std::string> meta)
+    : series_(std::move(series)), meta_(std::move(meta)) {
+    if (series_.empty()) throw ValidationError("dataset must contain at least one series");
+    dim_ = series_.front().dim();
+    const bool labeled = series_.front().label().has_value();
+    for (std::size_t i = 0; i < series_.size(); ++i) {
+        if (series_[i].dim() != dim_) {
+            throw ValidationError("series " + std::to_string(i) + " has dimensionality " +
+                                  std::to_string(series_[i].dim()) + ", dataset has " +
+                                  std::to_string(dim_));
+        }
+        if (series_[i].label().has_value() != labeled) {
+            throw ValidationError("labels must be present on every series or on none (series " +
+                                  std::to_string(i) + ")");
+        }
+    }
+    store_ = std::make_shared<detail::DeviceStore>();
+}
+
+detail::DeviceStore& Dataset::device_store() const {
+    std::lock_guard<std::mutex> lk(store_->mu);
+    if (!store_->h) {
+        std::vector<double> values;
+        std::vector<uint64_t> lengths(series_.size());
+        std::size_t total = 0;
+        for (const auto& s : series_) total += s.flat().size();
+        values.reserve(total);
+        for (std::size_t i = 0; i < series_.size(); ++i) {
+            const auto f = series_[i].flat();
+            values.insert(values.end(), f.begin(), f.end());
+            lengths[i] = series_[i].length();
+        }
+        int dev = 0;
+        const int rc = tsw_store_create(values.data(), lengths.data(), 0, series_.size(), dim_, dev,
+                                        &store_->h);
+        if (rc != TSW_OK) detail::rethrow(rc);
+    }
+    return *store_;
+}
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+
+void check_query(const TimeSeries& query, const Dataset& data, bool equal_lengths, const char* op) {
+    if (query.dim() != data.dim()) {
+        throw std::invalid_argument(std::string(op) + ": query dim " + std::to_string(query.dim()) +
+                                    " != dataset dim " + std::to_string(data.dim()));
+    }
+    if (equal_lengths) {
+        for (std::size_t i = 0; i < data.size(); ++i) {
+            if (data[i].length() != query.length()) {
+                throw std::invalid_argument(std::string(op) + ": series " + std::to_string(i) +
+                                            " length differs from the query (lower bounds "
+                                            "require equal lengths)");
+            }
+        }
+    }
+}
+
+std::vector<SearchReport> run_knn(const std::vector<TimeSeries>& queries, const Dataset& data,
+                                  std::size_t k, int metric, std::size_t r, const char* op) {
+    if (k == 0) throw std::invalid_argument(std::string(op) + ": k must be positive");
+    std::vector<SearchReport> reps(queries.size());
+    if (queries.empty()) return reps;
+    const std::size_t qlen = queries.front().length();
+    for (const auto& q : queries) {
+        check_query(q, data, metric == TSW_METRIC_DTW, op);
+        if (q.length() != qlen)
+            throw std::invalid_argument(std::string(op) + ": batched queries must share a length");
+    }
+    const auto start = Clock::now();
+    auto& st = data.device_store();
+    std::vector<double> flat;
+    flat.reserve(queries.size() * qlen * data.dim());
+    for (const auto& q : queries) flat.insert(flat.end(), q.flat().begin(), q.flat().end());
+    const std::size_t kk = std::min(k, data.size());
+    std::vector<tsw_neighbor> out(queries.size() * kk);
+    std::vector<tsw_counters> ctr(queries.size());
+    const int rc = tsw_knn(st.h, flat.data(), queries.size(), qlen, metric, r, k, out.data(),
+                           ctr.data());
+    if (rc != TSW_OK) detail::rethrow(rc);
+    const double wall = std::chrono::duration<double>(Clock::now() - start).count();
+    for (std::size_t q = 0; q < queries.size(); ++q) {
+        auto& rep = reps[q];
+        rep.neighbors.resize(kk);
+        for (std::size_t j = 0; j < kk; ++j)
+            rep.neighbors[j] = {static_cast<std::size_t>(out[q * kk + j].index), out[q * kk + j].distance};
+        rep.counters = {ctr[q].lb_computed, ctr[q].lb_pruned, ctr[q].full_dp, ctr[q].early_abandoned,
+                        ctr[q].gdk_calls};
+        rep.wall_time_seconds = wall / static_cast<double>(queries.size());
+    }
+    return reps;
+}
+
+}  // namespace
+
+SearchReport knn_dtw(const TimeSeries& query, const Dataset& data, std::size_t k, BandRadius r, int) {
+    return run_knn({query}, data, k, TSW_METRIC_DTW, r.value, "knn_dtw").front();
+}
+
+SearchReport knn_dk(const TimeSeries& query, const Dataset& data, std::size_t k, int) {
+    return run_knn({query}, data, k, TSW_METRIC_DK, 0, "knn_dk").front();
+}
+
+std::vector<SearchReport> knn_dtw_batch(const std::vector<TimeSeries>& queries, const Dataset& data,
+                                        std::size_t k, BandRadius r) {
+    return run_knn(queries, data, k, TSW_METRIC_DTW, r.value, "knn_dtw");
+}
+
+std::vector<SearchReport> knn_dk_batch(const std::vector<TimeSeries>& queries, const Dataset& data,
+                                       std::size_t k) {
+    return run_knn(queries, data, k, TSW_METRIC_DK, 0, "knn_dk");
+}
+
+SearchReport epsnn_dk(const TimeSeries& query, const Dataset& data, double eps, int) {
+    if (eps < 0) throw std::invalid_argument("epsnn_dk: eps must be nonnegative");
+    check_query(query, data, false, "epsnn_dk");
+    const auto start = Clock::now();
+    auto& st = data.device_store();
+    std::vector<tsw_neighbor> out(data.size());
+    uint64_t count = 0;
+    tsw_counters c{};
+    const int rc = tsw_epsnn_dk(st.h, query.flat().data(), query.length(), eps, out.data(),
+                                out.size(), &count, &c);
+    if (rc != TSW_OK) detail::rethrow(rc);
+    SearchReport rep;
+    rep.neighbors.resize(count);
+    for (uint64_t j = 0; j < count; ++j)
+        rep.neighbors[j] = {static_cast<std::size_t>(out[j].index), out[j].distance};
+    rep.counters = {c.lb_computed, c.lb_pruned, c.full_dp, c.early_abandoned, c.gdk_calls};
+    rep.wall_time_seconds = std::chrono::duration<double>(Clock::now() - start).count();
+    return rep;
+}
+
+}  // namespace tswarp

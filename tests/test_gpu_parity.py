@@ -1,0 +1,266 @@
+"""GPU parity: every kernel and both k-NN drivers against the CPU oracle on the same inputs.
+
+Bar (BASELINE.json north_star): neighbour indices and order bit-exact under the (distance,
+index) tie rule; DK distances bit-exact; DTW distances bit-exact (allowed: 1e-12 relative,
+asserted exactly here because the suffix-order recursion is reproduced).
+LB_Box is summed in a different order, so it is compared with rel. tolerance 1e-12.
+All calls go through the C ABI (libtswarp_b200.so).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+RNG = np.random.default_rng(20181127)
+
+
+def walks(rng, n, L, d):
+    return rng.standard_normal((n, L, d)).cumsum(1)
+
+
+def assert_knn_equal(gi, gd, oi, od, msg=""):
+    assert np.array_equal(np.asarray(gi, dtype=np.uint64), np.asarray(oi, dtype=np.uint64)), \
+        f"{msg} indices gpu={gi} oracle={oi}"
+    assert np.array_equal(np.asarray(gd).view(np.uint64), np.asarray(od).view(np.uint64)), \
+        f"{msg} distances gpu={gd!r} oracle={od!r}"
+
+
+# ---- K1 envelope ------------------------------------------------------------------------
+@pytest.mark.parametrize("L,d,r", [(1, 1, 0), (3, 1, 1), (17, 3, 0), (64, 2, 5), (128, 3, 13),
+                                   (50, 4, 100), (256, 16, 26)])
+def test_envelope_exact(tsw, port, L, d, r):
+    s = RNG.standard_normal((L, d)).cumsum(0)
+    lo, hi = tsw.envelope(s, r)
+    olo, ohi = port.envelope(s, r)
+    assert np.array_equal(lo, olo) and np.array_equal(hi, ohi)
+
+
+def test_envelope_spec_kat(tsw):
+    # t=((1),(3),(2)), r=1 -> lower ((1),(1),(2)), upper ((3),(3),(3))
+    lo, hi = tsw.envelope(np.array([[1.0], [3.0], [2.0]]), 1)
+    assert lo.ravel().tolist() == [1, 1, 2] and hi.ravel().tolist() == [3, 3, 3]
+
+
+# ---- K2 LB_Box + seed upper bound --------------------------------------------------------
+@pytest.mark.parametrize("N,L,d,r", [(300, 32, 1, 3), (500, 64, 3, 6), (200, 128, 2, 13),
+                                     (100, 256, 16, 26), (64, 33, 3, 4), (50, 1, 2, 0)])
+def test_lb_box_all(tsw, port, N, L, d, r):
+    X = walks(RNG, N, L, d)
+    q = walks(RNG, 1, L, d)[0]
+    lb, ub = tsw.lb_box_all(tsw.Store(X), q, r)
+    olb = np.array([port.lb_box(X[i], q, r) for i in range(N)])
+    np.testing.assert_allclose(lb, olb, rtol=1e-12, atol=0)
+    dtw = np.array([port.dtw_banded(q, X[i], r) for i in range(N)])
+    assert np.all(ub >= dtw), "diagonal upper bound below computed DTW"
+    assert np.all(lb <= dtw * (1 + 1e-12)), "LB_Box above DTW"
+
+
+def test_lb_box_sneak_past(tsw, port):
+    # SPEC.md:144-147 Fig. 3: t=((0,1),(0,0),(1,0)), r=2, s=((1,1),(1,1),(1,1)) -> lb_box 0 < dtw
+    t = np.array([[0.0, 1.0], [0.0, 0.0], [1.0, 0.0]])
+    s = np.ones((3, 2))
+    lb, _ = tsw.lb_box_all(tsw.Store(s[None]), t, 2)
+    assert lb[0] == 0.0
+    ex, val = tsw.dist_all(tsw.Store(s[None]), t, "dtw", 2)
+    assert ex[0] and val[0] == port.dtw_banded(t, s, 2) and val[0] > 0
+
+
+# ---- K4 DTW DP ---------------------------------------------------------------------------
+@pytest.mark.parametrize("N,L,d,r", [(200, 1, 1, 0), (200, 2, 1, 1), (300, 16, 2, 0),
+                                     (300, 40, 3, 3), (300, 64, 1, 64), (200, 128, 3, 13),
+                                     (100, 256, 2, 26), (60, 256, 16, 26), (40, 97, 5, 40),
+                                     (20, 300, 3, 70), (10, 1024, 3, 51), (16, 200, 2, 150)])
+def test_dtw_all_bit_exact(tsw, port, N, L, d, r):
+    X = walks(RNG, N, L, d)
+    q = walks(RNG, 1, L, d)[0]
+    st = tsw.Store(X)
+    ex, val = tsw.dist_all(st, q, "dtw", r)
+    ref = port.dtw_all(q, __import__("oracle").Dataset(X), r)
+    assert ex.all()
+    assert np.array_equal(val.view(np.uint64), ref.view(np.uint64))
+    # thresholded: Exact iff d <= eps (dtw_early_abandon, dtw.cpp:82-90)
+    eps = float(np.median(ref))
+    ex2, val2 = tsw.dist_all(st, q, "dtw", r, eps)
+    for i in range(N):
+        oe, ov = port.dtw_early_abandon(q, X[i], r, eps)
+        assert ex2[i] == oe and val2[i] == ov, (i, ex2[i], val2[i], oe, ov)
+
+
+def test_dtw_spec_kats(tsw):
+    # s=((0),(0)), t=((1),(1)), r=1 -> 2 ; s=t -> 0
+    ex, val = tsw.dist_all(tsw.Store(np.ones((1, 2, 1))), np.zeros((2, 1)), "dtw", 1)
+    assert ex[0] and val[0] == 2.0
+    ex, val = tsw.dist_all(tsw.Store(np.arange(5.0).reshape(1, 5, 1)), np.arange(5.0).reshape(5, 1), "dtw", 2)
+    assert val[0] == 0.0
+    # eps = 0 with positive first-cell cost -> Exceeds(0)
+    ex, val = tsw.dist_all(tsw.Store(np.ones((1, 2, 1))), np.zeros((2, 1)), "dtw", 1, 0.0)
+    assert not ex[0] and val[0] == 0.0
+
+
+# ---- K5 DK DP ----------------------------------------------------------------------------
+@pytest.mark.parametrize("N,L,d", [(200, 1, 1), (200, 2, 2), (300, 16, 2), (300, 33, 3),
+                                   (200, 64, 1), (200, 128, 2), (100, 256, 16), (20, 1024, 3),
+                                   (50, 70, 5)])
+def test_dk_all_bit_exact(tsw, port, N, L, d):
+    import oracle
+
+    X = walks(RNG, N, L, d)
+    q = walks(RNG, 1, L, d)[0]
+    st = tsw.Store(X)
+    ex, val = tsw.dist_all(st, q, "dk")
+    ref = port.dk_all(q, oracle.Dataset(X))
+    assert ex.all()
+    assert np.array_equal(val.view(np.uint64), ref.view(np.uint64))
+    for eps in (float(np.quantile(ref, 0.1)), float(np.median(ref)), 0.0):
+        ex2, val2 = tsw.dist_all(st, q, "dk", 0, eps)
+        for i in range(N):
+            oe, ov = port.sparse_dk(q, X[i], eps)
+            assert ex2[i] == oe and val2[i] == ov, (eps, i, ex2[i], val2[i], oe, ov)
+
+
+def test_dk_ragged_lengths(tsw, port):
+    series = [RNG.standard_normal((int(RNG.integers(1, 90)), 3)).cumsum(0) for _ in range(150)]
+    q = RNG.standard_normal((57, 3)).cumsum(0)
+    ex, val = tsw.dist_all(tsw.Store(series), q, "dk")
+    ref = np.array([port.dk_full(q, s) for s in series])
+    assert ex.all() and np.array_equal(val.view(np.uint64), ref.view(np.uint64))
+
+
+def test_dk_spec_kats(tsw):
+    # s=((0),(0)), t=((1),(1)) -> 1 ; s=((0),(10),(0)), t=((0),(0)) -> 10
+    _, v = tsw.dist_all(tsw.Store(np.ones((1, 2, 1))), np.zeros((2, 1)), "dk")
+    assert v[0] == 1.0
+    _, v = tsw.dist_all(tsw.Store([np.zeros((2, 1))]), np.array([[0.0], [10.0], [0.0]]), "dk")
+    assert v[0] == 10.0
+
+
+# ---- k-NN drivers vs the reference (acceptance criterion 8) -----------------
+def _check_counters(c, n, metric):
+    if metric == "dtw":
+        assert c[0] == n and c[1] + c[2] + c[3] == n, c
+    else:
+        assert c[4] == n and c[2] + c[3] == n, c
+
+
+def test_knn_random_datasets(tsw, best_oracle):
+    import oracle
+
+    rng = np.random.default_rng(8)
+    for trial in range(100):
+        n = int(rng.integers(1, 200))
+        L = int(rng.integers(1, 64))
+        d = int(rng.integers(1, 5))
+        r = int(rng.integers(0, max(1, L // 3) + 1))
+        k = int(rng.integers(1, 12))
+        X = walks(rng, n, L, d)
+        Q = walks(rng, 3, L, d)
+        if trial % 10 == 0:
+            Q[0] = X[int(rng.integers(0, n))]  # query in data: self-match at distance 0
+        ds = tsw.Dataset(X)
+        ods = oracle.Dataset(X)
+        for metric in ("dtw", "dk"):
+            gi, gd, gc = tsw.knn(ds, Q, k, metric, r)
+            for q in range(len(Q)):
+                oi, od, _ = best_oracle.knn(Q[q], ods, k, metric, r)
+                assert_knn_equal(gi[q], gd[q], oi, od, f"trial {trial} {metric} q{q}")
+                _check_counters(gc[q], n, metric)
+
+
+def test_knn_ties_and_duplicates(tsw, best_oracle):
+    import oracle
+
+    base = walks(RNG, 20, 24, 2)
+    X = np.concatenate([base, base, base[::-1]])  # exact duplicates -> equal distances
+    q = base[3] + 0.01
+    for metric in ("dtw", "dk"):
+        for k in (1, 2, 3, 7, 40, 60):
+            gi, gd, _ = tsw.knn(tsw.Dataset(X), q[None], k, metric, 4)
+            oi, od, _ = best_oracle.knn(q, oracle.Dataset(X), k, metric, 4)
+            assert_knn_equal(gi[0], gd[0], oi, od, f"{metric} k={k}")
+
+
+def test_knn_k_larger_than_kmax_and_n(tsw, best_oracle):
+    import oracle
+
+    X = walks(RNG, 150, 20, 2)
+    q = walks(RNG, 1, 20, 2)[0]
+    for metric in ("dtw", "dk"):
+        for k in (65, 100, 150, 1000):
+            gi, gd, gc = tsw.knn(tsw.Dataset(X), q[None], k, metric, 3)
+            oi, od, _ = best_oracle.knn(q, oracle.Dataset(X), k, metric, 3)
+            assert_knn_equal(gi[0], gd[0], oi, od, f"{metric} k={k}")
+            _check_counters(gc[0], 150, metric)
+
+
+def test_knn_constant_and_degenerate(tsw, best_oracle):
+    import oracle
+
+    X = np.zeros((30, 10, 2))
+    X[5] += 1.0
+    q = np.zeros((10, 2))
+    for metric in ("dtw", "dk"):
+        gi, gd, _ = tsw.knn(tsw.Dataset(X), q[None], 4, metric, 2)
+        oi, od, _ = best_oracle.knn(q, oracle.Dataset(X), 4, metric, 2)
+        assert_knn_equal(gi[0], gd[0], oi, od, metric)
+
+
+def test_knn_dk_ragged(tsw, best_oracle):
+    import oracle
+
+    series = [RNG.standard_normal((int(RNG.integers(1, 80)), 2)).cumsum(0) for _ in range(120)]
+    for k in (1, 5):
+        q = RNG.standard_normal((40, 2)).cumsum(0)
+        rep = tsw.knn_dk(q, tsw.Dataset(series), k)
+        oi, od, _ = best_oracle.knn(q, oracle.Dataset(series), k, "dk")
+        assert_knn_equal([nb.index for nb in rep.neighbors], [nb.distance for nb in rep.neighbors], oi, od)
+
+
+def test_errors_mirror_reference(tsw):
+    X = walks(RNG, 10, 12, 2)
+    ds = tsw.Dataset(X)
+    with pytest.raises(ValueError, match="k must be positive"):
+        tsw.knn_dtw(X[0], ds, 0, 2)
+    with pytest.raises(ValueError, match="query dim"):
+        tsw.knn_dk(np.zeros((12, 3)), ds, 1)
+    with pytest.raises(ValueError, match="length differs"):
+        tsw.knn_dtw(np.zeros((11, 2)), ds, 1, 2)
+    with pytest.raises(ValueError, match="eps must be nonnegative"):
+        tsw.epsnn_dk(X[0], ds, -1.0)
+    with pytest.raises(tsw.ValidationError):
+        tsw.Store(np.full((2, 3, 1), np.nan))
+
+
+def test_epsnn_dk(tsw, best_oracle):
+    import oracle
+
+    X = walks(RNG, 300, 30, 3)
+    q = walks(RNG, 1, 30, 3)[0]
+    ods = oracle.Dataset(X)
+    dks = np.array([best_oracle.dk_full(q, x) for x in X])
+    for eps in (0.0, float(np.quantile(dks, 0.05)), float(np.median(dks)), float("inf")):
+        rep = tsw.epsnn_dk(q, tsw.Dataset(X), eps)
+        oi, od, _ = best_oracle.epsnn_dk(q, ods, eps)
+        assert_knn_equal([nb.index for nb in rep.neighbors], [nb.distance for nb in rep.neighbors], oi, od)
+        assert rep.counters.full_dp + rep.counters.early_abandoned == 300
+
+
+def test_plan_reuse_and_device_queries(tsw, best_oracle):
+    import oracle
+    import torch
+
+    X = walks(RNG, 500, 64, 3)
+    Q = walks(RNG, 6, 64, 3)
+    ds = tsw.Dataset(X)
+    plan = tsw.Plan(ds, 8, 64, "dtw", 6, 3)
+    plan.set_queries(Q)
+    plan.execute()
+    a = plan.fetch()
+    dq = torch.from_numpy(Q).cuda()
+    stream = torch.cuda.current_stream()
+    plan.set_queries_device(dq.data_ptr(), 6, stream.cuda_stream)
+    plan.execute(stream.cuda_stream)
+    b = plan.fetch(stream.cuda_stream)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+    for q in range(6):
+        oi, od, _ = best_oracle.knn(Q[q], oracle.Dataset(X), 3, "dtw", 6)
+        assert_knn_equal(a[0][q], a[1][q], oi, od)
