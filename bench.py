@@ -1,0 +1,380 @@
+#!/usr/bin/env python
+"""Benchmark: batched k-NN queries/sec on one B200 (or N replicas), driver contract.
+
+A step = one pass of the hot path over one batch: every query of the configuration against
+the whole device-resident database (BASELINE.json configs; default config 2 = configs[1]:
+1-NN DTW r=13 + LB_Box, N=20,000, d=3, L=128, 64 queries), i.e. the batched equivalent of
+64 reference knn_dtw calls.  Inputs are seeded synthetic series with the configs' shapes.
+
+value : queries/s with queries and database resident in HBM (device-to-device query load +
+        the full pipeline; results stay on the device), CUDA events on the launching
+        stream, L2 flushed (256 MiB write) between timed steps.
+e2e   : the same metric through the public C ABI call tsw_knn with HOST query / result
+        buffers (H2D + pipeline + D2H + host finalisation inside the timed region).
+Multi-GPU (torchrun): replicas -- every rank holds its own store and runs its own query batch
+(different query seed); weak scaling, value = all ranks' queries / max-over-ranks time.
+
+--impl reference: the reference's own CPU implementation of the path (oracle/_ref, compiled
+from /root/reference's sources; the C port oracle/ when it is absent) on this host's cores,
+query-parallel with every core, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "k-NN queries/sec and DP cell-updates/sec (GCUPS); LB_Box HBM GB/s vs peak"
+DEFAULT_METRIC = {1: "dk", 2: "dtw", 3: "dtw", 4: "dtw", 5: "dtw"}
+SEED = 20181127
+FLUSH_BYTES = 256 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--metric", default=None, choices=["dtw", "dk"])
+    ap.add_argument("--seed", type=int, default=SEED)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0,
+                    help="target CPU work for the bounded cpu_baseline / reference sample")
+    ap.add_argument("--out", default=None, help="also append the JSON line to this file")
+    return ap.parse_args()
+
+
+def workload(cfg: int, metric: str, sh: dict, nq: int) -> dict:
+    return {
+        "workload": f"config{cfg}: {sh['k']}-NN {metric.upper()}"
+                    + (f" r={sh['r']} + LB_Box" if metric == "dtw" else " (dog-keeper)")
+                    + f", N={sh['count']}, d={sh['d']}, L={sh['len']}, {nq} queries/step",
+        "config_id": cfg, "n": sh["count"], "d": sh["d"], "L": sh["len"], "k": sh["k"],
+        "r": sh["r"] if metric == "dtw" else None, "queries_per_step": nq, "metric": metric,
+        "l2": "flushed between timed steps (256 MiB device write)",
+    }
+
+
+def dist_init():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def emit(line: dict, out: str | None):
+    s = json.dumps(line)
+    print(s, flush=True)
+    if out:
+        with open(out, "a") as f:
+            f.write(s + "\n")
+
+
+# ---- CPU reference / baseline ---------------------------------------------------------------
+def cpu_reference(cfg, metric, sh, db, queries, target_s, steps=1, warmup=0):
+    """Times the reference CPU implementation on a bounded query sample.
+    Returns (queries/s per step list, info dict, answers)."""
+    import oracle
+
+    try:
+        orc = oracle.ref()
+        kind = "reference"
+    except Exception:
+        orc = oracle.port()
+        kind = "port"
+    cores = os.cpu_count() or 1
+    ds = oracle.Dataset(db)
+    k, r = sh["k"], sh["r"]
+    # calibrate: one query, single thread
+    t0 = time.perf_counter()
+    orc.knn(queries[0], ds, k, metric, r)
+    t1 = max(time.perf_counter() - t0, 1e-4)
+    par = cores if kind == "reference" else 1
+    nsample = int(max(1, min(len(queries), round(target_s * par / t1))))
+    if kind == "reference":
+        nsample = max(nsample, min(len(queries), par))
+    sample = queries[:nsample]
+    rates, durs = [], []
+    for it in range(warmup + steps):
+        t0 = time.perf_counter()
+        if kind == "reference":
+            orc.knn_batch(sample, ds, k, metric, r, threads=par)
+        else:
+            for q in sample:
+                orc.knn(q, ds, k, metric, r)
+        dt = time.perf_counter() - t0
+        if it >= warmup:
+            rates.append(nsample / dt)
+            durs.append(dt)
+    info = {"kind": kind, "cores": par,
+            "sample": f"{nsample} of {len(queries)} config-{cfg} queries against the full "
+                      f"N={sh['count']} database, {'query-parallel over ' + str(par) + ' threads (threads=1 per knn call)' if par > 1 else 'single thread'}",
+            "cpu": _cpu_model(), "seconds_per_step": float(np.mean(durs))}
+    return rates, info
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def run_reference_arm(a, sh, metric):
+    ws, rank, _ = dist_init()
+    if rank != 0:
+        return
+    import paper_1811_11076_b200 as t
+
+    db, _ = t.synth(a.config, 0, a.seed)
+    qs, _ = t.synth(a.config, 1, a.seed)
+    per_step = max(3.0, min(a.cpu_seconds, 60.0))
+    rates, info = cpu_reference(a.config, metric, sh, db, qs, per_step, steps=a.steps,
+                                warmup=a.warmup)
+    v = float(np.mean(rates))
+    line = {"metric": METRIC, "value": v, "unit": "queries/s", "impl": "reference",
+            "n_gpus": ws, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": 1000.0 * info["seconds_per_step"],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded random walks, BASELINE.json shapes)",
+            "config": workload(a.config, metric, sh, len(qs)),
+            "cpu_baseline": {"value": v, "unit": "queries/s", **info},
+            "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    emit(line, a.out)
+
+
+# ---- GPU arm ------------------------------------------------------------------------------
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+def load_traffic(cfg, metric):
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(f"config{cfg}_{metric}")
+    except Exception:
+        return None
+
+
+def main():
+    a = parse()
+    metric = a.metric or DEFAULT_METRIC[a.config]
+    import paper_1811_11076_b200 as t
+
+    sh = t.synth_shape(a.config, 0)
+    if a.impl == "reference":
+        run_reference_arm(a, sh, metric)
+        return
+
+    import torch
+
+    ws, rank, local = dist_init()
+    if ws > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.cuda.current_device()
+
+    db, _ = t.synth(a.config, 0, a.seed)
+    qs, _ = t.synth(a.config, 1, a.seed + rank)
+    nq, L, d = qs.shape
+    k, r = sh["k"], sh["r"]
+    store = t.Store(db, device=dev)
+    plan = t.Plan(store, nq, L, metric, r, k)
+    stream = torch.cuda.current_stream()
+    sptr = stream.cuda_stream
+    dq = torch.from_numpy(qs).to(f"cuda:{dev}")
+    flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=f"cuda:{dev}")
+
+    def step():
+        plan.set_queries_device(dq.data_ptr(), nq, sptr)
+        plan.execute(sptr)
+
+    def do_flush():
+        t.l2_flush(flush.data_ptr(), FLUSH_BYTES, sptr)
+
+    for _ in range(a.warmup):
+        step()
+        do_flush()
+    torch.cuda.synchronize()
+    # correctness guard on the warmed-up answer (cheap; not timed)
+    res_idx, res_dist, res_ctr = plan.fetch(sptr)
+
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(a.steps)]
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(dev) as clk:
+        for i in range(a.steps):
+            evs[i][0].record(stream)
+            step()
+            evs[i][1].record(stream)
+            do_flush()
+        torch.cuda.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    step_ms = [s.elapsed_time(e) for s, e in evs]
+    total_ms = float(sum(step_ms))
+    if ws > 1:
+        tt = torch.tensor([total_ms], device=f"cuda:{dev}", dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    value = ws * nq * a.steps / (total_ms / 1000.0)
+
+    # ---- instrumented pass: per-phase device times, cells, bytes (not the headline) -----
+    plan.set_timing(True)
+    phases = []
+    for _ in range(max(3, min(a.steps, 10))):
+        step()
+        st = plan.stats()
+        phases.append(st)
+        do_flush()
+    torch.cuda.synchronize()
+    plan.set_timing(False)
+    ph = {key: float(np.median([p[key] for p in phases])) for key in phases[0]}
+    launches_per_step = int(ph["kernel_launches"]) + 1  # + query transpose
+
+    # ---- e2e through the public C ABI with host buffers ---------------------------------
+    e2e_ms = []
+    for i in range(a.warmup + a.steps):
+        do_flush()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        idx2, dist2, _ = t.knn(store, qs, k, metric, r)
+        dt = time.perf_counter() - t0
+        if i >= a.warmup:
+            e2e_ms.append(dt * 1000.0)
+    h2d, d2h = t.last_transfer_bytes()
+    assert np.array_equal(idx2, res_idx) and np.array_equal(dist2, res_dist), "e2e answer mismatch"
+    e2e_total = float(sum(e2e_ms))
+    if ws > 1:
+        tt = torch.tensor([e2e_total], device=f"cuda:{dev}", dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        e2e_total = float(tt.item())
+    e2e_value = ws * nq * a.steps / (e2e_total / 1000.0)
+
+    # ---- rooflines ------------------------------------------------------------------------
+    peaks, peak_kind = load_peaks()
+    fp64_tflops = t.fp64_peak() / 1e12
+    lb_ms = ph["ms_bound"]
+    lb_gbs = ph["bound_bytes"] / (lb_ms * 1e-3) / 1e9 if lb_ms > 0 else None
+    dp_ms = ph["ms_dp"] + ph["ms_probe_dp"]
+    cells = ph["dp_cells"]
+    ops_per_cell = 3 * d + 2
+    gcups = cells / (dp_ms * 1e-3) / 1e9 if dp_ms > 0 else None
+    dp_tflops = gcups * ops_per_cell / 1e3 if gcups else None
+    roof_lb = {"bound": "hbm", "kernel": "lb_ub_kernel" if metric == "dtw" else "dk_bounds_kernel",
+               "achieved": lb_gbs, "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
+               "frac": (lb_gbs / peaks["hbm_gbs"]) if lb_gbs else None,
+               "traffic": (load_traffic(a.config, metric) or {}).get("bound"),
+               "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json copy rate)",
+               "algorithmic_bytes_per_launch": ph["bound_bytes"] / max(1.0, ph["bound_passes"]),
+               "share_of_step": lb_ms / ph["ms_total"] if ph["ms_total"] else None}
+    roof_dp = {"bound": "fp64", "kernel": "dtw_dp_kernel" if metric == "dtw" else "dk_dp_kernel",
+               "achieved": dp_tflops, "peak": fp64_tflops, "unit": "TFLOP/s",
+               "frac": (dp_tflops / fp64_tflops) if dp_tflops and fp64_tflops else None,
+               "traffic": (load_traffic(a.config, metric) or {}).get("dp"),
+               "peak_source": "measured live: FP64 DMUL+DADD probe kernel (tsw_fp64_peak)",
+               "gcups": gcups, "fp64_ops_per_cell": ops_per_cell, "cells_per_step": cells,
+               "share_of_step": dp_ms / ph["ms_total"] if ph["ms_total"] else None}
+    dominant = roof_dp if dp_ms >= lb_ms else roof_lb
+
+    line = {"metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": ws,
+            "steps": a.steps, "warmup": a.warmup, "ms_per_step": total_ms / a.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded random walks, BASELINE.json shapes; no public dataset)",
+            "config": workload(a.config, metric, sh, nq),
+            "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h,
+                    "api": "tsw_knn (C ABI) with host query/result buffers"},
+            "gpu_launches": launches_per_step * a.steps,
+            "roofline": dominant, "roofline_lb": roof_lb, "roofline_dp": roof_dp,
+            "gcups": gcups, "lb_hbm_gbs": lb_gbs,
+            "phases_ms": {k2: ph[k2] for k2 in ("ms_total", "ms_envelope", "ms_bound", "ms_select",
+                                               "ms_probe_dp", "ms_compact", "ms_dp")},
+            "dp_pairs_per_step": ph["dp_pairs"],
+            "counters_q0": [int(x) for x in res_ctr[0]],
+            "clocks": clk.summary()}
+
+    if rank == 0 and ws == 1 and not a.no_cpu_baseline:
+        rates, info = cpu_reference(a.config, metric, sh, db, qs, a.cpu_seconds)
+        line["cpu_baseline"] = {"value": float(np.mean(rates)), "unit": "queries/s", **info}
+    if rank == 0:
+        emit(line, a.out)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -141,6 +141,14 @@ int tsw_lb_box_all(tsw_store* store, const double* query, uint64_t qlen, uint64_
 int tsw_dist_all(tsw_store* store, const double* query, uint64_t qlen, int metric, uint64_t r,
                  double eps, int* exact, double* value);
 
+/* ---- diagnostics ---------------------------------------------------------------------------
+ * Host<->device bytes moved by the calling thread's last tsw_knn / plan set_queries+fetch. */
+int tsw_last_transfer_bytes(uint64_t* h2d, uint64_t* d2h);
+/* Measured FP64 instruction throughput of the current device (DADD/DMUL lane-ops per s). */
+int tsw_fp64_peak(double* ops_per_s);
+/* Overwrite `bytes` of a device buffer (used to flush L2 between timed benchmark steps). */
+int tsw_l2_flush(void* dev_buf, uint64_t bytes, void* stream);
+
 /* ---- seeded synthetic inputs for the five benchmark configurations (BASELINE.json) --------
  * part 0 = database, 1 = queries.  Writes count x len x d row-major values into `out` (caller
  * allocates; query tsw_synth_shape first) and, for the class-structured config 3, labels. */

@@ -31,6 +31,7 @@ using namespace tswb;
 namespace {
 
 thread_local std::string g_err;
+thread_local uint64_t g_h2d = 0, g_d2h = 0;
 
 struct Error {
     int code;
@@ -293,6 +294,7 @@ void set_queries_impl(tsw_plan* p, const double* q, uint64_t nq, bool device, cu
     ck(cudaMemcpyAsync(p->q_rm.p, q, bytes, device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
                        st),
        "query upload");
+    g_h2d = device ? 0 : bytes;
     launch_rowmajor_to_soa(p->q_rm.p, (uint32_t)nq, (uint32_t)p->qlen, (uint32_t)d,
                            (uint32_t)p->ldq, p->q_soa.p, st);
     p->nq = nq;
@@ -420,6 +422,8 @@ void fetch_impl(tsw_plan* p, tsw_neighbor* out, tsw_counters* counters, cudaStre
            "fetch result counts");
     }
     ck(cudaStreamSynchronize(st), "pipeline");
+    g_d2h = nq * sizeof(QState) + td.size() * sizeof(double) + ti.size() * sizeof(uint32_t) +
+            rn.size() * sizeof(unsigned);
     for (uint64_t q = 0; q < nq; ++q) {
         tsw_neighbor* o = out ? out + q * kk : nullptr;
         if (kk <= (uint64_t)kKMax) {
@@ -434,6 +438,7 @@ void fetch_impl(tsw_plan* p, tsw_neighbor* out, tsw_counters* counters, cudaStre
                "fetch results");
             ck(cudaMemcpy(ri.data(), p->res_i.p + q * n, cnt * sizeof(uint32_t), cudaMemcpyDeviceToHost),
                "fetch results");
+            g_d2h += cnt * (sizeof(double) + sizeof(uint32_t));
             std::vector<tsw_neighbor> all(cnt);
             for (unsigned j = 0; j < cnt; ++j) all[j] = {ri[j], rd[j]};
             std::sort(all.begin(), all.end(), [](const tsw_neighbor& a, const tsw_neighbor& b) {
@@ -473,6 +478,12 @@ extern "C" {
 
 const char* tsw_last_error(void) { return g_err.c_str(); }
 int tsw_version(void) { return 1; }
+
+int tsw_last_transfer_bytes(uint64_t* h2d, uint64_t* d2h) {
+    if (h2d) *h2d = g_h2d;
+    if (d2h) *d2h = g_d2h;
+    return TSW_OK;
+}
 
 int tsw_device_count(void) {
     int n = 0;
@@ -681,12 +692,17 @@ int tsw_knn(tsw_store* s, const double* queries, uint64_t nq, uint64_t qlen, int
         DeviceGuard dg(s->device);
         tsw_plan* p = cached_plan(s, nq, qlen, metric, r, k);
         const uint64_t kk = p->kk;
+        uint64_t h2d = 0, d2h = 0;
         for (uint64_t q0 = 0; q0 < nq; q0 += p->nq_max) {
             const uint64_t nb = std::min(p->nq_max, nq - q0);
             set_queries_impl(p, queries + q0 * qlen * s->d, nb, false, p->own);
             execute_impl(p, p->own);
             fetch_impl(p, out ? out + q0 * kk : nullptr, counters ? counters + q0 : nullptr, p->own);
+            h2d += g_h2d;
+            d2h += g_d2h;
         }
+        g_h2d = h2d;
+        g_d2h = d2h;
     });
 }
 

@@ -100,6 +100,9 @@ def lib():
     L.tsw_envelope.argtypes = [_dp, _u64, _u64, _u64, _dp, _dp]
     L.tsw_lb_box_all.argtypes = [_vp, _dp, _u64, _u64, _dp, _dp]
     L.tsw_dist_all.argtypes = [_vp, _dp, _u64, C.c_int, _u64, C.c_double, _ip, _dp]
+    L.tsw_last_transfer_bytes.argtypes = [_up, _up]
+    L.tsw_fp64_peak.argtypes = [_dp]
+    L.tsw_l2_flush.argtypes = [_vp, _u64, _vp]
     L.tsw_synth_shape.argtypes = [C.c_int, C.c_int, _up, _up, _up, _up, _up]
     L.tsw_synth_generate.argtypes = [C.c_int, C.c_int, _u64, _dp, C.POINTER(C.c_int32)]
     _lib = L
@@ -121,6 +124,23 @@ def _check(rc: int) -> None:
 
 def device_count() -> int:
     return int(lib().tsw_device_count())
+
+
+def last_transfer_bytes() -> tuple[int, int]:
+    h2d, d2h = _u64(), _u64()
+    lib().tsw_last_transfer_bytes(C.byref(h2d), C.byref(d2h))
+    return h2d.value, d2h.value
+
+
+def fp64_peak() -> float:
+    """Measured FP64 DADD/DMUL throughput of the current device, lane-ops per second."""
+    v = C.c_double()
+    _check(lib().tsw_fp64_peak(C.byref(v)))
+    return v.value
+
+
+def l2_flush(dev_ptr: int, nbytes: int, stream: int | None = None) -> None:
+    _check(lib().tsw_l2_flush(dev_ptr, nbytes, stream))
 
 
 def _series(x) -> np.ndarray:
