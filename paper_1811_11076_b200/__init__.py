@@ -7,12 +7,13 @@ C++ drop-in header (include/tswarp_b200.hpp) and this Python mirror (tswarp.py).
 """
 from .tswarp import (  # noqa: F401
     Dataset, Neighbor, Plan, SearchCounters, SearchReport, Store, TswError, ValidationError,
-    device_count, dist_all, envelope, epsnn_dk, knn, knn_dk, knn_dtw, lb_box_all, lib, synth,
-    synth_shape,
+    device_count, dist_all, envelope, epsnn_dk, fp64_peak, knn, knn_dk, knn_dtw, l2_flush,
+    last_transfer_bytes, lb_box_all, lib, synth, synth_shape,
 )
 
 __all__ = [
     "Dataset", "Neighbor", "Plan", "SearchCounters", "SearchReport", "Store", "TswError",
-    "ValidationError", "device_count", "dist_all", "envelope", "epsnn_dk", "knn", "knn_dk",
-    "knn_dtw", "lb_box_all", "lib", "synth", "synth_shape",
+    "ValidationError", "device_count", "dist_all", "envelope", "epsnn_dk", "fp64_peak", "knn",
+    "knn_dk", "knn_dtw", "l2_flush", "last_transfer_bytes", "lb_box_all", "lib", "synth",
+    "synth_shape",
 ]
