@@ -251,7 +251,10 @@ def main():
     k, r = sh["k"], sh["r"]
     store = t.Store(db, device=dev)
     plan = t.Plan(store, nq, L, metric, r, k)
-    stream = torch.cuda.current_stream()
+    # a dedicated (non-default) stream: the library launches on exactly this stream, so the
+    # CUDA events below bracket its kernels (handle 0 would mean the plan's own stream)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     sptr = stream.cuda_stream
     dq = torch.from_numpy(qs).to(f"cuda:{dev}")
     flush = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device=f"cuda:{dev}")

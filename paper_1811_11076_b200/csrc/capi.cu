@@ -395,6 +395,7 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
     mark(5);
     run_dp(p->queue.p, p->counters.p + 2, p->counters.p + 3, nq * n);
     mark(6);
+    ck(cudaEventRecord(p->ev[7], st), "cudaEventRecord");
     ck(cudaGetLastError(), "kernel launch");
     p->launches = launches;
     p->executed = true;
@@ -655,6 +656,7 @@ int tsw_plan_stats(tsw_plan* p, tsw_stats* out) {
         std::memset(out, 0, sizeof(*out));
         unsigned cnt[8] = {0};
         unsigned long long cells = 0;
+        if (p->executed) ck(cudaEventSynchronize(p->ev[7]), "stats");
         ck(cudaMemcpy(cnt, p->counters.p, sizeof(cnt), cudaMemcpyDeviceToHost), "stats");
         ck(cudaMemcpy(&cells, p->cells.p, sizeof(cells), cudaMemcpyDeviceToHost), "stats");
         out->dp_pairs = (uint64_t)cnt[0] + cnt[2];
