@@ -134,46 +134,52 @@ struct tsw_plan;
 
 struct tsw_store {
     int device = 0;
-    uint64_t n = 0, d = 0, ulen = 0, uld = 0, max_len = 0;
+    uint64_t n = 0, d = 0, ulen = 0, ustride = 0, max_len = 0;
     DevBuf<double> data;
+    DevBuf<float> data32;
     DevBuf<uint64_t> off;
     DevBuf<uint32_t> len;
     std::vector<uint32_t> host_len;
-    uint64_t bytes = 0;
+    uint64_t bytes = 0;      // fp64 store bytes
+    float err32 = 0.0f;      // >= max |x - fp32(x)| over the store
     std::mutex mu;
     std::unique_ptr<tsw_plan> cached_plan;
     StoreDev dev() const {
         StoreDev s{};
         s.data = data.p;
+        s.data32 = data32.p;
         s.off = off.p;
         s.len = len.p;
         s.n = (uint32_t)n;
         s.d = (uint32_t)d;
         s.ulen = (uint32_t)ulen;
-        s.uld = (uint32_t)uld;
+        s.ustride = ustride;
         return s;
     }
     ~tsw_store();
 };
 
+// counters layout of a plan
+enum { C_PFRONT = 0, C_PBACK, C_PHEAD, C_MFRONT, C_MBACK, C_MHEAD, C_COUNT = 8 };
+
 struct tsw_plan {
     tsw_store* store = nullptr;
-    uint64_t nq_max = 0, qlen = 0, ldq = 0, r = 0, k = 0, kk = 0, P = 0, probe = 0;
+    uint64_t nq_max = 0, qlen = 0, qstride = 0, r = 0, k = 0, kk = 0, P = 0, probe = 0, S = 0;
     int metric = 0;
     uint64_t nq = 0;  // queries of the last set_queries
     cudaStream_t own = nullptr;
-    DevBuf<double> q_rm, q_soa, env_lo, env_hi, bnd_a, bnd_b, sel_sv, sel_v, top_d;
+    DevBuf<double> q, ub, sel_sv, sel_v, top_d;
+    DevBuf<float> env_lo, env_hi;
     DevBuf<uint32_t> sel_si, sel_i, top_i;
     DevBuf<QState> state;
     DevBuf<uint8_t> probed;
-    DevBuf<Pair> probe_q, queue;
-    DevBuf<unsigned> counters;  // [0] probe_len [1] probe_head [2] queue_len [3] queue_head
+    DevBuf<QEntry> probe_q, queue;
+    DevBuf<unsigned> counters;
     DevBuf<unsigned long long> cells;
-    DevBuf<unsigned long long> cum_cells;
     DevBuf<double> res_d;
     DevBuf<uint32_t> res_i;
     DevBuf<unsigned> res_n;
-    double margin = 1.0, ub_scale = 1.0;
+    double margin = 1.0, ub_scale = 1.0, near_frac = 0.5;
     bool timing = false;
     cudaEvent_t ev[8] = {};
     int launches = 0;
@@ -182,6 +188,14 @@ struct tsw_plan {
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
         if (own) cudaStreamDestroy(own);
+    }
+    WorkQueue probe_wq() const {
+        return WorkQueue{probe_q.p, counters.p + C_PFRONT, counters.p + C_PBACK, counters.p + C_PHEAD,
+                         (uint32_t)probe_q.n};
+    }
+    WorkQueue main_wq() const {
+        return WorkQueue{queue.p, counters.p + C_MFRONT, counters.p + C_MBACK, counters.p + C_MHEAD,
+                         (uint32_t)queue.n};
     }
 };
 
@@ -204,6 +218,14 @@ struct DeviceGuard {
     }
 };
 
+uint64_t stride_of(uint64_t len, uint64_t d) { return (len * d + 3) & ~3ull; }
+
+// margin for "bound > T * margin => distance > T": covers the fl error of the
+// DTW path sum (<= 2L-1 additions + d+1 roundings per cell) and of the bound itself.
+double dtw_margin(uint64_t L, uint64_t d) {
+    return up_factor(2.0 * (2.0 * (double)L + (double)d + 8.0) + 8.0);
+}
+
 std::unique_ptr<tsw_plan> make_plan(tsw_store* s, uint64_t nq_max, uint64_t qlen, int metric,
                                     uint64_t r, uint64_t k) {
     if (k == 0)
@@ -211,41 +233,40 @@ std::unique_ptr<tsw_plan> make_plan(tsw_store* s, uint64_t nq_max, uint64_t qlen
                                                   : "knn_dk: k must be positive");
     if (qlen == 0) fail(TSW_EVALIDATION, "time series values must hold n >= 1 complete points");
     if (metric != TSW_METRIC_DTW && metric != TSW_METRIC_DK) fail(TSW_EINVAL, "unknown metric");
-    if (metric == TSW_METRIC_DTW) {
-        if (s->ulen != qlen) {
-            // check_query(equal_lengths=true), search.cpp:106-113: report the first offender
-            for (uint64_t i = 0; i < s->n; ++i)
-                if (s->host_len[i] != qlen)
-                    fail(TSW_EINVAL, "knn_dtw: series " + std::to_string(i) +
-                                         " length differs from the query (lower bounds require "
-                                         "equal lengths)");
-        }
+    if (metric == TSW_METRIC_DTW && s->ulen != qlen) {
+        // check_query(equal_lengths=true), search.cpp:106-113: report the first offender
+        for (uint64_t i = 0; i < s->n; ++i)
+            if (s->host_len[i] != qlen)
+                fail(TSW_EINVAL, "knn_dtw: series " + std::to_string(i) +
+                                     " length differs from the query (lower bounds require "
+                                     "equal lengths)");
     }
     if (nq_max == 0) nq_max = 1;
     auto p = std::make_unique<tsw_plan>();
     p->store = s;
     p->nq_max = nq_max;
     p->qlen = qlen;
-    p->ldq = round_even((uint32_t)qlen);
+    p->qstride = stride_of(qlen, s->d);
     p->metric = metric;
     p->r = r;
     p->k = k;
-    const uint64_t n = s->n, d = s->d;
+    const uint64_t n = s->n;
     p->kk = std::min<uint64_t>(k, n);
-    p->probe = p->kk <= (uint64_t)kKMax ? std::min<uint64_t>({n, (uint64_t)kKMax, std::max<uint64_t>(8, 2 * p->kk)}) : 0;
+    p->S = std::min<uint64_t>(n, 2048);
+    p->probe = p->kk <= (uint64_t)kKMax
+                   ? std::min<uint64_t>({p->S, (uint64_t)kKMax, std::max<uint64_t>(8, 2 * p->kk)})
+                   : 0;
     p->P = std::max<uint64_t>(1, std::min<uint64_t>(kKMax, std::max(p->kk, p->probe)));
     ck(cudaStreamCreateWithFlags(&p->own, cudaStreamNonBlocking), "cudaStreamCreate");
     for (auto& e : p->ev) ck(cudaEventCreate(&e), "cudaEventCreate");
-    const uint64_t qe = nq_max * d * p->ldq;
-    p->q_rm.alloc(nq_max * qlen * d);
-    p->q_soa.alloc(qe);
+    p->q.alloc(nq_max * p->qstride);
+    ck(cudaMemset(p->q.p, 0, p->q.n * sizeof(double)), "memset");  // zero padding, once
     if (metric == TSW_METRIC_DTW) {
-        p->env_lo.alloc(qe);
-        p->env_hi.alloc(qe);
+        p->env_lo.alloc(nq_max * p->qstride);
+        p->env_hi.alloc(nq_max * p->qstride);
     }
-    p->bnd_a.alloc(nq_max * n);
-    p->bnd_b.alloc(nq_max * n);
-    const uint64_t chunks = (n + kSelChunk - 1) / kSelChunk;
+    p->ub.alloc(nq_max * p->S);
+    const uint64_t chunks = (p->S + kSelChunk - 1) / kSelChunk;
     p->sel_sv.alloc(2 * nq_max * chunks * p->P);
     p->sel_si.alloc(2 * nq_max * chunks * p->P);
     p->sel_v.alloc(nq_max * p->P);
@@ -256,7 +277,7 @@ std::unique_ptr<tsw_plan> make_plan(tsw_store* s, uint64_t nq_max, uint64_t qlen
     p->probed.alloc(nq_max * n);
     p->probe_q.alloc(std::max<uint64_t>(1, nq_max * p->probe));
     p->queue.alloc(nq_max * n);
-    p->counters.alloc(8);
+    p->counters.alloc(C_COUNT);
     p->cells.alloc(1);
     if (p->kk > (uint64_t)kKMax) {  // no device list: exact results go to the append buffer
         p->res_d.alloc(nq_max * n);
@@ -264,39 +285,23 @@ std::unique_ptr<tsw_plan> make_plan(tsw_store* s, uint64_t nq_max, uint64_t qlen
         p->res_n.alloc(nq_max);
     }
     if (metric == TSW_METRIC_DTW) {
-        const uint64_t L = qlen;
-        const uint64_t re = std::min<uint64_t>(r, L - 1);
-        std::vector<unsigned long long> cum(2 * L - 1);
-        unsigned long long acc = 0;
-        for (uint64_t a = 0; a < 2 * L - 1; ++a) {
-            // cells (i, j) with i + j = a, |i - j| <= re, 0 <= i, j < L
-            const int64_t ilo = std::max<int64_t>(0, (int64_t)a - (int64_t)(L - 1));
-            const int64_t ihi = std::min<int64_t>((int64_t)a, (int64_t)(L - 1));
-            for (int64_t i = ilo; i <= ihi; ++i)
-                if (std::llabs((int64_t)a - 2 * i) <= (int64_t)re) ++acc;
-            cum[a] = acc;
-        }
-        p->cum_cells.alloc(cum.size());
-        ck(cudaMemcpy(p->cum_cells.p, cum.data(), cum.size() * sizeof(unsigned long long),
-                      cudaMemcpyHostToDevice),
-           "upload cum_cells");
-        const double Ld = (double)L * (double)d;
-        p->margin = up_factor(2.0 * (Ld + 2.0 * (double)L + (double)d + 8.0));
-        p->ub_scale = up_factor(2.0 * (Ld + (double)L + (double)d + 4.0));
+        const double L = (double)qlen, dd = (double)s->d;
+        p->margin = dtw_margin(qlen, s->d);
+        p->ub_scale = up_factor(2.0 * (L * dd + L + dd + 4.0));
+    } else {
+        p->margin = 1.0;
     }
     return p;
 }
 
 void set_queries_impl(tsw_plan* p, const double* q, uint64_t nq, bool device, cudaStream_t st) {
     if (nq == 0 || nq > p->nq_max) fail(TSW_EINVAL, "query count out of range for this plan");
-    const uint64_t d = p->store->d;
-    const size_t bytes = nq * p->qlen * d * sizeof(double);
-    ck(cudaMemcpyAsync(p->q_rm.p, q, bytes, device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
-                       st),
+    const uint64_t row = p->qlen * p->store->d;
+    ck(cudaMemcpy2DAsync(p->q.p, p->qstride * sizeof(double), q, row * sizeof(double),
+                         row * sizeof(double), nq,
+                         device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st),
        "query upload");
-    g_h2d = device ? 0 : bytes;
-    launch_rowmajor_to_soa(p->q_rm.p, (uint32_t)nq, (uint32_t)p->qlen, (uint32_t)d,
-                           (uint32_t)p->ldq, p->q_soa.p, st);
+    g_h2d = device ? 0 : nq * row * sizeof(double);
     p->nq = nq;
 }
 
@@ -311,90 +316,99 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
     };
     mark(0);
     ck(cudaMemsetAsync(p->probed.p, 0, (size_t)nq * n, st), "memset");
-    ck(cudaMemsetAsync(p->counters.p, 0, 8 * sizeof(unsigned), st), "memset");
+    ck(cudaMemsetAsync(p->counters.p, 0, C_COUNT * sizeof(unsigned), st), "memset");
     ck(cudaMemsetAsync(p->cells.p, 0, sizeof(unsigned long long), st), "memset");
     if (p->res_n.p) ck(cudaMemsetAsync(p->res_n.p, 0, nq * sizeof(unsigned), st), "memset");
-
-    BoundArgs ba{};
-    ba.store = s->dev();
-    ba.queries = p->q_soa.p;
-    ba.nq = nq;
-    ba.qlen = (uint32_t)p->qlen;
-    ba.ldq = (uint32_t)p->ldq;
-    ba.out_a = p->bnd_a.p;
-    ba.out_b = p->bnd_b.p;
     if (!dk) {
-        launch_envelope(p->q_soa.p, nq, (uint32_t)s->d, (uint32_t)p->qlen, (uint32_t)p->ldq,
-                        (uint32_t)std::min<uint64_t>(p->r, 0xffffffffu), p->env_lo.p, p->env_hi.p, st);
+        launch_envelope32(p->q.p, nq, (uint32_t)s->d, (uint32_t)p->qlen, p->qstride,
+                          (uint32_t)std::min<uint64_t>(p->r, 0xffffffffu), s->err32, p->env_lo.p,
+                          p->env_hi.p, st);
         ++launches;
-        mark(1);
-        ba.env_lo = p->env_lo.p;
-        ba.env_hi = p->env_hi.p;
-        ba.ub_scale = p->ub_scale;
-        launch_lb_ub(ba, st);
-        launches += (nq + 7) / 8;
-    } else {
-        mark(1);
-        launch_dk_bounds(ba, st);
-        launches += (nq + 7) / 8;
     }
-    mark(2);
-    launch_select_smallest(p->bnd_b.p, nq, n, (uint32_t)p->P, p->sel_sv.p, p->sel_si.p,
-                           p->sel_v.p, p->sel_i.p, st, &launches);
-    SeedArgs sa{};
-    sa.sel_v = p->sel_v.p;
-    sa.sel_i = p->sel_i.p;
+    mark(1);
+    SampleArgs sa{};
+    sa.store = s->dev();
+    sa.queries = p->q.p;
     sa.nq = nq;
-    sa.n = n;
-    sa.P = (uint32_t)p->P;
-    sa.k = (uint32_t)std::min<uint64_t>(p->k, 0xffffffffu);
-    sa.probe = (uint32_t)p->probe;
+    sa.qlen = (uint32_t)p->qlen;
+    sa.qstride = p->qstride;
+    sa.S = (uint32_t)p->S;
+    sa.ub_scale = p->ub_scale;
     sa.dk = dk;
-    sa.state = p->state.p;
-    sa.probe_queue = p->probe_q.p;
-    sa.probe_len = p->counters.p + 0;
-    sa.probed = p->probed.p;
-    launch_seed(sa, st);
+    sa.out_ub = p->ub.p;
+    launch_sample_ub(sa, st);
     ++launches;
-    mark(3);
+    launch_select_smallest(p->ub.p, nq, (uint32_t)p->S, (uint32_t)p->P, p->sel_sv.p, p->sel_si.p,
+                           p->sel_v.p, p->sel_i.p, st, &launches);
+    SeedArgs se{};
+    se.sel_v = p->sel_v.p;
+    se.sel_i = p->sel_i.p;
+    se.nq = nq;
+    se.n = n;
+    se.P = (uint32_t)p->P;
+    se.k = (uint32_t)std::min<uint64_t>(p->k, 0xffffffffu);
+    se.probe = (uint32_t)p->probe;
+    se.S = (uint32_t)p->S;
+    se.dk = dk;
+    se.state = p->state.p;
+    se.probe_q = p->probe_wq();
+    se.probed = p->probed.p;
+    launch_seed(se, st);
+    ++launches;
+    mark(2);
 
     DpArgs da{};
     da.store = s->dev();
-    da.queries = p->q_soa.p;
+    da.queries = p->q.p;
+    da.env_lo = p->env_lo.p;
+    da.env_hi = p->env_hi.p;
     da.qlen = (uint32_t)p->qlen;
-    da.ldq = (uint32_t)p->ldq;
+    da.qstride = p->qstride;
     da.r = (uint32_t)std::min<uint64_t>(p->r, 0xffffffffu);
     da.state = p->state.p;
     da.top_d = p->top_d.p;
     da.top_i = p->top_i.p;
+    da.margin = p->margin;
     da.cells = p->cells.p;
-    da.cum_cells = p->cum_cells.p;
     if (p->res_d.p) da.results = ResultBuf{p->res_d.p, p->res_i.p, p->res_n.p, n};
-    auto run_dp = [&](const Pair* q, unsigned* len, unsigned* head, uint32_t max_pairs) {
-        da.queue = q;
-        da.queue_len = len;
-        da.queue_head = head;
+    auto run_dp = [&](const WorkQueue& w, uint32_t max_pairs) {
+        da.queue = w;
         if (dk) launch_dk_dp(da, max_pairs, (uint32_t)s->max_len, st);
         else launch_dtw_dp(da, max_pairs, st);
         ++launches;
     };
-    if (p->probe) run_dp(p->probe_q.p, p->counters.p + 0, p->counters.p + 1, nq * (uint32_t)p->probe);
-    mark(4);
-    CompactArgs ca{};
-    ca.key = p->bnd_a.p;
-    ca.nq = nq;
-    ca.n = n;
-    ca.margin = p->margin;
-    ca.dk = dk;
-    ca.state = p->state.p;
-    ca.probed = p->probed.p;
-    ca.queue = p->queue.p;
-    ca.queue_len = p->counters.p + 2;
-    launch_compact(ca, st);
+    if (p->probe) run_dp(p->probe_wq(), nq * (uint32_t)p->probe);
+    mark(3);
+    if (!dk) {
+        LbCompactArgs la{};
+        la.store = s->dev();
+        la.env_lo = p->env_lo.p;
+        la.env_hi = p->env_hi.p;
+        la.nq = nq;
+        la.qstride = p->qstride;
+        la.margin = p->margin;
+        la.near_frac = p->near_frac;
+        la.state = p->state.p;
+        la.probed = p->probed.p;
+        la.queue = p->main_wq();
+        launch_lb_compact(la, st);
+    } else {
+        DkCompactArgs ka{};
+        ka.store = s->dev();
+        ka.queries = p->q.p;
+        ka.nq = nq;
+        ka.qlen = (uint32_t)p->qlen;
+        ka.qstride = p->qstride;
+        ka.near_frac = p->near_frac;
+        ka.state = p->state.p;
+        ka.probed = p->probed.p;
+        ka.queue = p->main_wq();
+        launch_dk_compact(ka, st);
+    }
     ++launches;
+    mark(4);
+    run_dp(p->main_wq(), nq * n);
     mark(5);
-    run_dp(p->queue.p, p->counters.p + 2, p->counters.p + 3, nq * n);
-    mark(6);
     ck(cudaEventRecord(p->ev[7], st), "cudaEventRecord");
     ck(cudaGetLastError(), "kernel launch");
     p->launches = launches;
@@ -411,11 +425,14 @@ void fetch_impl(tsw_plan* p, tsw_neighbor* out, tsw_counters* counters, cudaStre
     std::vector<uint32_t> ti;
     std::vector<unsigned> rn;
     if (kk <= (uint64_t)kKMax) {
-        td.resize(nq * kKMax);
-        ti.resize(nq * kKMax);
-        ck(cudaMemcpyAsync(td.data(), p->top_d.p, td.size() * sizeof(double), cudaMemcpyDeviceToHost, st),
+        // top-k rows are kKMax apart; copy only the first kk of each row
+        td.resize(nq * kk);
+        ti.resize(nq * kk);
+        ck(cudaMemcpy2DAsync(td.data(), kk * sizeof(double), p->top_d.p, kKMax * sizeof(double),
+                             kk * sizeof(double), nq, cudaMemcpyDeviceToHost, st),
            "fetch top-k");
-        ck(cudaMemcpyAsync(ti.data(), p->top_i.p, ti.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost, st),
+        ck(cudaMemcpy2DAsync(ti.data(), kk * sizeof(uint32_t), p->top_i.p, kKMax * sizeof(uint32_t),
+                             kk * sizeof(uint32_t), nq, cudaMemcpyDeviceToHost, st),
            "fetch top-k");
     } else {
         rn.resize(nq);
@@ -430,7 +447,7 @@ void fetch_impl(tsw_plan* p, tsw_neighbor* out, tsw_counters* counters, cudaStre
         if (kk <= (uint64_t)kKMax) {
             if (stv[q].count != kk)
                 fail(TSW_ECUDA, "internal: device top-k incomplete for query " + std::to_string(q));
-            for (uint64_t j = 0; o && j < kk; ++j) o[j] = {ti[q * kKMax + j], td[q * kKMax + j]};
+            for (uint64_t j = 0; o && j < kk; ++j) o[j] = {ti[q * kk + j], td[q * kk + j]};
         } else {
             const unsigned cnt = std::min<unsigned>(rn[q], (unsigned)n);
             std::vector<double> rd(cnt);
@@ -529,49 +546,48 @@ int tsw_store_create(const double* values, const uint64_t* lengths, uint64_t uni
         s->d = d;
         s->max_len = mx;
         s->host_len = lens;
+        uint64_t elems = 0;
         if (uniform) {
+            // point-major rows exactly as given (TimeSeries::flat()), stride padded to 4 elements
             s->ulen = lens[0];
-            s->uld = round_even(lens[0]);
-            const uint64_t per = d * s->uld;
-            s->data.alloc(n * per);
-            // transpose in batches of series through a bounded staging buffer
-            const uint64_t per_rm = lens[0] * d;
-            const uint64_t batch = std::max<uint64_t>(1, std::min<uint64_t>(n, (256ull << 20) / (per_rm * 8)));
-            DevBuf<double> stage(batch * per_rm);
-            for (uint64_t b0 = 0; b0 < n; b0 += batch) {
-                const uint64_t nb = std::min(batch, n - b0);
-                ck(cudaMemcpy(stage.p, values + b0 * per_rm, nb * per_rm * sizeof(double),
-                              cudaMemcpyHostToDevice),
-                   "store upload");
-                launch_rowmajor_to_soa(stage.p, (uint32_t)nb, lens[0], (uint32_t)d, (uint32_t)s->uld,
-                                       s->data.p + b0 * per, 0);
-                ck(cudaGetLastError(), "store transpose");
-            }
-            ck(cudaDeviceSynchronize(), "store transpose");
-            s->bytes = n * per * sizeof(double);
+            s->ustride = stride_of(lens[0], d);
+            elems = n * s->ustride;
+            s->data.alloc(elems);
+            const uint64_t row = lens[0] * d;
+            if (s->ustride != row) ck(cudaMemset(s->data.p, 0, elems * sizeof(double)), "memset");
+            ck(cudaMemcpy2D(s->data.p, s->ustride * sizeof(double), values, row * sizeof(double),
+                            row * sizeof(double), n, cudaMemcpyHostToDevice),
+               "store upload");
         } else {
             std::vector<uint64_t> off(n);
-            uint64_t acc = 0;
             for (uint64_t i = 0; i < n; ++i) {
-                off[i] = acc;
-                acc += d * round_even(lens[i]);
+                off[i] = elems;
+                elems += stride_of(lens[i], d);
             }
-            std::vector<double> soa(acc, 0.0);
+            std::vector<double> buf(elems, 0.0);
             uint64_t src = 0;
             for (uint64_t i = 0; i < n; ++i) {
-                const uint64_t L = lens[i], ld = round_even(lens[i]);
-                for (uint64_t p = 0; p < L; ++p)
-                    for (uint64_t k = 0; k < d; ++k) soa[off[i] + k * ld + p] = values[(src + p) * d + k];
-                src += L;
+                std::memcpy(buf.data() + off[i], values + src, lens[i] * d * sizeof(double));
+                src += lens[i] * d;
             }
-            s->data.alloc(acc);
+            s->data.alloc(elems);
             s->off.alloc(n);
             s->len.alloc(n);
-            ck(cudaMemcpy(s->data.p, soa.data(), acc * sizeof(double), cudaMemcpyHostToDevice), "store upload");
+            ck(cudaMemcpy(s->data.p, buf.data(), elems * sizeof(double), cudaMemcpyHostToDevice), "store upload");
             ck(cudaMemcpy(s->off.p, off.data(), n * sizeof(uint64_t), cudaMemcpyHostToDevice), "store upload");
             ck(cudaMemcpy(s->len.p, lens.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice), "store upload");
-            s->bytes = acc * sizeof(double);
         }
+        s->bytes = elems * sizeof(double);
+        // fp32 copy for the LB_Box pass + the rounding bound err32 >= max |x - fp32(x)|
+        s->data32.alloc(elems);
+        launch_to_float(s->data.p, elems, s->data32.p, 0);
+        DevBuf<double> mxb(1);
+        launch_absmax(s->data.p, elems, mxb.p, 0);
+        double xmax = 0.0;
+        ck(cudaMemcpy(&xmax, mxb.p, sizeof(double), cudaMemcpyDeviceToHost), "store absmax");
+        s->err32 = std::nextafter((float)(xmax * 0x1p-24), INFINITY);
+        if (!(s->err32 < INFINITY)) fail(TSW_EVALIDATION, "dataset values too large for the fp32 bound");
+        ck(cudaDeviceSynchronize(), "store create");
         *out = s.release();
     });
 }
@@ -654,28 +670,31 @@ int tsw_plan_stats(tsw_plan* p, tsw_stats* out) {
         if (!p || !out) fail(TSW_EINVAL, "null argument");
         DeviceGuard dg(p->store->device);
         std::memset(out, 0, sizeof(*out));
-        unsigned cnt[8] = {0};
+        unsigned cnt[C_COUNT] = {0};
         unsigned long long cells = 0;
         if (p->executed) ck(cudaEventSynchronize(p->ev[7]), "stats");
         ck(cudaMemcpy(cnt, p->counters.p, sizeof(cnt), cudaMemcpyDeviceToHost), "stats");
         ck(cudaMemcpy(&cells, p->cells.p, sizeof(cells), cudaMemcpyDeviceToHost), "stats");
-        out->dp_pairs = (uint64_t)cnt[0] + cnt[2];
+        out->dp_pairs = (uint64_t)cnt[C_PFRONT] + cnt[C_MFRONT] + cnt[C_MBACK];
         out->dp_cells = cells;
-        out->bound_passes = (p->nq + 7) / 8;
-        out->bound_bytes = out->bound_passes * p->store->bytes;
+        const bool dk = p->metric == TSW_METRIC_DK;
+        out->bound_passes = dk ? 0 : 1;
+        // DTW: the fp32 copy of the store is streamed once per execute (query blocks of one
+        // candidate tile are served from L1/L2);  DK bounds read 2 points per pair
+        out->bound_bytes = dk ? (uint64_t)p->nq * p->store->n * 2 * p->store->d * sizeof(double)
+                              : p->store->bytes / 2;
         out->kernel_launches = (uint64_t)p->launches;
         if (p->timing && p->executed) {
-            ck(cudaEventSynchronize(p->ev[6]), "stats");
-            float ms[7] = {0};
-            for (int i = 1; i <= 6; ++i) cudaEventElapsedTime(&ms[i], p->ev[i - 1], p->ev[i]);
-            cudaEventElapsedTime(&ms[0], p->ev[0], p->ev[6]);
+            float ms[6] = {0};
+            for (int i = 1; i <= 5; ++i) cudaEventElapsedTime(&ms[i], p->ev[i - 1], p->ev[i]);
+            cudaEventElapsedTime(&ms[0], p->ev[0], p->ev[5]);
             out->ms_total = ms[0];
             out->ms_envelope = ms[1];
-            out->ms_bound = ms[2];
-            out->ms_select = ms[3];
-            out->ms_probe_dp = ms[4];
-            out->ms_compact = ms[5];
-            out->ms_dp = ms[6];
+            out->ms_select = ms[2];
+            out->ms_probe_dp = ms[3];
+            out->ms_bound = ms[4];
+            out->ms_compact = 0.0;  // fused into the bound pass
+            out->ms_dp = ms[5];
         }
     });
 }
@@ -717,50 +736,40 @@ int tsw_epsnn_dk(tsw_store* s, const double* query, uint64_t qlen, double eps,
         check_finite(query, qlen * s->d, "query");
         std::lock_guard<std::mutex> lk(s->mu);
         DeviceGuard dg(s->device);
-        const uint64_t n = s->n, d = s->d;
-        const uint32_t ldq = round_even((uint32_t)qlen);
+        const uint64_t n = s->n, d = s->d, qs = stride_of(qlen, d);
         cudaStream_t st = 0;
-        DevBuf<double> qrm(qlen * d), qsoa(d * ldq), ba(n), bb(n), rd(n);
+        DevBuf<double> q(qs), rd(n);
         DevBuf<uint32_t> ri(n);
         DevBuf<unsigned> rn(1), ctr(4);
         DevBuf<unsigned long long> pruned(1);
-        DevBuf<Pair> queue(n);
-        ck(cudaMemcpy(qrm.p, query, qlen * d * sizeof(double), cudaMemcpyHostToDevice), "upload");
-        launch_rowmajor_to_soa(qrm.p, 1, (uint32_t)qlen, (uint32_t)d, ldq, qsoa.p, st);
+        DevBuf<QEntry> queue(n);
+        ck(cudaMemset(q.p, 0, qs * sizeof(double)), "memset");
+        ck(cudaMemcpy(q.p, query, qlen * d * sizeof(double), cudaMemcpyHostToDevice), "upload");
         ck(cudaMemset(rn.p, 0, sizeof(unsigned)), "memset");
         ck(cudaMemset(ctr.p, 0, 4 * sizeof(unsigned)), "memset");
         ck(cudaMemset(pruned.p, 0, sizeof(unsigned long long)), "memset");
-        BoundArgs b{};
-        b.store = s->dev();
-        b.queries = qsoa.p;
-        b.nq = 1;
-        b.qlen = (uint32_t)qlen;
-        b.ldq = ldq;
-        b.out_a = ba.p;
-        b.out_b = bb.p;
-        launch_dk_bounds(b, st);
         const double eps_sq = host_sq_threshold(eps);
-        CompactArgs ca{};
-        ca.key = ba.p;
-        ca.nq = 1;
-        ca.n = (uint32_t)n;
-        ca.dk = 1;
-        ca.fixed_eps = eps;
-        ca.fixed_eps_sq = eps_sq;
-        ca.fixed_pruned = pruned.p;
-        ca.queue = queue.p;
-        ca.queue_len = ctr.p;
-        launch_compact(ca, st);
+        const WorkQueue wq{queue.p, ctr.p, ctr.p + 1, ctr.p + 2, (uint32_t)n};
+        DkCompactArgs ka{};
+        ka.store = s->dev();
+        ka.queries = q.p;
+        ka.nq = 1;
+        ka.qlen = (uint32_t)qlen;
+        ka.qstride = qs;
+        ka.near_frac = 1.0;
+        ka.fixed_eps_sq = eps_sq;
+        ka.fixed_pruned = pruned.p;
+        ka.queue = wq;
+        launch_dk_compact(ka, st);
         DpArgs da{};
         da.store = s->dev();
-        da.queries = qsoa.p;
+        da.queries = q.p;
         da.qlen = (uint32_t)qlen;
-        da.ldq = ldq;
-        da.queue = queue.p;
-        da.queue_len = ctr.p;
-        da.queue_head = ctr.p + 1;
+        da.qstride = qs;
+        da.queue = wq;
         da.fixed_eps = eps;
         da.fixed_eps_sq = eps_sq;
+        da.margin = 1.0;
         da.results = ResultBuf{rd.p, ri.p, rn.p, (uint32_t)n};
         launch_dk_dp(da, (uint32_t)n, (uint32_t)s->max_len, st);
         ck(cudaGetLastError(), "kernel launch");
@@ -778,9 +787,7 @@ int tsw_epsnn_dk(tsw_store* s, const double* query, uint64_t qlen, double eps,
         });
         if (count) *count = cnt;
         for (uint64_t j = 0; out && j < cnt && j < cap; ++j) out[j] = all[j];
-        if (counters) {
-            *counters = tsw_counters{0, 0, cnt, n - cnt, 0};
-        }
+        if (counters) *counters = tsw_counters{0, 0, cnt, n - cnt, 0};
     });
 }
 
@@ -790,21 +797,16 @@ int tsw_envelope(const double* series, uint64_t n, uint64_t d, uint64_t r, doubl
         if (n == 0 || d == 0) fail(TSW_EVALIDATION, "time series values must hold n >= 1 complete points");
         check_finite(series, n * d, "series");
         require_device();
-        const uint32_t ld = round_even((uint32_t)n);
-        DevBuf<double> rm(n * d), soa(d * ld), l(d * ld), h(d * ld);
-        ck(cudaMemcpy(rm.p, series, n * d * sizeof(double), cudaMemcpyHostToDevice), "upload");
-        launch_rowmajor_to_soa(rm.p, 1, (uint32_t)n, (uint32_t)d, ld, soa.p, 0);
-        launch_envelope(soa.p, 1, (uint32_t)d, (uint32_t)n, ld, (uint32_t)std::min<uint64_t>(r, 0xffffffffu),
-                        l.p, h.p, 0);
+        // K1 in its exact fp64 form (the pipeline uses the fp32 outward-rounded variant)
+        const uint64_t qs = stride_of(n, d);
+        DevBuf<double> q(qs), l(qs), h(qs);
+        ck(cudaMemset(q.p, 0, qs * sizeof(double)), "memset");
+        ck(cudaMemcpy(q.p, series, n * d * sizeof(double), cudaMemcpyHostToDevice), "upload");
+        launch_envelope64(q.p, 1, (uint32_t)d, (uint32_t)n, qs,
+                          (uint32_t)std::min<uint64_t>(r, 0xffffffffu), l.p, h.p, 0);
         ck(cudaGetLastError(), "envelope");
-        std::vector<double> hl(d * ld), hh(d * ld);
-        ck(cudaMemcpy(hl.data(), l.p, hl.size() * sizeof(double), cudaMemcpyDeviceToHost), "fetch");
-        ck(cudaMemcpy(hh.data(), h.p, hh.size() * sizeof(double), cudaMemcpyDeviceToHost), "fetch");
-        for (uint64_t i = 0; i < n; ++i)
-            for (uint64_t k = 0; k < d; ++k) {
-                lo[i * d + k] = hl[k * ld + i];
-                hi[i * d + k] = hh[k * ld + i];
-            }
+        ck(cudaMemcpy(lo, l.p, n * d * sizeof(double), cudaMemcpyDeviceToHost), "fetch");
+        ck(cudaMemcpy(hi, h.p, n * d * sizeof(double), cudaMemcpyDeviceToHost), "fetch");
     });
 }
 
@@ -813,28 +815,41 @@ int tsw_lb_box_all(tsw_store* s, const double* query, uint64_t qlen, uint64_t r,
     return guard([&] {
         if (!s || !query) fail(TSW_EINVAL, "null argument");
         check_finite(query, qlen * s->d, "query");
+        if (s->ulen != qlen) fail(TSW_EINVAL, "lb_box: every series must have the query length");
         std::lock_guard<std::mutex> lk(s->mu);
         DeviceGuard dg(s->device);
-        tsw_plan* p = cached_plan(s, 1, qlen, TSW_METRIC_DTW, r, 1);
-        set_queries_impl(p, query, 1, false, p->own);
-        launch_envelope(p->q_soa.p, 1, (uint32_t)s->d, (uint32_t)qlen, (uint32_t)p->ldq,
-                        (uint32_t)std::min<uint64_t>(r, 0xffffffffu), p->env_lo.p, p->env_hi.p, p->own);
-        BoundArgs ba{};
-        ba.store = s->dev();
-        ba.queries = p->q_soa.p;
-        ba.env_lo = p->env_lo.p;
-        ba.env_hi = p->env_hi.p;
-        ba.nq = 1;
-        ba.qlen = (uint32_t)qlen;
-        ba.ldq = (uint32_t)p->ldq;
-        ba.ub_scale = p->ub_scale;
-        ba.out_a = p->bnd_a.p;
-        ba.out_b = p->bnd_b.p;
-        launch_lb_ub(ba, p->own);
+        const uint64_t n = s->n, d = s->d, qs = stride_of(qlen, d);
+        DevBuf<double> q(qs), ub(n);
+        DevBuf<float> el(qs), eh(qs), lb(n);
+        ck(cudaMemset(q.p, 0, qs * sizeof(double)), "memset");
+        ck(cudaMemcpy(q.p, query, qlen * d * sizeof(double), cudaMemcpyHostToDevice), "upload");
+        launch_envelope32(q.p, 1, (uint32_t)d, (uint32_t)qlen, qs,
+                          (uint32_t)std::min<uint64_t>(r, 0xffffffffu), s->err32, el.p, eh.p, 0);
+        LbCompactArgs la{};
+        la.store = s->dev();
+        la.env_lo = el.p;
+        la.env_hi = eh.p;
+        la.nq = 1;
+        la.qstride = qs;
+        la.lb_out = lb.p;
+        launch_lb_compact(la, 0);
+        SampleArgs sa{};
+        sa.store = s->dev();
+        sa.queries = q.p;
+        sa.nq = 1;
+        sa.qlen = (uint32_t)qlen;
+        sa.qstride = qs;
+        sa.S = (uint32_t)n;
+        sa.ub_scale = up_factor(2.0 * ((double)qlen * d + qlen + d + 4.0));
+        sa.dk = 0;
+        sa.out_ub = ub.p;
+        launch_sample_ub(sa, 0);
         ck(cudaGetLastError(), "lb kernel");
-        if (lb_out) ck(cudaMemcpyAsync(lb_out, p->bnd_a.p, s->n * sizeof(double), cudaMemcpyDeviceToHost, p->own), "fetch");
-        if (ub_out) ck(cudaMemcpyAsync(ub_out, p->bnd_b.p, s->n * sizeof(double), cudaMemcpyDeviceToHost, p->own), "fetch");
-        ck(cudaStreamSynchronize(p->own), "lb kernel");
+        std::vector<float> hl(n);
+        ck(cudaMemcpy(hl.data(), lb.p, n * sizeof(float), cudaMemcpyDeviceToHost), "fetch");
+        if (lb_out)
+            for (uint64_t i = 0; i < n; ++i) lb_out[i] = hl[i];
+        if (ub_out) ck(cudaMemcpy(ub_out, ub.p, n * sizeof(double), cudaMemcpyDeviceToHost), "fetch");
     });
 }
 
@@ -849,44 +864,32 @@ int tsw_dist_all(tsw_store* s, const double* query, uint64_t qlen, int metric, u
             fail(TSW_EINVAL, "dist_all(dtw): every series must have the query length");
         std::lock_guard<std::mutex> lk(s->mu);
         DeviceGuard dg(s->device);
-        const uint64_t n = s->n, d = s->d;
-        const uint32_t ldq = round_even((uint32_t)qlen);
-        DevBuf<double> qrm(qlen * d), qsoa(d * ldq), val(n);
+        const uint64_t n = s->n, d = s->d, qs = stride_of(qlen, d);
+        DevBuf<double> q(qs), val(n);
         DevBuf<int> ex(n);
         DevBuf<unsigned> ctr(4);
-        DevBuf<Pair> queue(n);
-        DevBuf<unsigned long long> cum;
-        std::vector<Pair> hq(n);
-        for (uint64_t i = 0; i < n; ++i) hq[i] = Pair{0, (uint32_t)i};
-        const unsigned nn = (unsigned)n;
-        ck(cudaMemcpy(queue.p, hq.data(), n * sizeof(Pair), cudaMemcpyHostToDevice), "upload");
-        ck(cudaMemcpy(qrm.p, query, qlen * d * sizeof(double), cudaMemcpyHostToDevice), "upload");
-        ck(cudaMemset(ctr.p, 0, 4 * sizeof(unsigned)), "memset");
-        ck(cudaMemcpy(ctr.p, &nn, sizeof(unsigned), cudaMemcpyHostToDevice), "upload");
-        launch_rowmajor_to_soa(qrm.p, 1, (uint32_t)qlen, (uint32_t)d, ldq, qsoa.p, 0);
+        DevBuf<QEntry> queue(n);
+        std::vector<QEntry> hq(n);
+        for (uint64_t i = 0; i < n; ++i) hq[i] = QEntry{0, (uint32_t)i, 0.0};
+        const unsigned cnt[4] = {(unsigned)n, 0u, 0u, 0u};
+        ck(cudaMemcpy(queue.p, hq.data(), n * sizeof(QEntry), cudaMemcpyHostToDevice), "upload");
+        ck(cudaMemcpy(ctr.p, cnt, sizeof(cnt), cudaMemcpyHostToDevice), "upload");
+        ck(cudaMemset(q.p, 0, qs * sizeof(double)), "memset");
+        ck(cudaMemcpy(q.p, query, qlen * d * sizeof(double), cudaMemcpyHostToDevice), "upload");
         DpArgs da{};
         da.store = s->dev();
-        da.queries = qsoa.p;
+        da.queries = q.p;
         da.qlen = (uint32_t)qlen;
-        da.ldq = ldq;
+        da.qstride = qs;
         da.r = (uint32_t)std::min<uint64_t>(r, 0xffffffffu);
-        da.queue = queue.p;
-        da.queue_len = ctr.p;
-        da.queue_head = ctr.p + 1;
+        da.queue = WorkQueue{queue.p, ctr.p, ctr.p + 1, ctr.p + 2, (uint32_t)n};
         da.fixed_eps = eps;
         da.fixed_eps_sq = host_sq_threshold(eps);
+        da.margin = 1.0;
         da.out_exact = ex.p;
         da.out_val = val.p;
-        if (metric == TSW_METRIC_DTW) {
-            const uint64_t L = qlen;
-            std::vector<unsigned long long> c(2 * L - 1, 0ull);
-            cum.alloc(c.size());
-            ck(cudaMemcpy(cum.p, c.data(), c.size() * sizeof(unsigned long long), cudaMemcpyHostToDevice), "upload");
-            da.cum_cells = cum.p;
-            launch_dtw_dp(da, (uint32_t)n, 0);
-        } else {
-            launch_dk_dp(da, (uint32_t)n, (uint32_t)s->max_len, 0);
-        }
+        if (metric == TSW_METRIC_DTW) launch_dtw_dp(da, (uint32_t)n, 0);
+        else launch_dk_dp(da, (uint32_t)n, (uint32_t)s->max_len, 0);
         ck(cudaGetLastError(), "kernel launch");
         ck(cudaMemcpy(exact, ex.p, n * sizeof(int), cudaMemcpyDeviceToHost), "fetch");
         ck(cudaMemcpy(value, val.p, n * sizeof(double), cudaMemcpyDeviceToHost), "fetch");

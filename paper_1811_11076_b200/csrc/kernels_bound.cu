@@ -1,211 +1,320 @@
-// K1 envelope, K2 LB_Box (+ diagonal-path DTW upper bound), DK cell bounds, and the one-time
-// row-major -> dimension-major store transpose.
+// K1 envelope, the sampled seed upper bounds, K2 LB_Box fused with K3 compaction (DTW), and the
+// DK first/last-cell bound fused with compaction.
 //
-// K2 is the HBM-streaming pass: one warp per candidate, 128-bit loads of the candidate's
-// [d][L] block, QB queries per pass (the candidate bytes are read once per pass and combined
-// with QB cached query envelopes), warp-shuffle tree reductions.
+// K2 is the streaming pass over the whole store.  It runs in fp32 with directed rounding on a
+// float copy of the store (half the bytes of fp64) against a directed-rounded query envelope,
+// so every LB value is a rigorous lower bound of the real LB_Box and pruning
+// stays exact.  One warp owns a tile of CB consecutive candidates x QB queries: each 128-bit
+// candidate load is reused for QB queries and each envelope load for CB candidates.
+#include <algorithm>
+
 #include "tsw_internal.cuh"
 
 namespace tswb {
 
-// ---- row-major [nser][len][d] -> SoA [nser][d][ld] (zero padding) ------------------------
-__global__ void rowmajor_to_soa_kernel(const double* __restrict__ src, uint32_t nser, uint32_t len,
-                                       uint32_t d, uint32_t ld, double* __restrict__ dst) {
-    const size_t total = (size_t)nser * d * ld;
-    for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < total;
-         g += (size_t)gridDim.x * blockDim.x) {
-        const size_t ser = g / ((size_t)d * ld);
-        const uint32_t rem = (uint32_t)(g - ser * (size_t)d * ld);
-        const uint32_t k = rem / ld, i = rem - k * ld;
-        dst[g] = i < len ? src[(ser * len + i) * d + k] : 0.0;
-    }
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+
+// ---- helpers ------------------------------------------------------------------------------
+__global__ void to_float_kernel(const double* __restrict__ src, uint64_t n, float* __restrict__ dst) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        dst[i] = __double2float_rn(src[i]);
 }
 
-void launch_rowmajor_to_soa(const double* src, uint32_t nser, uint32_t len, uint32_t d,
-                            uint32_t ld, double* dst, cudaStream_t st) {
-    const size_t total = (size_t)nser * d * ld;
-    const int blocks = (int)std::min<size_t>((total + 255) / 256, (size_t)sm_count() * 16);
-    rowmajor_to_soa_kernel<<<std::max(blocks, 1), 256, 0, st>>>(src, nser, len, d, ld, dst);
+void launch_to_float(const double* src, uint64_t count, float* dst, cudaStream_t st) {
+    const int blocks = (int)std::min<uint64_t>((count + 255) / 256, (uint64_t)sm_count() * 16);
+    to_float_kernel<<<std::max(blocks, 1), 256, 0, st>>>(src, count, dst);
+}
+
+__global__ void absmax_kernel(const double* __restrict__ src, uint64_t n, unsigned long long* out) {
+    double m = 0.0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        m = fmax(m, fabs(src[i]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane_id() == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
+}
+
+void launch_absmax(const double* src, uint64_t count, double* out, cudaStream_t st) {
+    cudaMemsetAsync(out, 0, sizeof(double), st);
+    const int blocks = (int)std::min<uint64_t>((count + 255) / 256, (uint64_t)sm_count() * 8);
+    absmax_kernel<<<std::max(blocks, 1), 256, 0, st>>>(src, count,
+                                                       reinterpret_cast<unsigned long long*>(out));
 }
 
 // ---- K1: per-dimension windowed min / max over [i-r, i+r] clamped (envelope.cpp:25-59) ------
-// One thread per (query, dim, point).  Min / max are exact, so the direct window scan is
-// value-identical to the reference's monotonic-deque algorithm.
+// One thread per (query, point, dim).  Min / max are exact, so the direct window scan equals
+// the reference's monotonic-deque result; it is then rounded outward to fp32 and widened by
+// `err` (>= |x - fp32(x)| over the store) so fp32 terms bound the fp64 ones from below.
+template <typename OutT>
 __global__ void envelope_kernel(const double* __restrict__ q, uint32_t nq, uint32_t d,
-                                uint32_t len, uint32_t ld, uint32_t r, double* __restrict__ lo,
-                                double* __restrict__ hi) {
-    const size_t total = (size_t)nq * d * ld;
-    for (size_t g = blockIdx.x * (size_t)blockDim.x + threadIdx.x; g < total;
-         g += (size_t)gridDim.x * blockDim.x) {
-        const uint32_t i = (uint32_t)(g % ld);
-        const double* row = q + (g - i);
-        if (i >= len) {
-            lo[g] = 0.0;
-            hi[g] = 0.0;
+                                uint32_t len, uint64_t qstride, uint32_t r, float err,
+                                OutT* __restrict__ lo, OutT* __restrict__ hi) {
+    const uint64_t total = (uint64_t)nq * qstride;
+    for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total;
+         g += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t qi = g / qstride;
+        const uint32_t f = (uint32_t)(g - qi * qstride);
+        if (f >= len * d) {
+            lo[g] = OutT(0);
+            hi[g] = OutT(0);
             continue;
         }
+        const uint32_t i = f / d, k = f - i * d;
+        const double* row = q + qi * qstride + k;
         const uint32_t a = i >= r ? i - r : 0u;
         const uint32_t b = (uint64_t)i + r < len ? i + r : len - 1;
-        double mn = row[a], mx = row[a];
+        double mn = row[(uint64_t)a * d], mx = mn;
         for (uint32_t w = a + 1; w <= b; ++w) {
-            const double v = row[w];
+            const double v = row[(uint64_t)w * d];
             mn = v < mn ? v : mn;
             mx = v > mx ? v : mx;
         }
-        lo[g] = mn;
-        hi[g] = mx;
-    }
-}
-
-void launch_envelope(const double* q, uint32_t nq, uint32_t d, uint32_t len, uint32_t ld,
-                     uint32_t r, double* lo, double* hi, cudaStream_t st) {
-    const size_t total = (size_t)nq * d * ld;
-    const int blocks = (int)std::min<size_t>((total + 255) / 256, (size_t)sm_count() * 8);
-    envelope_kernel<<<std::max(blocks, 1), 256, 0, st>>>(q, nq, d, len, ld, r, lo, hi);
-}
-
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = dadd(v, __shfl_xor_sync(0xffffffffu, v, o));
-    return v;
-}
-__device__ __forceinline__ double warp_max(double v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = dmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-    return v;
-}
-
-// ---- K2: LB_Box + diagonal upper bound ---------------------------------------------------------
-// lb(q, c) = sum over (i, k) of dist(x, [lo, hi])^2 with x = candidate value and lo/hi the
-// QUERY envelope (role swap, search.cpp:132,148; box_bound, lower_bounds.cpp:19-46).  The
-// sum runs in warp-tree order, so it may differ from the serial reference sum in the last
-// bits; it only gates pruning, which uses an admissibility margin.
-// ub(q, c) = sum of squared point distances along the diagonal path, any order, scaled up by
-// `ub_scale` so that it bounds the suffix-ordered fl sum, itself >= the computed DTW
-// (SURVEY §7.3 #7).
-template <int QB>
-__global__ void __launch_bounds__(256) lb_ub_kernel(BoundArgs a, uint32_t q0) {
-    const int lane = threadIdx.x & 31;
-    const uint32_t wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-    const uint32_t d = a.store.d;
-    const uint32_t ld = a.store.uld;
-    const uint32_t total2 = d * ld / 2;  // ld is even
-    const uint32_t nqb = min((uint32_t)QB, a.nq - q0);
-    const size_t qstride = (size_t)d * a.ldq;
-    for (uint32_t c = wid; c < a.store.n; c += nwarps) {
-        const double2* x2 = reinterpret_cast<const double2*>(series_ptr(a.store, c));
-        double lb[QB], ub[QB];
-#pragma unroll
-        for (int j = 0; j < QB; ++j) lb[j] = ub[j] = 0.0;
-        for (uint32_t f = lane; f < total2; f += 32) {
-            const double2 x = __ldg(x2 + f);
-#pragma unroll
-            for (int j = 0; j < QB; ++j) {
-                if (j < (int)nqb) {
-                    const size_t qo = (size_t)(q0 + j) * qstride / 2 + f;
-                    const double2 l = __ldg(reinterpret_cast<const double2*>(a.env_lo) + qo);
-                    const double2 h = __ldg(reinterpret_cast<const double2*>(a.env_hi) + qo);
-                    const double2 s = __ldg(reinterpret_cast<const double2*>(a.queries) + qo);
-                    double t0 = 0.0, t1 = 0.0;
-                    if (x.x < l.x) { const double e = dsub(l.x, x.x); t0 = dmul(e, e); }
-                    else if (x.x > h.x) { const double e = dsub(x.x, h.x); t0 = dmul(e, e); }
-                    if (x.y < l.y) { const double e = dsub(l.y, x.y); t1 = dmul(e, e); }
-                    else if (x.y > h.y) { const double e = dsub(x.y, h.y); t1 = dmul(e, e); }
-                    lb[j] = dadd(lb[j], dadd(t0, t1));
-                    const double e0 = dsub(s.x, x.x), e1 = dsub(s.y, x.y);
-                    ub[j] = dadd(ub[j], dadd(dmul(e0, e0), dmul(e1, e1)));
-                }
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < QB; ++j) {
-            if (j < (int)nqb) {
-                const double l = warp_sum(lb[j]);
-                const double u = warp_sum(ub[j]);
-                if (lane == j) {
-                    a.out_a[(size_t)(q0 + j) * a.store.n + c] = l;
-                    a.out_b[(size_t)(q0 + j) * a.store.n + c] = __dmul_ru(u, a.ub_scale);
-                }
-            }
+        if constexpr (sizeof(OutT) == sizeof(float)) {
+            lo[g] = __fsub_rd(__double2float_rd(mn), err);
+            hi[g] = __fadd_ru(__double2float_ru(mx), err);
+        } else {
+            lo[g] = mn;
+            hi[g] = mx;
         }
     }
 }
 
-void launch_lb_ub(const BoundArgs& a, cudaStream_t st) {
-    constexpr int QB = 8;
-    const int blocks = (int)std::min<uint64_t>(((uint64_t)a.store.n * 32 + 255) / 256,
-                                               (uint64_t)sm_count() * 8);
-    for (uint32_t q0 = 0; q0 < a.nq; q0 += QB)
-        lb_ub_kernel<QB><<<std::max(blocks, 1), 256, 0, st>>>(a, q0);
+void launch_envelope32(const double* q, uint32_t nq, uint32_t d, uint32_t len, uint64_t qstride,
+                       uint32_t r, float err, float* lo, float* hi, cudaStream_t st) {
+    const uint64_t total = (uint64_t)nq * qstride;
+    const int blocks = (int)std::min<uint64_t>((total + 255) / 256, (uint64_t)sm_count() * 8);
+    envelope_kernel<float><<<std::max(blocks, 1), 256, 0, st>>>(q, nq, d, len, qstride, r, err, lo, hi);
 }
 
-// ---- DK cell bounds ------------------------------------------------------------------------
-// out_a = max(c(0,0), c(m-1,n-1)): both cells lie on every warping path, so
-//         sqrt(out_a) <= dk (exact, squared domain);
-// out_b = max of c over the diagonal-then-forced-tail path (i, j) = (min(t, m-1), min(t, n-1)):
-//         a valid warping path, so sqrt(out_b) >= dk (the seed; replaces the greedy walk
-//         gdk, dogkeeper.cpp:52-94, whose only role in knn_dk is to seed the threshold).
-// c is the squared point distance in the reference order (types.hpp:126-133); the max / min
-// structure of DK commutes with the monotone sqrt.
-template <int QB>
-__global__ void __launch_bounds__(256) dk_bounds_kernel(BoundArgs a, uint32_t q0) {
-    const int lane = threadIdx.x & 31;
-    const uint32_t wid = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-    const uint32_t d = a.store.d;
-    const uint32_t m = a.qlen;
-    const uint32_t nqb = min((uint32_t)QB, a.nq - q0);
-    for (uint32_t c = wid; c < a.store.n; c += nwarps) {
-        const double* t = series_ptr(a.store, c);
+void launch_envelope64(const double* q, uint32_t nq, uint32_t d, uint32_t len, uint64_t qstride,
+                       uint32_t r, double* lo, double* hi, cudaStream_t st) {
+    const uint64_t total = (uint64_t)nq * qstride;
+    const int blocks = (int)std::min<uint64_t>((total + 255) / 256, (uint64_t)sm_count() * 8);
+    envelope_kernel<double><<<std::max(blocks, 1), 256, 0, st>>>(q, nq, d, len, qstride, r, 0.0f, lo, hi);
+}
+
+// ---- sampled seed upper bounds ----------------------------------------------------------------
+// One warp per (query, sampled candidate).  Per-point costs are exact detail::sq_dist.
+//  DTW: sum of c(i, i) along the diagonal (any order), scaled up by ub_scale so that it bounds
+//       the suffix-ordered fl sum, itself >= the computed DTW.
+//  DK : max of c over the diagonal-then-forced-tail path (i, j) = (min(p, m-1), min(p, n-1)),
+//       a valid warping path, so sqrt(max) >= dk.  (Replaces the greedy walk gdk,
+//       dogkeeper.cpp:52-94, whose role in knn_dk is only to seed the threshold.)
+__global__ void __launch_bounds__(256) sample_ub_kernel(SampleArgs a) {
+    const unsigned lane = lane_id();
+    const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint32_t d = a.store.d, m = a.qlen;
+    for (uint64_t w = wid; w < (uint64_t)a.nq * a.S; w += nw) {
+        const uint32_t q = (uint32_t)(w / a.S), j = (uint32_t)(w - (uint64_t)q * a.S);
+        const uint32_t c = (uint32_t)((uint64_t)j * a.store.n / a.S);
+        const double* s = a.queries + (uint64_t)q * a.qstride;
+        const double* t = a.store.data + series_off(a.store, c);
         const uint32_t n = series_len(a.store, c);
-        const uint32_t ldt = a.store.off ? round_even(n) : a.store.uld;
-        const uint32_t steps = max(m, n);
-        double mx[QB], ends[QB];
-#pragma unroll
-        for (int j = 0; j < QB; ++j) mx[j] = ends[j] = 0.0;
+        const uint32_t steps = a.dk ? max(m, n) : m;
+        double acc = 0.0;
         for (uint32_t p = lane; p < steps; p += 32) {
             const uint32_t i = min(p, m - 1), jj = min(p, n - 1);
-            double acc[QB];
-#pragma unroll
-            for (int j = 0; j < QB; ++j) acc[j] = 0.0;
+            double cst = 0.0;
             for (uint32_t k = 0; k < d; ++k) {
-                const double x = __ldg(t + (size_t)k * ldt + jj);
-#pragma unroll
-                for (int j = 0; j < QB; ++j) {
-                    if (j < (int)nqb) {
-                        const double s = __ldg(a.queries + ((size_t)(q0 + j) * d + k) * a.ldq + i);
-                        const double e = dsub(s, x);
-                        acc[j] = dadd(acc[j], dmul(e, e));
-                    }
-                }
+                const double e = dsub(s[(uint64_t)i * d + k], t[(uint64_t)jj * d + k]);
+                cst = dadd(cst, dmul(e, e));
             }
-#pragma unroll
-            for (int j = 0; j < QB; ++j) {
-                mx[j] = dmax(mx[j], acc[j]);
-                if (p == 0 || p == steps - 1) ends[j] = dmax(ends[j], acc[j]);
-            }
+            acc = a.dk ? dmax(acc, cst) : dadd(acc, cst);
         }
 #pragma unroll
-        for (int j = 0; j < QB; ++j) {
-            if (j < (int)nqb) {
-                const double u = warp_max(mx[j]);
-                const double e = warp_max(ends[j]);
-                if (lane == j) {
-                    a.out_a[(size_t)(q0 + j) * a.store.n + c] = e;
-                    a.out_b[(size_t)(q0 + j) * a.store.n + c] = u;
+        for (int o = 16; o > 0; o >>= 1) {
+            const double v = __shfl_xor_sync(0xffffffffu, acc, o);
+            acc = a.dk ? dmax(acc, v) : dadd(acc, v);
+        }
+        if (lane == 0) a.out_ub[w] = a.dk ? acc : __dmul_ru(acc, a.ub_scale);
+    }
+}
+
+void launch_sample_ub(const SampleArgs& a, cudaStream_t st) {
+    const uint64_t warps = (uint64_t)a.nq * a.S;
+    const int blocks = (int)std::min<uint64_t>((warps * 32 + 255) / 256, (uint64_t)sm_count() * 16);
+    sample_ub_kernel<<<std::max(blocks, 1), 256, 0, st>>>(a);
+}
+
+// ---- warp-aggregated enqueue into the two-region work queue ----------------------------------
+__device__ __forceinline__ void enqueue(const WorkQueue& w, bool take, bool near, uint32_t q,
+                                        uint32_t c, double key) {
+    const unsigned lane = lane_id();
+    const unsigned fm = __ballot_sync(0xffffffffu, take && near);
+    const unsigned bm = __ballot_sync(0xffffffffu, take && !near);
+    unsigned fb = 0, bb = 0;
+    if (lane == 0) {
+        if (fm) fb = atomicAdd(w.front, (unsigned)__popc(fm));
+        if (bm) bb = atomicAdd(w.back, (unsigned)__popc(bm));
+    }
+    fb = __shfl_sync(0xffffffffu, fb, 0);
+    bb = __shfl_sync(0xffffffffu, bb, 0);
+    const unsigned below = (1u << lane) - 1u;
+    if (take) {
+        const QEntry e{q, c, key};
+        if (near) w.e[fb + __popc(fm & below)] = e;
+        else w.e[w.cap - 1 - (bb + __popc(bm & below))] = e;
+    }
+}
+
+// ---- K2 + K3: fp32 LB_Box tile kernel fused with compaction --------------------------------
+// Tile = CB consecutive candidates x QB queries per warp; after the warp reduction lane
+// j = qb * CB + cb owns pair (q0 + qb, c0 + cb).
+template <int QB, int CB>
+__global__ void __launch_bounds__(256) lb_compact_kernel(LbCompactArgs a) {
+    static_assert(QB * CB == 32, "one pair per lane after the reduction");
+    const unsigned lane = lane_id();
+    const uint32_t n = a.store.n;
+    const uint64_t ngroups = (n + CB - 1) / CB;
+    const uint32_t nqb = (a.nq + QB - 1) / QB;
+    const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    const uint32_t total4 = (uint32_t)(a.store.ustride / 4);  // ustride % 4 == 0 (host pads)
+    for (uint64_t w = wid; w < ngroups * nqb; w += nw) {
+        // candidate-major order: the nqb query blocks of one candidate group run on adjacent
+        // warps, so the group's bytes come from HBM once and are re-read from L1/L2
+        const uint64_t cg = w / nqb;
+        const uint32_t qbk = (uint32_t)(w - cg * nqb);
+        const uint32_t c0 = (uint32_t)cg * CB;
+        const uint32_t q0 = qbk * QB;
+        const float4* x4[CB];
+#pragma unroll
+        for (int cb = 0; cb < CB; ++cb)
+            x4[cb] = reinterpret_cast<const float4*>(a.store.data32 +
+                                                     (uint64_t)min(c0 + cb, n - 1) * a.store.ustride);
+        const float4* lo4[QB];
+        const float4* hi4[QB];
+#pragma unroll
+        for (int qb = 0; qb < QB; ++qb) {
+            const uint64_t qo = (uint64_t)min(q0 + qb, a.nq - 1) * a.qstride;
+            lo4[qb] = reinterpret_cast<const float4*>(a.env_lo + qo);
+            hi4[qb] = reinterpret_cast<const float4*>(a.env_hi + qo);
+        }
+        float acc[QB][CB];
+#pragma unroll
+        for (int qb = 0; qb < QB; ++qb)
+#pragma unroll
+            for (int cb = 0; cb < CB; ++cb) acc[qb][cb] = 0.0f;
+        for (uint32_t f = lane; f < total4; f += 32) {
+            float4 x[CB];
+#pragma unroll
+            for (int cb = 0; cb < CB; ++cb) x[cb] = __ldg(x4[cb] + f);
+#pragma unroll
+            for (int qb = 0; qb < QB; ++qb) {
+                const float4 l = __ldg(lo4[qb] + f);
+                const float4 h = __ldg(hi4[qb] + f);
+#pragma unroll
+                for (int cb = 0; cb < CB; ++cb) {
+                    float s = acc[qb][cb];
+                    s = lb_term_rd(s, x[cb].x, l.x, h.x);
+                    s = lb_term_rd(s, x[cb].y, l.y, h.y);
+                    s = lb_term_rd(s, x[cb].z, l.z, h.z);
+                    s = lb_term_rd(s, x[cb].w, l.w, h.w);
+                    acc[qb][cb] = s;
                 }
+            }
+        }
+        // warp reduction (round-down adds keep the lower-bound property in any order)
+        float mine = 0.0f;
+#pragma unroll
+        for (int qb = 0; qb < QB; ++qb)
+#pragma unroll
+            for (int cb = 0; cb < CB; ++cb) {
+                float v = acc[qb][cb];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v = __fadd_rd(v, __shfl_xor_sync(0xffffffffu, v, o));
+                if (lane == (unsigned)(qb * CB + cb)) mine = v;
+            }
+        const uint32_t q = q0 + lane / CB, c = c0 + lane % CB;
+        const bool valid = q < a.nq && c < n;
+        bool take = false, near = false;
+        if (valid) {
+            const double lb = (double)mine;
+            if (a.lb_out) a.lb_out[(uint64_t)q * n + c] = mine;
+            if (a.state) {
+                const double T = a.state[q].T;
+                const bool probed = a.probed && a.probed[(uint64_t)q * n + c];
+                take = !probed && lb <= __dmul_ru(T, a.margin);
+                near = lb <= a.near_frac * T;
+            }
+        }
+        if (a.state) {
+            enqueue(a.queue, take, near, q, c, (double)mine);
+            // pruned counts: lanes qb*CB .. qb*CB+CB-1 share query q0+qb
+            bool pruned = valid && !take && !(a.probed && a.probed[(uint64_t)q * n + c]);
+            const unsigned pm = __ballot_sync(0xffffffffu, pruned);
+            if (valid && lane % CB == 0) {
+                const unsigned cnt = __popc(pm & (((1u << CB) - 1u) << lane));
+                if (cnt) atomicAdd(const_cast<unsigned long long*>(&a.state[q].lb_pruned), (unsigned long long)cnt);
             }
         }
     }
 }
 
-void launch_dk_bounds(const BoundArgs& a, cudaStream_t st) {
-    constexpr int QB = 8;
-    const int blocks = (int)std::min<uint64_t>(((uint64_t)a.store.n * 32 + 255) / 256,
-                                               (uint64_t)sm_count() * 8);
-    for (uint32_t q0 = 0; q0 < a.nq; q0 += QB)
-        dk_bounds_kernel<QB><<<std::max(blocks, 1), 256, 0, st>>>(a, q0);
+void launch_lb_compact(const LbCompactArgs& a, cudaStream_t st) {
+    constexpr int QB = 8, CB = 4;
+    const uint64_t tiles = (uint64_t)((a.store.n + CB - 1) / CB) * ((a.nq + QB - 1) / QB);
+    const int blocks = (int)std::min<uint64_t>((tiles * 32 + 255) / 256, (uint64_t)sm_count() * 8);
+    lb_compact_kernel<QB, CB><<<std::max(blocks, 1), 256, 0, st>>>(a);
+}
+
+// ---- DK: first / last cell bound fused with compaction ------------------------------------
+// Both cells lie on every warping path, so max(c(0,0), c(m-1,n-1)) > Tsq  =>  dk > T (exact).
+__global__ void __launch_bounds__(256) dk_compact_kernel(DkCompactArgs a) {
+    const uint32_t n = a.store.n, d = a.store.d, m = a.qlen;
+    const uint64_t total = (uint64_t)a.nq * n;
+    const unsigned lane = lane_id();
+    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < total;
+         base += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t g = base + threadIdx.x;
+        const bool in = g < total;
+        uint32_t q = 0, c = 0;
+        bool take = false, near = false, pruned = false;
+        double key = 0.0;
+        if (in) {
+            q = (uint32_t)(g / n);
+            c = (uint32_t)(g - (uint64_t)q * n);
+            if (!(a.probed && a.probed[g])) {
+                const double* s = a.queries + (uint64_t)q * a.qstride;
+                const double* t = a.store.data + series_off(a.store, c);
+                const uint32_t len = series_len(a.store, c);
+                double c0 = 0.0, c1 = 0.0;
+                for (uint32_t k = 0; k < d; ++k) {
+                    const double e0 = dsub(s[k], t[k]);
+                    c0 = dadd(c0, dmul(e0, e0));
+                    const double e1 = dsub(s[(uint64_t)(m - 1) * d + k], t[(uint64_t)(len - 1) * d + k]);
+                    c1 = dadd(c1, dmul(e1, e1));
+                }
+                key = dmax(c0, c1);
+                const double Tsq = a.state ? a.state[q].Tsq : a.fixed_eps_sq;
+                take = key <= Tsq;
+                near = key <= a.near_frac * Tsq;
+                pruned = !take;
+            }
+        }
+        enqueue(a.queue, take, near, q, c, key);
+        const unsigned pm = __ballot_sync(0xffffffffu, pruned);
+        if (pm) {
+            const unsigned grp = __match_any_sync(0xffffffffu, in ? q : 0xffffffffu);
+            const unsigned mine = pm & grp;
+            if (pruned && lane == (unsigned)(__ffs(mine) - 1)) {
+                if (a.state)
+                    atomicAdd(const_cast<unsigned long long*>(&a.state[q].early_abandoned),
+                              (unsigned long long)__popc(mine));
+                else if (a.fixed_pruned)
+                    atomicAdd(a.fixed_pruned, (unsigned long long)__popc(mine));
+            }
+        }
+    }
+}
+
+void launch_dk_compact(const DkCompactArgs& a, cudaStream_t st) {
+    const uint64_t total = (uint64_t)a.nq * a.store.n;
+    const int blocks = (int)std::min<uint64_t>((total + 255) / 256, (uint64_t)sm_count() * 8);
+    dk_compact_kernel<<<std::max(blocks, 1), 256, 0, st>>>(a);
 }
 
 }  // namespace tswb

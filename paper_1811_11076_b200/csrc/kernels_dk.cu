@@ -9,10 +9,10 @@
 // Thresholds compare against Tsq = max{x : sqrt(x) <= T}, so "sq <= Tsq" <=> "dist <= T".
 //
 // Pruning, as in sparse_engine<false> (dogkeeper.cpp:120-223) but on a dense strip sweep:
-//  * cells are never modified; a cell with value > T can only produce values > T, so every
-//    cell whose true value is <= T is computed exactly even when dead regions are skipped;
+//  * cell values are never altered; a cell whose true value is <= T only depends on cells
+//    <= T, so every such cell is computed exactly even when dead regions are skipped;
 //  * a strip starts at the first column whose boundary-row cell is <= T (everything left of it
-//    is provably > T) and stops when two consecutive skewed steps hold no cell <= T and the
+//    is provably > T) and stops once two consecutive skewed steps hold no cell <= T and the
 //    boundary row has no live cell right of lane 0 (a cut);
 //  * the pair is Exceeds as soon as a boundary row holds no live cell (the frontier died,
 //    dogkeeper.cpp:205-207), Exact iff the final cell is <= T.
@@ -25,24 +25,89 @@ namespace tswb {
 namespace {
 
 template <int D>
-__device__ __forceinline__ double cost_reg(const double (&sp)[D > 0 ? D : 1],
-                                           const double* __restrict__ s, uint32_t lds, uint32_t si,
-                                           const double* __restrict__ t, uint32_t ldt, uint32_t tj,
-                                           uint32_t d) {
-    double acc = 0.0;
-    if (D > 0) {
+__device__ __forceinline__ void load_point(const double* __restrict__ p, double (&x)[D > 0 ? D : 1]) {
+    if (D > 0 && D % 2 == 0) {
 #pragma unroll
-        for (int k = 0; k < D; ++k) {
-            const double e = dsub(sp[k], __ldg(t + (size_t)k * ldt + tj));
+        for (int k = 0; k < D; k += 2) {
+            const double2 v = __ldg(reinterpret_cast<const double2*>(p) + k / 2);
+            x[k] = v.x;
+            x[k + 1] = v.y;
+        }
+    } else if (D > 0) {
+#pragma unroll
+        for (int k = 0; k < D; ++k) x[k] = __ldg(p + k);
+    }
+}
+
+template <int D>
+__device__ __forceinline__ double cost(const double (&sp)[D > 0 ? D : 1], const double* __restrict__ srow,
+                                       const double* __restrict__ tp, uint32_t d) {
+    if (D > 0) {
+        double tv[D > 0 ? D : 1];
+        load_point<D>(tp, tv);
+        double e = dsub(sp[0], tv[0]);
+        double acc = dmul(e, e);  // 0.0 + x == x (squares are never -0)
+#pragma unroll
+        for (int k = 1; k < D; ++k) {
+            e = dsub(sp[k], tv[k]);
             acc = dadd(acc, dmul(e, e));
         }
+        return acc;
     } else {
+        double acc = 0.0;
         for (uint32_t k = 0; k < d; ++k) {
-            const double e = dsub(__ldg(s + (size_t)k * lds + si), __ldg(t + (size_t)k * ldt + tj));
+            const double e = dsub(__ldg(srow + k), __ldg(tp + k));
             acc = dadd(acc, dmul(e, e));
+        }
+        return acc;
+    }
+}
+
+struct Strip {
+    int R, rows, cstart, b_hi, b_alive_hi;
+    bool write_bnd, first;
+};
+
+template <int D>
+__device__ __forceinline__ void dk_step(const Strip& S, int k, int lane, int m, int n,
+                                        const double (&sp)[D > 0 ? D : 1],
+                                        const double* __restrict__ srow,
+                                        const double* __restrict__ t, uint32_t d,
+                                        double* __restrict__ bnd, double Tsq, double& left,
+                                        double& mine, double& up_prev, double& fin, int& nb_first,
+                                        int& nb_last, int& nb_hi, bool& live,
+                                        unsigned long long& cells) {
+    const int stride = D > 0 ? D : (int)d;
+    const int j = S.cstart + k - lane;
+    const bool active = lane < S.rows && (unsigned)(k - lane) <= (unsigned)(n - 1 - S.cstart);
+    double up = __shfl_up_sync(0xffffffffu, mine, 1);
+    double dg = up_prev;
+    if (lane == 0) {
+        // boundary row (row R-1): written on [b_lo, b_hi] with b_lo <= cstart; dg = bnd[j-1]
+        // was this lane's `up` one step earlier (inf on the first step of a strip)
+        up = (!S.first && j <= S.b_hi) ? bnd[j] : kInf;
+    }
+    up_prev = up;
+    double v = kInf;
+    if (active) {
+        const double c = cost<D>(sp, srow, t + (size_t)j * stride, d);
+        double pred = dmin(dmin(left, up), dg);
+        if (S.first && lane == 0 && j == 0) pred = 0.0;  // virtual start (whole matching)
+        v = dmax(c, pred);
+        left = v;
+        ++cells;
+        if (S.R + lane == m - 1 && j == n - 1) fin = v;
+    }
+    mine = v;
+    live = active && v <= Tsq;
+    if (S.write_bnd && lane == 31 && active) {
+        bnd[j] = v;  // in place: lane 0 has already consumed columns < j + 30
+        nb_hi = j;
+        if (live) {
+            if (nb_first < 0) nb_first = j;
+            nb_last = j;
         }
     }
-    return acc;
 }
 
 template <int D>
@@ -52,94 +117,71 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
     double* bnd = smem + (size_t)(threadIdx.x >> 5) * max_len;
     const uint32_t d = a.store.d;
     const int m = (int)a.qlen;
-    const uint32_t lds = a.ldq;
+    const int stride = D > 0 ? D : (int)d;
     unsigned long long cells = 0;
-    const unsigned qtotal = *a.queue_len;
+    const unsigned nf = *a.queue.front, nbk = *a.queue.back;
     for (;;) {
         unsigned slot = 0;
-        if (lane == 0) slot = atomicAdd(a.queue_head, 1u);
+        if (lane == 0) slot = atomicAdd(a.queue.head, 1u);
         slot = __shfl_sync(0xffffffffu, slot, 0);
-        if (slot >= qtotal) break;
-        const Pair pr = a.queue[slot];
-        const double* s = a.queries + (size_t)pr.q * d * lds;
-        const double* t = series_ptr(a.store, pr.c);
-        const int n = (int)series_len(a.store, pr.c);
-        const uint32_t ldt = a.store.off ? round_even((uint32_t)n) : a.store.uld;
+        QEntry pr;
+        if (!queue_get(a.queue, nf, nbk, slot, pr)) break;
         QState* st = a.state ? a.state + pr.q : nullptr;
         double Tsq = st ? ld_volatile(&st->Tsq) : a.fixed_eps_sq;
+        if (!(pr.key <= Tsq)) {  // re-check the admitting first/last-cell bound at dequeue
+            if (lane == 0 && st) atomicAdd(&st->early_abandoned, 1ull);
+            continue;
+        }
+        const double* s = a.queries + (uint64_t)pr.q * a.qstride;
+        const double* t = a.store.data + series_off(a.store, pr.c);
+        const int n = (int)series_len(a.store, pr.c);
 
-        // boundary row (row R-1) metadata: written range and live range
-        int b_lo = 0, b_hi = -1, b_alive_lo = 0, b_alive_hi = 0;  // R == 0: virtual start
+        Strip S;
+        S.b_hi = -1;
+        S.b_alive_hi = 0;  // virtual start at (0, 0)
+        int b_alive_lo = 0;
         bool dead = false;
         double fin = kInf;
-        for (int R = 0; R < m && !dead; R += 32) {
-            const int rows = min(32, m - R);
-            const bool lane_row = lane < rows;
-            const bool write_bnd = R + 32 < m;
+        for (int R = 0; R < m; R += 32) {
+            S.R = R;
+            S.rows = min(32, m - R);
+            S.first = R == 0;
+            S.write_bnd = R + 32 < m;
+            S.cstart = b_alive_lo;
+            const double* srow = s + (size_t)min(R + lane, m - 1) * stride;
             double sp[D > 0 ? D : 1];
-            if (D > 0) {
-#pragma unroll
-                for (int k = 0; k < (D > 0 ? D : 1); ++k)
-                    sp[k] = lane_row ? __ldg(s + (size_t)k * lds + R + lane) : 0.0;
-            }
-            const int cstart = b_alive_lo;
+            if (D > 0) load_point<D>(srow, sp);
             double left = kInf, mine = kInf, up_prev = kInf;
-            int nb_first = -1, nb_last = -1, nb_hi = cstart - 1;
-            unsigned hist = 1;  // bit set: some live cell in that step
-            const int kmax = (n - 1 - cstart) + rows - 1;
-            for (int k = 0; k <= kmax; ++k) {
-                const int j = cstart + k - lane;
-                const bool active = lane_row && j >= cstart && j < n;
-                double up = __shfl_up_sync(0xffffffffu, mine, 1);
-                double dg = up_prev;
-                if (lane == 0) {
-                    if (R == 0) {
-                        up = kInf;
-                        dg = kInf;
-                    } else {
-                        up = (j >= b_lo && j <= b_hi) ? bnd[j] : kInf;
-                        dg = (j - 1 >= b_lo && j - 1 <= b_hi) ? bnd[j - 1] : kInf;
-                    }
-                }
-                up_prev = up;
-                double v = kInf;
-                if (active) {
-                    const double c = cost_reg<D>(sp, s, lds, (uint32_t)(R + lane), t, ldt,
-                                                 (uint32_t)j, d);
-                    double pred = dmin(dmin(left, up), dg);
-                    if (R == 0 && lane == 0 && j == 0) pred = 0.0;  // virtual start (whole match)
-                    v = dmax(c, pred);
-                    left = v;
-                    ++cells;
-                    if (R + lane == m - 1 && j == n - 1) fin = v;
-                }
-                mine = v;
-                const bool live = active && v <= Tsq;
-                if (write_bnd && lane == 31 && active) {
-                    bnd[j] = v;  // in place: lane 0 has already consumed columns <= j + 29
-                    nb_hi = j;
-                    if (live) {
-                        if (nb_first < 0) nb_first = j;
-                        nb_last = j;
-                    }
-                }
-                hist = (hist << 1) | (__any_sync(0xffffffffu, live) ? 1u : 0u);
-                if ((hist & 3u) == 0u && cstart + k > b_alive_hi) break;  // dead cut
-                if (st && (k & 63) == 63) Tsq = ld_volatile(&st->Tsq);
+            int nb_first = -1, nb_last = -1, nb_hi = S.cstart - 1;
+            const int kmax = (n - 1 - S.cstart) + S.rows - 1;
+            bool l0, l1, l2, l3;
+            for (int k = 0; k <= kmax; k += 4) {
+                dk_step<D>(S, k, lane, m, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, fin,
+                           nb_first, nb_last, nb_hi, l0, cells);
+                dk_step<D>(S, k + 1, lane, m, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, fin,
+                           nb_first, nb_last, nb_hi, l1, cells);
+                dk_step<D>(S, k + 2, lane, m, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, fin,
+                           nb_first, nb_last, nb_hi, l2, cells);
+                dk_step<D>(S, k + 3, lane, m, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, fin,
+                           nb_first, nb_last, nb_hi, l3, cells);
+                // dead cut: no live cell on steps k+2, k+3 and nothing live ahead of lane 0
+                if (!__any_sync(0xffffffffu, l2 || l3) && S.cstart + k + 3 > S.b_alive_hi) break;
+                if (st && (k & 60) == 60) Tsq = ld_volatile(&st->Tsq);
             }
-            if (write_bnd) {
+            (void)l0;
+            (void)l1;
+            if (S.write_bnd) {
                 __syncwarp();
                 nb_first = __shfl_sync(0xffffffffu, nb_first, 31);
                 nb_last = __shfl_sync(0xffffffffu, nb_last, 31);
                 nb_hi = __shfl_sync(0xffffffffu, nb_hi, 31);
                 if (nb_first < 0) {
                     dead = true;
-                } else {
-                    b_lo = cstart;
-                    b_hi = nb_hi;
-                    b_alive_lo = nb_first;
-                    b_alive_hi = nb_last;
+                    break;
                 }
+                S.b_hi = nb_hi;
+                b_alive_lo = nb_first;
+                S.b_alive_hi = nb_last;
             }
         }
         // final cell lives in the lane of row m-1
@@ -149,8 +191,8 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
             const bool exact = !dead && fin <= Tsq;
             const double dist = __dsqrt_rn(fin);
             if (a.out_exact) {
-                a.out_exact[slot] = exact ? 1 : 0;
-                a.out_val[slot] = exact ? dist : (st ? ld_volatile(&st->T) : a.fixed_eps);
+                a.out_exact[pr.c] = exact ? 1 : 0;
+                a.out_val[pr.c] = exact ? dist : (st ? ld_volatile(&st->T) : a.fixed_eps);
             }
             if (exact) {
                 if (st) {
@@ -180,12 +222,8 @@ template <int D>
 void run_dk(const DpArgs& a, uint32_t max_pairs, uint32_t max_len, cudaStream_t st) {
     const int threads = 128;
     const size_t smem = (size_t)(threads / 32) * max_len * sizeof(double);
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(dk_dp_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             200 * 1024);
-        attr_set = true;
-    }
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(dk_dp_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, dk_dp_kernel<D>, threads, smem);
     const uint64_t want = ((uint64_t)max_pairs * 32 + threads - 1) / threads;
@@ -199,6 +237,7 @@ void run_dk(const DpArgs& a, uint32_t max_pairs, uint32_t max_len, cudaStream_t 
 void launch_dk_dp(const DpArgs& a, uint32_t max_pairs, uint32_t max_len, cudaStream_t st) {
     const uint32_t ml = std::max<uint32_t>(max_len, 2);
     switch (a.store.d) {
+        case 1: run_dk<1>(a, max_pairs, ml, st); break;
         case 2: run_dk<2>(a, max_pairs, ml, st); break;
         case 3: run_dk<3>(a, max_pairs, ml, st); break;
         case 16: run_dk<16>(a, max_pairs, ml, st); break;

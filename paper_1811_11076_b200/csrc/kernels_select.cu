@@ -1,5 +1,5 @@
-// Seed selection (P smallest upper bounds per query), threshold seeding + probe queue, and K3
-// survivor compaction (warp ballot + one atomic per warp into the DP work queue).
+// Seed selection (the P smallest sampled upper bounds per query) and threshold seeding + the
+// probe queue.
 #include <algorithm>
 
 #include "tsw_internal.cuh"
@@ -18,9 +18,14 @@ __global__ void __launch_bounds__(512) select_chunk_kernel(const double* __restr
     __shared__ uint32_t si[kSelChunk];
     const uint32_t q = blockIdx.y, chunk = blockIdx.x, nchunks = gridDim.x;
     const size_t base = (size_t)q * n_in;
-    for (uint32_t t = threadIdx.x; t < kSelChunk; t += blockDim.x) {
+    // sort only the power of two that covers this chunk's data
+    const uint64_t rest = (uint64_t)n_in - (uint64_t)chunk * kSelChunk;
+    const uint32_t have = rest < (uint64_t)kSelChunk ? (uint32_t)rest : (uint32_t)kSelChunk;
+    uint32_t N = 2;
+    while (N < have) N <<= 1;
+    for (uint32_t t = threadIdx.x; t < N; t += blockDim.x) {
         const uint64_t g = (uint64_t)chunk * kSelChunk + t;
-        if (g < n_in) {
+        if (t < have) {
             sv[t] = in_v[base + g];
             si[t] = in_i ? in_i[base + g] : (uint32_t)g;
         } else {
@@ -29,16 +34,15 @@ __global__ void __launch_bounds__(512) select_chunk_kernel(const double* __restr
         }
     }
     __syncthreads();
-    for (uint32_t size = 2; size <= kSelChunk; size <<= 1) {
+    for (uint32_t size = 2; size <= N; size <<= 1) {
         for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
-            for (uint32_t t = threadIdx.x; t < kSelChunk / 2; t += blockDim.x) {
+            for (uint32_t t = threadIdx.x; t < N / 2; t += blockDim.x) {
                 const uint32_t lo = 2 * t - (t & (stride - 1));
                 const uint32_t hi = lo + stride;
                 const bool up = (lo & size) == 0;
                 const double a = sv[lo], b = sv[hi];
                 const uint32_t ia = si[lo], ib = si[hi];
-                const bool b_less = pair_less(b, ib, a, ia);
-                if (b_less == up) {
+                if (pair_less(b, ib, a, ia) == up) {
                     sv[lo] = b; sv[hi] = a;
                     si[lo] = ib; si[hi] = ia;
                 }
@@ -48,8 +52,8 @@ __global__ void __launch_bounds__(512) select_chunk_kernel(const double* __restr
     }
     const size_t ob = ((size_t)q * nchunks + chunk) * P;
     for (uint32_t t = threadIdx.x; t < P; t += blockDim.x) {
-        out_v[ob + t] = sv[t];
-        out_i[ob + t] = si[t];
+        out_v[ob + t] = t < N ? sv[t] : kInf;
+        out_i[ob + t] = t < N ? si[t] : 0xffffffffu;
     }
 }
 
@@ -82,7 +86,9 @@ void launch_select_smallest(const double* vals, uint32_t nq, uint32_t n, uint32_
     }
 }
 
-// ---- seed: threshold = k-th smallest upper bound; probe queue = `probe` smallest -----------
+// ---- seed: threshold = k-th smallest sampled upper bound; probe queue = `probe` smallest -----
+// Any k distinct candidates' upper bounds bound the k-th nearest distance from above, so the
+// seed is a valid abandoning threshold (search.cpp:180-191 uses GDK bounds the same way).
 __global__ void seed_kernel(SeedArgs a) {
     const uint32_t q = blockIdx.x;
     const double* v = a.sel_v + (size_t)q * a.P;
@@ -91,7 +97,7 @@ __global__ void seed_kernel(SeedArgs a) {
     if (threadIdx.x == 0) {
         QState* st = a.state + q;
         double T = kInf;
-        if (kk <= (uint32_t)kKMax && kk <= a.P) {
+        if (kk <= (uint32_t)kKMax && kk <= a.P && kk <= a.S) {
             const double ub = v[kk - 1];
             T = a.dk ? __dsqrt_rn(ub) : ub;
         }
@@ -103,73 +109,18 @@ __global__ void seed_kernel(SeedArgs a) {
         st->lb_pruned = st->full_dp = st->early_abandoned = 0ull;
     }
     for (uint32_t j = threadIdx.x; j < a.probe; j += blockDim.x) {
-        const uint32_t c = ix[j];
-        a.probe_queue[(size_t)q * a.probe + j] = Pair{q, c};
+        const uint32_t c = (uint32_t)((uint64_t)ix[j] * a.n / a.S);
+        a.probe_q.e[(size_t)q * a.probe + j] = QEntry{q, c, 0.0};
         a.probed[(size_t)q * a.n + c] = 1;
     }
-    if (q == 0 && threadIdx.x == 0) *a.probe_len = a.nq * a.probe;
+    if (q == 0 && threadIdx.x == 0) {
+        *a.probe_q.front = a.nq * a.probe;
+        *a.probe_q.back = 0;
+    }
 }
 
 void launch_seed(const SeedArgs& a, cudaStream_t st) {
     seed_kernel<<<a.nq, 64, 0, st>>>(a);
-}
-
-// ---- K3: survivor compaction --------------------------------------------------------------
-// DTW: prune iff lb > T * margin (margin covers the fl error of both sums);
-//      strict, because offers do not arrive in index order on the GPU.
-// DK : prune iff max(c(0,0), c(m-1,n-1)) > Tsq  (exact; both cells are on every path).
-__global__ void __launch_bounds__(256) compact_kernel(CompactArgs a) {
-    const uint64_t total = (uint64_t)a.nq * a.n;
-    const int lane = threadIdx.x & 31;
-    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < total;
-         base += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t g = base + threadIdx.x;
-        const bool in = g < total;
-        uint32_t q = 0, c = 0;
-        bool survive = false, pruned = false;
-        if (in) {
-            q = (uint32_t)(g / a.n);
-            c = (uint32_t)(g - (uint64_t)q * a.n);
-            if (!(a.probed && a.probed[g])) {
-                const double key = a.key[g];
-                if (a.state) {
-                    const QState& st = a.state[q];
-                    survive = a.dk ? key <= st.Tsq : key <= __dmul_ru(st.T, a.margin);
-                } else {
-                    survive = a.dk ? key <= a.fixed_eps_sq : key <= __dmul_ru(a.fixed_eps, a.margin);
-                }
-                pruned = !survive;
-            }
-        }
-        const unsigned sm = __ballot_sync(0xffffffffu, survive);
-        if (sm) {
-            unsigned pos = 0;
-            if (lane == 0) pos = atomicAdd(a.queue_len, (unsigned)__popc(sm));
-            pos = __shfl_sync(0xffffffffu, pos, 0);
-            if (survive) a.queue[pos + __popc(sm & ((1u << lane) - 1u))] = Pair{q, c};
-        }
-        // pruned counts, aggregated over lanes of the same query
-        const unsigned pm = __ballot_sync(0xffffffffu, pruned);
-        if (pm) {
-            const unsigned grp = __match_any_sync(0xffffffffu, in ? q : 0xffffffffu);
-            const unsigned mine = pm & grp;
-            if (pruned && lane == __ffs(mine) - 1) {
-                if (a.state) {
-                    QState* st = const_cast<QState*>(a.state) + q;
-                    atomicAdd(a.dk ? &st->early_abandoned : &st->lb_pruned,
-                              (unsigned long long)__popc(mine));
-                } else if (a.fixed_pruned) {
-                    atomicAdd(a.fixed_pruned, (unsigned long long)__popc(mine));
-                }
-            }
-        }
-    }
-}
-
-void launch_compact(const CompactArgs& a, cudaStream_t st) {
-    const uint64_t total = (uint64_t)a.nq * a.n;
-    const int blocks = (int)std::min<uint64_t>((total + 255) / 256, (uint64_t)sm_count() * 8);
-    compact_kernel<<<std::max(blocks, 1), 256, 0, st>>>(a);
 }
 
 }  // namespace tswb

@@ -1,12 +1,14 @@
 // Internal device-side types and helpers shared by the tswarp_b200 kernels.
 //
 // HBM layout:
-//   store   : candidate i at data + off(i), dimension-major [d][ld_i] doubles, ld_i = len_i
-//             rounded up to even (16-byte rows for 128-bit loads; padding is zero).
-//   queries : [nq][d][ldq] doubles, same convention.
-//   envelope: lo / hi [nq][d][ldq] doubles.
-// All arithmetic is fp64 with separate mul / add (built with -fmad=false) so that every cell
-// cost is bit-identical to detail::sq_dist (types.hpp:126-133).
+//   store   : series c at data + off(c), point-major [len][d] doubles (exactly the reference's
+//             TimeSeries::flat(), types.hpp:43-58), series stride rounded up to an even number
+//             of doubles (16-byte aligned rows, zero padding).  A float copy `data32`
+//             (round-to-nearest, same layout) feeds the fp32 LB_Box lower bound.
+//   queries : [nq][qstride] doubles, same convention; envelope lo/hi: [nq][qstride] floats,
+//             directed-rounded so that fp32 LB terms are rigorous lower bounds.
+// All fp64 arithmetic uses separate mul / add (built with -fmad=false) so that every cell cost
+// is bit-identical to detail::sq_dist (types.hpp:126-133).
 #pragma once
 
 #include <cstdint>
@@ -17,21 +19,23 @@ namespace tswb {
 constexpr int kWarp = 32;
 constexpr int kKMax = 64;       // device top-k list capacity (threshold tightening)
 constexpr int kSelChunk = 4096; // bitonic selection chunk
-constexpr int kSelMaxP = 64;    // max entries kept per selection chunk
 constexpr double kInf = __builtin_huge_val();
 
 struct StoreDev {
     const double* data;
+    const float* data32;
     const uint64_t* off;  // per-series offset in doubles (ragged stores); nullptr if uniform
     const uint32_t* len;  // per-series length (ragged); nullptr if uniform
     uint32_t n, d;
-    uint32_t ulen, uld;   // uniform length / row stride
+    uint32_t ulen;        // uniform length (0 if ragged)
+    uint64_t ustride;     // uniform series stride in elements
 };
 
+__host__ __device__ inline uint64_t round_even64(uint64_t x) { return (x + 1u) & ~1ull; }
 __host__ __device__ inline uint32_t round_even(uint32_t x) { return (x + 1u) & ~1u; }
 
-__device__ __forceinline__ const double* series_ptr(const StoreDev& s, uint32_t i) {
-    return s.off ? s.data + s.off[i] : s.data + (size_t)i * s.d * s.uld;
+__device__ __forceinline__ uint64_t series_off(const StoreDev& s, uint32_t i) {
+    return s.off ? s.off[i] : (uint64_t)i * s.ustride;
 }
 __device__ __forceinline__ uint32_t series_len(const StoreDev& s, uint32_t i) {
     return s.len ? s.len[i] : s.ulen;
@@ -57,14 +61,39 @@ struct ResultBuf {
     uint32_t cap;
 };
 
-struct Pair {
+// DP work item: query, candidate and the lower bound that admitted it (re-checked at dequeue
+// against the then-current threshold).  DTW: fp32 LB_Box; DK: max(first, last) squared cost.
+struct QEntry {
     uint32_t q, c;
+    double key;
 };
+
+// Work queue with two regions: "near" entries fill from the front, "far" entries from the back
+// (a 2-bucket ordering by key / threshold: likely neighbours are processed first).
+struct WorkQueue {
+    QEntry* e;
+    unsigned* front;  // count of front entries
+    unsigned* back;   // count of back entries
+    unsigned* head;   // dequeue counter
+    uint32_t cap;
+};
+
+__device__ __forceinline__ bool queue_get(const WorkQueue& w, unsigned nf, unsigned nb,
+                                          unsigned slot, QEntry& out) {
+    if (slot < nf) {
+        out = w.e[slot];
+        return true;
+    }
+    if (slot < nf + nb) {
+        out = w.e[w.cap - 1 - (slot - nf)];
+        return true;
+    }
+    return false;
+}
 
 // largest x with sqrt(x) <= T (correctly rounded sqrt is monotone, so {x: sqrt(x) <= T} is
 // [0, x*]).  Exact for every finite T >= 0; +inf stays +inf.
-__device__ __host__ inline double sq_threshold(double T) {
-#ifdef __CUDA_ARCH__
+__device__ inline double sq_threshold(double T) {
     if (!(T < kInf)) return kInf;
     double x = __dmul_rn(T, T);
     while (__dsqrt_rn(x) > T) x = __longlong_as_double(__double_as_longlong(x) - 1);
@@ -73,17 +102,15 @@ __device__ __host__ inline double sq_threshold(double T) {
         if (__dsqrt_rn(nx) <= T) x = nx; else break;
     }
     return x;
-#else
-    return T;  // host path lives in capi.cu
-#endif
 }
 
 // fp64 helpers with explicit rounding (no contraction possible).
 __device__ __forceinline__ double dsub(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
-__device__ __forceinline__ double dmin(double a, double b) { return fmin(a, b); }
-__device__ __forceinline__ double dmax(double a, double b) { return fmax(a, b); }
+// min / max of non-NaN values: DSETP + 2 SEL
+__device__ __forceinline__ double dmin(double a, double b) { return b < a ? b : a; }
+__device__ __forceinline__ double dmax(double a, double b) { return a < b ? b : a; }
 
 __device__ __forceinline__ double ld_volatile(const double* p) {
     return *reinterpret_cast<const volatile double*>(p);
@@ -92,6 +119,13 @@ __device__ __forceinline__ double ld_volatile(const double* p) {
 // (a, ia) < (b, ib) lexicographically -- the tie rule of search.cpp:63-64,90-92.
 __device__ __forceinline__ bool pair_less(double a, uint32_t ia, double b, uint32_t ib) {
     return a < b || (a == b && ia < ib);
+}
+
+// fp32 lower-bound LB_Box term of one element against a directed-rounded envelope:
+// returns acc + max(lo - x, x - hi, 0)^2 rounded down, a rigorous lower bound.
+__device__ __forceinline__ float lb_term_rd(float acc, float x, float lo, float hi) {
+    const float e = fmaxf(fmaxf(__fsub_rd(lo, x), __fsub_rd(x, hi)), 0.0f);
+    return __fmaf_rd(e, e, acc);
 }
 
 // Offer an exact result to query q's device top-k list; called by ONE lane.
@@ -136,74 +170,91 @@ __device__ inline void topk_offer(QState* st, double* td, uint32_t* ti, double d
 }
 
 // ---- launch wrappers (defined in the kernel .cu files) --------------------------------------
-struct BoundArgs {
+// queries: [nq][qstride] doubles (point-major); envelope floats, same layout.
+void launch_envelope32(const double* q, uint32_t nq, uint32_t d, uint32_t len, uint64_t qstride,
+                       uint32_t r, float err, float* lo, float* hi, cudaStream_t st);
+void launch_envelope64(const double* q, uint32_t nq, uint32_t d, uint32_t len, uint64_t qstride,
+                       uint32_t r, double* lo, double* hi, cudaStream_t st);
+void launch_to_float(const double* src, uint64_t count, float* dst, cudaStream_t st);
+void launch_absmax(const double* src, uint64_t count, double* out, cudaStream_t st);
+
+struct SampleArgs {
     StoreDev store;
-    const double* queries;  // [nq][d][ldq]
-    const double* env_lo;   // DTW only
-    const double* env_hi;
-    uint32_t nq, qlen, ldq;
-    double ub_scale;        // DTW: diagonal-sum inflation factor (rounded up)
-    double* out_a;          // DTW: lb [nq][n]      DK: max(first, last cell) sq [nq][n]
-    double* out_b;          // DTW: ub [nq][n]      DK: diagonal-path max sq      [nq][n]
+    const double* queries;
+    uint32_t nq, qlen;
+    uint64_t qstride;
+    uint32_t S;           // sample size (candidates c = j * n / S)
+    double ub_scale;      // DTW: diagonal-sum inflation factor (rounded up)
+    int dk;
+    double* out_ub;       // [nq][S]  DTW: diagonal upper bound; DK: diagonal-path max sq
 };
+void launch_sample_ub(const SampleArgs& a, cudaStream_t st);
+
+// selection: the P smallest (value, index) pairs per query of `n` values per query.
+void launch_select_smallest(const double* vals, uint32_t nq, uint32_t n, uint32_t P, double* scratch_v, uint32_t* scratch_i,
+                            double* out_v, uint32_t* out_i, cudaStream_t st, int* launches);
+
+struct SeedArgs {
+    const double* sel_v;  // [nq][P] sorted smallest sampled upper bounds (DTW value / DK sq)
+    const uint32_t* sel_i;
+    uint32_t nq, n, P, k, probe, S;  // sample slot j <-> candidate j * n / S
+    int dk;
+    QState* state;
+    WorkQueue probe_q;
+    uint8_t* probed;      // [nq][n]
+};
+void launch_seed(const SeedArgs& a, cudaStream_t st);
+
+// DTW: fp32 LB_Box of every (query, candidate) pair fused with compaction.
+struct LbCompactArgs {
+    StoreDev store;
+    const float* env_lo;
+    const float* env_hi;
+    uint32_t nq;
+    uint64_t qstride;
+    double margin;        // prune iff lb > T * margin (rounded up)
+    double near_frac;     // front region iff lb <= near_frac * T
+    const QState* state;
+    const uint8_t* probed;
+    WorkQueue queue;
+    float* lb_out;        // optional [nq][n] (diagnostics / tsw_lb_box_all)
+};
+void launch_lb_compact(const LbCompactArgs& a, cudaStream_t st);
+
+// DK: first/last cell bound of every pair fused with compaction (exact, squared domain).
+struct DkCompactArgs {
+    StoreDev store;
+    const double* queries;
+    uint32_t nq, qlen;
+    uint64_t qstride;
+    double near_frac;
+    const QState* state;      // nullptr: fixed threshold (eps-NN)
+    double fixed_eps_sq;
+    unsigned long long* fixed_pruned;
+    const uint8_t* probed;
+    WorkQueue queue;
+};
+void launch_dk_compact(const DkCompactArgs& a, cudaStream_t st);
 
 struct DpArgs {
     StoreDev store;
     const double* queries;
-    uint32_t qlen, ldq, r;
-    const Pair* queue;
-    const unsigned* queue_len;  // device counter
-    unsigned* queue_head;       // device work counter (persistent warps)
+    const float* env_lo;        // DTW: fp32 envelope for the cumulative bound
+    const float* env_hi;
+    uint32_t qlen, r;
+    uint64_t qstride;
+    WorkQueue queue;
     QState* state;              // per query (nullptr in fixed-eps mode)
     double* top_d;              // [nq][kKMax]
     uint32_t* top_i;
     double fixed_eps;           // used when state == nullptr
     double fixed_eps_sq;
-    int* out_exact;             // per queue slot (dist_all mode), nullable
+    double margin;              // DTW: bound > T * margin  =>  distance > T
+    int* out_exact;             // per candidate (dist_all mode), nullable
     double* out_val;
     ResultBuf results;          // append buffer (results.dist == nullptr: off)
     unsigned long long* cells;  // DP cells evaluated (global accumulator)
-    const unsigned long long* cum_cells;  // DTW: valid band cells on anti-diagonals 0..a
 };
-
-void launch_envelope(const double* q, uint32_t nq, uint32_t d, uint32_t len, uint32_t ld,
-                     uint32_t r, double* lo, double* hi, cudaStream_t st);
-void launch_lb_ub(const BoundArgs& a, cudaStream_t st);
-void launch_dk_bounds(const BoundArgs& a, cudaStream_t st);
-void launch_rowmajor_to_soa(const double* src, uint32_t nser, uint32_t len, uint32_t d,
-                            uint32_t ld, double* dst, cudaStream_t st);
-
-// selection: P smallest (value, index) per query out of `n` values per query.
-// scratch must hold 2 * nq * ceil(n / kSelChunk) * P entries of (double, uint32).
-void launch_select_smallest(const double* vals, uint32_t nq, uint32_t n, uint32_t P,
-                            double* scratch_v, uint32_t* scratch_i, double* out_v,
-                            uint32_t* out_i, cudaStream_t st, int* launches);
-
-struct SeedArgs {
-    const double* sel_v;  // [nq][P] sorted smallest upper bounds (DTW value / DK sq)
-    const uint32_t* sel_i;
-    uint32_t nq, n, P, k, probe;
-    int dk;
-    QState* state;
-    Pair* probe_queue;
-    unsigned* probe_len;
-    uint8_t* probed;      // [nq][n]
-};
-void launch_seed(const SeedArgs& a, cudaStream_t st);
-
-struct CompactArgs {
-    const double* key;   // DTW: lb ; DK: max(first, last) sq
-    uint32_t nq, n;
-    double margin;       // DTW: prune iff lb > T * margin (rounded up); DK unused
-    int dk;
-    const QState* state;
-    const uint8_t* probed;
-    double fixed_eps, fixed_eps_sq;  // when state == nullptr (eps-NN)
-    unsigned long long* fixed_pruned;  // eps-NN: pruned count
-    Pair* queue;
-    unsigned* queue_len;
-};
-void launch_compact(const CompactArgs& a, cudaStream_t st);
 
 void launch_dtw_dp(const DpArgs& a, uint32_t max_pairs, cudaStream_t st);
 void launch_dk_dp(const DpArgs& a, uint32_t max_pairs, uint32_t max_len, cudaStream_t st);

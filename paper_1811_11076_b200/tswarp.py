@@ -359,6 +359,9 @@ def envelope(series, r: int):
 
 
 def lb_box_all(data, query, r: int):
+    """-> (lb, ub): the fp32 directed-rounded LB_Box lower bound of every candidate (K2; a
+    rigorous lower bound of lb_box(data[i], envelope(query, r))) and the diagonal DTW upper
+    bound used to seed the threshold."""
     st = _as_store(data)
     q = _series(query)
     lb = np.empty(st.n)

@@ -49,7 +49,10 @@ def test_lb_box_all(tsw, port, N, L, d, r):
     q = walks(RNG, 1, L, d)[0]
     lb, ub = tsw.lb_box_all(tsw.Store(X), q, r)
     olb = np.array([port.lb_box(X[i], q, r) for i in range(N)])
-    np.testing.assert_allclose(lb, olb, rtol=1e-12, atol=0)
+    # K2 runs in fp32 with directed rounding: a rigorous lower bound of the fp64 LB_Box that is
+    # tight to fp32 precision
+    assert np.all(lb <= olb), "fp32 LB_Box above the reference lb_box"
+    np.testing.assert_allclose(lb, olb, rtol=2e-5, atol=1e-6)
     dtw = np.array([port.dtw_banded(q, X[i], r) for i in range(N)])
     assert np.all(ub >= dtw), "diagonal upper bound below computed DTW"
     assert np.all(lb <= dtw * (1 + 1e-12)), "LB_Box above DTW"
