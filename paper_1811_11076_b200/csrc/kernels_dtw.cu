@@ -59,8 +59,8 @@ struct Lane {
     int obase, r2, L;
     __device__ __forceinline__ int off(int e) const { return obase + e; }
     __device__ __forceinline__ int hs(int e) const { return (obase + e) >> 1; }  // floor(o / 2)
-    // first valid iteration and hi - lo (unsigned compare trick); never-valid slots get a span
-    // of 0xffffffff and lo beyond any iteration
+    // first valid iteration and hi - lo (unsigned compare trick); never-valid slots get lo
+    // beyond any iteration and span 0, so (unsigned)(it - lo) <= span never holds
     __device__ __forceinline__ int lo(int e) const {
         const int o = obase + e, h = o >> 1;
         return valid_slot(e) ? max(h, h - o) : 0x3fffffff;
@@ -68,7 +68,7 @@ struct Lane {
     __device__ __forceinline__ unsigned span(int e) const {
         const int o = obase + e, h = o >> 1;
         const int lo_ = max(h, h - o), hi_ = L - 1 + min(h, h - o);
-        return valid_slot(e) ? (unsigned)(hi_ - lo_) : 0xffffffffu;
+        return valid_slot(e) ? (unsigned)(hi_ - lo_) : 0u;
     }
     __device__ __forceinline__ bool valid_slot(int e) const {
         const int o = obase + e, h = o >> 1;
