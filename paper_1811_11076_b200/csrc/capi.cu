@@ -168,7 +168,7 @@ struct tsw_plan {
     int metric = 0;
     uint64_t nq = 0;  // queries of the last set_queries
     cudaStream_t own = nullptr;
-    DevBuf<double> q, ub, sel_sv, sel_v, top_d;
+    DevBuf<double> q, q_rm, ub, sel_sv, sel_v, top_d;
     DevBuf<float> env_lo, env_hi;
     DevBuf<uint32_t> sel_si, sel_i, top_i;
     DevBuf<QState> state;
@@ -218,7 +218,15 @@ struct DeviceGuard {
     }
 };
 
-uint64_t stride_of(uint64_t len, uint64_t d) { return (len * d + 3) & ~3ull; }
+uint64_t stride_of(uint64_t len, uint64_t d) { return tiled_stride(len, d); }
+
+// row-major series (TimeSeries::flat()) -> tiled layout, host side
+std::vector<double> tiled_host(const double* rm, uint64_t len, uint64_t d) {
+    std::vector<double> out(stride_of(len, d), 0.0);
+    for (uint64_t p = 0; p < len; ++p)
+        for (uint64_t k = 0; k < d; ++k) out[tidx((uint32_t)p, (uint32_t)k, (uint32_t)d)] = rm[p * d + k];
+    return out;
+}
 
 // margin for "bound > T * margin => distance > T": covers the fl error of the
 // DTW path sum (<= 2L-1 additions + d+1 roundings per cell) and of the bound itself.
@@ -260,7 +268,7 @@ std::unique_ptr<tsw_plan> make_plan(tsw_store* s, uint64_t nq_max, uint64_t qlen
     ck(cudaStreamCreateWithFlags(&p->own, cudaStreamNonBlocking), "cudaStreamCreate");
     for (auto& e : p->ev) ck(cudaEventCreate(&e), "cudaEventCreate");
     p->q.alloc(nq_max * p->qstride);
-    ck(cudaMemset(p->q.p, 0, p->q.n * sizeof(double)), "memset");  // zero padding, once
+    p->q_rm.alloc(nq_max * qlen * s->d);
     if (metric == TSW_METRIC_DTW) {
         p->env_lo.alloc(nq_max * p->qstride);
         p->env_hi.alloc(nq_max * p->qstride);
@@ -297,10 +305,13 @@ std::unique_ptr<tsw_plan> make_plan(tsw_store* s, uint64_t nq_max, uint64_t qlen
 void set_queries_impl(tsw_plan* p, const double* q, uint64_t nq, bool device, cudaStream_t st) {
     if (nq == 0 || nq > p->nq_max) fail(TSW_EINVAL, "query count out of range for this plan");
     const uint64_t row = p->qlen * p->store->d;
-    ck(cudaMemcpy2DAsync(p->q.p, p->qstride * sizeof(double), q, row * sizeof(double),
-                         row * sizeof(double), nq,
-                         device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st),
-       "query upload");
+    const double* src = q;
+    if (!device) {
+        ck(cudaMemcpyAsync(p->q_rm.p, q, nq * row * sizeof(double), cudaMemcpyHostToDevice, st),
+           "query upload");
+        src = p->q_rm.p;
+    }
+    launch_rowmajor_to_tiled(src, nq, (uint32_t)p->qlen, (uint32_t)p->store->d, p->qstride, p->q.p, st);
     g_h2d = device ? 0 : nq * row * sizeof(double);
     p->nq = nq;
 }
@@ -553,11 +564,19 @@ int tsw_store_create(const double* values, const uint64_t* lengths, uint64_t uni
             s->ustride = stride_of(lens[0], d);
             elems = n * s->ustride;
             s->data.alloc(elems);
+            // upload row-major through a bounded staging buffer, re-tile on the device
             const uint64_t row = lens[0] * d;
-            if (s->ustride != row) ck(cudaMemset(s->data.p, 0, elems * sizeof(double)), "memset");
-            ck(cudaMemcpy2D(s->data.p, s->ustride * sizeof(double), values, row * sizeof(double),
-                            row * sizeof(double), n, cudaMemcpyHostToDevice),
-               "store upload");
+            const uint64_t batch = std::max<uint64_t>(1, std::min<uint64_t>(n, (256ull << 20) / (row * 8)));
+            DevBuf<double> stage(batch * row);
+            for (uint64_t b0 = 0; b0 < n; b0 += batch) {
+                const uint64_t nb = std::min(batch, n - b0);
+                ck(cudaMemcpy(stage.p, values + b0 * row, nb * row * sizeof(double),
+                              cudaMemcpyHostToDevice),
+                   "store upload");
+                launch_rowmajor_to_tiled(stage.p, nb, lens[0], (uint32_t)d, s->ustride,
+                                         s->data.p + b0 * s->ustride, 0);
+                ck(cudaDeviceSynchronize(), "store tiling");
+            }
         } else {
             std::vector<uint64_t> off(n);
             for (uint64_t i = 0; i < n; ++i) {
@@ -567,7 +586,8 @@ int tsw_store_create(const double* values, const uint64_t* lengths, uint64_t uni
             std::vector<double> buf(elems, 0.0);
             uint64_t src = 0;
             for (uint64_t i = 0; i < n; ++i) {
-                std::memcpy(buf.data() + off[i], values + src, lens[i] * d * sizeof(double));
+                const std::vector<double> t = tiled_host(values + src, lens[i], d);
+                std::memcpy(buf.data() + off[i], t.data(), t.size() * sizeof(double));
                 src += lens[i] * d;
             }
             s->data.alloc(elems);
@@ -743,8 +763,10 @@ int tsw_epsnn_dk(tsw_store* s, const double* query, uint64_t qlen, double eps,
         DevBuf<unsigned> rn(1), ctr(4);
         DevBuf<unsigned long long> pruned(1);
         DevBuf<QEntry> queue(n);
-        ck(cudaMemset(q.p, 0, qs * sizeof(double)), "memset");
-        ck(cudaMemcpy(q.p, query, qlen * d * sizeof(double), cudaMemcpyHostToDevice), "upload");
+        {
+            const std::vector<double> tq = tiled_host(query, qlen, d);
+            ck(cudaMemcpy(q.p, tq.data(), qs * sizeof(double), cudaMemcpyHostToDevice), "upload");
+        }
         ck(cudaMemset(rn.p, 0, sizeof(unsigned)), "memset");
         ck(cudaMemset(ctr.p, 0, 4 * sizeof(unsigned)), "memset");
         ck(cudaMemset(pruned.p, 0, sizeof(unsigned long long)), "memset");
@@ -800,13 +822,21 @@ int tsw_envelope(const double* series, uint64_t n, uint64_t d, uint64_t r, doubl
         // K1 in its exact fp64 form (the pipeline uses the fp32 outward-rounded variant)
         const uint64_t qs = stride_of(n, d);
         DevBuf<double> q(qs), l(qs), h(qs);
-        ck(cudaMemset(q.p, 0, qs * sizeof(double)), "memset");
-        ck(cudaMemcpy(q.p, series, n * d * sizeof(double), cudaMemcpyHostToDevice), "upload");
+        {
+            const std::vector<double> tq = tiled_host(series, n, d);
+            ck(cudaMemcpy(q.p, tq.data(), qs * sizeof(double), cudaMemcpyHostToDevice), "upload");
+        }
         launch_envelope64(q.p, 1, (uint32_t)d, (uint32_t)n, qs,
                           (uint32_t)std::min<uint64_t>(r, 0xffffffffu), l.p, h.p, 0);
         ck(cudaGetLastError(), "envelope");
-        ck(cudaMemcpy(lo, l.p, n * d * sizeof(double), cudaMemcpyDeviceToHost), "fetch");
-        ck(cudaMemcpy(hi, h.p, n * d * sizeof(double), cudaMemcpyDeviceToHost), "fetch");
+        std::vector<double> hl(qs), hh(qs);
+        ck(cudaMemcpy(hl.data(), l.p, qs * sizeof(double), cudaMemcpyDeviceToHost), "fetch");
+        ck(cudaMemcpy(hh.data(), h.p, qs * sizeof(double), cudaMemcpyDeviceToHost), "fetch");
+        for (uint64_t p = 0; p < n; ++p)
+            for (uint64_t k = 0; k < d; ++k) {
+                lo[p * d + k] = hl[tidx((uint32_t)p, (uint32_t)k, (uint32_t)d)];
+                hi[p * d + k] = hh[tidx((uint32_t)p, (uint32_t)k, (uint32_t)d)];
+            }
     });
 }
 
@@ -821,8 +851,10 @@ int tsw_lb_box_all(tsw_store* s, const double* query, uint64_t qlen, uint64_t r,
         const uint64_t n = s->n, d = s->d, qs = stride_of(qlen, d);
         DevBuf<double> q(qs), ub(n);
         DevBuf<float> el(qs), eh(qs), lb(n);
-        ck(cudaMemset(q.p, 0, qs * sizeof(double)), "memset");
-        ck(cudaMemcpy(q.p, query, qlen * d * sizeof(double), cudaMemcpyHostToDevice), "upload");
+        {
+            const std::vector<double> tq = tiled_host(query, qlen, d);
+            ck(cudaMemcpy(q.p, tq.data(), qs * sizeof(double), cudaMemcpyHostToDevice), "upload");
+        }
         launch_envelope32(q.p, 1, (uint32_t)d, (uint32_t)qlen, qs,
                           (uint32_t)std::min<uint64_t>(r, 0xffffffffu), s->err32, el.p, eh.p, 0);
         LbCompactArgs la{};
@@ -874,8 +906,10 @@ int tsw_dist_all(tsw_store* s, const double* query, uint64_t qlen, int metric, u
         const unsigned cnt[4] = {(unsigned)n, 0u, 0u, 0u};
         ck(cudaMemcpy(queue.p, hq.data(), n * sizeof(QEntry), cudaMemcpyHostToDevice), "upload");
         ck(cudaMemcpy(ctr.p, cnt, sizeof(cnt), cudaMemcpyHostToDevice), "upload");
-        ck(cudaMemset(q.p, 0, qs * sizeof(double)), "memset");
-        ck(cudaMemcpy(q.p, query, qlen * d * sizeof(double), cudaMemcpyHostToDevice), "upload");
+        {
+            const std::vector<double> tq = tiled_host(query, qlen, d);
+            ck(cudaMemcpy(q.p, tq.data(), qs * sizeof(double), cudaMemcpyHostToDevice), "upload");
+        }
         DpArgs da{};
         da.store = s->dev();
         da.queries = q.p;

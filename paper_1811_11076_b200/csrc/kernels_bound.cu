@@ -15,6 +15,26 @@ namespace tswb {
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
 // ---- helpers ------------------------------------------------------------------------------
+__global__ void rowmajor_to_tiled_kernel(const double* __restrict__ src, uint64_t nser, uint32_t len,
+                                         uint32_t d, uint64_t stride, double* __restrict__ dst) {
+    const uint64_t total = nser * stride;
+    for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total;
+         g += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t ser = g / stride;
+        const uint32_t f = (uint32_t)(g - ser * stride);
+        const uint32_t tile = f / (kTile * d), rem = f - tile * (kTile * d);
+        const uint32_t k = rem / kTile, p = tile * kTile + rem % kTile;
+        dst[g] = p < len ? src[(ser * len + p) * d + k] : 0.0;
+    }
+}
+
+void launch_rowmajor_to_tiled(const double* src, uint64_t nser, uint32_t len, uint32_t d,
+                              uint64_t stride, double* dst, cudaStream_t st) {
+    const uint64_t total = nser * stride;
+    const int blocks = (int)std::min<uint64_t>((total + 255) / 256, (uint64_t)sm_count() * 16);
+    rowmajor_to_tiled_kernel<<<std::max(blocks, 1), 256, 0, st>>>(src, nser, len, d, stride, dst);
+}
+
 __global__ void to_float_kernel(const double* __restrict__ src, uint64_t n, float* __restrict__ dst) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x)
@@ -56,18 +76,19 @@ __global__ void envelope_kernel(const double* __restrict__ q, uint32_t nq, uint3
          g += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t qi = g / qstride;
         const uint32_t f = (uint32_t)(g - qi * qstride);
-        if (f >= len * d) {
+        const uint32_t tile = f / (kTile * d), rem = f - tile * (kTile * d);
+        const uint32_t k = rem / kTile, i = tile * kTile + rem % kTile;
+        if (i >= len) {
             lo[g] = OutT(0);
             hi[g] = OutT(0);
             continue;
         }
-        const uint32_t i = f / d, k = f - i * d;
-        const double* row = q + qi * qstride + k;
+        const double* row = q + qi * qstride;
         const uint32_t a = i >= r ? i - r : 0u;
         const uint32_t b = (uint64_t)i + r < len ? i + r : len - 1;
-        double mn = row[(uint64_t)a * d], mx = mn;
+        double mn = row[tidx(a, k, d)], mx = mn;
         for (uint32_t w = a + 1; w <= b; ++w) {
-            const double v = row[(uint64_t)w * d];
+            const double v = row[tidx(w, k, d)];
             mn = v < mn ? v : mn;
             mx = v > mx ? v : mx;
         }
@@ -119,7 +140,7 @@ __global__ void __launch_bounds__(256) sample_ub_kernel(SampleArgs a) {
             const uint32_t i = min(p, m - 1), jj = min(p, n - 1);
             double cst = 0.0;
             for (uint32_t k = 0; k < d; ++k) {
-                const double e = dsub(s[(uint64_t)i * d + k], t[(uint64_t)jj * d + k]);
+                const double e = dsub(s[tidx(i, k, d)], t[tidx(jj, k, d)]);
                 cst = dadd(cst, dmul(e, e));
             }
             acc = a.dk ? dmax(acc, cst) : dadd(acc, cst);
@@ -172,7 +193,7 @@ __global__ void __launch_bounds__(256) lb_compact_kernel(LbCompactArgs a) {
     const uint32_t nqb = (a.nq + QB - 1) / QB;
     const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    const uint32_t total4 = (uint32_t)(a.store.ustride / 4);  // ustride % 4 == 0 (host pads)
+    const uint32_t total4 = (uint32_t)(a.store.ustride / 4);  // ustride is a multiple of 32d
     for (uint64_t w = wid; w < ngroups * nqb; w += nw) {
         // candidate-major order: the nqb query blocks of one candidate group run on adjacent
         // warps, so the group's bytes come from HBM once and are re-read from L1/L2
@@ -283,9 +304,9 @@ __global__ void __launch_bounds__(256) dk_compact_kernel(DkCompactArgs a) {
                 const uint32_t len = series_len(a.store, c);
                 double c0 = 0.0, c1 = 0.0;
                 for (uint32_t k = 0; k < d; ++k) {
-                    const double e0 = dsub(s[k], t[k]);
+                    const double e0 = dsub(s[tidx(0, k, d)], t[tidx(0, k, d)]);
                     c0 = dadd(c0, dmul(e0, e0));
-                    const double e1 = dsub(s[(uint64_t)(m - 1) * d + k], t[(uint64_t)(len - 1) * d + k]);
+                    const double e1 = dsub(s[tidx(m - 1, k, d)], t[tidx(len - 1, k, d)]);
                     c1 = dadd(c1, dmul(e1, e1));
                 }
                 key = dmax(c0, c1);

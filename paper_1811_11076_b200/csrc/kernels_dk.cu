@@ -26,16 +26,9 @@ namespace {
 
 template <int D>
 __device__ __forceinline__ void load_point(const double* __restrict__ p, double (&x)[D > 0 ? D : 1]) {
-    if (D > 0 && D % 2 == 0) {
+    if (D > 0) {
 #pragma unroll
-        for (int k = 0; k < D; k += 2) {
-            const double2 v = __ldg(reinterpret_cast<const double2*>(p) + k / 2);
-            x[k] = v.x;
-            x[k + 1] = v.y;
-        }
-    } else if (D > 0) {
-#pragma unroll
-        for (int k = 0; k < D; ++k) x[k] = __ldg(p + k);
+        for (int k = 0; k < D; ++k) x[k] = __ldg(p + k * kTile);  // tiled layout: dims 32 apart
     }
 }
 
@@ -56,7 +49,7 @@ __device__ __forceinline__ double cost(const double (&sp)[D > 0 ? D : 1], const 
     } else {
         double acc = 0.0;
         for (uint32_t k = 0; k < d; ++k) {
-            const double e = dsub(__ldg(srow + k), __ldg(tp + k));
+            const double e = dsub(__ldg(srow + k * kTile), __ldg(tp + k * kTile));
             acc = dadd(acc, dmul(e, e));
         }
         return acc;
@@ -90,7 +83,7 @@ __device__ __forceinline__ void dk_step(const Strip& S, int k, int lane, int m, 
     up_prev = up;
     double v = kInf;
     if (active) {
-        const double c = cost<D>(sp, srow, t + (size_t)j * stride, d);
+        const double c = cost<D>(sp, srow, t + tidx((uint32_t)j, 0, stride), d);
         double pred = dmin(dmin(left, up), dg);
         if (S.first && lane == 0 && j == 0) pred = 0.0;  // virtual start (whole matching)
         v = dmax(c, pred);
@@ -148,7 +141,7 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
             S.first = R == 0;
             S.write_bnd = R + 32 < m;
             S.cstart = b_alive_lo;
-            const double* srow = s + (size_t)min(R + lane, m - 1) * stride;
+            const double* srow = s + tidx((uint32_t)min(R + lane, m - 1), 0, stride);
             double sp[D > 0 ? D : 1];
             if (D > 0) load_point<D>(srow, sp);
             double left = kInf, mine = kInf, up_prev = kInf;

@@ -38,14 +38,14 @@ __device__ __forceinline__ double point_cost(const double* __restrict__ sp,
         double acc = dmul(e, e);
 #pragma unroll
         for (int k = 1; k < D; ++k) {
-            e = dsub(sp[k], tp[k]);
+            e = dsub(sp[k * kTile], tp[k * kTile]);
             acc = dadd(acc, dmul(e, e));
         }
         return acc;
     } else {
         double acc = 0.0;
         for (uint32_t k = 0; k < d; ++k) {
-            const double e = dsub(sp[k], tp[k]);
+            const double e = dsub(sp[k * kTile], tp[k * kTile]);
             acc = dadd(acc, dmul(e, e));
         }
         return acc;
@@ -102,7 +102,7 @@ __device__ __forceinline__ void dtw_step(double (&v)[2 * G], const Lane<G>& ln, 
         if (valid) {
             const int si = L - 1 - it + ln.hs(e);
             const int tj = si - ln.off(e);
-            const double c = point_cost<D>(s + (size_t)si * stride, t + (size_t)tj * stride, d);
+            const double c = point_cost<D>(s + tidx((uint32_t)si, 0, stride), t + tidx((uint32_t)tj, 0, stride), d);
             const double m = dmin(dmin(left, down), diag);
             nv = (it == 0 && ln.off(e) == 0) ? c : dadd(c, m);
             if (CHECK) alive |= dadd(nv, (double)pfx[tj]) <= Tm;
@@ -175,8 +175,8 @@ __global__ void __launch_bounds__(256) dtw_dp_kernel(DpArgs a, uint32_t pstride)
                         float term = 0.0f;
                         if (j < L)
                             for (int k = 0; k < stride; ++k)
-                                term = lb_term_rd(term, x32[(size_t)j * stride + k],
-                                                  el[(size_t)j * stride + k], eh[(size_t)j * stride + k]);
+                                term = lb_term_rd(term, x32[tidx(j, k, stride)],
+                                                  el[tidx(j, k, stride)], eh[tidx(j, k, stride)]);
 #pragma unroll
                         for (int o = 1; o < WL; o <<= 1) {
                             const float y = __shfl_up_sync(gmask, term, o, WL);

@@ -1,11 +1,12 @@
 // Internal device-side types and helpers shared by the tswarp_b200 kernels.
 //
-// HBM layout:
-//   store   : series c at data + off(c), point-major [len][d] doubles (exactly the reference's
-//             TimeSeries::flat(), types.hpp:43-58), series stride rounded up to an even number
-//             of doubles (16-byte aligned rows, zero padding).  A float copy `data32`
-//             (round-to-nearest, same layout) feeds the fp32 LB_Box lower bound.
-//   queries : [nq][qstride] doubles, same convention; envelope lo/hi: [nq][qstride] floats,
+// HBM layout: every series is stored in 32-point tiles, dimension-major inside a
+// tile -- element (point p, dim k) at tidx(p, k, d) = (p / 32) * 32d + 32k + p % 32 (zero
+// padding up to a whole tile).  Lanes that read 32 consecutive points of one dimension touch
+// 2 cache lines per load, and the d dimensions of a point sit at immediate offsets 32k.
+//   store   : series c at data + off(c); a float copy `data32` (round-to-nearest, same layout)
+//             feeds the fp32 LB_Box lower bound.
+//   queries : [nq][qstride] doubles, same layout; envelope lo/hi: [nq][qstride] floats,
 //             directed-rounded so that fp32 LB terms are rigorous lower bounds.
 // All fp64 arithmetic uses separate mul / add (built with -fmad=false) so that every cell cost
 // is bit-identical to detail::sq_dist (types.hpp:126-133).
@@ -20,6 +21,15 @@ constexpr int kWarp = 32;
 constexpr int kKMax = 64;       // device top-k list capacity (threshold tightening)
 constexpr int kSelChunk = 4096; // bitonic selection chunk
 constexpr double kInf = __builtin_huge_val();
+constexpr uint32_t kTile = 32;  // points per layout tile
+
+// element offset of (point p, dim k) in a tiled series of dimension d
+__host__ __device__ __forceinline__ uint64_t tidx(uint32_t p, uint32_t k, uint32_t d) {
+    return (uint64_t)(p >> 5) * (kTile * d) + k * kTile + (p & (kTile - 1));
+}
+__host__ __device__ inline uint64_t tiled_stride(uint64_t len, uint64_t d) {
+    return (len + kTile - 1) / kTile * kTile * d;
+}
 
 struct StoreDev {
     const double* data;
@@ -170,11 +180,14 @@ __device__ inline void topk_offer(QState* st, double* td, uint32_t* ti, double d
 }
 
 // ---- launch wrappers (defined in the kernel .cu files) --------------------------------------
-// queries: [nq][qstride] doubles (point-major); envelope floats, same layout.
+// queries: [nq][qstride] doubles (tiled); envelope floats, same layout.
 void launch_envelope32(const double* q, uint32_t nq, uint32_t d, uint32_t len, uint64_t qstride,
                        uint32_t r, float err, float* lo, float* hi, cudaStream_t st);
 void launch_envelope64(const double* q, uint32_t nq, uint32_t d, uint32_t len, uint64_t qstride,
                        uint32_t r, double* lo, double* hi, cudaStream_t st);
+// row-major [nser][len][d] -> tiled [nser][stride] (zero padding)
+void launch_rowmajor_to_tiled(const double* src, uint64_t nser, uint32_t len, uint32_t d,
+                              uint64_t stride, double* dst, cudaStream_t st);
 void launch_to_float(const double* src, uint64_t count, float* dst, cudaStream_t st);
 void launch_absmax(const double* src, uint64_t count, double* out, cudaStream_t st);
 
