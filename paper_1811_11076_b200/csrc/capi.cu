@@ -16,7 +16,10 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <ctime>
 #include <memory>
 #include <mutex>
 #include <new>
@@ -71,6 +74,20 @@ void require_device() {
         fail(TSW_ECUDA, "no CUDA device available (tswarp_b200 has no CPU fallback)");
     }
 }
+
+template <class T>
+struct HostBuf {  // pinned host memory
+    T* p = nullptr;
+    void alloc(size_t count) {
+        release();
+        if (count) ck(cudaMallocHost(&p, count * sizeof(T)), "cudaMallocHost");
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+    }
+    ~HostBuf() { release(); }
+};
 
 template <class T>
 struct DevBuf {
@@ -168,9 +185,10 @@ struct tsw_plan {
     int metric = 0;
     uint64_t nq = 0;  // queries of the last set_queries
     cudaStream_t own = nullptr;
-    DevBuf<double> q, q_rm, ub, sel_sv, sel_v, top_d;
+    DevBuf<double> q, q_rm, ub, sel_sv, sel_v, slots, top_d;
     DevBuf<float> env_lo, env_hi;
-    DevBuf<uint32_t> sel_si, sel_i, top_i;
+    DevBuf<uint32_t> sel_si, sel_i, top_i, fin_si;
+    DevBuf<double> fin_sv;
     DevBuf<QState> state;
     DevBuf<uint8_t> probed;
     DevBuf<QEntry> probe_q, queue;
@@ -179,6 +197,10 @@ struct tsw_plan {
     DevBuf<double> res_d;
     DevBuf<uint32_t> res_i;
     DevBuf<unsigned> res_n;
+    HostBuf<QState> h_state;
+    HostBuf<double> h_top_d;
+    HostBuf<uint32_t> h_top_i;
+    HostBuf<unsigned> h_res_n;
     double margin = 1.0, ub_scale = 1.0, near_frac = 0.5;
     bool timing = false;
     cudaEvent_t ev[8] = {};
@@ -280,17 +302,28 @@ std::unique_ptr<tsw_plan> make_plan(tsw_store* s, uint64_t nq_max, uint64_t qlen
     p->sel_v.alloc(nq_max * p->P);
     p->sel_i.alloc(nq_max * p->P);
     p->state.alloc(nq_max);
-    p->top_d.alloc(nq_max * kKMax);
-    p->top_i.alloc(nq_max * kKMax);
+    p->slots.alloc(nq_max * kKMax);
+    if (p->kk <= (uint64_t)kKMax) {
+        p->top_d.alloc(nq_max * p->kk);
+        p->top_i.alloc(nq_max * p->kk);
+        const uint64_t fch = (n + kSelChunk - 1) / kSelChunk;
+        p->fin_sv.alloc(2 * nq_max * fch * p->kk);
+        p->fin_si.alloc(2 * nq_max * fch * p->kk);
+    }
     p->probed.alloc(nq_max * n);
     p->probe_q.alloc(std::max<uint64_t>(1, nq_max * p->probe));
     p->queue.alloc(nq_max * n);
     p->counters.alloc(C_COUNT);
     p->cells.alloc(1);
-    if (p->kk > (uint64_t)kKMax) {  // no device list: exact results go to the append buffer
-        p->res_d.alloc(nq_max * n);
-        p->res_i.alloc(nq_max * n);
-        p->res_n.alloc(nq_max);
+    // exact-result append buffers (the device KBest feeds on them, see QState)
+    p->res_d.alloc(nq_max * n);
+    p->res_i.alloc(nq_max * n);
+    p->res_n.alloc(nq_max);
+    p->h_state.alloc(nq_max);
+    p->h_res_n.alloc(nq_max);
+    if (p->kk <= (uint64_t)kKMax) {
+        p->h_top_d.alloc(nq_max * p->kk);
+        p->h_top_i.alloc(nq_max * p->kk);
     }
     if (metric == TSW_METRIC_DTW) {
         const double L = (double)qlen, dd = (double)s->d;
@@ -322,14 +355,22 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
     if (nq == 0) fail(TSW_EINVAL, "no queries set on this plan");
     const bool dk = p->metric == TSW_METRIC_DK;
     int launches = 0;
+    static const bool dbg = std::getenv("TSW_DEBUG_SYNC") != nullptr;
     auto mark = [&](int i) {
         if (p->timing) ck(cudaEventRecord(p->ev[i], st), "cudaEventRecord");
+        if (dbg) {
+            ck(cudaStreamSynchronize(st), "debug sync");
+            unsigned c[C_COUNT];
+            cudaMemcpy(c, p->counters.p, sizeof(c), cudaMemcpyDeviceToHost);
+            std::fprintf(stderr, "[tsw] phase %d done; probe f=%u head=%u main f=%u b=%u head=%u\n", i,
+                         c[C_PFRONT], c[C_PHEAD], c[C_MFRONT], c[C_MBACK], c[C_MHEAD]);
+        }
     };
     mark(0);
     ck(cudaMemsetAsync(p->probed.p, 0, (size_t)nq * n, st), "memset");
     ck(cudaMemsetAsync(p->counters.p, 0, C_COUNT * sizeof(unsigned), st), "memset");
     ck(cudaMemsetAsync(p->cells.p, 0, sizeof(unsigned long long), st), "memset");
-    if (p->res_n.p) ck(cudaMemsetAsync(p->res_n.p, 0, nq * sizeof(unsigned), st), "memset");
+    ck(cudaMemsetAsync(p->res_n.p, 0, nq * sizeof(unsigned), st), "memset");
     if (!dk) {
         launch_envelope32(p->q.p, nq, (uint32_t)s->d, (uint32_t)p->qlen, p->qstride,
                           (uint32_t)std::min<uint64_t>(p->r, 0xffffffffu), s->err32, p->env_lo.p,
@@ -349,8 +390,8 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
     sa.out_ub = p->ub.p;
     launch_sample_ub(sa, st);
     ++launches;
-    launch_select_smallest(p->ub.p, nq, (uint32_t)p->S, (uint32_t)p->P, p->sel_sv.p, p->sel_si.p,
-                           p->sel_v.p, p->sel_i.p, st, &launches);
+    launch_select_smallest(p->ub.p, nullptr, nullptr, nq, (uint32_t)p->S, (uint32_t)p->P,
+                           p->sel_sv.p, p->sel_si.p, p->sel_v.p, p->sel_i.p, st, &launches);
     SeedArgs se{};
     se.sel_v = p->sel_v.p;
     se.sel_i = p->sel_i.p;
@@ -362,6 +403,7 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
     se.S = (uint32_t)p->S;
     se.dk = dk;
     se.state = p->state.p;
+    se.slots = p->slots.p;
     se.probe_q = p->probe_wq();
     se.probed = p->probed.p;
     launch_seed(se, st);
@@ -377,11 +419,10 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
     da.qstride = p->qstride;
     da.r = (uint32_t)std::min<uint64_t>(p->r, 0xffffffffu);
     da.state = p->state.p;
-    da.top_d = p->top_d.p;
-    da.top_i = p->top_i.p;
+    da.slots = p->slots.p;
     da.margin = p->margin;
     da.cells = p->cells.p;
-    if (p->res_d.p) da.results = ResultBuf{p->res_d.p, p->res_i.p, p->res_n.p, n};
+    da.results = ResultBuf{p->res_d.p, p->res_i.p, p->res_n.p, n};
     auto run_dp = [&](const WorkQueue& w, uint32_t max_pairs) {
         da.queue = w;
         if (dk) launch_dk_dp(da, max_pairs, (uint32_t)s->max_len, st);
@@ -419,6 +460,11 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
     ++launches;
     mark(4);
     run_dp(p->main_wq(), nq * n);
+    // final device top-k: the kk smallest (distance, index) of every query's exact results
+    if (p->kk <= (uint64_t)kKMax) {
+        launch_select_smallest(p->res_d.p, p->res_i.p, p->res_n.p, nq, n, (uint32_t)p->kk,
+                               p->fin_sv.p, p->fin_si.p, p->top_d.p, p->top_i.p, st, &launches);
+    }
     mark(5);
     ck(cudaEventRecord(p->ev[7], st), "cudaEventRecord");
     ck(cudaGetLastError(), "kernel launch");
@@ -429,38 +475,56 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
 void fetch_impl(tsw_plan* p, tsw_neighbor* out, tsw_counters* counters, cudaStream_t st) {
     if (!p->executed) fail(TSW_EINVAL, "plan has not been executed");
     const uint64_t nq = p->nq, n = p->store->n, kk = p->kk;
-    std::vector<QState> stv(nq);
-    ck(cudaMemcpyAsync(stv.data(), p->state.p, nq * sizeof(QState), cudaMemcpyDeviceToHost, st),
-       "fetch state");
-    std::vector<double> td;
-    std::vector<uint32_t> ti;
-    std::vector<unsigned> rn;
-    if (kk <= (uint64_t)kKMax) {
-        // top-k rows are kKMax apart; copy only the first kk of each row
-        td.resize(nq * kk);
-        ti.resize(nq * kk);
-        ck(cudaMemcpy2DAsync(td.data(), kk * sizeof(double), p->top_d.p, kKMax * sizeof(double),
-                             kk * sizeof(double), nq, cudaMemcpyDeviceToHost, st),
-           "fetch top-k");
-        ck(cudaMemcpy2DAsync(ti.data(), kk * sizeof(uint32_t), p->top_i.p, kKMax * sizeof(uint32_t),
-                             kk * sizeof(uint32_t), nq, cudaMemcpyDeviceToHost, st),
-           "fetch top-k");
-    } else {
-        rn.resize(nq);
-        ck(cudaMemcpyAsync(rn.data(), p->res_n.p, nq * sizeof(unsigned), cudaMemcpyDeviceToHost, st),
-           "fetch result counts");
+    if (std::getenv("TSW_DEBUG_WATCH")) {
+        // debug: poll the stream; on a stall dump queue counters and per-query state through a
+        // second stream (device memory is readable while the kernels run)
+        for (int it = 0; cudaStreamQuery(st) == cudaErrorNotReady; ++it) {
+            if (it == 200) {
+                cudaStream_t s2;
+                cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking);
+                unsigned c[C_COUNT];
+                std::vector<QState> sv(nq);
+                cudaMemcpyAsync(c, p->counters.p, sizeof(c), cudaMemcpyDeviceToHost, s2);
+                cudaMemcpyAsync(sv.data(), p->state.p, nq * sizeof(QState), cudaMemcpyDeviceToHost, s2);
+                cudaStreamSynchronize(s2);
+                std::fprintf(stderr, "[tsw] STALL probe f=%u head=%u main f=%u b=%u head=%u\n", c[C_PFRONT],
+                             c[C_PHEAD], c[C_MFRONT], c[C_MBACK], c[C_MHEAD]);
+                for (uint64_t q = 0; q < nq; ++q)
+                    std::fprintf(stderr, "[tsw]  q%llu T=%.17g k=%u full=%llu ab=%llu pr=%llu\n",
+                                 (unsigned long long)q, sv[q].T, sv[q].k, sv[q].full_dp,
+                                 sv[q].early_abandoned, sv[q].lb_pruned);
+                std::fflush(stderr);
+                std::abort();
+            }
+            struct timespec ts{0, 100000000};
+            nanosleep(&ts, nullptr);
+        }
     }
+    // pinned staging: the copies are truly asynchronous on `st`
+    QState* hs = p->h_state.p;
+    ck(cudaMemcpyAsync(hs, p->state.p, nq * sizeof(QState), cudaMemcpyDeviceToHost, st), "fetch state");
+    if (kk <= (uint64_t)kKMax) {
+        ck(cudaMemcpyAsync(p->h_top_d.p, p->top_d.p, nq * kk * sizeof(double), cudaMemcpyDeviceToHost, st),
+           "fetch top-k");
+        ck(cudaMemcpyAsync(p->h_top_i.p, p->top_i.p, nq * kk * sizeof(uint32_t), cudaMemcpyDeviceToHost, st),
+           "fetch top-k");
+    }
+    ck(cudaMemcpyAsync(p->h_res_n.p, p->res_n.p, nq * sizeof(unsigned), cudaMemcpyDeviceToHost, st),
+       "fetch result counts");
     ck(cudaStreamSynchronize(st), "pipeline");
-    g_d2h = nq * sizeof(QState) + td.size() * sizeof(double) + ti.size() * sizeof(uint32_t) +
-            rn.size() * sizeof(unsigned);
+    g_d2h = nq * (sizeof(QState) + sizeof(unsigned)) +
+            (kk <= (uint64_t)kKMax ? nq * kk * (sizeof(double) + sizeof(uint32_t)) : 0);
     for (uint64_t q = 0; q < nq; ++q) {
         tsw_neighbor* o = out ? out + q * kk : nullptr;
+        if (p->h_res_n.p[q] < kk || p->h_res_n.p[q] > n)
+            fail(TSW_ECUDA, "internal: " + std::to_string(p->h_res_n.p[q]) +
+                                " exact results for query " + std::to_string(q));
         if (kk <= (uint64_t)kKMax) {
-            if (stv[q].count != kk)
-                fail(TSW_ECUDA, "internal: device top-k incomplete for query " + std::to_string(q));
-            for (uint64_t j = 0; o && j < kk; ++j) o[j] = {ti[q * kk + j], td[q * kk + j]};
+            for (uint64_t j = 0; o && j < kk; ++j)
+                o[j] = {p->h_top_i.p[q * kk + j], p->h_top_d.p[q * kk + j]};
         } else {
-            const unsigned cnt = std::min<unsigned>(rn[q], (unsigned)n);
+            // k > kKMax: sort the (rare, large-k) exact-result buffer on the host
+            const unsigned cnt = p->h_res_n.p[q];
             std::vector<double> rd(cnt);
             std::vector<uint32_t> ri(cnt);
             ck(cudaMemcpy(rd.data(), p->res_d.p + q * n, cnt * sizeof(double), cudaMemcpyDeviceToHost),
@@ -473,15 +537,14 @@ void fetch_impl(tsw_plan* p, tsw_neighbor* out, tsw_counters* counters, cudaStre
             std::sort(all.begin(), all.end(), [](const tsw_neighbor& a, const tsw_neighbor& b) {
                 return a.distance < b.distance || (a.distance == b.distance && a.index < b.index);
             });
-            if (all.size() < kk) fail(TSW_ECUDA, "internal: fewer exact results than k");
             for (uint64_t j = 0; o && j < kk; ++j) o[j] = all[j];
         }
         if (counters) {
             tsw_counters& c = counters[q];
             c.lb_computed = p->metric == TSW_METRIC_DTW ? n : 0;
-            c.lb_pruned = stv[q].lb_pruned;
-            c.full_dp = stv[q].full_dp;
-            c.early_abandoned = stv[q].early_abandoned;
+            c.lb_pruned = hs[q].lb_pruned;
+            c.full_dp = hs[q].full_dp;
+            c.early_abandoned = hs[q].early_abandoned;
             c.gdk_calls = p->metric == TSW_METRIC_DK ? n : 0;
         }
     }

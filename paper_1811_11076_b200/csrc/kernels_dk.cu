@@ -190,10 +190,9 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
             if (exact) {
                 if (st) {
                     atomicAdd(&st->full_dp, 1ull);
-                    topk_offer(st, a.top_d + (size_t)pr.q * kKMax, a.top_i + (size_t)pr.q * kKMax,
-                               dist, pr.c, true);
-                }
-                if (a.results.dist) {
+                    offer_exact(st, a.slots + (size_t)pr.q * kKMax, a.results, pr.q, dist, pr.c,
+                                true);
+                } else if (a.results.dist) {  // fixed threshold (eps-NN): append only
                     const unsigned pos = atomicAdd(a.results.count + pr.q, 1u);
                     if (pos < a.results.cap) {
                         a.results.dist[(size_t)pr.q * a.results.cap + pos] = dist;

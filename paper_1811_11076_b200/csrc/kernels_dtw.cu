@@ -246,10 +246,9 @@ __global__ void __launch_bounds__(256) dtw_dp_kernel(DpArgs a, uint32_t pstride)
                 if (exact) {
                     if (st) {
                         atomicAdd(&st->full_dp, 1ull);
-                        topk_offer(st, a.top_d + (size_t)pr.q * kKMax,
-                                   a.top_i + (size_t)pr.q * kKMax, fin, pr.c, false);
-                    }
-                    if (a.results.dist) {
+                        offer_exact(st, a.slots + (size_t)pr.q * kKMax, a.results, pr.q, fin, pr.c,
+                                    false);
+                    } else if (a.results.dist) {  // fixed threshold (eps-NN): append only
                         const unsigned pos = atomicAdd(a.results.count + pr.q, 1u);
                         if (pos < a.results.cap) {
                             a.results.dist[(size_t)pr.q * a.results.cap + pos] = fin;

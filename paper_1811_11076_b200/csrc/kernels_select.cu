@@ -11,6 +11,7 @@ namespace tswb {
 // under the (distance, index) tie rule and writes its P smallest.
 __global__ void __launch_bounds__(512) select_chunk_kernel(const double* __restrict__ in_v,
                                                            const uint32_t* __restrict__ in_i,
+                                                           const unsigned* __restrict__ counts,
                                                            uint32_t n_in, uint32_t P,
                                                            double* __restrict__ out_v,
                                                            uint32_t* __restrict__ out_i) {
@@ -19,7 +20,8 @@ __global__ void __launch_bounds__(512) select_chunk_kernel(const double* __restr
     const uint32_t q = blockIdx.y, chunk = blockIdx.x, nchunks = gridDim.x;
     const size_t base = (size_t)q * n_in;
     // sort only the power of two that covers this chunk's data
-    const uint64_t rest = (uint64_t)n_in - (uint64_t)chunk * kSelChunk;
+    const uint64_t valid = counts ? (uint64_t)min(counts[q], n_in) : (uint64_t)n_in;
+    const uint64_t rest = valid > (uint64_t)chunk * kSelChunk ? valid - (uint64_t)chunk * kSelChunk : 0;
     const uint32_t have = rest < (uint64_t)kSelChunk ? (uint32_t)rest : (uint32_t)kSelChunk;
     uint32_t N = 2;
     while (N < have) N <<= 1;
@@ -57,11 +59,13 @@ __global__ void __launch_bounds__(512) select_chunk_kernel(const double* __restr
     }
 }
 
-void launch_select_smallest(const double* vals, uint32_t nq, uint32_t n, uint32_t P,
+void launch_select_smallest(const double* vals, const uint32_t* idx, const unsigned* counts,
+                            uint32_t nq, uint32_t n, uint32_t P,
                             double* scratch_v, uint32_t* scratch_i, double* out_v,
                             uint32_t* out_i, cudaStream_t st, int* launches) {
     const double* cur_v = vals;
-    const uint32_t* cur_i = nullptr;
+    const uint32_t* cur_i = idx;
+    const unsigned* cur_c = counts;
     uint32_t cur_n = n;
     const size_t half = (size_t)nq * ((n + kSelChunk - 1) / kSelChunk) * P;
     int ping = 0;
@@ -76,11 +80,12 @@ void launch_select_smallest(const double* vals, uint32_t nq, uint32_t n, uint32_
             dv = scratch_v + ping * half;
             di = scratch_i + ping * half;
         }
-        select_chunk_kernel<<<dim3(nchunks, nq), 512, 0, st>>>(cur_v, cur_i, cur_n, P, dv, di);
+        select_chunk_kernel<<<dim3(nchunks, nq), 512, 0, st>>>(cur_v, cur_i, cur_c, cur_n, P, dv, di);
         if (launches) ++*launches;
         if (nchunks == 1) break;
         cur_v = dv;
         cur_i = di;
+        cur_c = nullptr;
         cur_n = nchunks * P;
         ping ^= 1;
     }
@@ -103,11 +108,10 @@ __global__ void seed_kernel(SeedArgs a) {
         }
         st->T = T;
         st->Tsq = a.dk ? sq_threshold(T) : T;
-        st->lock = 0;
-        st->count = 0;
         st->k = kk <= (uint32_t)kKMax ? kk : 0u;
         st->lb_pruned = st->full_dp = st->early_abandoned = 0ull;
     }
+    for (uint32_t j = threadIdx.x; j < (uint32_t)kKMax; j += blockDim.x) a.slots[(size_t)q * kKMax + j] = kInf;
     for (uint32_t j = threadIdx.x; j < a.probe; j += blockDim.x) {
         const uint32_t c = (uint32_t)((uint64_t)ix[j] * a.n / a.S);
         a.probe_q.e[(size_t)q * a.probe + j] = QEntry{q, c, 0.0};

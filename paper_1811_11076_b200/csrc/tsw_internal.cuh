@@ -51,23 +51,26 @@ __device__ __forceinline__ uint32_t series_len(const StoreDev& s, uint32_t i) {
     return s.len ? s.len[i] : s.ulen;
 }
 
-// Per-query search state in device memory: the broadcast threshold plus a (distance, index)
-// sorted top-k list guarded by a spin lock (device-side KBest, search.cpp:40-97).
+// Per-query search state in device memory (device-side KBest, search.cpp:40-97, lock-free):
+//  * every exact result (distance <= threshold at its check) is appended to the query's result
+//    buffer; the final (distance, index) top-k is selected from it on the device;
+//  * the broadcast threshold T = min(seed, max of k slots), where the slots hold k exact
+//    distances of distinct candidates (insertion = CAS on the current maximum slot), so T is
+//    always an upper bound of the true k-th distance; it only ever decreases (atomicMin on the
+//    bit pattern, valid for non-negative doubles).
 struct QState {
     double T;          // current threshold, distance domain (DTW: squared-sum semantics)
     double Tsq;        // DK only: largest x with sqrt(x) <= T (sqrt monotone)
-    unsigned lock;
-    unsigned count;
-    unsigned k;        // min(k, n) if k <= kKMax, else 0 (no list: threshold stays at the seed)
+    unsigned k;        // min(k, n) if k <= kKMax (slots active), else 0 (threshold stays at seed)
     unsigned pad;
     unsigned long long lb_pruned, full_dp, early_abandoned;
 };
 
-// Result append buffer (eps-NN and k > kKMax): per query `cap` slots.
+// Result append buffer: per query `cap` slots (cap = n: a candidate is appended at most once).
 struct ResultBuf {
     double* dist;
     uint32_t* idx;
-    unsigned* count;
+    unsigned* count;  // per query
     uint32_t cap;
 };
 
@@ -138,45 +141,41 @@ __device__ __forceinline__ float lb_term_rd(float acc, float x, float lo, float 
     return __fmaf_rd(e, e, acc);
 }
 
-// Offer an exact result to query q's device top-k list; called by ONE lane.
-// Updates the broadcast threshold when the list is full.  dk: also refresh Tsq.
-__device__ inline void topk_offer(QState* st, double* td, uint32_t* ti, double d, uint32_t idx,
-                                  bool dk) {
-    if (st->k == 0) return;
-    while (atomicCAS(&st->lock, 0u, 1u) != 0u) {
+__device__ __forceinline__ void atomic_min_pos(double* p, double v) {
+    atomicMin(reinterpret_cast<unsigned long long*>(p), (unsigned long long)__double_as_longlong(v));
+}
+
+// Offer an exact result of query q (called by ONE lane): append it, then tighten the threshold
+// through the k lock-free slots.  dk: also tighten Tsq.
+__device__ inline void offer_exact(QState* st, double* slots, const ResultBuf& rb, uint32_t q,
+                                   double d, uint32_t idx, bool dk) {
+    const unsigned pos = atomicAdd(rb.count + q, 1u);
+    if (pos < rb.cap) {
+        rb.dist[(size_t)q * rb.cap + pos] = d;
+        rb.idx[(size_t)q * rb.cap + pos] = idx;
     }
-    __threadfence();
-    volatile double* vd = td;
-    volatile uint32_t* vi = ti;
-    unsigned cnt = *reinterpret_cast<volatile unsigned*>(&st->count);
     const unsigned k = st->k;
-    int pos = -1;
-    if (cnt < k) {
-        pos = (int)cnt;
-        cnt += 1;
-    } else if (pair_less(d, idx, vd[k - 1], vi[k - 1])) {
-        pos = (int)k - 1;
-    }
-    if (pos >= 0) {
-        while (pos > 0 && pair_less(d, idx, vd[pos - 1], vi[pos - 1])) {
-            vd[pos] = vd[pos - 1];
-            vi[pos] = vi[pos - 1];
-            --pos;
+    if (k == 0) return;
+    volatile double* vs = slots;
+    for (;;) {
+        unsigned jm = 0;
+        double vm = vs[0];
+        for (unsigned j = 1; j < k; ++j) {
+            const double v = vs[j];
+            if (v > vm) { vm = v; jm = j; }
         }
-        vd[pos] = d;
-        vi[pos] = idx;
-        *reinterpret_cast<volatile unsigned*>(&st->count) = cnt;
-        if (cnt == k) {
-            const double nt = vd[k - 1];
-            if (nt < ld_volatile(&st->T)) {
-                if (dk) *reinterpret_cast<volatile double*>(&st->Tsq) = sq_threshold(nt);
-                __threadfence();
-                *reinterpret_cast<volatile double*>(&st->T) = nt;
-            }
-        }
+        if (!(d < vm)) break;
+        const unsigned long long old = atomicCAS(reinterpret_cast<unsigned long long*>(slots + jm),
+                                                 (unsigned long long)__double_as_longlong(vm),
+                                                 (unsigned long long)__double_as_longlong(d));
+        if (old == (unsigned long long)__double_as_longlong(vm)) break;
     }
-    __threadfence();
-    atomicExch(&st->lock, 0u);
+    double nm = vs[0];
+    for (unsigned j = 1; j < k; ++j) nm = fmax(nm, vs[j]);
+    if (nm < ld_volatile(&st->T)) {
+        if (dk) atomic_min_pos(&st->Tsq, sq_threshold(nm));
+        atomic_min_pos(&st->T, nm);
+    }
 }
 
 // ---- launch wrappers (defined in the kernel .cu files) --------------------------------------
@@ -204,7 +203,9 @@ struct SampleArgs {
 void launch_sample_ub(const SampleArgs& a, cudaStream_t st);
 
 // selection: the P smallest (value, index) pairs per query of `n` values per query.
-void launch_select_smallest(const double* vals, uint32_t nq, uint32_t n, uint32_t P, double* scratch_v, uint32_t* scratch_i,
+// counts: optional per-query number of valid values (the rest count as +inf).
+void launch_select_smallest(const double* vals, const uint32_t* idx, const unsigned* counts,
+                            uint32_t nq, uint32_t n, uint32_t P, double* scratch_v, uint32_t* scratch_i,
                             double* out_v, uint32_t* out_i, cudaStream_t st, int* launches);
 
 struct SeedArgs {
@@ -213,6 +214,7 @@ struct SeedArgs {
     uint32_t nq, n, P, k, probe, S;  // sample slot j <-> candidate j * n / S
     int dk;
     QState* state;
+    double* slots;
     WorkQueue probe_q;
     uint8_t* probed;      // [nq][n]
 };
@@ -258,14 +260,13 @@ struct DpArgs {
     uint64_t qstride;
     WorkQueue queue;
     QState* state;              // per query (nullptr in fixed-eps mode)
-    double* top_d;              // [nq][kKMax]
-    uint32_t* top_i;
+    double* slots;              // [nq][kKMax] threshold slots
     double fixed_eps;           // used when state == nullptr
     double fixed_eps_sq;
     double margin;              // DTW: bound > T * margin  =>  distance > T
     int* out_exact;             // per candidate (dist_all mode), nullable
     double* out_val;
-    ResultBuf results;          // append buffer (results.dist == nullptr: off)
+    ResultBuf results;          // exact-result append buffer (results.dist == nullptr: off)
     unsigned long long* cells;  // DP cells evaluated (global accumulator)
 };
 
