@@ -269,15 +269,16 @@ def _as_store(data) -> Store:
 def knn(data, queries, k: int, metric: str = "dtw", r: int = 0):
     """Batched k-NN: queries [nq, L, d] -> (indices u64[nq, kk], distances f64[nq, kk],
     counters u64[nq, 5]) with kk = min(k, n)."""
-    st = _as_store(data)
     qs = np.ascontiguousarray(queries, dtype=np.float64)
     if qs.ndim == 2:
         qs = qs[None]
     nq, qlen, d = qs.shape
-    if d != st.dim:
-        raise ValueError(f"knn_{metric}: query dim {d} != dataset dim {st.dim}")
+    # argument checks first, as the reference does before touching the data (search.cpp:127)
     if k == 0:
         raise ValueError(f"knn_{metric}: k must be positive")
+    if d != data.dim:
+        raise ValueError(f"knn_{metric}: query dim {d} != dataset dim {data.dim}")
+    st = _as_store(data)
     kk = min(k, st.n)
     out = (Neighbor_t * max(1, nq * kk))()
     ctr = (Counters_t * max(1, nq))()
@@ -300,6 +301,8 @@ def knn_dtw(query, data, k: int, r, threads: int = 1) -> SearchReport:
     """tswarp::knn_dtw(query, data, k, BandRadius r, threads) -- search.hpp:46-47."""
     rv = r.value if hasattr(r, "value") else int(r)
     q = _series(query)
+    if k == 0:
+        raise ValueError("knn_dtw: k must be positive")
     _check_query(q, data, True, "knn_dtw")
     t0 = time.perf_counter()
     idx, dist, c = knn(data, q[None], k, "dtw", rv)
@@ -309,6 +312,8 @@ def knn_dtw(query, data, k: int, r, threads: int = 1) -> SearchReport:
 def knn_dk(query, data, k: int, threads: int = 1) -> SearchReport:
     """tswarp::knn_dk(query, data, k, threads) -- search.hpp:56-57."""
     q = _series(query)
+    if k == 0:
+        raise ValueError("knn_dk: k must be positive")
     _check_query(q, data, False, "knn_dk")
     t0 = time.perf_counter()
     idx, dist, c = knn(data, q[None], k, "dk")

@@ -1,0 +1,105 @@
+"""Generate the golden parity fixtures from the REFERENCE itself (oracle/_ref, compiled from
+/root/reference/proj/core/src by oracle/Makefile).  Run in the build container:
+
+    python tests/golden/make_golden.py
+
+Writes tests/golden/reference_vectors.json: small seeded datasets with the reference's own
+outputs for every hot-path function (knn_dtw, knn_dk incl. counters, epsnn_dk, dtw_banded,
+dtw_early_abandon, dk_full, sparse_dk, gdk, lb_box, envelope, znormalize).  Doubles are stored
+as float.hex() strings so the fixtures are bit-exact.  /root/reference does not exist on the GPU
+box; the committed JSON travels instead.
+"""
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+import oracle  # noqa: E402
+
+SEED = 1811_11076
+
+
+def hx(a):
+    return [float(x).hex() for x in np.asarray(a, dtype=np.float64).ravel()]
+
+
+def walks(rng, n, L, d):
+    x = rng.standard_normal((n, L, d)).cumsum(1)
+    return x
+
+
+def main():
+    R = oracle.ref()
+    rng = np.random.default_rng(SEED)
+    cases = []
+    shapes = [  # (n, L, d, r, ks, nq, ragged)
+        (40, 16, 1, 2, [1, 3], 2, False),
+        (64, 24, 2, 3, [1, 5], 2, False),
+        (50, 32, 3, 4, [1, 4, 50], 2, False),
+        (30, 20, 16, 2, [1, 2], 2, False),
+        (25, 12, 2, 0, [1, 30], 2, False),
+        (45, 1, 2, 0, [1, 3], 1, False),
+        (36, 0, 3, 0, [1, 6], 2, True),   # ragged lengths (DK only)
+    ]
+    for ci, (n, L, d, r, ks, nq, ragged) in enumerate(shapes):
+        if ragged:
+            series = [rng.standard_normal((int(rng.integers(1, 30)), d)).cumsum(0) for _ in range(n)]
+            qlen = 17
+            queries = [rng.standard_normal((qlen, d)).cumsum(0) for _ in range(nq)]
+        else:
+            X = walks(rng, n, L, d)
+            if ci == 2:
+                X[7] = X[3]  # exact duplicate: tie broken by lower index
+            series = list(X)
+            queries = list(walks(rng, nq, L, d))
+            if ci == 1:
+                queries[0] = X[11].copy()  # self-match at distance 0
+        ds = oracle.Dataset(series)
+        case = {"name": f"case{ci}", "d": d, "r": r, "ragged": ragged,
+                "series": [hx(s) for s in series], "lengths": [len(s) for s in series],
+                "queries": [hx(q) for q in queries], "qlen": len(queries[0]), "knn": [],
+                "pair": []}
+        for qi, q in enumerate(queries):
+            for metric in (["dk"] if ragged else ["dtw", "dk"]):
+                for k in ks:
+                    idx, dist, ctr = R.knn(q, ds, k, metric, r)
+                    case["knn"].append({"q": qi, "metric": metric, "k": k,
+                                        "index": [int(i) for i in idx], "distance": hx(dist),
+                                        "counters": [int(c) for c in ctr]})
+            dks = [R.dk_full(q, s) for s in series]
+            eps = float(np.median(dks))
+            ei, ed, _ = R.epsnn_dk(q, ds, eps)
+            case.setdefault("epsnn", []).append({"q": qi, "eps": float(eps).hex(),
+                                                 "index": [int(i) for i in ei], "distance": hx(ed)})
+        # per-pair primitives against the first query
+        q = queries[0]
+        for si, s in enumerate(series[:12]):
+            ent = {"i": si, "dk_full": float(R.dk_full(q, s)).hex(),
+                   "gdk": float(R.gdk(q, s)).hex()}
+            ex, v = R.sparse_dk(q, s, float(R.dk_full(q, s)) * 0.999)
+            ent["sparse_dk_below"] = [ex, float(v).hex()]
+            if not ragged:
+                ent["dtw_banded"] = float(R.dtw_banded(q, s, r)).hex()
+                ex, v = R.dtw_early_abandon(q, s, r, float(R.dtw_banded(q, s, r)))
+                ent["dtw_early_abandon_at_d"] = [ex, float(v).hex()]
+                ent["lb_box"] = float(R.lb_box(s, q, r)).hex()
+            case["pair"].append(ent)
+        if not ragged:
+            lo, hi = R.envelope(q, r)
+            case["envelope_q0"] = {"lo": hx(lo), "hi": hx(hi)}
+            case["znormalize_q0"] = hx(R.znormalize(q))
+        cases.append(case)
+    out = {"generator": "tests/golden/make_golden.py", "reference": "oracle/_ref/libtswarp_ref.so "
+           "(reference sources compiled with -O3 -DNDEBUG -ffp-contract=off)", "seed": SEED,
+           "cases": cases}
+    path = os.path.join(HERE, "reference_vectors.json")
+    with open(path, "w") as f:
+        json.dump(out, f, separators=(",", ":"))
+    print(f"wrote {path} ({os.path.getsize(path) / 1024:.0f} KiB, {len(cases)} cases)")
+
+
+if __name__ == "__main__":
+    main()
