@@ -8,11 +8,18 @@
 // indices (i' = L-1-i, j' = L-1-j) as a prefix DP over anti-diagonals a = i' + j'.
 //
 // Mapping: the band |i' - j'| <= r has offsets o = j' - i' in [-r, r], u = o + r in [0, 2r].
-// Lane p of a WL-lane group owns offsets u in [2Gp, 2Gp + 2G).  One loop iteration `it`
-// computes anti-diagonals 2it (even offsets) and 2it+1 (odd offsets); offset o then holds cell
-// (i', j') = (it - floor(o/2), it - floor(o/2) + o), so every lane computes G cells per step and
-// the only cross-lane traffic is one 64-bit shuffle per step.  With r + 1 <= 16 two pairs share
-// a warp (WL = 16).
+// Lane p of a WL-lane group owns offsets u in [2Gp, 2Gp + 2G).  Iteration `it` computes
+// anti-diagonals 2it (even offsets) and 2it+1 (odd offsets); offset o then holds cell
+// (i', j') = (it - floor(o/2), it - floor(o/2) + o).  Each lane computes G cells per step; the
+// only cross-lane traffic is one 64-bit shuffle per step.  With r + 1 <= 16 two pairs share a
+// warp (WL = 16).  Cells are branch-free (out-of-band cells read clamped data and are masked
+// to +inf), and cell (0,0) needs no special case: its diagonal predecessor register starts at
+// 0.0 and c + 0.0 == c.
+//
+// Point reuse (compile-time d): a lane's G+1 query points and G+1 candidate points slide by one
+// position per iteration, so each iteration loads ONE new query point and ONE new candidate
+// point into register windows, prefetched an iteration ahead.  The windows rotate through G+2
+// physical slots by unrolling the iteration loop G+2 times (no register moves).
 //
 // Early abandon (cut + cumulative lower bound, the UCR-suite idea on top of dtw.cpp:53-58):
 // every monotone path crosses anti-diagonal 2it or 2it+1; for a cut cell (i', j') the final
@@ -28,105 +35,167 @@ namespace tswb {
 
 namespace {
 
+constexpr unsigned kFull = 0xffffffffu;
+
 template <int D>
-__device__ __forceinline__ double point_cost(const double* __restrict__ sp,
-                                             const double* __restrict__ tp, uint32_t d) {
-    // detail::sq_dist (types.hpp:126-133): acc = 0.0; acc += (a_k - b_k)^2 for k ascending.
-    // (0.0 + x == x for the first term: squares are never -0.)
-    if (D > 0) {
-        double e = dsub(sp[0], tp[0]);
-        double acc = dmul(e, e);
+struct Pt {
+    double x[D];
+};
+
+template <int D>
+__device__ __forceinline__ void load_pt(Pt<D>& p, const double* __restrict__ base, int idx, int L) {
+    idx = min(max(idx, 0), L - 1);  // clamped: out-of-band cells read harmless data
+    const double* a = base + tidx((uint32_t)idx, 0, D);
 #pragma unroll
-        for (int k = 1; k < D; ++k) {
-            e = dsub(sp[k * kTile], tp[k * kTile]);
-            acc = dadd(acc, dmul(e, e));
+    for (int k = 0; k < D; ++k) p.x[k] = __ldg(a + k * kTile);
+}
+
+// detail::sq_dist (types.hpp:126-133): acc = 0.0; acc += (a_k - b_k)^2 for k ascending
+// (0.0 + x == x for the first term: squares are never -0).
+template <int D>
+__device__ __forceinline__ double cost(const Pt<D>& a, const Pt<D>& b) {
+    double e = dsub(a.x[0], b.x[0]);
+    double acc = dmul(e, e);
+#pragma unroll
+    for (int k = 1; k < D; ++k) {
+        e = dsub(a.x[k], b.x[k]);
+        acc = dadd(acc, dmul(e, e));
+    }
+    return acc;
+}
+
+__device__ __forceinline__ double cost_rt(const double* __restrict__ s, const double* __restrict__ t,
+                                          int si, int tj, int L, uint32_t d) {
+    si = min(max(si, 0), L - 1);
+    tj = min(max(tj, 0), L - 1);
+    const double* a = s + tidx((uint32_t)si, 0, d);
+    const double* b = t + tidx((uint32_t)tj, 0, d);
+    double acc = 0.0;
+    for (uint32_t k = 0; k < d; ++k) {
+        const double e = dsub(__ldg(a + k * kTile), __ldg(b + k * kTile));
+        acc = dadd(acc, dmul(e, e));
+    }
+    return acc;
+}
+
+// iterations per loop body: one per window phase (compile-time d), else 1
+template <int G, int D>
+struct Period {
+    static constexpr int value = D > 0 ? G + 2 : 1;
+};
+
+// Per-group pair state.
+template <int G, int D>
+struct PairState {
+    static constexpr int DD = D > 0 ? D : 1;
+    static constexpr int NS = D > 0 ? G + 2 : 1;
+    double v[2 * G];
+    int sb0;           // query window base index at it = 0 (original indexing)
+    int tb0;           // candidate window base index at it = 0
+    Pt<DD> S[NS];      // physical query-point slots
+    Pt<DD> T[NS];      // physical candidate-point slots
+};
+
+// One iteration `it` at compile-time phase PH (it % (G+2) == PH): anti-diagonals 2it, 2it+1.
+template <int G, int RPAR, int D, int WL, bool CHECK, int PH>
+__device__ __forceinline__ void dtw_iter(PairState<G, D>& ps, int it, int gl,
+                                         const int (&lo)[2 * G], const unsigned (&span)[2 * G],
+                                         int L, const double* __restrict__ s,
+                                         const double* __restrict__ t, uint32_t d,
+                                         const float* __restrict__ pfx, double Tm, bool& alive) {
+    constexpr int P = G + 2;
+    constexpr int DD = PairState<G, D>::DD;
+    if (D > 0) {  // prefetch the two new points of iteration it+1 into the free slots
+        load_pt<DD>(ps.S[((-(PH + 1)) % P + P) % P], s, ps.sb0 - (it + 1), L);
+        load_pt<DD>(ps.T[(G + 1 + PH) % P], t, ps.tb0 - (it + 1) - G, L);
+    }
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+        const int par = half == 0 ? RPAR : 1 - RPAR;
+        double nb;
+        if (par == 0) {
+            nb = __shfl_up_sync(kFull, ps.v[2 * G - 1], 1, WL);
+            if (gl == 0) nb = kInf;
+        } else {
+            nb = __shfl_down_sync(kFull, ps.v[0], 1, WL);
+            if (gl == WL - 1) nb = kInf;
         }
-        return acc;
-    } else {
-        double acc = 0.0;
-        for (uint32_t k = 0; k < d; ++k) {
-            const double e = dsub(sp[k * kTile], tp[k * kTile]);
-            acc = dadd(acc, dmul(e, e));
+#pragma unroll
+        for (int h = 0; h < G; ++h) {
+            const int e = par + 2 * h;
+            const int ss = (e + RPAR) >> 1;  // query window slot of this offset
+            const int tt = e - ss;           // candidate window slot
+            const bool valid = (unsigned)(it - lo[e]) <= span[e];
+            const double left = (e == 0) ? nb : ps.v[(e + 2 * G - 1) % (2 * G)];
+            const double down = (e == 2 * G - 1) ? nb : ps.v[(e + 1) % (2 * G)];
+            const double diag = ps.v[e];
+            double c;
+            if (D > 0) c = cost<DD>(ps.S[((ss - PH) % P + P) % P], ps.T[(tt + PH) % P]);
+            else c = cost_rt(s, t, ps.sb0 - it + ss, ps.tb0 - it - tt, L, d);
+            const double nv = dadd(c, dmin(dmin(left, down), diag));
+            ps.v[e] = valid ? nv : kInf;
+            if (CHECK) {
+                const int tj = min(max(ps.tb0 - it - tt, 0), L - 1);
+                alive |= valid && dadd(nv, (double)pfx[tj]) <= Tm;
+            }
         }
-        return acc;
     }
 }
 
-// Per-lane band geometry: offset o = obase + e of local slot e.  For small G the per-slot
-// values live in registers; for large G they are recomputed (register pressure).
-template <int G>
-struct Lane {
-    int obase, r2, L;
-    __device__ __forceinline__ int off(int e) const { return obase + e; }
-    __device__ __forceinline__ int hs(int e) const { return (obase + e) >> 1; }  // floor(o / 2)
-    // first valid iteration and hi - lo (unsigned compare trick); never-valid slots get lo
-    // beyond any iteration and span 0, so (unsigned)(it - lo) <= span never holds
-    __device__ __forceinline__ int lo(int e) const {
-        const int o = obase + e, h = o >> 1;
-        return valid_slot(e) ? max(h, h - o) : 0x3fffffff;
-    }
-    __device__ __forceinline__ unsigned span(int e) const {
-        const int o = obase + e, h = o >> 1;
-        const int lo_ = max(h, h - o), hi_ = L - 1 + min(h, h - o);
-        return valid_slot(e) ? (unsigned)(hi_ - lo_) : 0u;
-    }
-    __device__ __forceinline__ bool valid_slot(int e) const {
-        const int o = obase + e, h = o >> 1;
-        return o + r2 / 2 <= r2 && L - 1 + min(h, h - o) >= max(h, h - o);
-    }
-};
-
-// One anti-diagonal step over the offsets of parity PAR (e = PAR, PAR+2, ...).
-template <int G, int PAR, int D, int WL, bool CHECK>
-__device__ __forceinline__ void dtw_step(double (&v)[2 * G], const Lane<G>& ln, int it, int gl,
-                                         unsigned gmask, int L, const double* __restrict__ s,
+template <int G, int RPAR, int D, int WL, bool CHECK>
+__device__ __forceinline__ void dtw_body(PairState<G, D>& ps, int it, int gl,
+                                         const int (&lo)[2 * G], const unsigned (&span)[2 * G],
+                                         int L, const double* __restrict__ s,
                                          const double* __restrict__ t, uint32_t d,
-                                         const float* __restrict__ pfx, double Tm, bool& alive) {
-    double nb;
-    if (PAR == 0) {
-        nb = __shfl_up_sync(gmask, v[2 * G - 1], 1, WL);
-        if (gl == 0) nb = kInf;
-    } else {
-        nb = __shfl_down_sync(gmask, v[0], 1, WL);
-        if (gl == WL - 1) nb = kInf;
+                                         const float* __restrict__ pfx, double Tm, bool& alive,
+                                         double& fin, int estar) {
+    constexpr int P = Period<G, D>::value;
+    static_assert(P <= 6, "phase table covers G <= 4");
+    // P iterations, one per window phase; only the last one feeds the abandon check
+#define TSW_ITER(PH)                                                                         \
+    if constexpr (PH < P) {                                                                  \
+        dtw_iter<G, RPAR, D, WL, (CHECK && PH == P - 1), PH>(ps, it + PH, gl, lo, span, L, s, \
+                                                             t, d, pfx, Tm, alive);          \
+        if (it + PH == L - 1) {                                                              \
+            _Pragma("unroll") for (int e = 0; e < 2 * G; ++e) if (e == estar) fin = ps.v[e]; \
+        }                                                                                    \
     }
-    const int stride = D > 0 ? D : (int)d;
-#pragma unroll
-    for (int h = 0; h < G; ++h) {
-        const int e = PAR + 2 * h;
-        const bool valid = (unsigned)(it - ln.lo(e)) <= ln.span(e);
-        const double left = (e == 0) ? nb : v[(e + 2 * G - 1) % (2 * G)];
-        const double down = (e == 2 * G - 1) ? nb : v[(e + 1) % (2 * G)];
-        const double diag = v[e];
-        double nv = kInf;
-        if (valid) {
-            const int si = L - 1 - it + ln.hs(e);
-            const int tj = si - ln.off(e);
-            const double c = point_cost<D>(s + tidx((uint32_t)si, 0, stride), t + tidx((uint32_t)tj, 0, stride), d);
-            const double m = dmin(dmin(left, down), diag);
-            nv = (it == 0 && ln.off(e) == 0) ? c : dadd(c, m);
-            if (CHECK) alive |= dadd(nv, (double)pfx[tj]) <= Tm;
-        }
-        v[e] = nv;
-    }
+    TSW_ITER(0)
+    TSW_ITER(1)
+    TSW_ITER(2)
+    TSW_ITER(3)
+    TSW_ITER(4)
+    TSW_ITER(5)
+#undef TSW_ITER
 }
 
 template <int G, int RPAR, int D, int WL>
 __global__ void __launch_bounds__(256) dtw_dp_kernel(DpArgs a, uint32_t pstride) {
     extern __shared__ float smem_pfx[];
+    constexpr int P = Period<G, D>::value;
+    constexpr int DD = PairState<G, D>::DD;
     const int lane = threadIdx.x & 31;
     const int gl = lane % WL;
-    const unsigned gmask = WL == 32 ? 0xffffffffu : (0xffffu << (lane & 16));
+    const unsigned gmask = WL == 32 ? kFull : (0xffffu << (lane & 16));
     float* pfx = smem_pfx + (size_t)(threadIdx.x / WL) * pstride;
     const uint32_t d = a.store.d;
     const int L = (int)a.qlen;
     const int r = (int)min(a.r, a.qlen - 1);  // a band wider than the matrix is the full band
     const int stride = D > 0 ? D : (int)d;
 
-    Lane<G> ln;
-    ln.obase = 2 * G * gl - r;
-    ln.r2 = 2 * r;
-    ln.L = L;
+    // static per-lane band geometry: slot e holds offset o = obase + e
+    const int obase = 2 * G * gl - r;
+    int lo[2 * G];
+    unsigned span[2 * G];
+    bool slot_ok[2 * G];
+#pragma unroll
+    for (int e = 0; e < 2 * G; ++e) {
+        const int o = obase + e, h = o >> 1;  // floor(o / 2)
+        const int l = max(h, h - o), hi = L - 1 + min(h, h - o);
+        slot_ok[e] = o <= r && hi >= l;
+        lo[e] = slot_ok[e] ? l : 0x3fffffff;
+        span[e] = slot_ok[e] ? (unsigned)(hi - l) : 0u;
+    }
     const int pstar = r / (2 * G), estar = r % (2 * G);
 
     const unsigned nf = *a.queue.front, nb = *a.queue.back;
@@ -138,9 +207,13 @@ __global__ void __launch_bounds__(256) dtw_dp_kernel(DpArgs a, uint32_t pstride)
     QState* st = nullptr;
     double T = a.fixed_eps, Tm = kInf;
     int it = 0;
-    double v[2 * G];
+    double fin = kInf;
+    PairState<G, D> ps;
+#pragma unroll
+    for (int e = 0; e < 2 * G; ++e) ps.v[e] = kInf;
+    ps.sb0 = ps.tb0 = 0;
 
-    for (int wit = 0;; ++wit) {
+    for (int body = 0;; ++body) {
         // ---- groups without a pair fetch one (divergent per group) -------------------------
         if (!have && !done) {
             for (;;) {
@@ -175,8 +248,8 @@ __global__ void __launch_bounds__(256) dtw_dp_kernel(DpArgs a, uint32_t pstride)
                         float term = 0.0f;
                         if (j < L)
                             for (int k = 0; k < stride; ++k)
-                                term = lb_term_rd(term, x32[tidx(j, k, stride)],
-                                                  el[tidx(j, k, stride)], eh[tidx(j, k, stride)]);
+                                term = lb_term_rd(term, x32[tidx(j, k, stride)], el[tidx(j, k, stride)],
+                                                  eh[tidx(j, k, stride)]);
 #pragma unroll
                         for (int o = 1; o < WL; o <<= 1) {
                             const float y = __shfl_up_sync(gmask, term, o, WL);
@@ -190,68 +263,72 @@ __global__ void __launch_bounds__(256) dtw_dp_kernel(DpArgs a, uint32_t pstride)
                     for (int j = gl; j <= L; j += WL) pfx[j] = 0.0f;
                 }
                 __syncwarp(gmask);
+                // band registers; (0,0)'s diagonal predecessor is 0 so that v(0,0) = c + 0 = c
 #pragma unroll
-                for (int e = 0; e < 2 * G; ++e) v[e] = kInf;
+                for (int e = 0; e < 2 * G; ++e) ps.v[e] = (gl == pstar && e == estar) ? 0.0 : kInf;
+                ps.sb0 = L - 1 + (obase >> 1);
+                ps.tb0 = ps.sb0 - obase;
+                if (D > 0) {
+#pragma unroll
+                    for (int g = 0; g <= G && g < PairState<G, D>::NS; ++g) {
+                        load_pt<DD>(ps.S[g], s, ps.sb0 + g, L);  // phase 0: physical == logical
+                        load_pt<DD>(ps.T[g], t, ps.tb0 - g, L);
+                    }
+                }
                 it = 0;
+                fin = kInf;
                 have = true;
             }
         }
         __syncwarp();
-        if (!__any_sync(0xffffffffu, have)) break;
+        if (!__any_sync(kFull, have)) break;
 
-        // ---- one iteration: anti-diagonals 2it and 2it+1 ----------------------------------
-        const bool check = (wit & 3) == 3 || it == L - 1;
+        // ---- P iterations (phase-unrolled); abandon check on the last one ------------------
+        const bool check = P > 1 || (body & 3) == 3;
         bool alive = false;
         if (check) {
             if (st) {
                 T = ld_volatile(&st->T);
                 Tm = __dmul_ru(T, a.margin);
             }
-            dtw_step<G, RPAR, D, WL, true>(v, ln, it, gl, gmask, L, s, t, d, pfx, Tm, alive);
-            dtw_step<G, 1 - RPAR, D, WL, true>(v, ln, it, gl, gmask, L, s, t, d, pfx, Tm, alive);
+            dtw_body<G, RPAR, D, WL, true>(ps, it, gl, lo, span, L, s, t, d, pfx, Tm, alive, fin, estar);
         } else {
-            dtw_step<G, RPAR, D, WL, false>(v, ln, it, gl, gmask, L, s, t, d, pfx, Tm, alive);
-            dtw_step<G, 1 - RPAR, D, WL, false>(v, ln, it, gl, gmask, L, s, t, d, pfx, Tm, alive);
+            dtw_body<G, RPAR, D, WL, false>(ps, it, gl, lo, span, L, s, t, d, pfx, Tm, alive, fin, estar);
         }
-        ++it;
-        bool finished = false, exact = false;
-        double fin = kInf;
+        it += P;
+        bool finished = false;
         if (check) {
-            const unsigned bal = __ballot_sync(0xffffffffu, alive) & gmask;
-            if (have && bal == 0u) finished = true;  // abandoned on a dead cut
+            const unsigned bal = __ballot_sync(kFull, alive) & gmask;
+            if (have && it < L && bal == 0u) finished = true;  // abandoned on a dead cut
         }
-        if (have && !finished && it == L) {
-            finished = true;
-#pragma unroll
-            for (int e = 0; e < 2 * G; ++e)
-                if (e == estar) fin = v[e];
-        }
-        fin = __shfl_sync(0xffffffffu, fin, (lane - gl) + pstar);
+        const bool completed = have && it >= L;
+        if (completed) finished = true;
+        const double f = __shfl_sync(kFull, fin, (lane - gl) + pstar);
         if (have && finished) {
-            const int it_end = it;
+            const int it_end = min(it, L);
 #pragma unroll
             for (int e = 0; e < 2 * G; ++e) {
-                if (ln.valid_slot(e)) {
-                    const int c = min(it_end, ln.lo(e) + (int)ln.span(e) + 1) - ln.lo(e);
+                if (slot_ok[e]) {
+                    const int c = min(it_end, lo[e] + (int)span[e] + 1) - lo[e];
                     cells += c > 0 ? (unsigned long long)c : 0ull;
                 }
             }
             if (gl == 0) {
                 if (st) T = ld_volatile(&st->T);
-                exact = it_end == L && fin <= T;
+                const bool exact = completed && f <= T;
                 if (a.out_exact) {
                     a.out_exact[pr.c] = exact ? 1 : 0;
-                    a.out_val[pr.c] = exact ? fin : T;
+                    a.out_val[pr.c] = exact ? f : T;
                 }
                 if (exact) {
                     if (st) {
                         atomicAdd(&st->full_dp, 1ull);
-                        offer_exact(st, a.slots + (size_t)pr.q * kKMax, a.results, pr.q, fin, pr.c,
+                        offer_exact(st, a.slots + (size_t)pr.q * kKMax, a.results, pr.q, f, pr.c,
                                     false);
-                    } else if (a.results.dist) {  // fixed threshold (eps-NN): append only
+                    } else if (a.results.dist) {  // fixed threshold: append only
                         const unsigned pos = atomicAdd(a.results.count + pr.q, 1u);
                         if (pos < a.results.cap) {
-                            a.results.dist[(size_t)pr.q * a.results.cap + pos] = fin;
+                            a.results.dist[(size_t)pr.q * a.results.cap + pos] = f;
                             a.results.idx[(size_t)pr.q * a.results.cap + pos] = pr.c;
                         }
                     }
@@ -263,7 +340,7 @@ __global__ void __launch_bounds__(256) dtw_dp_kernel(DpArgs a, uint32_t pstride)
         }
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) cells += __shfl_xor_sync(0xffffffffu, cells, o);
+    for (int o = 16; o > 0; o >>= 1) cells += __shfl_xor_sync(kFull, cells, o);
     if (lane == 0 && a.cells) atomicAdd(a.cells, cells);
 }
 
@@ -289,8 +366,8 @@ void run_d(const DpArgs& a, uint32_t max_pairs, cudaStream_t st) {
         case 1: run<G, RPAR, 1, WL>(a, max_pairs, st); break;
         case 2: run<G, RPAR, 2, WL>(a, max_pairs, st); break;
         case 3: run<G, RPAR, 3, WL>(a, max_pairs, st); break;
-        case 16: run<G, RPAR, 16, WL>(a, max_pairs, st); break;
-        default: run<G, RPAR, 0, WL>(a, max_pairs, st); break;
+        case 4: run<G, RPAR, 4, WL>(a, max_pairs, st); break;
+        default: run<G, RPAR, 0, WL>(a, max_pairs, st); break;  // d > 4: direct loads
     }
 }
 
@@ -298,6 +375,13 @@ template <int G, int WL>
 void run_par(const DpArgs& a, uint32_t max_pairs, int rpar, cudaStream_t st) {
     if (rpar) run_d<G, 1, WL>(a, max_pairs, st);
     else run_d<G, 0, WL>(a, max_pairs, st);
+}
+
+// wide bands: runtime-d path only (no point windows), any G
+template <int G>
+void run_wide(const DpArgs& a, uint32_t max_pairs, int rpar, cudaStream_t st) {
+    if (rpar) run<G, 1, 0, 32>(a, max_pairs, st);
+    else run<G, 0, 0, 32>(a, max_pairs, st);
 }
 
 }  // namespace
@@ -310,9 +394,9 @@ void launch_dtw_dp(const DpArgs& a, uint32_t max_pairs, cudaStream_t st) {
     else if (need <= 32) run_par<1, 32>(a, max_pairs, rpar, st);
     else if (need <= 64) run_par<2, 32>(a, max_pairs, rpar, st);
     else if (need <= 128) run_par<4, 32>(a, max_pairs, rpar, st);
-    else if (need <= 256) run_par<8, 32>(a, max_pairs, rpar, st);
-    else if (need <= 512) run_par<16, 32>(a, max_pairs, rpar, st);
-    else run_par<32, 32>(a, max_pairs, rpar, st);
+    else if (need <= 256) run_wide<8>(a, max_pairs, rpar, st);
+    else if (need <= 512) run_wide<16>(a, max_pairs, rpar, st);
+    else run_wide<32>(a, max_pairs, rpar, st);
 }
 
 }  // namespace tswb
