@@ -169,8 +169,8 @@ __device__ __forceinline__ void dtw_body(PairState<G, D>& ps, int it, int gl,
 #undef TSW_ITER
 }
 
-template <int G, int RPAR, int D, int WL>
-__global__ void __launch_bounds__(256) dtw_dp_kernel(DpArgs a, uint32_t pstride) {
+template <int G, int RPAR, int D, int WL, int TPB, int MINB>
+__global__ void __launch_bounds__(TPB, MINB) dtw_dp_kernel(DpArgs a, uint32_t pstride) {
     extern __shared__ float smem_pfx[];
     constexpr int P = Period<G, D>::value;
     constexpr int DD = PairState<G, D>::DD;
@@ -236,28 +236,48 @@ __global__ void __launch_bounds__(256) dtw_dp_kernel(DpArgs a, uint32_t pstride)
             if (!done) {
                 s = a.queries + (uint64_t)pr.q * a.qstride;
                 t = a.store.data + series_off(a.store, pr.c);
-                // cumulative bound: pfx[m] = sum_{j < m} LB_Box term of candidate point j
+                // cumulative bound: pfx[m] = sum_{j < m} LB_Box term of candidate point j,
+                // 4 consecutive points per lane (float4 over the tiled layout; padding reads 0)
                 if (a.env_lo) {
                     const float* x32 = a.store.data32 + series_off(a.store, pr.c);
                     const float* el = a.env_lo + (uint64_t)pr.q * a.qstride;
                     const float* eh = a.env_hi + (uint64_t)pr.q * a.qstride;
                     float carry = 0.0f;
                     if (gl == 0) pfx[0] = 0.0f;
-                    for (int j0 = 0; j0 < L; j0 += WL) {
-                        const int j = j0 + gl;
-                        float term = 0.0f;
-                        if (j < L)
-                            for (int k = 0; k < stride; ++k)
-                                term = lb_term_rd(term, x32[tidx(j, k, stride)], el[tidx(j, k, stride)],
-                                                  eh[tidx(j, k, stride)]);
+                    for (int j0 = 0; j0 < L; j0 += 4 * WL) {
+                        const int p0 = j0 + 4 * gl;
+                        float t0 = 0.0f, t1 = 0.0f, t2 = 0.0f, t3 = 0.0f;
+                        if (p0 < L) {
+                            for (int k = 0; k < stride; ++k) {
+                                const uint64_t o = tidx((uint32_t)p0, (uint32_t)k, (uint32_t)stride);
+                                const float4 x = __ldg(reinterpret_cast<const float4*>(x32 + o));
+                                const float4 l = __ldg(reinterpret_cast<const float4*>(el + o));
+                                const float4 hh = __ldg(reinterpret_cast<const float4*>(eh + o));
+                                t0 = lb_term_rd(t0, x.x, l.x, hh.x);
+                                t1 = lb_term_rd(t1, x.y, l.y, hh.y);
+                                t2 = lb_term_rd(t2, x.z, l.z, hh.z);
+                                t3 = lb_term_rd(t3, x.w, l.w, hh.w);
+                            }
+                        }
+                        // local inclusive scan, then a group scan of the lane totals (RD adds
+                        // in any order keep every prefix a lower bound)
+                        t1 = __fadd_rd(t1, t0);
+                        t2 = __fadd_rd(t2, t1);
+                        t3 = __fadd_rd(t3, t2);
+                        float inc = t3;
 #pragma unroll
                         for (int o = 1; o < WL; o <<= 1) {
-                            const float y = __shfl_up_sync(gmask, term, o, WL);
-                            if (gl >= o) term = __fadd_rd(term, y);
+                            const float y = __shfl_up_sync(gmask, inc, o, WL);
+                            if (gl >= o) inc = __fadd_rd(inc, y);
                         }
-                        term = __fadd_rd(term, carry);
-                        if (j < L) pfx[j + 1] = term;
-                        carry = __shfl_sync(gmask, term, WL - 1, WL);
+                        float base = __shfl_up_sync(gmask, inc, 1, WL);
+                        if (gl == 0) base = 0.0f;
+                        base = __fadd_rd(base, carry);
+                        if (p0 + 1 <= L) pfx[p0 + 1] = __fadd_rd(base, t0);
+                        if (p0 + 2 <= L) pfx[p0 + 2] = __fadd_rd(base, t1);
+                        if (p0 + 3 <= L) pfx[p0 + 3] = __fadd_rd(base, t2);
+                        if (p0 + 4 <= L) pfx[p0 + 4] = __fadd_rd(base, t3);
+                        carry = __fadd_rd(carry, __shfl_sync(gmask, inc, WL - 1, WL));
                     }
                 } else {
                     for (int j = gl; j <= L; j += WL) pfx[j] = 0.0f;
@@ -346,10 +366,13 @@ __global__ void __launch_bounds__(256) dtw_dp_kernel(DpArgs a, uint32_t pstride)
 
 template <int G, int RPAR, int D, int WL>
 void run(const DpArgs& a, uint32_t max_pairs, cudaStream_t st) {
-    const int threads = 256;
+    // register-heavy instances (wide point windows) run 128-thread blocks
+    constexpr int TPB = (D >= 8 || G >= 4) ? 128 : 256;
+    constexpr int MINB = (D >= 8) ? 3 : (G >= 8 ? 1 : (G >= 2 ? 2 : 3));
+    const int threads = TPB;
     const uint32_t pstride = ((a.qlen + 1) + 3) & ~3u;
     const size_t smem = (size_t)(threads / WL) * pstride * sizeof(float);
-    auto kern = dtw_dp_kernel<G, RPAR, D, WL>;
+    auto kern = dtw_dp_kernel<G, RPAR, D, WL, TPB, MINB>;
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
@@ -367,7 +390,10 @@ void run_d(const DpArgs& a, uint32_t max_pairs, cudaStream_t st) {
         case 2: run<G, RPAR, 2, WL>(a, max_pairs, st); break;
         case 3: run<G, RPAR, 3, WL>(a, max_pairs, st); break;
         case 4: run<G, RPAR, 4, WL>(a, max_pairs, st); break;
-        default: run<G, RPAR, 0, WL>(a, max_pairs, st); break;  // d > 4: direct loads
+        case 16:
+            if constexpr (G == 1) { run<G, RPAR, 16, WL>(a, max_pairs, st); break; }
+            [[fallthrough]];
+        default: run<G, RPAR, 0, WL>(a, max_pairs, st); break;  // other d: direct loads
     }
 }
 
