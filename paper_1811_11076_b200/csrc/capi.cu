@@ -154,6 +154,7 @@ struct tsw_store {
     uint64_t n = 0, d = 0, ulen = 0, ustride = 0, max_len = 0;
     DevBuf<double> data;
     DevBuf<float> data32;
+    DevBuf<double> ends;
     DevBuf<uint64_t> off;
     DevBuf<uint32_t> len;
     std::vector<uint32_t> host_len;
@@ -165,6 +166,7 @@ struct tsw_store {
         StoreDev s{};
         s.data = data.p;
         s.data32 = data32.p;
+        s.ends = ends.p;
         s.off = off.p;
         s.len = len.p;
         s.n = (uint32_t)n;
@@ -283,9 +285,11 @@ std::unique_ptr<tsw_plan> make_plan(tsw_store* s, uint64_t nq_max, uint64_t qlen
     const uint64_t n = s->n;
     p->kk = std::min<uint64_t>(k, n);
     p->S = std::min<uint64_t>(n, 2048);
-    p->probe = p->kk <= (uint64_t)kKMax
-                   ? std::min<uint64_t>({p->S, (uint64_t)kKMax, std::max<uint64_t>(8, 2 * p->kk)})
-                   : 0;
+    // probe = the most promising sampled candidates, DP'd first to tighten the threshold.  DTW
+    // probes are cheap (banded, abandoning) and feed the LB compaction: 2k (>= 8).  A DK probe
+    // runs a near-full L^2 DP under the loose seed, so DK probes only k.
+    const uint64_t want_probe = metric == TSW_METRIC_DTW ? std::max<uint64_t>(8, 2 * p->kk) : p->kk;
+    p->probe = p->kk <= (uint64_t)kKMax ? std::min<uint64_t>({p->S, (uint64_t)kKMax, want_probe}) : 0;
     p->P = std::max<uint64_t>(1, std::min<uint64_t>(kKMax, std::max(p->kk, p->probe)));
     ck(cudaStreamCreateWithFlags(&p->own, cudaStreamNonBlocking), "cudaStreamCreate");
     for (auto& e : p->ev) ck(cudaEventCreate(&e), "cudaEventCreate");
@@ -664,6 +668,8 @@ int tsw_store_create(const double* values, const uint64_t* lengths, uint64_t uni
         // fp32 copy for the LB_Box pass + the rounding bound err32 >= max |x - fp32(x)|
         s->data32.alloc(elems);
         launch_to_float(s->data.p, elems, s->data32.p, 0);
+        s->ends.alloc(n * 2 * d);
+        launch_series_ends(s->dev(), s->ends.p, 0);
         DevBuf<double> mxb(1);
         launch_absmax(s->data.p, elems, mxb.p, 0);
         double xmax = 0.0;

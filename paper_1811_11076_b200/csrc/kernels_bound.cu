@@ -46,6 +46,24 @@ void launch_to_float(const double* src, uint64_t count, float* dst, cudaStream_t
     to_float_kernel<<<std::max(blocks, 1), 256, 0, st>>>(src, count, dst);
 }
 
+__global__ void series_ends_kernel(StoreDev s, double* __restrict__ ends) {
+    const uint64_t total = (uint64_t)s.n * 2 * s.d;
+    for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total;
+         g += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t c = (uint32_t)(g / (2 * s.d));
+        const uint32_t rem = (uint32_t)(g - (uint64_t)c * 2 * s.d);
+        const uint32_t which = rem / s.d, k = rem - which * s.d;
+        const uint32_t p = which ? series_len(s, c) - 1 : 0;
+        ends[g] = s.data[series_off(s, c) + tidx(p, k, s.d)];
+    }
+}
+
+void launch_series_ends(const StoreDev& s, double* ends, cudaStream_t st) {
+    const uint64_t total = (uint64_t)s.n * 2 * s.d;
+    const int blocks = (int)std::min<uint64_t>((total + 255) / 256, (uint64_t)sm_count() * 8);
+    series_ends_kernel<<<std::max(blocks, 1), 256, 0, st>>>(s, ends);
+}
+
 __global__ void absmax_kernel(const double* __restrict__ src, uint64_t n, unsigned long long* out) {
     double m = 0.0;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
@@ -300,13 +318,12 @@ __global__ void __launch_bounds__(256) dk_compact_kernel(DkCompactArgs a) {
             c = (uint32_t)(g - (uint64_t)q * n);
             if (!(a.probed && a.probed[g])) {
                 const double* s = a.queries + (uint64_t)q * a.qstride;
-                const double* t = a.store.data + series_off(a.store, c);
-                const uint32_t len = series_len(a.store, c);
+                const double* e = a.store.ends + (uint64_t)c * 2 * d;  // first, last point
                 double c0 = 0.0, c1 = 0.0;
                 for (uint32_t k = 0; k < d; ++k) {
-                    const double e0 = dsub(s[tidx(0, k, d)], t[tidx(0, k, d)]);
+                    const double e0 = dsub(s[tidx(0, k, d)], e[k]);
                     c0 = dadd(c0, dmul(e0, e0));
-                    const double e1 = dsub(s[tidx(m - 1, k, d)], t[tidx(len - 1, k, d)]);
+                    const double e1 = dsub(s[tidx(m - 1, k, d)], e[d + k]);
                     c1 = dadd(c1, dmul(e1, e1));
                 }
                 key = dmax(c0, c1);

@@ -16,6 +16,8 @@
 //    boundary row has no live cell right of lane 0 (a cut);
 //  * the pair is Exceeds as soon as a boundary row holds no live cell (the frontier died,
 //    dogkeeper.cpp:205-207), Exact iff the final cell is <= T.
+// Steps are branch-free: inactive lanes compute on clamped data and are masked to +inf; the
+// boundary row's live range is found by one cooperative scan per strip.
 #include <algorithm>
 
 #include "tsw_internal.cuh"
@@ -24,25 +26,22 @@ namespace tswb {
 
 namespace {
 
-template <int D>
-__device__ __forceinline__ void load_point(const double* __restrict__ p, double (&x)[D > 0 ? D : 1]) {
-    if (D > 0) {
-#pragma unroll
-        for (int k = 0; k < D; ++k) x[k] = __ldg(p + k * kTile);  // tiled layout: dims 32 apart
-    }
-}
+constexpr unsigned kFull = 0xffffffffu;
 
 template <int D>
-__device__ __forceinline__ double cost(const double (&sp)[D > 0 ? D : 1], const double* __restrict__ srow,
+struct Pt {
+    double x[D > 0 ? D : 1];
+};
+
+template <int D>
+__device__ __forceinline__ double cost(const Pt<D>& sp, const double* __restrict__ srow,
                                        const double* __restrict__ tp, uint32_t d) {
     if (D > 0) {
-        double tv[D > 0 ? D : 1];
-        load_point<D>(tp, tv);
-        double e = dsub(sp[0], tv[0]);
+        double e = dsub(sp.x[0], __ldg(tp));
         double acc = dmul(e, e);  // 0.0 + x == x (squares are never -0)
 #pragma unroll
-        for (int k = 1; k < D; ++k) {
-            e = dsub(sp[k], tv[k]);
+        for (int k = 1; k < (D > 0 ? D : 1); ++k) {
+            e = dsub(sp.x[k], __ldg(tp + k * kTile));
             acc = dadd(acc, dmul(e, e));
         }
         return acc;
@@ -61,46 +60,31 @@ struct Strip {
     bool write_bnd, first;
 };
 
-template <int D>
-__device__ __forceinline__ void dk_step(const Strip& S, int k, int lane, int m, int n,
-                                        const double (&sp)[D > 0 ? D : 1],
-                                        const double* __restrict__ srow,
+// One skewed step k: lane l computes cell (R + l, cstart + k - l).
+template <int D, bool LIVE>
+__device__ __forceinline__ void dk_step(const Strip& S, int k, int lane, int n,
+                                        const Pt<D>& sp, const double* __restrict__ srow,
                                         const double* __restrict__ t, uint32_t d,
                                         double* __restrict__ bnd, double Tsq, double& left,
-                                        double& mine, double& up_prev, double& fin, int& nb_first,
-                                        int& nb_last, int& nb_hi, bool& live,
-                                        unsigned long long& cells) {
+                                        double& mine, double& up_prev, bool& live) {
     const int stride = D > 0 ? D : (int)d;
     const int j = S.cstart + k - lane;
     const bool active = lane < S.rows && (unsigned)(k - lane) <= (unsigned)(n - 1 - S.cstart);
-    double up = __shfl_up_sync(0xffffffffu, mine, 1);
-    double dg = up_prev;
-    if (lane == 0) {
-        // boundary row (row R-1): written on [b_lo, b_hi] with b_lo <= cstart; dg = bnd[j-1]
-        // was this lane's `up` one step earlier (inf on the first step of a strip)
-        up = (!S.first && j <= S.b_hi) ? bnd[j] : kInf;
-    }
+    double up = __shfl_up_sync(kFull, mine, 1);
+    const double dg = up_prev;  // lane 0: bnd[j-1] from its previous step (inf at strip start)
+    const int jc = min(max(j, 0), n - 1);
+    // lane 0 reads the boundary row (row R-1), written on [b_lo, b_hi] with b_lo <= cstart
+    const double b = bnd[jc];
+    if (lane == 0) up = (!S.first && j <= S.b_hi) ? b : kInf;
     up_prev = up;
-    double v = kInf;
-    if (active) {
-        const double c = cost<D>(sp, srow, t + tidx((uint32_t)j, 0, stride), d);
-        double pred = dmin(dmin(left, up), dg);
-        if (S.first && lane == 0 && j == 0) pred = 0.0;  // virtual start (whole matching)
-        v = dmax(c, pred);
-        left = v;
-        ++cells;
-        if (S.R + lane == m - 1 && j == n - 1) fin = v;
-    }
+    const double c = cost<D>(sp, srow, t + tidx((uint32_t)jc, 0, (uint32_t)stride), d);
+    double pred = dmin(dmin(left, up), dg);
+    if (S.first && lane == 0 && j == 0) pred = 0.0;  // virtual start (whole matching)
+    const double v = active ? dmax(c, pred) : kInf;
+    left = active ? v : left;
     mine = v;
-    live = active && v <= Tsq;
-    if (S.write_bnd && lane == 31 && active) {
-        bnd[j] = v;  // in place: lane 0 has already consumed columns < j + 30
-        nb_hi = j;
-        if (live) {
-            if (nb_first < 0) nb_first = j;
-            nb_last = j;
-        }
-    }
+    if (S.write_bnd && lane == 31 && active) bnd[j] = v;  // in place: lane 0 is >= 30 columns ahead
+    if (LIVE) live = v <= Tsq;
 }
 
 template <int D>
@@ -116,7 +100,7 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
     for (;;) {
         unsigned slot = 0;
         if (lane == 0) slot = atomicAdd(a.queue.head, 1u);
-        slot = __shfl_sync(0xffffffffu, slot, 0);
+        slot = __shfl_sync(kFull, slot, 0);
         QEntry pr;
         if (!queue_get(a.queue, nf, nbk, slot, pr)) break;
         QState* st = a.state ? a.state + pr.q : nullptr;
@@ -141,44 +125,60 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
             S.first = R == 0;
             S.write_bnd = R + 32 < m;
             S.cstart = b_alive_lo;
-            const double* srow = s + tidx((uint32_t)min(R + lane, m - 1), 0, stride);
-            double sp[D > 0 ? D : 1];
-            if (D > 0) load_point<D>(srow, sp);
+            const double* srow = s + tidx((uint32_t)min(R + lane, m - 1), 0, (uint32_t)stride);
+            Pt<D> sp;
+            if (D > 0) {
+#pragma unroll
+                for (int k = 0; k < (D > 0 ? D : 1); ++k) sp.x[k] = __ldg(srow + k * kTile);
+            }
             double left = kInf, mine = kInf, up_prev = kInf;
-            int nb_first = -1, nb_last = -1, nb_hi = S.cstart - 1;
             const int kmax = (n - 1 - S.cstart) + S.rows - 1;
-            bool l0, l1, l2, l3;
+            bool l2 = false, l3 = false, dummy = false;
+            int k_done = -1;
             for (int k = 0; k <= kmax; k += 4) {
-                dk_step<D>(S, k, lane, m, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, fin,
-                           nb_first, nb_last, nb_hi, l0, cells);
-                dk_step<D>(S, k + 1, lane, m, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, fin,
-                           nb_first, nb_last, nb_hi, l1, cells);
-                dk_step<D>(S, k + 2, lane, m, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, fin,
-                           nb_first, nb_last, nb_hi, l2, cells);
-                dk_step<D>(S, k + 3, lane, m, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, fin,
-                           nb_first, nb_last, nb_hi, l3, cells);
+                dk_step<D, false>(S, k, lane, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, dummy);
+                dk_step<D, false>(S, k + 1, lane, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, dummy);
+                dk_step<D, true>(S, k + 2, lane, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, l2);
+                dk_step<D, true>(S, k + 3, lane, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, l3);
+                k_done = k + 3;
                 // dead cut: no live cell on steps k+2, k+3 and nothing live ahead of lane 0
-                if (!__any_sync(0xffffffffu, l2 || l3) && S.cstart + k + 3 > S.b_alive_hi) break;
+                if (!__any_sync(kFull, l2 || l3) && S.cstart + k + 3 > S.b_alive_hi) break;
                 if (st && (k & 60) == 60) Tsq = ld_volatile(&st->Tsq);
             }
-            (void)l0;
-            (void)l1;
+            const int k_last = min(k_done, kmax);  // last step whose cells were computed
+            if (lane < S.rows) {  // cells computed by this lane in this strip
+                const int c = min(k_last - lane, n - 1 - S.cstart) + 1;
+                cells += c > 0 ? (unsigned long long)c : 0ull;
+            }
             if (S.write_bnd) {
                 __syncwarp();
-                nb_first = __shfl_sync(0xffffffffu, nb_first, 31);
-                nb_last = __shfl_sync(0xffffffffu, nb_last, 31);
-                nb_hi = __shfl_sync(0xffffffffu, nb_hi, 31);
-                if (nb_first < 0) {
+                // next boundary row = lane 31's row, written on [cstart, min(n-1, cstart+k_last-31)]
+                const int hi = min(n - 1, S.cstart + k_last - 31);
+                int first = -1, last = -1;
+                for (int j0 = S.cstart; j0 <= hi; j0 += 32) {
+                    const int j = j0 + lane;
+                    const bool lv = j <= hi && bnd[j] <= Tsq;
+                    const unsigned bm = __ballot_sync(kFull, lv);
+                    if (bm) {
+                        if (first < 0) first = j0 + __ffs(bm) - 1;
+                        last = j0 + 31 - __clz(bm);
+                    }
+                }
+                __syncwarp();
+                if (first < 0) {
                     dead = true;
                     break;
                 }
-                S.b_hi = nb_hi;
-                b_alive_lo = nb_first;
-                S.b_alive_hi = nb_last;
+                S.b_hi = hi;
+                b_alive_lo = first;
+                S.b_alive_hi = last;
+            } else {
+                // final strip: the lane of row m-1 (the last row lane) ends on column n-1 iff the
+                // sweep reached kmax
+                const double lv = __shfl_sync(kFull, left, (m - 1) & 31);
+                if (k_last >= kmax) fin = lv;
             }
         }
-        // final cell lives in the lane of row m-1
-        fin = __shfl_sync(0xffffffffu, fin, (m - 1) & 31);
         if (lane == 0) {
             if (st) Tsq = ld_volatile(&st->Tsq);
             const bool exact = !dead && fin <= Tsq;
@@ -190,8 +190,7 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
             if (exact) {
                 if (st) {
                     atomicAdd(&st->full_dp, 1ull);
-                    offer_exact(st, a.slots + (size_t)pr.q * kKMax, a.results, pr.q, dist, pr.c,
-                                true);
+                    offer_exact(st, a.slots + (size_t)pr.q * kKMax, a.results, pr.q, dist, pr.c, true);
                 } else if (a.results.dist) {  // fixed threshold (eps-NN): append only
                     const unsigned pos = atomicAdd(a.results.count + pr.q, 1u);
                     if (pos < a.results.cap) {
@@ -206,7 +205,7 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
         __syncwarp();
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) cells += __shfl_xor_sync(0xffffffffu, cells, o);
+    for (int o = 16; o > 0; o >>= 1) cells += __shfl_xor_sync(kFull, cells, o);
     if (lane == 0 && a.cells) atomicAdd(a.cells, cells);
 }
 

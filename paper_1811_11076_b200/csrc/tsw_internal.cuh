@@ -34,6 +34,7 @@ __host__ __device__ inline uint64_t tiled_stride(uint64_t len, uint64_t d) {
 struct StoreDev {
     const double* data;
     const float* data32;
+    const double* ends;   // [n][2][d]: first and last point of every series (DK cell bounds)
     const uint64_t* off;  // per-series offset in doubles (ragged stores); nullptr if uniform
     const uint32_t* len;  // per-series length (ragged); nullptr if uniform
     uint32_t n, d;
@@ -187,6 +188,8 @@ void launch_envelope64(const double* q, uint32_t nq, uint32_t d, uint32_t len, u
 // row-major [nser][len][d] -> tiled [nser][stride] (zero padding)
 void launch_rowmajor_to_tiled(const double* src, uint64_t nser, uint32_t len, uint32_t d,
                               uint64_t stride, double* dst, cudaStream_t st);
+// ends[c] = (first point, last point) of every series of a store
+void launch_series_ends(const StoreDev& s, double* ends, cudaStream_t st);
 void launch_to_float(const double* src, uint64_t count, float* dst, cudaStream_t st);
 void launch_absmax(const double* src, uint64_t count, double* out, cudaStream_t st);
 
