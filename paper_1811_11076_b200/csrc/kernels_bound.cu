@@ -147,7 +147,8 @@ __global__ void __launch_bounds__(256) sample_ub_kernel(SampleArgs a) {
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const uint32_t d = a.store.d, m = a.qlen;
     for (uint64_t w = wid; w < (uint64_t)a.nq * a.S; w += nw) {
-        const uint32_t q = (uint32_t)(w / a.S), j = (uint32_t)(w - (uint64_t)q * a.S);
+        // candidate-major: adjacent warps share a sampled candidate (L1 reuse across queries)
+        const uint32_t j = (uint32_t)(w / a.nq), q = (uint32_t)(w - (uint64_t)j * a.nq);
         const uint32_t c = (uint32_t)((uint64_t)j * a.store.n / a.S);
         const double* s = a.queries + (uint64_t)q * a.qstride;
         const double* t = a.store.data + series_off(a.store, c);
@@ -168,7 +169,7 @@ __global__ void __launch_bounds__(256) sample_ub_kernel(SampleArgs a) {
             const double v = __shfl_xor_sync(0xffffffffu, acc, o);
             acc = a.dk ? dmax(acc, v) : dadd(acc, v);
         }
-        if (lane == 0) a.out_ub[w] = a.dk ? acc : __dmul_ru(acc, a.ub_scale);
+        if (lane == 0) a.out_ub[(uint64_t)q * a.S + j] = a.dk ? acc : __dmul_ru(acc, a.ub_scale);
     }
 }
 
@@ -203,7 +204,7 @@ __device__ __forceinline__ void enqueue(const WorkQueue& w, bool take, bool near
 // Tile = CB consecutive candidates x QB queries per warp; after the warp reduction lane
 // j = qb * CB + cb owns pair (q0 + qb, c0 + cb).
 template <int QB, int CB>
-__global__ void __launch_bounds__(256) lb_compact_kernel(LbCompactArgs a) {
+__global__ void __launch_bounds__(256, 2) lb_compact_kernel(LbCompactArgs a) {
     static_assert(QB * CB == 32, "one pair per lane after the reduction");
     const unsigned lane = lane_id();
     const uint32_t n = a.store.n;
@@ -219,19 +220,14 @@ __global__ void __launch_bounds__(256) lb_compact_kernel(LbCompactArgs a) {
         const uint32_t qbk = (uint32_t)(w - cg * nqb);
         const uint32_t c0 = (uint32_t)cg * CB;
         const uint32_t q0 = qbk * QB;
-        const float4* x4[CB];
-#pragma unroll
-        for (int cb = 0; cb < CB; ++cb)
-            x4[cb] = reinterpret_cast<const float4*>(a.store.data32 +
-                                                     (uint64_t)min(c0 + cb, n - 1) * a.store.ustride);
-        const float4* lo4[QB];
-        const float4* hi4[QB];
-#pragma unroll
-        for (int qb = 0; qb < QB; ++qb) {
-            const uint64_t qo = (uint64_t)min(q0 + qb, a.nq - 1) * a.qstride;
-            lo4[qb] = reinterpret_cast<const float4*>(a.env_lo + qo);
-            hi4[qb] = reinterpret_cast<const float4*>(a.env_hi + qo);
-        }
+        // base pointers only (per-query / per-candidate offsets are recomputed: register budget)
+        const float4* xb = reinterpret_cast<const float4*>(a.store.data32) +
+                           (uint64_t)c0 * (a.store.ustride / 4);
+        const uint64_t xs = a.store.ustride / 4;
+        const float4* lob = reinterpret_cast<const float4*>(a.env_lo) + (uint64_t)q0 * (a.qstride / 4);
+        const float4* hib = reinterpret_cast<const float4*>(a.env_hi) + (uint64_t)q0 * (a.qstride / 4);
+        const uint64_t qs = a.qstride / 4;
+        const uint32_t cmax = n - 1 - c0, qmax = a.nq - 1 - q0;  // clamp tails to valid rows
         float acc[QB][CB];
 #pragma unroll
         for (int qb = 0; qb < QB; ++qb)
@@ -240,19 +236,20 @@ __global__ void __launch_bounds__(256) lb_compact_kernel(LbCompactArgs a) {
         for (uint32_t f = lane; f < total4; f += 32) {
             float4 x[CB];
 #pragma unroll
-            for (int cb = 0; cb < CB; ++cb) x[cb] = __ldg(x4[cb] + f);
+            for (int cb = 0; cb < CB; ++cb) x[cb] = __ldg(xb + (uint64_t)min((uint32_t)cb, cmax) * xs + f);
 #pragma unroll
             for (int qb = 0; qb < QB; ++qb) {
-                const float4 l = __ldg(lo4[qb] + f);
-                const float4 h = __ldg(hi4[qb] + f);
+                const uint64_t qo = (uint64_t)min((uint32_t)qb, qmax) * qs + f;
+                const float4 l = __ldg(lob + qo);
+                const float4 h = __ldg(hib + qo);
 #pragma unroll
                 for (int cb = 0; cb < CB; ++cb) {
-                    float s = acc[qb][cb];
-                    s = lb_term_rd(s, x[cb].x, l.x, h.x);
-                    s = lb_term_rd(s, x[cb].y, l.y, h.y);
-                    s = lb_term_rd(s, x[cb].z, l.z, h.z);
-                    s = lb_term_rd(s, x[cb].w, l.w, h.w);
-                    acc[qb][cb] = s;
+                    float sacc = acc[qb][cb];
+                    sacc = lb_term_rd(sacc, x[cb].x, l.x, h.x);
+                    sacc = lb_term_rd(sacc, x[cb].y, l.y, h.y);
+                    sacc = lb_term_rd(sacc, x[cb].z, l.z, h.z);
+                    sacc = lb_term_rd(sacc, x[cb].w, l.w, h.w);
+                    acc[qb][cb] = sacc;
                 }
             }
         }
