@@ -147,8 +147,7 @@ __global__ void __launch_bounds__(256) sample_ub_kernel(SampleArgs a) {
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const uint32_t d = a.store.d, m = a.qlen;
     for (uint64_t w = wid; w < (uint64_t)a.nq * a.S; w += nw) {
-        // candidate-major: adjacent warps share a sampled candidate (L1 reuse across queries)
-        const uint32_t j = (uint32_t)(w / a.nq), q = (uint32_t)(w - (uint64_t)j * a.nq);
+        const uint32_t q = (uint32_t)(w / a.S), j = (uint32_t)(w - (uint64_t)q * a.S);
         const uint32_t c = (uint32_t)((uint64_t)j * a.store.n / a.S);
         const double* s = a.queries + (uint64_t)q * a.qstride;
         const double* t = a.store.data + series_off(a.store, c);

@@ -97,9 +97,10 @@ struct PairState {
 };
 
 // One iteration `it` at compile-time phase PH (it % (G+2) == PH): anti-diagonals 2it, 2it+1.
-template <int G, int RPAR, int D, int WL, bool CHECK, int PH>
+template <int G, int RPAR, int D, int WL, bool CHECK, bool FULL, int PH>
 __device__ __forceinline__ void dtw_iter(PairState<G, D>& ps, int it, int gl,
                                          const int (&lo)[2 * G], const unsigned (&span)[2 * G],
+                                         const bool (&slot_ok)[2 * G],
                                          int L, const double* __restrict__ s,
                                          const double* __restrict__ t, uint32_t d,
                                          const float* __restrict__ pfx, double Tm, bool& alive) {
@@ -125,7 +126,9 @@ __device__ __forceinline__ void dtw_iter(PairState<G, D>& ps, int it, int gl,
             const int e = par + 2 * h;
             const int ss = (e + RPAR) >> 1;  // query window slot of this offset
             const int tt = e - ss;           // candidate window slot
-            const bool valid = (unsigned)(it - lo[e]) <= span[e];
+            // FULL: the whole body lies inside every valid slot's range (interior of the band):
+            // validity is the per-lane constant slot_ok
+            const bool valid = FULL ? slot_ok[e] : (unsigned)(it - lo[e]) <= span[e];
             const double left = (e == 0) ? nb : ps.v[(e + 2 * G - 1) % (2 * G)];
             const double down = (e == 2 * G - 1) ? nb : ps.v[(e + 1) % (2 * G)];
             const double diag = ps.v[e];
@@ -142,9 +145,10 @@ __device__ __forceinline__ void dtw_iter(PairState<G, D>& ps, int it, int gl,
     }
 }
 
-template <int G, int RPAR, int D, int WL, bool CHECK>
+template <int G, int RPAR, int D, int WL, bool CHECK, bool FULL>
 __device__ __forceinline__ void dtw_body(PairState<G, D>& ps, int it, int gl,
                                          const int (&lo)[2 * G], const unsigned (&span)[2 * G],
+                                         const bool (&slot_ok)[2 * G],
                                          int L, const double* __restrict__ s,
                                          const double* __restrict__ t, uint32_t d,
                                          const float* __restrict__ pfx, double Tm, bool& alive,
@@ -154,8 +158,9 @@ __device__ __forceinline__ void dtw_body(PairState<G, D>& ps, int it, int gl,
     // P iterations, one per window phase; only the last one feeds the abandon check
 #define TSW_ITER(PH)                                                                         \
     if constexpr (PH < P) {                                                                  \
-        dtw_iter<G, RPAR, D, WL, (CHECK && PH == P - 1), PH>(ps, it + PH, gl, lo, span, L, s, \
-                                                             t, d, pfx, Tm, alive);          \
+        dtw_iter<G, RPAR, D, WL, (CHECK && PH == P - 1), FULL, PH>(ps, it + PH, gl, lo, span,  \
+                                                             slot_ok, L, s, t, d, pfx, Tm,   \
+                                                             alive);                         \
         if (it + PH == L - 1) {                                                              \
             _Pragma("unroll") for (int e = 0; e < 2 * G; ++e) if (e == estar) fin = ps.v[e]; \
         }                                                                                    \
@@ -197,6 +202,19 @@ __global__ void __launch_bounds__(TPB, MINB) dtw_dp_kernel(DpArgs a, uint32_t ps
         span[e] = slot_ok[e] ? (unsigned)(hi - l) : 0u;
     }
     const int pstar = r / (2 * G), estar = r % (2 * G);
+    // iterations in which every valid slot of the warp is inside its band range
+    int full_lo = 0, full_hi = 0x3fffffff;
+#pragma unroll
+    for (int e = 0; e < 2 * G; ++e)
+        if (slot_ok[e]) {
+            full_lo = max(full_lo, lo[e]);
+            full_hi = min(full_hi, lo[e] + (int)span[e]);
+        }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        full_lo = max(full_lo, __shfl_xor_sync(kFull, full_lo, o));
+        full_hi = min(full_hi, __shfl_xor_sync(kFull, full_hi, o));
+    }
 
     const unsigned nf = *a.queue.front, nb = *a.queue.back;
     unsigned long long cells = 0;
@@ -305,15 +323,23 @@ __global__ void __launch_bounds__(TPB, MINB) dtw_dp_kernel(DpArgs a, uint32_t ps
 
         // ---- P iterations (phase-unrolled); abandon check on the last one ------------------
         const bool check = P > 1 || (body & 3) == 3;
+        // warp-uniform: both groups' next P iterations lie in the band interior
+        const bool full = __all_sync(kFull, !have || (it >= full_lo && it + P - 1 <= full_hi));
         bool alive = false;
         if (check) {
             if (st) {
                 T = ld_volatile(&st->T);
                 Tm = __dmul_ru(T, a.margin);
             }
-            dtw_body<G, RPAR, D, WL, true>(ps, it, gl, lo, span, L, s, t, d, pfx, Tm, alive, fin, estar);
+            if (full)
+                dtw_body<G, RPAR, D, WL, true, true>(ps, it, gl, lo, span, slot_ok, L, s, t, d, pfx, Tm, alive, fin, estar);
+            else
+                dtw_body<G, RPAR, D, WL, true, false>(ps, it, gl, lo, span, slot_ok, L, s, t, d, pfx, Tm, alive, fin, estar);
         } else {
-            dtw_body<G, RPAR, D, WL, false>(ps, it, gl, lo, span, L, s, t, d, pfx, Tm, alive, fin, estar);
+            if (full)
+                dtw_body<G, RPAR, D, WL, false, true>(ps, it, gl, lo, span, slot_ok, L, s, t, d, pfx, Tm, alive, fin, estar);
+            else
+                dtw_body<G, RPAR, D, WL, false, false>(ps, it, gl, lo, span, slot_ok, L, s, t, d, pfx, Tm, alive, fin, estar);
         }
         it += P;
         bool finished = false;
