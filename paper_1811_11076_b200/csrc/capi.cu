@@ -408,7 +408,10 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
     se.dk = dk;
     se.state = p->state.p;
     se.slots = p->slots.p;
-    se.probe_q = p->probe_wq();
+    // DTW: probes run first in their own launch (they tighten T before the LB compaction).
+    // DK: the compaction bound does not depend much on T, so the probes are simply placed at
+    // the front of the main queue (no GPU-starved separate launch of a few hundred warps).
+    se.probe_q = dk ? p->main_wq() : p->probe_wq();
     se.probed = p->probed.p;
     launch_seed(se, st);
     ++launches;
@@ -433,7 +436,7 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
         else launch_dtw_dp(da, max_pairs, st);
         ++launches;
     };
-    if (p->probe) run_dp(p->probe_wq(), nq * (uint32_t)p->probe);
+    if (p->probe && !dk) run_dp(p->probe_wq(), nq * (uint32_t)p->probe);
     mark(3);
     if (!dk) {
         LbCompactArgs la{};

@@ -1,6 +1,6 @@
 // K5: dog-keeper (discrete Frechet) DP with threshold pruning -- one warp per (query,
-// candidate) pair, 32-row strips (lane = query row), skewed column sweep, strip-boundary row
-// in shared memory.
+// candidate) pair, 64-row strips (lane l owns query rows R+2l, R+2l+1), skewed column sweep,
+// strip-boundary row in shared memory.
 //
 // Exactness: DK cell = max(dist(i, j), min(preds)) (dk_full, dogkeeper.cpp:19-43).  max / min
 // are exact, so any traversal gives identical values, and because correctly rounded sqrt is
@@ -16,8 +16,9 @@
 //    boundary row has no live cell right of lane 0 (a cut);
 //  * the pair is Exceeds as soon as a boundary row holds no live cell (the frontier died,
 //    dogkeeper.cpp:205-207), Exact iff the final cell is <= T.
-// Steps are branch-free: inactive lanes compute on clamped data and are masked to +inf; the
-// boundary row's live range is found by one cooperative scan per strip.
+// Steps are branch-free: inactive cells compute on clamped data and are masked to +inf.  Each
+// lane computes RPL = 2 rows per step, so one candidate-point load, one shuffle and the loop
+// overhead are shared by two cells.
 #include <algorithm>
 
 #include "tsw_internal.cuh"
@@ -27,6 +28,8 @@ namespace tswb {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
+constexpr int RPL = 2;               // query rows per lane
+constexpr int kStrip = 32 * RPL;     // rows per strip
 
 template <int D>
 struct Pt {
@@ -34,57 +37,72 @@ struct Pt {
 };
 
 template <int D>
-__device__ __forceinline__ double cost(const Pt<D>& sp, const double* __restrict__ srow,
-                                       const double* __restrict__ tp, uint32_t d) {
-    if (D > 0) {
-        double e = dsub(sp.x[0], __ldg(tp));
-        double acc = dmul(e, e);  // 0.0 + x == x (squares are never -0)
+__device__ __forceinline__ double cost(const Pt<D>& sp, const Pt<D>& tp) {
+    double e = dsub(sp.x[0], tp.x[0]);
+    double acc = dmul(e, e);  // 0.0 + x == x (squares are never -0)
 #pragma unroll
-        for (int k = 1; k < (D > 0 ? D : 1); ++k) {
-            e = dsub(sp.x[k], __ldg(tp + k * kTile));
-            acc = dadd(acc, dmul(e, e));
-        }
-        return acc;
-    } else {
-        double acc = 0.0;
-        for (uint32_t k = 0; k < d; ++k) {
-            const double e = dsub(__ldg(srow + k * kTile), __ldg(tp + k * kTile));
-            acc = dadd(acc, dmul(e, e));
-        }
-        return acc;
+    for (int k = 1; k < (D > 0 ? D : 1); ++k) {
+        e = dsub(sp.x[k], tp.x[k]);
+        acc = dadd(acc, dmul(e, e));
     }
+    return acc;
+}
+
+__device__ __forceinline__ double cost_rt(const double* __restrict__ srow,
+                                          const double* __restrict__ tp, uint32_t d) {
+    double acc = 0.0;
+    for (uint32_t k = 0; k < d; ++k) {
+        const double e = dsub(__ldg(srow + k * kTile), __ldg(tp + k * kTile));
+        acc = dadd(acc, dmul(e, e));
+    }
+    return acc;
 }
 
 struct Strip {
-    int R, rows, cstart, b_hi, b_alive_hi;
+    int R, cstart, b_hi, b_alive_hi;
+    int nrows;  // rows of this strip (<= kStrip)
     bool write_bnd, first;
 };
 
-// One skewed step k: lane l computes cell (R + l, cstart + k - l).
+// One skewed step k: lane l computes cells (R + RPL*l + q, cstart + k - l), q < RPL.
 template <int D, bool LIVE>
 __device__ __forceinline__ void dk_step(const Strip& S, int k, int lane, int n,
-                                        const Pt<D>& sp, const double* __restrict__ srow,
+                                        const Pt<D> (&sp)[RPL], const double* const (&srow)[RPL],
                                         const double* __restrict__ t, uint32_t d,
-                                        double* __restrict__ bnd, double Tsq, double& left,
-                                        double& mine, double& up_prev, bool& live) {
+                                        double* __restrict__ bnd, double Tsq,
+                                        double (&left)[RPL], double& mine, double& up_prev,
+                                        bool& live) {
     const int stride = D > 0 ? D : (int)d;
     const int j = S.cstart + k - lane;
-    const bool active = lane < S.rows && (unsigned)(k - lane) <= (unsigned)(n - 1 - S.cstart);
-    double up = __shfl_up_sync(kFull, mine, 1);
-    const double dg = up_prev;  // lane 0: bnd[j-1] from its previous step (inf at strip start)
+    const bool colok = (unsigned)(k - lane) <= (unsigned)(n - 1 - S.cstart);
+    double up = __shfl_up_sync(kFull, mine, 1);  // lane l-1's last row at column j
+    double dg = up_prev;                          // ... at column j-1 (previous step)
     const int jc = min(max(j, 0), n - 1);
-    // lane 0 reads the boundary row (row R-1), written on [b_lo, b_hi] with b_lo <= cstart
-    const double b = bnd[jc];
+    const double b = bnd[jc];  // boundary row (row R-1); only lane 0 uses it
     if (lane == 0) up = (!S.first && j <= S.b_hi) ? b : kInf;
     up_prev = up;
-    const double c = cost<D>(sp, srow, t + tidx((uint32_t)jc, 0, (uint32_t)stride), d);
-    double pred = dmin(dmin(left, up), dg);
-    if (S.first && lane == 0 && j == 0) pred = 0.0;  // virtual start (whole matching)
-    const double v = active ? dmax(c, pred) : kInf;
-    left = active ? v : left;
-    mine = v;
-    if (S.write_bnd && lane == 31 && active) bnd[j] = v;  // in place: lane 0 is >= 30 columns ahead
-    if (LIVE) live = v <= Tsq;
+    const double* tp = t + tidx((uint32_t)jc, 0, (uint32_t)stride);
+    Pt<D> tv;
+    if (D > 0) {
+#pragma unroll
+        for (int kk = 0; kk < (D > 0 ? D : 1); ++kk) tv.x[kk] = __ldg(tp + kk * kTile);
+    }
+    bool lv = false;
+#pragma unroll
+    for (int q = 0; q < RPL; ++q) {
+        const bool active = colok && RPL * lane + q < S.nrows;
+        const double c = D > 0 ? cost<D>(sp[q], tv) : cost_rt(srow[q], tp, d);
+        double pred = dmin(dmin(left[q], up), dg);
+        if (q == 0 && S.first && lane == 0 && j == 0) pred = 0.0;  // virtual start (whole match)
+        const double v = active ? dmax(c, pred) : kInf;
+        dg = left[q];           // next row's diagonal: this row at column j-1
+        left[q] = active ? v : left[q];
+        up = v;                 // next row's up: this row at column j
+        if (LIVE) lv |= v <= Tsq;
+    }
+    mine = up;  // last row of this lane (inf when inactive)
+    if (S.write_bnd && lane == 31 && colok) bnd[j] = mine;  // in place: lane 0 is >= 30 columns ahead
+    if (LIVE) live = lv;
 }
 
 template <int D>
@@ -119,20 +137,28 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
         int b_alive_lo = 0;
         bool dead = false;
         double fin = kInf;
-        for (int R = 0; R < m; R += 32) {
+        for (int R = 0; R < m; R += kStrip) {
             S.R = R;
-            S.rows = min(32, m - R);
+            S.nrows = min(kStrip, m - R);
             S.first = R == 0;
-            S.write_bnd = R + 32 < m;
+            S.write_bnd = R + kStrip < m;
             S.cstart = b_alive_lo;
-            const double* srow = s + tidx((uint32_t)min(R + lane, m - 1), 0, (uint32_t)stride);
-            Pt<D> sp;
-            if (D > 0) {
+            Pt<D> sp[RPL];
+            const double* srow[RPL];
 #pragma unroll
-                for (int k = 0; k < (D > 0 ? D : 1); ++k) sp.x[k] = __ldg(srow + k * kTile);
+            for (int q = 0; q < RPL; ++q) {
+                srow[q] = s + tidx((uint32_t)min(R + RPL * lane + q, m - 1), 0, (uint32_t)stride);
+                if (D > 0) {
+#pragma unroll
+                    for (int kk = 0; kk < (D > 0 ? D : 1); ++kk) sp[q].x[kk] = __ldg(srow[q] + kk * kTile);
+                }
             }
-            double left = kInf, mine = kInf, up_prev = kInf;
-            const int kmax = (n - 1 - S.cstart) + S.rows - 1;
+            double left[RPL];
+#pragma unroll
+            for (int q = 0; q < RPL; ++q) left[q] = kInf;
+            double mine = kInf, up_prev = kInf;
+            const int last_lane = (S.nrows - 1) / RPL;
+            const int kmax = (n - 1 - S.cstart) + last_lane;
             bool l2 = false, l3 = false, dummy = false;
             int k_done = -1;
             for (int k = 0; k <= kmax; k += 4) {
@@ -146,13 +172,14 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
                 if (st && (k & 60) == 60) Tsq = ld_volatile(&st->Tsq);
             }
             const int k_last = min(k_done, kmax);  // last step whose cells were computed
-            if (lane < S.rows) {  // cells computed by this lane in this strip
+            {   // cells computed by this lane in this strip (analytic count)
+                const int rows = min(RPL, max(0, S.nrows - RPL * lane));
                 const int c = min(k_last - lane, n - 1 - S.cstart) + 1;
-                cells += c > 0 ? (unsigned long long)c : 0ull;
+                cells += (c > 0 ? (unsigned long long)c : 0ull) * (unsigned long long)rows;
             }
             if (S.write_bnd) {
                 __syncwarp();
-                // next boundary row = lane 31's row, written on [cstart, min(n-1, cstart+k_last-31)]
+                // next boundary row = lane 31's last row, written on [cstart, min(n-1, cstart+k_last-31)]
                 const int hi = min(n - 1, S.cstart + k_last - 31);
                 int first = -1, last = -1;
                 for (int j0 = S.cstart; j0 <= hi; j0 += 32) {
@@ -173,9 +200,13 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
                 b_alive_lo = first;
                 S.b_alive_hi = last;
             } else {
-                // final strip: the lane of row m-1 (the last row lane) ends on column n-1 iff the
-                // sweep reached kmax
-                const double lv = __shfl_sync(kFull, left, (m - 1) & 31);
+                // final strip: the lane holding row m-1 ends on column n-1 iff the sweep reached kmax
+                const int fl = (m - 1 - R) / RPL, fq = (m - 1 - R) % RPL;
+                double mv = kInf;
+#pragma unroll
+                for (int q = 0; q < RPL; ++q)
+                    if (q == fq) mv = left[q];
+                const double lv = __shfl_sync(kFull, mv, fl);
                 if (k_last >= kmax) fin = lv;
             }
         }

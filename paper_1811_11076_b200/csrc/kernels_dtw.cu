@@ -324,20 +324,21 @@ __global__ void __launch_bounds__(TPB, MINB) dtw_dp_kernel(DpArgs a, uint32_t ps
         // ---- P iterations (phase-unrolled); abandon check on the last one ------------------
         const bool check = P > 1 || (body & 3) == 3;
         // warp-uniform: both groups' next P iterations lie in the band interior
-        const bool full = __all_sync(kFull, !have || (it >= full_lo && it + P - 1 <= full_hi));
+        // (G == 1 keeps a single body: the extra variant costs more registers than it saves)
+        const bool full = G >= 2 && __all_sync(kFull, !have || (it >= full_lo && it + P - 1 <= full_hi));
         bool alive = false;
         if (check) {
             if (st) {
                 T = ld_volatile(&st->T);
                 Tm = __dmul_ru(T, a.margin);
             }
-            if (full)
-                dtw_body<G, RPAR, D, WL, true, true>(ps, it, gl, lo, span, slot_ok, L, s, t, d, pfx, Tm, alive, fin, estar);
+            if (G >= 2 && full)
+                dtw_body<G, RPAR, D, WL, true, (G >= 2)>(ps, it, gl, lo, span, slot_ok, L, s, t, d, pfx, Tm, alive, fin, estar);
             else
                 dtw_body<G, RPAR, D, WL, true, false>(ps, it, gl, lo, span, slot_ok, L, s, t, d, pfx, Tm, alive, fin, estar);
         } else {
-            if (full)
-                dtw_body<G, RPAR, D, WL, false, true>(ps, it, gl, lo, span, slot_ok, L, s, t, d, pfx, Tm, alive, fin, estar);
+            if (G >= 2 && full)
+                dtw_body<G, RPAR, D, WL, false, (G >= 2)>(ps, it, gl, lo, span, slot_ok, L, s, t, d, pfx, Tm, alive, fin, estar);
             else
                 dtw_body<G, RPAR, D, WL, false, false>(ps, it, gl, lo, span, slot_ok, L, s, t, d, pfx, Tm, alive, fin, estar);
         }
