@@ -408,10 +408,12 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
     se.dk = dk;
     se.state = p->state.p;
     se.slots = p->slots.p;
-    // DTW: probes run first in their own launch (they tighten T before the LB compaction).
-    // DK: the compaction bound does not depend much on T, so the probes are simply placed at
-    // the front of the main queue (no GPU-starved separate launch of a few hundred warps).
-    se.probe_q = dk ? p->main_wq() : p->probe_wq();
+    // Probes run first in their own launch so that they tighten T before the compaction.  For
+    // DK a probe is a near-full L^2 DP under the loose seed; when there are too few of them to
+    // fill the GPU (nq * probe < 4 warps per SM) they are instead placed at the front of the
+    // main queue, overlapping with the bulk of the work.
+    const bool sep_probe = !dk || (uint64_t)nq * p->probe >= 4ull * (uint64_t)sm_count();
+    se.probe_q = sep_probe ? p->probe_wq() : p->main_wq();
     se.probed = p->probed.p;
     launch_seed(se, st);
     ++launches;
@@ -436,7 +438,7 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
         else launch_dtw_dp(da, max_pairs, st);
         ++launches;
     };
-    if (p->probe && !dk) run_dp(p->probe_wq(), nq * (uint32_t)p->probe);
+    if (p->probe && sep_probe) run_dp(p->probe_wq(), nq * (uint32_t)p->probe);
     mark(3);
     if (!dk) {
         LbCompactArgs la{};
