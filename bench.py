@@ -251,6 +251,7 @@ def main():
     k, r = sh["k"], sh["r"]
     store = t.Store(db, device=dev)
     plan = t.Plan(store, nq, L, metric, r, k)
+    plan.set_graph(True)  # the async pipeline runs as one captured CUDA graph
     # a dedicated (non-default) stream: the library launches on exactly this stream, so the
     # CUDA events below bracket its kernels (handle 0 would mean the plan's own stream)
     stream = torch.cuda.Stream()

@@ -122,6 +122,9 @@ int tsw_plan_set_queries_device(tsw_plan* plan, const double* dev_queries, uint6
 int tsw_plan_execute(tsw_plan* plan, void* stream);
 /* device -> host results of the last execute; synchronises `stream`. */
 int tsw_plan_fetch(tsw_plan* plan, tsw_neighbor* out, tsw_counters* counters, void* stream);
+/* capture the pipeline into a CUDA graph on the first execute (re-captured when the query
+ * count or stream changes); later executes are one graph launch.  Ignored while timing. */
+int tsw_plan_set_graph(tsw_plan* plan, int enable);
 /* enable per-phase CUDA-event timing (adds event records between kernels). */
 int tsw_plan_set_timing(tsw_plan* plan, int enable);
 int tsw_plan_stats(tsw_plan* plan, tsw_stats* stats);

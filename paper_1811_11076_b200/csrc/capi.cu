@@ -205,10 +205,17 @@ struct tsw_plan {
     HostBuf<unsigned> h_res_n;
     double margin = 1.0, ub_scale = 1.0, near_frac = 0.5;
     bool timing = false;
+    bool use_graph = false;
+    bool graph_warm = false;
+    cudaGraphExec_t graph = nullptr;  // captured pipeline for (graph_nq, graph_stream)
+    uint64_t graph_nq = 0;
+    cudaStream_t graph_stream = nullptr;
+    int graph_launches = 0;
     cudaEvent_t ev[8] = {};
     int launches = 0;
     bool executed = false;
     ~tsw_plan() {
+        if (graph) cudaGraphExecDestroy(graph);
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
         if (own) cudaStreamDestroy(own);
@@ -475,7 +482,9 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
                                p->fin_sv.p, p->fin_si.p, p->top_d.p, p->top_i.p, st, &launches);
     }
     mark(5);
-    ck(cudaEventRecord(p->ev[7], st), "cudaEventRecord");
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(st, &cap);
+    if (cap == cudaStreamCaptureStatusNone) ck(cudaEventRecord(p->ev[7], st), "cudaEventRecord");
     ck(cudaGetLastError(), "kernel launch");
     p->launches = launches;
     p->executed = true;
@@ -740,7 +749,45 @@ int tsw_plan_execute(tsw_plan* p, void* stream) {
     return guard([&] {
         if (!p) fail(TSW_EINVAL, "null plan");
         DeviceGuard dg(p->store->device);
-        execute_impl(p, pick(p, stream));
+        cudaStream_t st = pick(p, stream);
+        if (!p->use_graph || p->timing || std::getenv("TSW_DEBUG_SYNC") || !p->graph_warm) {
+            execute_impl(p, st);  // the first execution also runs the one-time kernel setup
+            p->graph_warm = true;
+            return;
+        }
+        // CUDA graph of the whole (host-sync-free) pipeline, re-captured when the query count
+        // or the stream changes: one launch instead of ~10 per execution
+        if (!p->graph || p->graph_nq != p->nq || p->graph_stream != st) {
+            if (p->graph) {
+                cudaGraphExecDestroy(p->graph);
+                p->graph = nullptr;
+            }
+            cudaGraph_t g = nullptr;
+            ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "graph capture");
+            try {
+                execute_impl(p, st);
+            } catch (...) {
+                cudaStreamEndCapture(st, &g);
+                if (g) cudaGraphDestroy(g);
+                throw;
+            }
+            ck(cudaStreamEndCapture(st, &g), "graph capture");
+            ck(cudaGraphInstantiate(&p->graph, g, 0), "graph instantiate");
+            cudaGraphDestroy(g);
+            p->graph_nq = p->nq;
+            p->graph_stream = st;
+            p->graph_launches = p->launches;
+        }
+        ck(cudaGraphLaunch(p->graph, st), "graph launch");
+        p->launches = p->graph_launches;
+        p->executed = true;
+    });
+}
+
+int tsw_plan_set_graph(tsw_plan* p, int enable) {
+    return guard([&] {
+        if (!p) fail(TSW_EINVAL, "null plan");
+        p->use_graph = enable != 0;
     });
 }
 

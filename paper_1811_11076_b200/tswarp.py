@@ -96,6 +96,7 @@ def lib():
     L.tsw_plan_execute.argtypes = [_vp, _vp]
     L.tsw_plan_fetch.argtypes = [_vp, C.POINTER(Neighbor_t), C.POINTER(Counters_t), _vp]
     L.tsw_plan_set_timing.argtypes = [_vp, C.c_int]
+    L.tsw_plan_set_graph.argtypes = [_vp, C.c_int]
     L.tsw_plan_stats.argtypes = [_vp, C.POINTER(Stats_t)]
     L.tsw_envelope.argtypes = [_dp, _u64, _u64, _u64, _dp, _dp]
     L.tsw_lb_box_all.argtypes = [_vp, _dp, _u64, _u64, _dp, _dp]
@@ -425,6 +426,10 @@ class Plan:
         c = np.frombuffer(ctr, dtype=np.uint64, count=self.nq * 5).reshape(self.nq, 5).copy()
         return (raw["index"].reshape(self.nq, self.kk).copy(),
                 raw["distance"].reshape(self.nq, self.kk).copy(), c)
+
+    def set_graph(self, on: bool):
+        """Run executions as one captured CUDA graph (re-captured on shape/stream change)."""
+        _check(lib().tsw_plan_set_graph(self._h, 1 if on else 0))
 
     def set_timing(self, on: bool):
         _check(lib().tsw_plan_set_timing(self._h, 1 if on else 0))

@@ -267,3 +267,20 @@ def test_plan_reuse_and_device_queries(tsw, best_oracle):
     for q in range(6):
         oi, od, _ = best_oracle.knn(Q[q], oracle.Dataset(X), 3, "dtw", 6)
         assert_knn_equal(a[0][q], a[1][q], oi, od)
+
+
+def test_plan_cuda_graph_matches_eager(tsw):
+    X = walks(RNG, 700, 64, 3)
+    Q = walks(RNG, 9, 64, 3)
+    for metric in ("dtw", "dk"):
+        eager = tsw.Plan(tsw.Dataset(X), 9, 64, metric, 6, 4)
+        eager.set_queries(Q)
+        eager.execute()
+        a = eager.fetch()
+        g = tsw.Plan(tsw.Dataset(X), 9, 64, metric, 6, 4)
+        g.set_graph(True)
+        for _ in range(3):  # warm execute, capture, replay
+            g.set_queries(Q)
+            g.execute()
+            b = g.fetch()
+            assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]) and np.array_equal(a[2], b[2])
