@@ -227,6 +227,17 @@ __global__ void __launch_bounds__(TPB, MINB) dtw_dp_kernel(DpArgs a, uint32_t ps
     int it = 0;
     double fin = kInf;
     PairState<G, D> ps;
+    // one-pair-ahead prefetch of the work queue
+    QEntry nx{0, 0, 0.0};
+    bool nx_ok;
+    double nxT;
+    {
+        unsigned slot = 0;
+        if (gl == 0) slot = atomicAdd(a.queue.head, 1u);
+        slot = __shfl_sync(gmask, slot, 0, WL);
+        nx_ok = queue_get(a.queue, nf, nb, slot, nx);
+        nxT = (nx_ok && a.state) ? ld_volatile(&a.state[nx.q].T) : a.fixed_eps;
+    }
 #pragma unroll
     for (int e = 0; e < 2 * G; ++e) ps.v[e] = kInf;
     ps.sb0 = ps.tb0 = 0;
@@ -235,15 +246,22 @@ __global__ void __launch_bounds__(TPB, MINB) dtw_dp_kernel(DpArgs a, uint32_t ps
         // ---- groups without a pair fetch one (divergent per group) -------------------------
         if (!have && !done) {
             for (;;) {
-                unsigned slot = 0;
-                if (gl == 0) slot = atomicAdd(a.queue.head, 1u);
-                slot = __shfl_sync(gmask, slot, 0, WL);
-                if (!queue_get(a.queue, nf, nb, slot, pr)) {
+                // consume the prefetched entry (slot, entry and its query's threshold were
+                // loaded one pair ahead; a stale threshold is still a valid, larger one)
+                if (!nx_ok) {
                     done = true;
                     break;
                 }
+                pr = nx;
                 st = a.state ? a.state + pr.q : nullptr;
-                T = st ? ld_volatile(&st->T) : a.fixed_eps;
+                T = nxT;
+                {   // prefetch the next one
+                    unsigned slot = 0;
+                    if (gl == 0) slot = atomicAdd(a.queue.head, 1u);
+                    slot = __shfl_sync(gmask, slot, 0, WL);
+                    nx_ok = queue_get(a.queue, nf, nb, slot, nx);
+                    nxT = (nx_ok && a.state) ? ld_volatile(&a.state[nx.q].T) : a.fixed_eps;
+                }
                 Tm = __dmul_ru(T, a.margin);
                 if (!(pr.key <= Tm)) {  // re-check the admitting lower bound at dequeue
                     if (gl == 0 && st) atomicAdd(&st->lb_pruned, 1ull);
