@@ -78,17 +78,24 @@ __device__ __forceinline__ double cost_rt(const double* __restrict__ s, const do
     return acc;
 }
 
+// Point windows prefetch one iteration ahead for small d (G+2 slots); for large d the extra
+// slot costs more registers than the latency it hides, so the new points are loaded at the top
+// of the iteration into the slot just freed (G+1 slots).
+template <int D>
+struct Prefetch {
+    static constexpr bool value = D > 0 && D <= 4;
+};
 // iterations per loop body: one per window phase (compile-time d), else 1
 template <int G, int D>
 struct Period {
-    static constexpr int value = D > 0 ? G + 2 : 1;
+    static constexpr int value = D > 0 ? (Prefetch<D>::value ? G + 2 : G + 1) : 1;
 };
 
 // Per-group pair state.
 template <int G, int D>
 struct PairState {
     static constexpr int DD = D > 0 ? D : 1;
-    static constexpr int NS = D > 0 ? G + 2 : 1;
+    static constexpr int NS = D > 0 ? (Prefetch<D>::value ? G + 2 : G + 1) : 1;
     double v[2 * G];
     int sb0;           // query window base index at it = 0 (original indexing)
     int tb0;           // candidate window base index at it = 0
@@ -104,11 +111,14 @@ __device__ __forceinline__ void dtw_iter(PairState<G, D>& ps, int it, int gl,
                                          int L, const double* __restrict__ s,
                                          const double* __restrict__ t, uint32_t d,
                                          const float* __restrict__ pfx, double Tm, bool& alive) {
-    constexpr int P = G + 2;
+    constexpr int P = Period<G, D>::value;
     constexpr int DD = PairState<G, D>::DD;
-    if (D > 0) {  // prefetch the two new points of iteration it+1 into the free slots
+    if (D > 0 && Prefetch<D>::value) {  // prefetch the two new points of it+1 into the free slots
         load_pt<DD>(ps.S[((-(PH + 1)) % P + P) % P], s, ps.sb0 - (it + 1), L);
         load_pt<DD>(ps.T[(G + 1 + PH) % P], t, ps.tb0 - (it + 1) - G, L);
+    } else if (D > 0) {  // load this iteration's two new points into the slots just freed
+        load_pt<DD>(ps.S[((-PH) % P + P) % P], s, ps.sb0 - it, L);
+        load_pt<DD>(ps.T[(G + PH) % P], t, ps.tb0 - it - G, L);
     }
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
@@ -227,17 +237,6 @@ __global__ void __launch_bounds__(TPB, MINB) dtw_dp_kernel(DpArgs a, uint32_t ps
     int it = 0;
     double fin = kInf;
     PairState<G, D> ps;
-    // one-pair-ahead prefetch of the work queue
-    QEntry nx{0, 0, 0.0};
-    bool nx_ok;
-    double nxT;
-    {
-        unsigned slot = 0;
-        if (gl == 0) slot = atomicAdd(a.queue.head, 1u);
-        slot = __shfl_sync(gmask, slot, 0, WL);
-        nx_ok = queue_get(a.queue, nf, nb, slot, nx);
-        nxT = (nx_ok && a.state) ? ld_volatile(&a.state[nx.q].T) : a.fixed_eps;
-    }
 #pragma unroll
     for (int e = 0; e < 2 * G; ++e) ps.v[e] = kInf;
     ps.sb0 = ps.tb0 = 0;
@@ -246,22 +245,15 @@ __global__ void __launch_bounds__(TPB, MINB) dtw_dp_kernel(DpArgs a, uint32_t ps
         // ---- groups without a pair fetch one (divergent per group) -------------------------
         if (!have && !done) {
             for (;;) {
-                // consume the prefetched entry (slot, entry and its query's threshold were
-                // loaded one pair ahead; a stale threshold is still a valid, larger one)
-                if (!nx_ok) {
+                unsigned slot = 0;
+                if (gl == 0) slot = atomicAdd(a.queue.head, 1u);
+                slot = __shfl_sync(gmask, slot, 0, WL);
+                if (!queue_get(a.queue, nf, nb, slot, pr)) {
                     done = true;
                     break;
                 }
-                pr = nx;
                 st = a.state ? a.state + pr.q : nullptr;
-                T = nxT;
-                {   // prefetch the next one
-                    unsigned slot = 0;
-                    if (gl == 0) slot = atomicAdd(a.queue.head, 1u);
-                    slot = __shfl_sync(gmask, slot, 0, WL);
-                    nx_ok = queue_get(a.queue, nf, nb, slot, nx);
-                    nxT = (nx_ok && a.state) ? ld_volatile(&a.state[nx.q].T) : a.fixed_eps;
-                }
+                T = st ? ld_volatile(&st->T) : a.fixed_eps;
                 Tm = __dmul_ru(T, a.margin);
                 if (!(pr.key <= Tm)) {  // re-check the admitting lower bound at dequeue
                     if (gl == 0 && st) atomicAdd(&st->lb_pruned, 1ull);
@@ -413,7 +405,7 @@ template <int G, int RPAR, int D, int WL>
 void run(const DpArgs& a, uint32_t max_pairs, cudaStream_t st) {
     // register-heavy instances (wide point windows) run 128-thread blocks
     constexpr int TPB = (D >= 8 || G >= 4) ? 128 : 256;
-    constexpr int MINB = (D >= 8) ? 3 : (G >= 8 ? 1 : (G >= 2 ? 2 : 3));
+    constexpr int MINB = (D >= 8) ? 4 : (G >= 8 ? 1 : (G >= 2 ? 2 : 3));
     const int threads = TPB;
     const uint32_t pstride = ((a.qlen + 1) + 3) & ~3u;
     const size_t smem = (size_t)(threads / WL) * pstride * sizeof(float);
