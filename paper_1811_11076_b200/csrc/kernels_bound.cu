@@ -203,7 +203,7 @@ __device__ __forceinline__ void enqueue(const WorkQueue& w, bool take, bool near
 // Tile = CB consecutive candidates x QB queries per warp; after the warp reduction lane
 // j = qb * CB + cb owns pair (q0 + qb, c0 + cb).
 template <int QB, int CB>
-__global__ void __launch_bounds__(256, 2) lb_compact_kernel(LbCompactArgs a) {
+__global__ void __launch_bounds__(256, 3) lb_compact_kernel(LbCompactArgs a) {
     static_assert(QB * CB == 32, "one pair per lane after the reduction");
     const unsigned lane = lane_id();
     const uint32_t n = a.store.n;
