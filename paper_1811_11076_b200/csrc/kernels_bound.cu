@@ -83,8 +83,9 @@ void launch_absmax(const double* src, uint64_t count, double* out, cudaStream_t 
 
 // ---- K1: per-dimension windowed min / max over [i-r, i+r] clamped (envelope.cpp:25-59) ------
 // One thread per (query, point, dim).  Min / max are exact, so the direct window scan equals
-// the reference's monotonic-deque result; it is then rounded outward to fp32 and widened by
-// `err` (>= |x - fp32(x)| over the store) so fp32 terms bound the fp64 ones from below.
+// the reference's monotonic-deque result.  The fp32 pipeline form stores (midpoint m,
+// half-width h) with h >= max(m - lo, hi - m) + err rounded up (err >= |x - fp32(x)| over the
+// store), so the fp32 terms bound the fp64 ones from below.
 template <typename OutT>
 __global__ void envelope_kernel(const double* __restrict__ q, uint32_t nq, uint32_t d,
                                 uint32_t len, uint64_t qstride, uint32_t r, float err,
@@ -111,8 +112,12 @@ __global__ void envelope_kernel(const double* __restrict__ q, uint32_t nq, uint3
             mx = v > mx ? v : mx;
         }
         if constexpr (sizeof(OutT) == sizeof(float)) {
-            lo[g] = __fsub_rd(__double2float_rd(mn), err);
-            hi[g] = __fadd_ru(__double2float_ru(mx), err);
+            // fp32 (midpoint, half-width) form: any midpoint m works as long as the half-width
+            // covers the interval from m, rounded up, plus the store's fp32 rounding err
+            const float m32 = __double2float_rn(0.5 * (mn + mx));
+            const double hw = fmax(__dsub_ru((double)m32, mn), __dsub_ru(mx, (double)m32));
+            lo[g] = m32;
+            hi[g] = __fadd_ru(__double2float_ru(hw), err);
         } else {
             lo[g] = mn;
             hi[g] = mx;
@@ -203,7 +208,7 @@ __device__ __forceinline__ void enqueue(const WorkQueue& w, bool take, bool near
 // Tile = CB consecutive candidates x QB queries per warp; after the warp reduction lane
 // j = qb * CB + cb owns pair (q0 + qb, c0 + cb).
 template <int QB, int CB>
-__global__ void __launch_bounds__(256, 3) lb_compact_kernel(LbCompactArgs a) {
+__global__ void __launch_bounds__(256, 2) lb_compact_kernel(LbCompactArgs a) {
     static_assert(QB * CB == 32, "one pair per lane after the reduction");
     const unsigned lane = lane_id();
     const uint32_t n = a.store.n;

@@ -6,8 +6,9 @@
 // 2 cache lines per load, and the d dimensions of a point sit at immediate offsets 32k.
 //   store   : series c at data + off(c); a float copy `data32` (round-to-nearest, same layout)
 //             feeds the fp32 LB_Box lower bound.
-//   queries : [nq][qstride] doubles, same layout; envelope lo/hi: [nq][qstride] floats,
-//             directed-rounded so that fp32 LB terms are rigorous lower bounds.
+//   queries : [nq][qstride] doubles, same layout; envelope: [nq][qstride] floats of midpoints
+//             (env_lo) and outward-rounded half-widths (env_hi), so that fp32 LB terms are
+//             rigorous lower bounds.
 // All fp64 arithmetic uses separate mul / add (built with -fmad=false) so that every cell cost
 // is bit-identical to detail::sq_dist (types.hpp:126-133).
 #pragma once
@@ -135,10 +136,11 @@ __device__ __forceinline__ bool pair_less(double a, uint32_t ia, double b, uint3
     return a < b || (a == b && ia < ib);
 }
 
-// fp32 lower-bound LB_Box term of one element against a directed-rounded envelope:
-// returns acc + max(lo - x, x - hi, 0)^2 rounded down, a rigorous lower bound.
-__device__ __forceinline__ float lb_term_rd(float acc, float x, float lo, float hi) {
-    const float e = fmaxf(fmaxf(__fsub_rd(lo, x), __fsub_rd(x, hi)), 0.0f);
+// fp32 lower-bound LB_Box term of one element against the (midpoint m, half-width h) envelope
+// (DESIGN §4.2): acc + max(|x - m| - h, 0)^2 with RZ / RD rounding, a rigorous lower bound of
+// acc + dist(x, [lo, hi])^2.  4 FP32 instructions (|.| is an operand modifier).
+__device__ __forceinline__ float lb_term_rd(float acc, float x, float m, float h) {
+    const float e = fmaxf(__fsub_rd(fabsf(__fsub_rz(x, m)), h), 0.0f);
     return __fmaf_rd(e, e, acc);
 }
 
