@@ -313,10 +313,13 @@ __global__ void __launch_bounds__(256) lb_queue_kernel(LbQueueArgs a) {
         bool take = false, near = false, pruned = false;
         double key = 0.0;
         if (in) {
-            q = (uint32_t)(g / a.n);
-            c = (uint32_t)(g - (uint64_t)q * a.n);
-            if (!(a.probed && a.probed[g])) {
-                key = (double)a.lb[g];
+            // candidate-major: the queries of one candidate enter the work queue together, so
+            // the DP warps that take them share the candidate's bytes in L1/L2
+            c = (uint32_t)(g / a.nq);
+            q = (uint32_t)(g - (uint64_t)c * a.nq);
+            const uint64_t gi = (uint64_t)q * a.n + c;
+            if (!(a.probed && a.probed[gi])) {
+                key = (double)a.lb[gi];
                 const double T = a.state[q].T;
                 take = key <= __dmul_ru(T, a.margin);
                 near = key <= a.near_frac * T;
@@ -355,9 +358,9 @@ __global__ void __launch_bounds__(256) dk_compact_kernel(DkCompactArgs a) {
         bool take = false, near = false, pruned = false;
         double key = 0.0;
         if (in) {
-            q = (uint32_t)(g / n);
-            c = (uint32_t)(g - (uint64_t)q * n);
-            if (!(a.probed && a.probed[g])) {
+            c = (uint32_t)(g / a.nq);  // candidate-major (cache reuse in the DP, see lb_queue)
+            q = (uint32_t)(g - (uint64_t)c * a.nq);
+            if (!(a.probed && a.probed[(uint64_t)q * n + c])) {
                 const double* s = a.queries + (uint64_t)q * a.qstride;
                 const double* e = a.store.ends + (uint64_t)c * 2 * d;  // first, last point
                 double c0 = 0.0, c1 = 0.0;
