@@ -187,9 +187,6 @@ struct tsw_plan {
     int metric = 0;
     uint64_t nq = 0;  // queries of the last set_queries
     cudaStream_t own = nullptr;
-    cudaStream_t aux = nullptr;              // K2 runs here, overlapping the seed/probe chain
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_lb[2] = {nullptr, nullptr};
-    DevBuf<float> lbv;                       // [nq_max][n] fp32 LB values (DTW)
     DevBuf<double> q, q_rm, ub, sel_sv, sel_v, slots, top_d;
     DevBuf<float> env_lo, env_hi;
     DevBuf<uint32_t> sel_si, sel_i, top_i, fin_si;
@@ -219,9 +216,6 @@ struct tsw_plan {
     bool executed = false;
     ~tsw_plan() {
         if (graph) cudaGraphExecDestroy(graph);
-        for (cudaEvent_t e : {ev_fork, ev_join, ev_lb[0], ev_lb[1]})
-            if (e) cudaEventDestroy(e);
-        if (aux) cudaStreamDestroy(aux);
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
         if (own) cudaStreamDestroy(own);
@@ -306,17 +300,11 @@ std::unique_ptr<tsw_plan> make_plan(tsw_store* s, uint64_t nq_max, uint64_t qlen
     p->P = std::max<uint64_t>(1, std::min<uint64_t>(kKMax, std::max(p->kk, p->probe)));
     ck(cudaStreamCreateWithFlags(&p->own, cudaStreamNonBlocking), "cudaStreamCreate");
     for (auto& e : p->ev) ck(cudaEventCreate(&e), "cudaEventCreate");
-    ck(cudaStreamCreateWithFlags(&p->aux, cudaStreamNonBlocking), "cudaStreamCreate");
-    ck(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming), "cudaEventCreate");
-    ck(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming), "cudaEventCreate");
-    ck(cudaEventCreate(&p->ev_lb[0]), "cudaEventCreate");
-    ck(cudaEventCreate(&p->ev_lb[1]), "cudaEventCreate");
     p->q.alloc(nq_max * p->qstride);
     p->q_rm.alloc(nq_max * qlen * s->d);
     if (metric == TSW_METRIC_DTW) {
         p->env_lo.alloc(nq_max * p->qstride);
         p->env_hi.alloc(nq_max * p->qstride);
-        p->lbv.alloc(nq_max * s->n);
     }
     p->ub.alloc(nq_max * p->S);
     const uint64_t chunks = (p->S + kSelChunk - 1) / kSelChunk;
@@ -399,21 +387,6 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
                           (uint32_t)std::min<uint64_t>(p->r, 0xffffffffu), s->err32, p->env_lo.p,
                           p->env_hi.p, st);
         ++launches;
-        // fork: K2 (fp32 LB_Box of every pair) on the aux stream, overlapping the seed chain
-        ck(cudaEventRecord(p->ev_fork, st), "cudaEventRecord");
-        ck(cudaStreamWaitEvent(p->aux, p->ev_fork, 0), "cudaStreamWaitEvent");
-        if (p->timing) ck(cudaEventRecord(p->ev_lb[0], p->aux), "cudaEventRecord");
-        LbCompactArgs la{};
-        la.store = s->dev();
-        la.env_lo = p->env_lo.p;
-        la.env_hi = p->env_hi.p;
-        la.nq = nq;
-        la.qstride = p->qstride;
-        la.lb_out = p->lbv.p;
-        launch_lb_compact(la, p->aux);
-        ++launches;
-        if (p->timing) ck(cudaEventRecord(p->ev_lb[1], p->aux), "cudaEventRecord");
-        ck(cudaEventRecord(p->ev_join, p->aux), "cudaEventRecord");
     }
     mark(1);
     SampleArgs sa{};
@@ -475,17 +448,18 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
     if (p->probe && sep_probe) run_dp(p->probe_wq(), nq * (uint32_t)p->probe);
     mark(3);
     if (!dk) {
-        ck(cudaStreamWaitEvent(st, p->ev_join, 0), "cudaStreamWaitEvent");  // join K2
-        LbQueueArgs qa{};
-        qa.lb = p->lbv.p;
-        qa.nq = nq;
-        qa.n = n;
-        qa.margin = p->margin;
-        qa.near_frac = p->near_frac;
-        qa.state = p->state.p;
-        qa.probed = p->probed.p;
-        qa.queue = p->main_wq();
-        launch_lb_queue(qa, st);
+        LbCompactArgs la{};
+        la.store = s->dev();
+        la.env_lo = p->env_lo.p;
+        la.env_hi = p->env_hi.p;
+        la.nq = nq;
+        la.qstride = p->qstride;
+        la.margin = p->margin;
+        la.near_frac = p->near_frac;
+        la.state = p->state.p;
+        la.probed = p->probed.p;
+        la.queue = p->main_wq();
+        launch_lb_compact(la, st);
     } else {
         DkCompactArgs ka{};
         ka.store = s->dev();
@@ -859,15 +833,8 @@ int tsw_plan_stats(tsw_plan* p, tsw_stats* out) {
             out->ms_envelope = ms[1];
             out->ms_select = ms[2];
             out->ms_probe_dp = ms[3];
-            if (p->metric == TSW_METRIC_DTW) {  // K2 ran on the aux stream (overlapped)
-                float lbms = 0.0f;
-                cudaEventElapsedTime(&lbms, p->ev_lb[0], p->ev_lb[1]);
-                out->ms_bound = lbms;
-                out->ms_compact = ms[4];
-            } else {
-                out->ms_bound = ms[4];  // DK cell bounds fused with compaction
-                out->ms_compact = 0.0;
-            }
+            out->ms_bound = ms[4];
+            out->ms_compact = 0.0;  // fused into the bound pass
             out->ms_dp = ms[5];
         }
     });

@@ -301,49 +301,6 @@ void launch_lb_compact(const LbCompactArgs& a, cudaStream_t st) {
     lb_compact_kernel<QB, CB><<<std::max(blocks, 1), 256, 0, st>>>(a);
 }
 
-// ---- DTW: compaction of stored LB values ------------------------------------------------------
-__global__ void __launch_bounds__(256) lb_queue_kernel(LbQueueArgs a) {
-    const uint64_t total = (uint64_t)a.nq * a.n;
-    const unsigned lane = lane_id();
-    for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < total;
-         base += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t g = base + threadIdx.x;
-        const bool in = g < total;
-        uint32_t q = 0, c = 0;
-        bool take = false, near = false, pruned = false;
-        double key = 0.0;
-        if (in) {
-            // candidate-major: the queries of one candidate enter the work queue together, so
-            // the DP warps that take them share the candidate's bytes in L1/L2
-            c = (uint32_t)(g / a.nq);
-            q = (uint32_t)(g - (uint64_t)c * a.nq);
-            const uint64_t gi = (uint64_t)q * a.n + c;
-            if (!(a.probed && a.probed[gi])) {
-                key = (double)a.lb[gi];
-                const double T = a.state[q].T;
-                take = key <= __dmul_ru(T, a.margin);
-                near = key <= a.near_frac * T;
-                pruned = !take;
-            }
-        }
-        enqueue(a.queue, take, near, q, c, key);
-        const unsigned pm = __ballot_sync(0xffffffffu, pruned);
-        if (pm) {
-            const unsigned grp = __match_any_sync(0xffffffffu, in ? q : 0xffffffffu);
-            const unsigned mine = pm & grp;
-            if (pruned && lane == (unsigned)(__ffs(mine) - 1))
-                atomicAdd(const_cast<unsigned long long*>(&a.state[q].lb_pruned),
-                          (unsigned long long)__popc(mine));
-        }
-    }
-}
-
-void launch_lb_queue(const LbQueueArgs& a, cudaStream_t st) {
-    const uint64_t total = (uint64_t)a.nq * a.n;
-    const int blocks = (int)std::min<uint64_t>((total + 255) / 256, (uint64_t)sm_count() * 8);
-    lb_queue_kernel<<<std::max(blocks, 1), 256, 0, st>>>(a);
-}
-
 // ---- DK: first / last cell bound fused with compaction ------------------------------------
 // Both cells lie on every warping path, so max(c(0,0), c(m-1,n-1)) > Tsq  =>  dk > T (exact).
 __global__ void __launch_bounds__(256) dk_compact_kernel(DkCompactArgs a) {

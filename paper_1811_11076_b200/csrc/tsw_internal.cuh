@@ -241,18 +241,6 @@ struct LbCompactArgs {
 };
 void launch_lb_compact(const LbCompactArgs& a, cudaStream_t st);
 
-// DTW: compaction of precomputed fp32 LB values (K2 run without state, concurrently with the
-// seed / probe chain): lb <= T * margin -> work queue.
-struct LbQueueArgs {
-    const float* lb;      // [nq][n]
-    uint32_t nq, n;
-    double margin, near_frac;
-    const QState* state;
-    const uint8_t* probed;
-    WorkQueue queue;
-};
-void launch_lb_queue(const LbQueueArgs& a, cudaStream_t st);
-
 // DK: first/last cell bound of every pair fused with compaction (exact, squared domain).
 struct DkCompactArgs {
     StoreDev store;

@@ -15,7 +15,7 @@ for f in sorted(glob.glob(sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/benc
     rdp, rlb = d["roofline_dp"], d["roofline_lb"]
     print(f"{f.split('/')[-1]:22s} cfg{c['config_id']} {c['metric']:3s} q/s={d['value']:10.1f} "
           f"ms/step={d['ms_per_step']:8.3f} e2e={d['e2e']['value']:10.1f} "
-          f"bound={ph['ms_bound']:.3f} cmp={ph['ms_compact']:.3f} sel={ph['ms_select']:.3f} probe={ph['ms_probe_dp']:.3f} "
+          f"bound={ph['ms_bound']:.3f} sel={ph['ms_select']:.3f} probe={ph['ms_probe_dp']:.3f} "
           f"dp={ph['ms_dp']:.3f} | GCUPS={rdp['gcups'] or 0:7.1f} fp64frac={rdp['frac'] or 0:.3f} "
           f"LB GB/s={rlb['achieved'] or 0:7.1f} pairs={d['dp_pairs_per_step']:.0f} "
           f"cpu={d.get('cpu_baseline', {}).get('value')} clk={d['clocks'].get('sm_mhz')}")
