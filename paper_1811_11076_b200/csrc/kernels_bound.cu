@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(256, 2) lb_compact_kernel(LbCompactArgs a) {
             if (a.lb_out) a.lb_out[(uint64_t)q * n + c] = mine;
             if (a.state) {
                 const double T = a.state[q].T;
-                const bool probed = a.probed && a.probed[(uint64_t)q * n + c];
+                const bool probed = a.probed && a.probed[(uint64_t)c * a.nq + q];
                 take = !probed && lb <= __dmul_ru(T, a.margin);
                 near = lb <= a.near_frac * T;
             }
@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(256, 2) lb_compact_kernel(LbCompactArgs a) {
         if (a.state) {
             enqueue(a.queue, take, near, q, c, (double)mine);
             // pruned counts: lanes qb*CB .. qb*CB+CB-1 share query q0+qb
-            bool pruned = valid && !take && !(a.probed && a.probed[(uint64_t)q * n + c]);
+            bool pruned = valid && !take && !(a.probed && a.probed[(uint64_t)c * a.nq + q]);
             const unsigned pm = __ballot_sync(0xffffffffu, pruned);
             if (valid && lane % CB == 0) {
                 const unsigned cnt = __popc(pm & (((1u << CB) - 1u) << lane));
@@ -315,9 +315,10 @@ __global__ void __launch_bounds__(256) dk_compact_kernel(DkCompactArgs a) {
         bool take = false, near = false, pruned = false;
         double key = 0.0;
         if (in) {
-            c = (uint32_t)(g / a.nq);  // candidate-major (cache reuse in the DP, see lb_queue)
+            c = (uint32_t)(g / a.nq);  // candidate-major: a candidate's queries enter the queue together
+            // (the DP warps that take them share the candidate's bytes in L1/L2)
             q = (uint32_t)(g - (uint64_t)c * a.nq);
-            if (!(a.probed && a.probed[(uint64_t)q * n + c])) {
+            if (!(a.probed && a.probed[g])) {  // probed flags are candidate-major too
                 const double* s = a.queries + (uint64_t)q * a.qstride;
                 const double* e = a.store.ends + (uint64_t)c * 2 * d;  // first, last point
                 double c0 = 0.0, c1 = 0.0;

@@ -221,7 +221,7 @@ struct SeedArgs {
     QState* state;
     double* slots;
     WorkQueue probe_q;
-    uint8_t* probed;      // [nq][n]
+    uint8_t* probed;      // [n][nq] (candidate-major)
 };
 void launch_seed(const SeedArgs& a, cudaStream_t st);
 
