@@ -187,6 +187,7 @@ struct tsw_plan {
     int metric = 0;
     uint64_t nq = 0;  // queries of the last set_queries
     cudaStream_t own = nullptr;
+    DevBuf<double> qends;  // DK compaction scratch [2d][nq_max]
     DevBuf<double> q, q_rm, ub, sel_sv, sel_v, slots, top_d;
     DevBuf<float> env_lo, env_hi;
     DevBuf<uint32_t> sel_si, sel_i, top_i, fin_si;
@@ -302,6 +303,7 @@ std::unique_ptr<tsw_plan> make_plan(tsw_store* s, uint64_t nq_max, uint64_t qlen
     for (auto& e : p->ev) ck(cudaEventCreate(&e), "cudaEventCreate");
     p->q.alloc(nq_max * p->qstride);
     p->q_rm.alloc(nq_max * qlen * s->d);
+    p->qends.alloc(2 * s->d * nq_max);
     if (metric == TSW_METRIC_DTW) {
         p->env_lo.alloc(nq_max * p->qstride);
         p->env_hi.alloc(nq_max * p->qstride);
@@ -464,6 +466,7 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
         DkCompactArgs ka{};
         ka.store = s->dev();
         ka.queries = p->q.p;
+        ka.qends = p->qends.p;
         ka.nq = nq;
         ka.qlen = (uint32_t)p->qlen;
         ka.qstride = p->qstride;
@@ -879,7 +882,7 @@ int tsw_epsnn_dk(tsw_store* s, const double* query, uint64_t qlen, double eps,
         DeviceGuard dg(s->device);
         const uint64_t n = s->n, d = s->d, qs = stride_of(qlen, d);
         cudaStream_t st = 0;
-        DevBuf<double> q(qs), rd(n);
+        DevBuf<double> q(qs), rd(n), qe(2 * d);
         DevBuf<uint32_t> ri(n);
         DevBuf<unsigned> rn(1), ctr(4);
         DevBuf<unsigned long long> pruned(1);
@@ -896,6 +899,7 @@ int tsw_epsnn_dk(tsw_store* s, const double* query, uint64_t qlen, double eps,
         DkCompactArgs ka{};
         ka.store = s->dev();
         ka.queries = q.p;
+        ka.qends = qe.p;
         ka.nq = 1;
         ka.qlen = (uint32_t)qlen;
         ka.qstride = qs;

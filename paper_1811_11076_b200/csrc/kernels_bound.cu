@@ -319,13 +319,14 @@ __global__ void __launch_bounds__(256) dk_compact_kernel(DkCompactArgs a) {
             // (the DP warps that take them share the candidate's bytes in L1/L2)
             q = (uint32_t)(g - (uint64_t)c * a.nq);
             if (!(a.probed && a.probed[g])) {  // probed flags are candidate-major too
-                const double* s = a.queries + (uint64_t)q * a.qstride;
+                // query endpoints from the query-minor scratch (coalesced across the warp's
+                // queries), candidate endpoints broadcast from the store's ends array
                 const double* e = a.store.ends + (uint64_t)c * 2 * d;  // first, last point
                 double c0 = 0.0, c1 = 0.0;
                 for (uint32_t k = 0; k < d; ++k) {
-                    const double e0 = dsub(s[tidx(0, k, d)], e[k]);
+                    const double e0 = dsub(a.qends[(uint64_t)k * a.nq + q], e[k]);
                     c0 = dadd(c0, dmul(e0, e0));
-                    const double e1 = dsub(s[tidx(m - 1, k, d)], e[d + k]);
+                    const double e1 = dsub(a.qends[(uint64_t)(d + k) * a.nq + q], e[d + k]);
                     c1 = dadd(c1, dmul(e1, e1));
                 }
                 key = dmax(c0, c1);
@@ -351,7 +352,19 @@ __global__ void __launch_bounds__(256) dk_compact_kernel(DkCompactArgs a) {
     }
 }
 
+__global__ void query_ends_kernel(const double* __restrict__ q, uint32_t nq, uint32_t m, uint32_t d,
+                                  uint64_t qstride, double* __restrict__ out) {
+    const uint32_t total = 2 * d * nq;
+    for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < total; g += gridDim.x * blockDim.x) {
+        const uint32_t qi = g % nq, wk = g / nq;          // wk = which * d + k
+        const uint32_t which = wk / d, k = wk - which * d;
+        out[g] = q[(uint64_t)qi * qstride + tidx(which ? m - 1 : 0, k, d)];
+    }
+}
+
 void launch_dk_compact(const DkCompactArgs& a, cudaStream_t st) {
+    query_ends_kernel<<<std::max(1u, std::min(64u, (2 * a.store.d * a.nq + 255) / 256)), 256, 0, st>>>(
+        a.queries, a.nq, a.qlen, a.store.d, a.qstride, a.qends);
     const uint64_t total = (uint64_t)a.nq * a.store.n;
     const int blocks = (int)std::min<uint64_t>((total + 255) / 256, (uint64_t)sm_count() * 8);
     dk_compact_kernel<<<std::max(blocks, 1), 256, 0, st>>>(a);

@@ -245,6 +245,7 @@ void launch_lb_compact(const LbCompactArgs& a, cudaStream_t st);
 struct DkCompactArgs {
     StoreDev store;
     const double* queries;
+    double* qends;            // scratch [2d][nq]: query first/last points, query-minor
     uint32_t nq, qlen;
     uint64_t qstride;
     double near_frac;
