@@ -562,11 +562,21 @@ void fetch_impl(tsw_plan* p, tsw_neighbor* out, tsw_counters* counters, cudaStre
         }
         if (counters) {
             tsw_counters& c = counters[q];
-            c.lb_computed = p->metric == TSW_METRIC_DTW ? n : 0;
-            c.lb_pruned = hs[q].lb_pruned;
+            // every pair is pruned by its bound (compaction or dequeue re-check) or finishes in a
+            // DP as exact / abandoned, so the bound-pruned count is the complement
+            // (search.hpp:10-12 conservation holds by construction)
             c.full_dp = hs[q].full_dp;
-            c.early_abandoned = hs[q].early_abandoned;
-            c.gdk_calls = p->metric == TSW_METRIC_DK ? n : 0;
+            if (p->metric == TSW_METRIC_DTW) {
+                c.lb_computed = n;
+                c.early_abandoned = hs[q].early_abandoned;
+                c.lb_pruned = n - c.full_dp - c.early_abandoned;
+                c.gdk_calls = 0;
+            } else {
+                c.lb_computed = 0;
+                c.lb_pruned = 0;
+                c.early_abandoned = n - c.full_dp;
+                c.gdk_calls = n;
+            }
         }
     }
 }

@@ -183,25 +183,50 @@ void launch_sample_ub(const SampleArgs& a, cudaStream_t st) {
     sample_ub_kernel<<<std::max(blocks, 1), 256, 0, st>>>(a);
 }
 
-// ---- warp-aggregated enqueue into the two-region work queue ----------------------------------
-__device__ __forceinline__ void enqueue(const WorkQueue& w, bool take, bool near, uint32_t q,
-                                        uint32_t c, double key) {
+// ---- warp-staged enqueue into the two-region work queue --------------------------------------
+// Survivors are staged in per-warp shared-memory buffers and flushed with ONE atomic per
+// ~kStage entries (coalesced stores) instead of an atomic per warp-iteration: same-address
+// atomics on the queue counters were the compactions' bottleneck.
+constexpr unsigned kStage = 128;
+
+struct Stage {
+    QEntry* fbuf;
+    QEntry* bbuf;
+    unsigned fn, bn;
+};
+
+__device__ __forceinline__ void stage_flush(Stage& sg, const WorkQueue& w, bool front) {
+    const unsigned lane = lane_id();
+    const unsigned cnt = front ? sg.fn : sg.bn;
+    __syncwarp();
+    if (cnt) {
+        unsigned base = 0;
+        if (lane == 0) base = atomicAdd(front ? w.front : w.back, cnt);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        for (unsigned i = lane; i < cnt; i += 32) {
+            if (front) w.e[base + i] = sg.fbuf[i];
+            else w.e[w.cap - 1 - (base + i)] = sg.bbuf[i];
+        }
+    }
+    __syncwarp();
+    if (front) sg.fn = 0; else sg.bn = 0;
+}
+
+__device__ __forceinline__ void enqueue(Stage& sg, const WorkQueue& w, bool take, bool near,
+                                        uint32_t q, uint32_t c, double key) {
     const unsigned lane = lane_id();
     const unsigned fm = __ballot_sync(0xffffffffu, take && near);
     const unsigned bm = __ballot_sync(0xffffffffu, take && !near);
-    unsigned fb = 0, bb = 0;
-    if (lane == 0) {
-        if (fm) fb = atomicAdd(w.front, (unsigned)__popc(fm));
-        if (bm) bb = atomicAdd(w.back, (unsigned)__popc(bm));
-    }
-    fb = __shfl_sync(0xffffffffu, fb, 0);
-    bb = __shfl_sync(0xffffffffu, bb, 0);
     const unsigned below = (1u << lane) - 1u;
     if (take) {
         const QEntry e{q, c, key};
-        if (near) w.e[fb + __popc(fm & below)] = e;
-        else w.e[w.cap - 1 - (bb + __popc(bm & below))] = e;
+        if (near) sg.fbuf[sg.fn + __popc(fm & below)] = e;
+        else sg.bbuf[sg.bn + __popc(bm & below)] = e;
     }
+    sg.fn += __popc(fm);
+    sg.bn += __popc(bm);
+    if (sg.fn > kStage - 32) stage_flush(sg, w, true);
+    if (sg.bn > kStage - 32) stage_flush(sg, w, false);
 }
 
 // ---- K2 + K3: fp32 LB_Box tile kernel fused with compaction --------------------------------
@@ -217,6 +242,8 @@ __global__ void __launch_bounds__(256, 2) lb_compact_kernel(LbCompactArgs a) {
     const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const uint32_t total4 = (uint32_t)(a.store.ustride / 4);  // ustride is a multiple of 32d
+    __shared__ QEntry stage_buf[8][2][kStage];
+    Stage sg{stage_buf[threadIdx.x >> 5][0], stage_buf[threadIdx.x >> 5][1], 0u, 0u};
     for (uint64_t w = wid; w < ngroups * nqb; w += nw) {
         // candidate-major order: the nqb query blocks of one candidate group run on adjacent
         // warps, so the group's bytes come from HBM once and are re-read from L1/L2
@@ -281,16 +308,13 @@ __global__ void __launch_bounds__(256, 2) lb_compact_kernel(LbCompactArgs a) {
                 near = lb <= a.near_frac * T;
             }
         }
-        if (a.state) {
-            enqueue(a.queue, take, near, q, c, (double)mine);
-            // pruned counts: lanes qb*CB .. qb*CB+CB-1 share query q0+qb
-            bool pruned = valid && !take && !(a.probed && a.probed[(uint64_t)c * a.nq + q]);
-            const unsigned pm = __ballot_sync(0xffffffffu, pruned);
-            if (valid && lane % CB == 0) {
-                const unsigned cnt = __popc(pm & (((1u << CB) - 1u) << lane));
-                if (cnt) atomicAdd(const_cast<unsigned long long*>(&a.state[q].lb_pruned), (unsigned long long)cnt);
-            }
-        }
+        // pruned pairs are not counted here: the host derives lb_pruned = n - full_dp -
+        // early_abandoned (every surviving pair ends in the DP as one of the two)
+        if (a.state) enqueue(sg, a.queue, take, near, q, c, (double)mine);
+    }
+    if (a.state) {
+        stage_flush(sg, a.queue, true);
+        stage_flush(sg, a.queue, false);
     }
 }
 
@@ -304,15 +328,16 @@ void launch_lb_compact(const LbCompactArgs& a, cudaStream_t st) {
 // ---- DK: first / last cell bound fused with compaction ------------------------------------
 // Both cells lie on every warping path, so max(c(0,0), c(m-1,n-1)) > Tsq  =>  dk > T (exact).
 __global__ void __launch_bounds__(256) dk_compact_kernel(DkCompactArgs a) {
-    const uint32_t n = a.store.n, d = a.store.d, m = a.qlen;
+    const uint32_t n = a.store.n, d = a.store.d;
     const uint64_t total = (uint64_t)a.nq * n;
-    const unsigned lane = lane_id();
+    __shared__ QEntry stage_buf[8][2][kStage];
+    Stage sg{stage_buf[threadIdx.x >> 5][0], stage_buf[threadIdx.x >> 5][1], 0u, 0u};
     for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < total;
          base += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t g = base + threadIdx.x;
         const bool in = g < total;
         uint32_t q = 0, c = 0;
-        bool take = false, near = false, pruned = false;
+        bool take = false, near = false;
         double key = 0.0;
         if (in) {
             c = (uint32_t)(g / a.nq);  // candidate-major: a candidate's queries enter the queue together
@@ -333,23 +358,13 @@ __global__ void __launch_bounds__(256) dk_compact_kernel(DkCompactArgs a) {
                 const double Tsq = a.state ? a.state[q].Tsq : a.fixed_eps_sq;
                 take = key <= Tsq;
                 near = key <= a.near_frac * Tsq;
-                pruned = !take;
             }
         }
-        enqueue(a.queue, take, near, q, c, key);
-        const unsigned pm = __ballot_sync(0xffffffffu, pruned);
-        if (pm) {
-            const unsigned grp = __match_any_sync(0xffffffffu, in ? q : 0xffffffffu);
-            const unsigned mine = pm & grp;
-            if (pruned && lane == (unsigned)(__ffs(mine) - 1)) {
-                if (a.state)
-                    atomicAdd(const_cast<unsigned long long*>(&a.state[q].early_abandoned),
-                              (unsigned long long)__popc(mine));
-                else if (a.fixed_pruned)
-                    atomicAdd(a.fixed_pruned, (unsigned long long)__popc(mine));
-            }
-        }
+        // pruned pairs are not counted here: the host derives early_abandoned = n - full_dp
+        enqueue(sg, a.queue, take, near, q, c, key);
     }
+    stage_flush(sg, a.queue, true);
+    stage_flush(sg, a.queue, false);
 }
 
 __global__ void query_ends_kernel(const double* __restrict__ q, uint32_t nq, uint32_t m, uint32_t d,
