@@ -31,6 +31,9 @@
 
 using namespace tswb;
 
+// survivors with LB block sums per plan (beyond: the DP falls back to a zero prefix, still exact)
+constexpr uint64_t kPfxCapMax = 1ull << 22;
+
 namespace {
 
 thread_local std::string g_err;
@@ -151,7 +154,8 @@ struct tsw_plan;
 
 struct tsw_store {
     int device = 0;
-    uint64_t n = 0, d = 0, ulen = 0, ustride = 0, max_len = 0;
+    uint64_t n = 0, d = 0, ulen = 0, ustride = 0, tstride = 0, max_len = 0;
+    uint64_t guard = 0;      // elements of the leading guard tile (data / data32 start after it)
     DevBuf<double> data;
     DevBuf<float> data32;
     DevBuf<double> ends;
@@ -164,8 +168,8 @@ struct tsw_store {
     std::unique_ptr<tsw_plan> cached_plan;
     StoreDev dev() const {
         StoreDev s{};
-        s.data = data.p;
-        s.data32 = data32.p;
+        s.data = data.p + guard;
+        s.data32 = data32.p + guard;
         s.ends = ends.p;
         s.off = off.p;
         s.len = len.p;
@@ -173,13 +177,14 @@ struct tsw_store {
         s.d = (uint32_t)d;
         s.ulen = (uint32_t)ulen;
         s.ustride = ustride;
+        s.tstride = tstride;
         return s;
     }
     ~tsw_store();
 };
 
 // counters layout of a plan
-enum { C_PFRONT = 0, C_PBACK, C_PHEAD, C_MFRONT, C_MBACK, C_MHEAD, C_COUNT = 8 };
+enum { C_PFRONT = 0, C_PBACK, C_PHEAD, C_MFRONT, C_MBACK, C_MHEAD, C_PFX, C_COUNT = 8 };
 
 struct tsw_plan {
     tsw_store* store = nullptr;
@@ -190,6 +195,8 @@ struct tsw_plan {
     DevBuf<double> qends;  // DK compaction scratch [2d][nq_max]
     DevBuf<double> q, q_rm, ub, sel_sv, sel_v, slots, top_d;
     DevBuf<float> env_lo, env_hi;
+    DevBuf<float> pfx;  // DTW: survivors' LB block sums [pfx_cap][kPfxBlocks]
+    uint32_t pfx_qn = 0, pfx_log = 0, pfx_cap = 0;
     DevBuf<uint32_t> sel_si, sel_i, top_i, fin_si;
     DevBuf<double> fin_sv;
     DevBuf<QState> state;
@@ -221,6 +228,7 @@ struct tsw_plan {
             if (e) cudaEventDestroy(e);
         if (own) cudaStreamDestroy(own);
     }
+    double* qg() const { return q.p + store->d * kTile; }  // first query (after the leading guard)
     WorkQueue probe_wq() const {
         return WorkQueue{probe_q.p, counters.p + C_PFRONT, counters.p + C_PBACK, counters.p + C_PHEAD,
                          (uint32_t)probe_q.n};
@@ -253,10 +261,19 @@ struct DeviceGuard {
 uint64_t stride_of(uint64_t len, uint64_t d) { return tiled_stride(len, d); }
 
 // row-major series (TimeSeries::flat()) -> tiled layout, host side
-std::vector<double> tiled_host(const double* rm, uint64_t len, uint64_t d) {
-    std::vector<double> out(stride_of(len, d), 0.0);
+std::vector<double> tiled_host(const double* rm, uint64_t len, uint64_t d, double pad = 0.0) {
+    std::vector<double> out(stride_of(len, d), pad);
     for (uint64_t p = 0; p < len; ++p)
         for (uint64_t k = 0; k < d; ++k) out[tidx((uint32_t)p, (uint32_t)k, (uint32_t)d)] = rm[p * d + k];
+    return out;
+}
+
+// one guarded query for the DTW kernels: [guard tile][tiles][guard tile], padding = +inf
+std::vector<double> guarded_host(const double* rm, uint64_t len, uint64_t d) {
+    const uint64_t g = kTile * d;
+    std::vector<double> out(2 * g + stride_of(len, d), INFINITY);
+    const std::vector<double> t = tiled_host(rm, len, d, INFINITY);
+    std::memcpy(out.data() + g, t.data(), t.size() * sizeof(double));
     return out;
 }
 
@@ -286,7 +303,7 @@ std::unique_ptr<tsw_plan> make_plan(tsw_store* s, uint64_t nq_max, uint64_t qlen
     p->store = s;
     p->nq_max = nq_max;
     p->qlen = qlen;
-    p->qstride = stride_of(qlen, s->d);
+    p->qstride = stride_of(qlen, s->d) + kTile * s->d;  // pitch: tiles + one guard tile
     p->metric = metric;
     p->r = r;
     p->k = k;
@@ -301,12 +318,23 @@ std::unique_ptr<tsw_plan> make_plan(tsw_store* s, uint64_t nq_max, uint64_t qlen
     p->P = std::max<uint64_t>(1, std::min<uint64_t>(kKMax, std::max(p->kk, p->probe)));
     ck(cudaStreamCreateWithFlags(&p->own, cudaStreamNonBlocking), "cudaStreamCreate");
     for (auto& e : p->ev) ck(cudaEventCreate(&e), "cudaEventCreate");
-    p->q.alloc(nq_max * p->qstride);
+    p->q.alloc(kTile * s->d + nq_max * p->qstride);
+    launch_fill(p->q.p, kTile * s->d, INFINITY, p->own);  // leading guard of query 0
+    ck(cudaStreamSynchronize(p->own), "plan init");
     p->q_rm.alloc(nq_max * qlen * s->d);
     p->qends.alloc(2 * s->d * nq_max);
     if (metric == TSW_METRIC_DTW) {
         p->env_lo.alloc(nq_max * p->qstride);
         p->env_hi.alloc(nq_max * p->qstride);
+        // LB block sums for the DP's cumulative bound when a lane of the LB warp covers at most
+        // 2 point quads per dimension (longer series: per-point prefix computed in the DP)
+        const uint64_t qn = (tiled_stride(qlen, 1) + 127) / 128;
+        if (qn <= 2) {
+            p->pfx_qn = (uint32_t)qn;
+            p->pfx_log = qn == 1 ? 2u : 3u;
+            p->pfx_cap = (uint32_t)std::min<uint64_t>(nq_max * n, kPfxCapMax);
+            p->pfx.alloc((uint64_t)p->pfx_cap * kPfxBlocks);
+        }
     }
     p->ub.alloc(nq_max * p->S);
     const uint64_t chunks = (p->S + kSelChunk - 1) / kSelChunk;
@@ -357,7 +385,8 @@ void set_queries_impl(tsw_plan* p, const double* q, uint64_t nq, bool device, cu
            "query upload");
         src = p->q_rm.p;
     }
-    launch_rowmajor_to_tiled(src, nq, (uint32_t)p->qlen, (uint32_t)p->store->d, p->qstride, p->q.p, st);
+    launch_rowmajor_to_tiled(src, nq, (uint32_t)p->qlen, (uint32_t)p->store->d,
+                             stride_of(p->qlen, p->store->d), p->qstride, INFINITY, p->qg(), st);
     g_h2d = device ? 0 : nq * row * sizeof(double);
     p->nq = nq;
 }
@@ -385,7 +414,7 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
     ck(cudaMemsetAsync(p->cells.p, 0, sizeof(unsigned long long), st), "memset");
     ck(cudaMemsetAsync(p->res_n.p, 0, nq * sizeof(unsigned), st), "memset");
     if (!dk) {
-        launch_envelope32(p->q.p, nq, (uint32_t)s->d, (uint32_t)p->qlen, p->qstride,
+        launch_envelope32(p->qg(), nq, (uint32_t)s->d, (uint32_t)p->qlen, p->qstride,
                           (uint32_t)std::min<uint64_t>(p->r, 0xffffffffu), s->err32, p->env_lo.p,
                           p->env_hi.p, st);
         ++launches;
@@ -393,7 +422,7 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
     mark(1);
     SampleArgs sa{};
     sa.store = s->dev();
-    sa.queries = p->q.p;
+    sa.queries = p->qg();
     sa.nq = nq;
     sa.qlen = (uint32_t)p->qlen;
     sa.qstride = p->qstride;
@@ -430,7 +459,8 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
 
     DpArgs da{};
     da.store = s->dev();
-    da.queries = p->q.p;
+    da.queries = p->qg();
+    da.guarded = 1;
     da.env_lo = p->env_lo.p;
     da.env_hi = p->env_hi.p;
     da.qlen = (uint32_t)p->qlen;
@@ -441,6 +471,8 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
     da.margin = p->margin;
     da.cells = p->cells.p;
     da.results = ResultBuf{p->res_d.p, p->res_i.p, p->res_n.p, n};
+    da.pfx_blocks = p->pfx_qn ? p->pfx.p : nullptr;
+    da.pfx_log = p->pfx_log;
     auto run_dp = [&](const WorkQueue& w, uint32_t max_pairs) {
         da.queue = w;
         if (dk) launch_dk_dp(da, max_pairs, (uint32_t)s->max_len, st);
@@ -461,11 +493,15 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
         la.state = p->state.p;
         la.probed = p->probed.p;
         la.queue = p->main_wq();
+        la.pfx_qn = p->pfx_qn;
+        la.pfx_out = p->pfx_qn ? p->pfx.p : nullptr;
+        la.pfx_count = p->counters.p + C_PFX;
+        la.pfx_cap = p->pfx_cap;
         launch_lb_compact(la, st);
     } else {
         DkCompactArgs ka{};
         ka.store = s->dev();
-        ka.queries = p->q.p;
+        ka.queries = p->qg();
         ka.qends = p->qends.p;
         ka.nq = nq;
         ka.qlen = (uint32_t)p->qlen;
@@ -652,12 +688,16 @@ int tsw_store_create(const double* values, const uint64_t* lengths, uint64_t uni
         s->max_len = mx;
         s->host_len = lens;
         uint64_t elems = 0;
+        const uint64_t g = kTile * d;  // guard tile: before every series and after the last
+        s->guard = g;
         if (uniform) {
-            // point-major rows exactly as given (TimeSeries::flat()), stride padded to 4 elements
+            // tiled series at a pitch of tiles + one guard tile (-inf)
             s->ulen = lens[0];
-            s->ustride = stride_of(lens[0], d);
-            elems = n * s->ustride;
+            s->tstride = stride_of(lens[0], d);
+            s->ustride = s->tstride + g;
+            elems = g + n * s->ustride;
             s->data.alloc(elems);
+            launch_fill(s->data.p, g, -INFINITY, 0);
             // upload row-major through a bounded staging buffer, re-tile on the device
             const uint64_t row = lens[0] * d;
             const uint64_t batch = std::max<uint64_t>(1, std::min<uint64_t>(n, (256ull << 20) / (row * 8)));
@@ -667,21 +707,23 @@ int tsw_store_create(const double* values, const uint64_t* lengths, uint64_t uni
                 ck(cudaMemcpy(stage.p, values + b0 * row, nb * row * sizeof(double),
                               cudaMemcpyHostToDevice),
                    "store upload");
-                launch_rowmajor_to_tiled(stage.p, nb, lens[0], (uint32_t)d, s->ustride,
-                                         s->data.p + b0 * s->ustride, 0);
+                launch_rowmajor_to_tiled(stage.p, nb, lens[0], (uint32_t)d, s->tstride, s->ustride,
+                                         -INFINITY, s->data.p + g + b0 * s->ustride, 0);
                 ck(cudaDeviceSynchronize(), "store tiling");
             }
         } else {
-            std::vector<uint64_t> off(n);
+            std::vector<uint64_t> off(n);  // relative to the first series (after the leading guard)
+            uint64_t rel = 0;
             for (uint64_t i = 0; i < n; ++i) {
-                off[i] = elems;
-                elems += stride_of(lens[i], d);
+                off[i] = rel;
+                rel += stride_of(lens[i], d) + g;
             }
-            std::vector<double> buf(elems, 0.0);
+            elems = g + rel;
+            std::vector<double> buf(elems, -INFINITY);
             uint64_t src = 0;
             for (uint64_t i = 0; i < n; ++i) {
-                const std::vector<double> t = tiled_host(values + src, lens[i], d);
-                std::memcpy(buf.data() + off[i], t.data(), t.size() * sizeof(double));
+                const std::vector<double> t = tiled_host(values + src, lens[i], d, -INFINITY);
+                std::memcpy(buf.data() + g + off[i], t.data(), t.size() * sizeof(double));
                 src += lens[i] * d;
             }
             s->data.alloc(elems);
@@ -1031,23 +1073,24 @@ int tsw_dist_all(tsw_store* s, const double* query, uint64_t qlen, int metric, u
             fail(TSW_EINVAL, "dist_all(dtw): every series must have the query length");
         std::lock_guard<std::mutex> lk(s->mu);
         DeviceGuard dg(s->device);
-        const uint64_t n = s->n, d = s->d, qs = stride_of(qlen, d);
-        DevBuf<double> q(qs), val(n);
+        const uint64_t n = s->n, d = s->d, g = kTile * d, qs = stride_of(qlen, d) + g;
+        DevBuf<double> q(qs + g), val(n);
         DevBuf<int> ex(n);
         DevBuf<unsigned> ctr(4);
         DevBuf<QEntry> queue(n);
         std::vector<QEntry> hq(n);
-        for (uint64_t i = 0; i < n; ++i) hq[i] = QEntry{0, (uint32_t)i, 0.0};
+        for (uint64_t i = 0; i < n; ++i) hq[i] = QEntry{0, (uint32_t)i, 0.0f, kNoPfx};
         const unsigned cnt[4] = {(unsigned)n, 0u, 0u, 0u};
         ck(cudaMemcpy(queue.p, hq.data(), n * sizeof(QEntry), cudaMemcpyHostToDevice), "upload");
         ck(cudaMemcpy(ctr.p, cnt, sizeof(cnt), cudaMemcpyHostToDevice), "upload");
         {
-            const std::vector<double> tq = tiled_host(query, qlen, d);
-            ck(cudaMemcpy(q.p, tq.data(), qs * sizeof(double), cudaMemcpyHostToDevice), "upload");
+            const std::vector<double> tq = guarded_host(query, qlen, d);
+            ck(cudaMemcpy(q.p, tq.data(), tq.size() * sizeof(double), cudaMemcpyHostToDevice), "upload");
         }
         DpArgs da{};
         da.store = s->dev();
-        da.queries = q.p;
+        da.queries = q.p + g;
+        da.guarded = 1;
         da.qlen = (uint32_t)qlen;
         da.qstride = qs;
         da.r = (uint32_t)std::min<uint64_t>(r, 0xffffffffu);

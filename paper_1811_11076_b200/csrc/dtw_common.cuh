@@ -1,0 +1,134 @@
+// Pieces shared by the two banded-DTW kernels (kernels_dtw.cu: generic d / wide bands with
+// clamped indexing; kernels_dtw4.cu: guarded small-d fast path).
+#pragma once
+
+#include "tsw_internal.cuh"
+
+namespace tswb {
+
+// Cumulative abandon bound of one (query, candidate) pair into the group's shared array:
+// pfx[b] = lower bound of the LB_Box terms of candidate points j < b * 2^pfx_log.  Block mode:
+// exclusive RD scan of the pair's 32 LB block sums written by the LB pass; else the per-point
+// fp32 terms are computed here (lower_bounds.cpp:19-46 restated with directed rounding).
+// Block mode, part 1: this lane's PER = 32 / WL block sums of the pair (0 when the pair has no
+// row: probes, or survivors beyond the buffer).  Issued early by the fast path (prefetch).
+template <int WL>
+__device__ __forceinline__ void load_pfx_row(const DpArgs& a, uint32_t ps, int gl,
+                                             float (&bv)[kPfxBlocks / WL]) {
+    constexpr int PER = kPfxBlocks / WL;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) bv[i] = 0.0f;
+    if (ps != kNoPfx) {
+        const float* row = a.pfx_blocks + (uint64_t)ps * kPfxBlocks + gl * PER;
+        if constexpr (PER == 4) {
+            const float4 v = __ldg(reinterpret_cast<const float4*>(row));
+            bv[0] = v.x; bv[1] = v.y; bv[2] = v.z; bv[3] = v.w;
+        } else if constexpr (PER == 2) {
+            const float2 v = __ldg(reinterpret_cast<const float2*>(row));
+            bv[0] = v.x; bv[1] = v.y;
+        } else {
+            bv[0] = __ldg(row);
+        }
+    }
+}
+
+// Block mode, part 2: exclusive round-down scan of the group's 32 block sums into pfx[0..32]
+// (RD adds in any order keep every prefix a lower bound).
+template <int WL>
+__device__ __forceinline__ void scan_pfx_row(float (&bv)[kPfxBlocks / WL], int gl, unsigned gmask,
+                                             float* pfx) {
+    constexpr int PER = kPfxBlocks / WL;
+#pragma unroll
+    for (int i = 1; i < PER; ++i) bv[i] = __fadd_rd(bv[i], bv[i - 1]);
+    float inc = bv[PER - 1];
+#pragma unroll
+    for (int o = 1; o < WL; o <<= 1) {
+        const float y = __shfl_up_sync(gmask, inc, o, WL);
+        if (gl >= o) inc = __fadd_rd(inc, y);
+    }
+    float base = __shfl_up_sync(gmask, inc, 1, WL);
+    if (gl == 0) base = 0.0f;
+    if (gl == 0) pfx[0] = 0.0f;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) pfx[1 + gl * PER + i] = __fadd_rd(base, bv[i]);
+}
+
+template <int WL>
+__device__ __forceinline__ void setup_pfx(const DpArgs& a, const QEntry& pr, int gl, unsigned gmask,
+                                          float* pfx, int L, int stride) {
+    if (a.pfx_blocks) {
+        float bv[kPfxBlocks / WL];
+        load_pfx_row<WL>(a, pr.ps, gl, bv);
+        scan_pfx_row<WL>(bv, gl, gmask, pfx);
+    } else if (a.env_lo) {
+        const float* x32 = a.store.data32 + series_off(a.store, pr.c);
+        const float* el = a.env_lo + (uint64_t)pr.q * a.qstride;
+        const float* eh = a.env_hi + (uint64_t)pr.q * a.qstride;
+        float carry = 0.0f;
+        if (gl == 0) pfx[0] = 0.0f;
+        for (int j0 = 0; j0 < L; j0 += 4 * WL) {
+            const int p0 = j0 + 4 * gl;
+            float t0 = 0.0f, t1 = 0.0f, t2 = 0.0f, t3 = 0.0f;
+            if (p0 < L) {
+                for (int k = 0; k < stride; ++k) {
+                    const uint64_t o = tidx((uint32_t)p0, (uint32_t)k, (uint32_t)stride);
+                    const float4 x = __ldg(reinterpret_cast<const float4*>(x32 + o));
+                    const float4 l = __ldg(reinterpret_cast<const float4*>(el + o));
+                    const float4 hh = __ldg(reinterpret_cast<const float4*>(eh + o));
+                    t0 = lb_term_rd(t0, x.x, l.x, hh.x);
+                    t1 = lb_term_rd(t1, x.y, l.y, hh.y);
+                    t2 = lb_term_rd(t2, x.z, l.z, hh.z);
+                    t3 = lb_term_rd(t3, x.w, l.w, hh.w);
+                }
+            }
+            // local inclusive scan, then a group scan of the lane totals (RD adds
+            // in any order keep every prefix a lower bound)
+            t1 = __fadd_rd(t1, t0);
+            t2 = __fadd_rd(t2, t1);
+            t3 = __fadd_rd(t3, t2);
+            float inc = t3;
+#pragma unroll
+            for (int o = 1; o < WL; o <<= 1) {
+                const float y = __shfl_up_sync(gmask, inc, o, WL);
+                if (gl >= o) inc = __fadd_rd(inc, y);
+            }
+            float base = __shfl_up_sync(gmask, inc, 1, WL);
+            if (gl == 0) base = 0.0f;
+            base = __fadd_rd(base, carry);
+            if (p0 + 1 <= L) pfx[p0 + 1] = __fadd_rd(base, t0);
+            if (p0 + 2 <= L) pfx[p0 + 2] = __fadd_rd(base, t1);
+            if (p0 + 3 <= L) pfx[p0 + 3] = __fadd_rd(base, t2);
+            if (p0 + 4 <= L) pfx[p0 + 4] = __fadd_rd(base, t3);
+            carry = __fadd_rd(carry, __shfl_sync(gmask, inc, WL - 1, WL));
+        }
+    } else {
+        for (int j = gl; j <= L; j += WL) pfx[j] = 0.0f;
+    }
+}
+
+// Report a finished pair (one lane): exact iff the DP completed with value <= T, as
+// dtw_early_abandon (dtw.cpp:82-90); exact results feed the device KBest.
+__device__ __forceinline__ void finish_pair(const DpArgs& a, QState* st, const QEntry& pr,
+                                            bool completed, double f, double T) {
+    const bool exact = completed && f <= T;
+    if (a.out_exact) {
+        a.out_exact[pr.c] = exact ? 1 : 0;
+        a.out_val[pr.c] = exact ? f : T;
+    }
+    if (exact) {
+        if (st) {
+            atomicAdd(&st->full_dp, 1ull);
+            offer_exact(st, a.slots + (size_t)pr.q * kKMax, a.results, pr.q, f, pr.c, false);
+        } else if (a.results.dist) {  // fixed threshold: append only
+            const unsigned pos = atomicAdd(a.results.count + pr.q, 1u);
+            if (pos < a.results.cap) {
+                a.results.dist[(size_t)pr.q * a.results.cap + pos] = f;
+                a.results.idx[(size_t)pr.q * a.results.cap + pos] = pr.c;
+            }
+        }
+    } else if (st) {
+        atomicAdd(&st->early_abandoned, 1ull);
+    }
+}
+
+}  // namespace tswb

@@ -16,29 +16,47 @@ __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 
 // ---- helpers ------------------------------------------------------------------------------
 __global__ void rowmajor_to_tiled_kernel(const double* __restrict__ src, uint64_t nser, uint32_t len,
-                                         uint32_t d, uint64_t stride, double* __restrict__ dst) {
-    const uint64_t total = nser * stride;
+                                         uint32_t d, uint64_t stride, uint64_t pitch, double pad,
+                                         double* __restrict__ dst) {
+    const uint64_t total = nser * pitch;
     for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total;
          g += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t ser = g / stride;
-        const uint32_t f = (uint32_t)(g - ser * stride);
+        const uint64_t ser = g / pitch;
+        const uint32_t f = (uint32_t)(g - ser * pitch);
+        if (f >= stride) {  // guard tile after the series
+            dst[g] = pad;
+            continue;
+        }
         const uint32_t tile = f / (kTile * d), rem = f - tile * (kTile * d);
         const uint32_t k = rem / kTile, p = tile * kTile + rem % kTile;
-        dst[g] = p < len ? src[(ser * len + p) * d + k] : 0.0;
+        dst[g] = p < len ? src[(ser * len + p) * d + k] : pad;
     }
 }
 
 void launch_rowmajor_to_tiled(const double* src, uint64_t nser, uint32_t len, uint32_t d,
-                              uint64_t stride, double* dst, cudaStream_t st) {
-    const uint64_t total = nser * stride;
+                              uint64_t stride, uint64_t pitch, double pad, double* dst,
+                              cudaStream_t st) {
+    const uint64_t total = nser * pitch;
     const int blocks = (int)std::min<uint64_t>((total + 255) / 256, (uint64_t)sm_count() * 16);
-    rowmajor_to_tiled_kernel<<<std::max(blocks, 1), 256, 0, st>>>(src, nser, len, d, stride, dst);
+    rowmajor_to_tiled_kernel<<<std::max(blocks, 1), 256, 0, st>>>(src, nser, len, d, stride, pitch,
+                                                                  pad, dst);
+}
+
+__global__ void fill_kernel(double* __restrict__ p, uint64_t n, double v) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        p[i] = v;
+}
+
+void launch_fill(double* p, uint64_t count, double v, cudaStream_t st) {
+    const int blocks = (int)std::min<uint64_t>((count + 255) / 256, (uint64_t)sm_count() * 8);
+    fill_kernel<<<std::max(blocks, 1), 256, 0, st>>>(p, count, v);
 }
 
 __global__ void to_float_kernel(const double* __restrict__ src, uint64_t n, float* __restrict__ dst) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x)
-        dst[i] = __double2float_rn(src[i]);
+        dst[i] = isinf(src[i]) ? 0.0f : __double2float_rn(src[i]);  // guards / padding -> 0
 }
 
 void launch_to_float(const double* src, uint64_t count, float* dst, cudaStream_t st) {
@@ -68,7 +86,7 @@ __global__ void absmax_kernel(const double* __restrict__ src, uint64_t n, unsign
     double m = 0.0;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x)
-        m = fmax(m, fabs(src[i]));
+        if (!isinf(src[i])) m = fmax(m, fabs(src[i]));  // skip the guard / padding values
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
     if (lane_id() == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
@@ -213,13 +231,13 @@ __device__ __forceinline__ void stage_flush(Stage& sg, const WorkQueue& w, bool 
 }
 
 __device__ __forceinline__ void enqueue(Stage& sg, const WorkQueue& w, bool take, bool near,
-                                        uint32_t q, uint32_t c, double key) {
+                                        uint32_t q, uint32_t c, float key, uint32_t ps) {
     const unsigned lane = lane_id();
     const unsigned fm = __ballot_sync(0xffffffffu, take && near);
     const unsigned bm = __ballot_sync(0xffffffffu, take && !near);
     const unsigned below = (1u << lane) - 1u;
     if (take) {
-        const QEntry e{q, c, key};
+        const QEntry e{q, c, key, ps};
         if (near) sg.fbuf[sg.fn + __popc(fm & below)] = e;
         else sg.bbuf[sg.bn + __popc(bm & below)] = e;
     }
@@ -241,7 +259,7 @@ __global__ void __launch_bounds__(256, 2) lb_compact_kernel(LbCompactArgs a) {
     const uint32_t nqb = (a.nq + QB - 1) / QB;
     const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    const uint32_t total4 = (uint32_t)(a.store.ustride / 4);  // ustride is a multiple of 32d
+    const uint32_t total4 = (uint32_t)(a.store.tstride / 4);  // tiles only (no guard), multiple of 32d
     __shared__ QEntry stage_buf[8][2][kStage];
     Stage sg{stage_buf[threadIdx.x >> 5][0], stage_buf[threadIdx.x >> 5][1], 0u, 0u};
     for (uint64_t w = wid; w < ngroups * nqb; w += nw) {
@@ -264,7 +282,7 @@ __global__ void __launch_bounds__(256, 2) lb_compact_kernel(LbCompactArgs a) {
         for (int qb = 0; qb < QB; ++qb)
 #pragma unroll
             for (int cb = 0; cb < CB; ++cb) acc[qb][cb] = 0.0f;
-        for (uint32_t f = lane; f < total4; f += 32) {
+        auto body = [&](uint32_t f) {
             float4 x[CB];
 #pragma unroll
             for (int cb = 0; cb < CB; ++cb) x[cb] = __ldg(xb + (uint64_t)min((uint32_t)cb, cmax) * xs + f);
@@ -283,6 +301,18 @@ __global__ void __launch_bounds__(256, 2) lb_compact_kernel(LbCompactArgs a) {
                     acc[qb][cb] = sacc;
                 }
             }
+        };
+        if (a.pfx_qn) {
+            // block mode: lane l owns the point quads [l*qn, (l+1)*qn) of every dimension, so its
+            // partial sums are the pair's LB block sums (points [4*l*qn, 4*(l+1)*qn))
+            const uint32_t d = a.store.d, nquad = total4 / d;
+            for (uint32_t j = 0; j < a.pfx_qn; ++j) {
+                const uint32_t g = lane * a.pfx_qn + j;
+                if (g < nquad)
+                    for (uint32_t k = 0; k < d; ++k) body((g >> 3) * 8 * d + 8 * k + (g & 7));
+            }
+        } else {
+            for (uint32_t f = lane; f < total4; f += 32) body(f);
         }
         // warp reduction (round-down adds keep the lower-bound property in any order)
         float mine = 0.0f;
@@ -310,7 +340,25 @@ __global__ void __launch_bounds__(256, 2) lb_compact_kernel(LbCompactArgs a) {
         }
         // pruned pairs are not counted here: the host derives lb_pruned = n - full_dp -
         // early_abandoned (every surviving pair ends in the DP as one of the two)
-        if (a.state) enqueue(sg, a.queue, take, near, q, c, (double)mine);
+        if (a.state) {
+            uint32_t ps = kNoPfx;
+            const unsigned tm = __ballot_sync(0xffffffffu, take);
+            if (a.pfx_out && tm) {
+                // survivors' block sums: one slot per survivor (one atomic per warp tile), each
+                // written by the 32 lanes as one coalesced 128-byte row
+                unsigned base = 0;
+                if (lane == 0) base = atomicAdd(a.pfx_count, (unsigned)__popc(tm));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                const unsigned my = base + __popc(tm & ((1u << lane) - 1u));
+                if (take && my < a.pfx_cap) ps = my;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const uint32_t pj = __shfl_sync(0xffffffffu, ps, j);
+                    if (pj != kNoPfx) a.pfx_out[(uint64_t)pj * kPfxBlocks + lane] = acc[j / CB][j % CB];
+                }
+            }
+            enqueue(sg, a.queue, take, near, q, c, mine, ps);
+        }
     }
     if (a.state) {
         stage_flush(sg, a.queue, true);
@@ -361,7 +409,7 @@ __global__ void __launch_bounds__(256) dk_compact_kernel(DkCompactArgs a) {
             }
         }
         // pruned pairs are not counted here: the host derives early_abandoned = n - full_dp
-        enqueue(sg, a.queue, take, near, q, c, key);
+        enqueue(sg, a.queue, take, near, q, c, __double2float_rd(key), kNoPfx);
     }
     stage_flush(sg, a.queue, true);
     stage_flush(sg, a.queue, false);

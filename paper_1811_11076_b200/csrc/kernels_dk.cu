@@ -122,7 +122,11 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
         QEntry pr;
         if (!queue_get(a.queue, nf, nbk, slot, pr)) break;
         QState* st = a.state ? a.state + pr.q : nullptr;
-        double Tsq = st ? ld_volatile(&st->Tsq) : a.fixed_eps_sq;
+        // one read per warp: the dequeue decision must be warp-uniform (Tsq can drop between
+        // two lanes' reads, and a split warp would deadlock on the next shuffle)
+        double Tsq = a.fixed_eps_sq;
+        if (st && lane == 0) Tsq = ld_volatile(&st->Tsq);
+        if (st) Tsq = __shfl_sync(kFull, Tsq, 0);
         if (!(pr.key <= Tsq)) {  // re-check the admitting first/last-cell bound at dequeue
             if (lane == 0 && st) atomicAdd(&st->early_abandoned, 1ull);
             continue;

@@ -28,8 +28,9 @@
 // every cut cell has v + R > T * margin (margin covers the fl rounding); the
 // final value is Exact iff it is <= T, exactly as dtw_early_abandon (dtw.cpp:82-90).
 #include <algorithm>
+#include <cstdlib>
 
-#include "tsw_internal.cuh"
+#include "dtw_common.cuh"
 
 namespace tswb {
 
@@ -110,7 +111,7 @@ __device__ __forceinline__ void dtw_iter(PairState<G, D>& ps, int it, int gl,
                                          const bool (&slot_ok)[2 * G],
                                          int L, const double* __restrict__ s,
                                          const double* __restrict__ t, uint32_t d,
-                                         const float* __restrict__ pfx, double Tm, bool& alive) {
+                                         const float* __restrict__ pfx, int plog, double Tm, bool& alive) {
     constexpr int P = Period<G, D>::value;
     constexpr int DD = PairState<G, D>::DD;
     if (D > 0 && Prefetch<D>::value) {  // prefetch the two new points of it+1 into the free slots
@@ -149,7 +150,7 @@ __device__ __forceinline__ void dtw_iter(PairState<G, D>& ps, int it, int gl,
             ps.v[e] = valid ? nv : kInf;
             if (CHECK) {
                 const int tj = min(max(ps.tb0 - it - tt, 0), L - 1);
-                alive |= valid && dadd(nv, (double)pfx[tj]) <= Tm;
+                alive |= valid && dadd(nv, (double)pfx[tj >> plog]) <= Tm;
             }
         }
     }
@@ -161,7 +162,7 @@ __device__ __forceinline__ void dtw_body(PairState<G, D>& ps, int it, int gl,
                                          const bool (&slot_ok)[2 * G],
                                          int L, const double* __restrict__ s,
                                          const double* __restrict__ t, uint32_t d,
-                                         const float* __restrict__ pfx, double Tm, bool& alive,
+                                         const float* __restrict__ pfx, int plog, double Tm, bool& alive,
                                          double& fin, int estar) {
     constexpr int P = Period<G, D>::value;
     static_assert(P <= 6, "phase table covers G <= 4");
@@ -169,7 +170,7 @@ __device__ __forceinline__ void dtw_body(PairState<G, D>& ps, int it, int gl,
 #define TSW_ITER(PH)                                                                         \
     if constexpr (PH < P) {                                                                  \
         dtw_iter<G, RPAR, D, WL, (CHECK && PH == P - 1), FULL, PH>(ps, it + PH, gl, lo, span,  \
-                                                             slot_ok, L, s, t, d, pfx, Tm,   \
+                                                             slot_ok, L, s, t, d, pfx, plog, Tm, \
                                                              alive);                         \
         if (it + PH == L - 1) {                                                              \
             _Pragma("unroll") for (int e = 0; e < 2 * G; ++e) if (e == estar) fin = ps.v[e]; \
@@ -197,6 +198,7 @@ __global__ void __launch_bounds__(TPB, MINB) dtw_dp_kernel(DpArgs a, uint32_t ps
     const int L = (int)a.qlen;
     const int r = (int)min(a.r, a.qlen - 1);  // a band wider than the matrix is the full band
     const int stride = D > 0 ? D : (int)d;
+    const int plog = a.pfx_blocks ? (int)a.pfx_log : 0;
 
     // static per-lane band geometry: slot e holds offset o = obase + e
     const int obase = 2 * G * gl - r;
@@ -253,7 +255,11 @@ __global__ void __launch_bounds__(TPB, MINB) dtw_dp_kernel(DpArgs a, uint32_t ps
                     break;
                 }
                 st = a.state ? a.state + pr.q : nullptr;
-                T = st ? ld_volatile(&st->T) : a.fixed_eps;
+                // one read per group: the dequeue decision must be group-uniform (T can drop
+                // between two lanes' reads, and a split group would deadlock on its shuffles)
+                T = a.fixed_eps;
+                if (st && gl == 0) T = ld_volatile(&st->T);
+                if (st) T = __shfl_sync(gmask, T, 0, WL);
                 Tm = __dmul_ru(T, a.margin);
                 if (!(pr.key <= Tm)) {  // re-check the admitting lower bound at dequeue
                     if (gl == 0 && st) atomicAdd(&st->lb_pruned, 1ull);
@@ -264,52 +270,7 @@ __global__ void __launch_bounds__(TPB, MINB) dtw_dp_kernel(DpArgs a, uint32_t ps
             if (!done) {
                 s = a.queries + (uint64_t)pr.q * a.qstride;
                 t = a.store.data + series_off(a.store, pr.c);
-                // cumulative bound: pfx[m] = sum_{j < m} LB_Box term of candidate point j,
-                // 4 consecutive points per lane (float4 over the tiled layout; padding reads 0)
-                if (a.env_lo) {
-                    const float* x32 = a.store.data32 + series_off(a.store, pr.c);
-                    const float* el = a.env_lo + (uint64_t)pr.q * a.qstride;
-                    const float* eh = a.env_hi + (uint64_t)pr.q * a.qstride;
-                    float carry = 0.0f;
-                    if (gl == 0) pfx[0] = 0.0f;
-                    for (int j0 = 0; j0 < L; j0 += 4 * WL) {
-                        const int p0 = j0 + 4 * gl;
-                        float t0 = 0.0f, t1 = 0.0f, t2 = 0.0f, t3 = 0.0f;
-                        if (p0 < L) {
-                            for (int k = 0; k < stride; ++k) {
-                                const uint64_t o = tidx((uint32_t)p0, (uint32_t)k, (uint32_t)stride);
-                                const float4 x = __ldg(reinterpret_cast<const float4*>(x32 + o));
-                                const float4 l = __ldg(reinterpret_cast<const float4*>(el + o));
-                                const float4 hh = __ldg(reinterpret_cast<const float4*>(eh + o));
-                                t0 = lb_term_rd(t0, x.x, l.x, hh.x);
-                                t1 = lb_term_rd(t1, x.y, l.y, hh.y);
-                                t2 = lb_term_rd(t2, x.z, l.z, hh.z);
-                                t3 = lb_term_rd(t3, x.w, l.w, hh.w);
-                            }
-                        }
-                        // local inclusive scan, then a group scan of the lane totals (RD adds
-                        // in any order keep every prefix a lower bound)
-                        t1 = __fadd_rd(t1, t0);
-                        t2 = __fadd_rd(t2, t1);
-                        t3 = __fadd_rd(t3, t2);
-                        float inc = t3;
-#pragma unroll
-                        for (int o = 1; o < WL; o <<= 1) {
-                            const float y = __shfl_up_sync(gmask, inc, o, WL);
-                            if (gl >= o) inc = __fadd_rd(inc, y);
-                        }
-                        float base = __shfl_up_sync(gmask, inc, 1, WL);
-                        if (gl == 0) base = 0.0f;
-                        base = __fadd_rd(base, carry);
-                        if (p0 + 1 <= L) pfx[p0 + 1] = __fadd_rd(base, t0);
-                        if (p0 + 2 <= L) pfx[p0 + 2] = __fadd_rd(base, t1);
-                        if (p0 + 3 <= L) pfx[p0 + 3] = __fadd_rd(base, t2);
-                        if (p0 + 4 <= L) pfx[p0 + 4] = __fadd_rd(base, t3);
-                        carry = __fadd_rd(carry, __shfl_sync(gmask, inc, WL - 1, WL));
-                    }
-                } else {
-                    for (int j = gl; j <= L; j += WL) pfx[j] = 0.0f;
-                }
+                setup_pfx<WL>(a, pr, gl, gmask, pfx, L, stride);
                 __syncwarp(gmask);
                 // band registers; (0,0)'s diagonal predecessor is 0 so that v(0,0) = c + 0 = c
 #pragma unroll
@@ -343,14 +304,14 @@ __global__ void __launch_bounds__(TPB, MINB) dtw_dp_kernel(DpArgs a, uint32_t ps
                 Tm = __dmul_ru(T, a.margin);
             }
             if (G >= 2 && full)
-                dtw_body<G, RPAR, D, WL, true, (G >= 2)>(ps, it, gl, lo, span, slot_ok, L, s, t, d, pfx, Tm, alive, fin, estar);
+                dtw_body<G, RPAR, D, WL, true, (G >= 2)>(ps, it, gl, lo, span, slot_ok, L, s, t, d, pfx, plog, Tm, alive, fin, estar);
             else
-                dtw_body<G, RPAR, D, WL, true, false>(ps, it, gl, lo, span, slot_ok, L, s, t, d, pfx, Tm, alive, fin, estar);
+                dtw_body<G, RPAR, D, WL, true, false>(ps, it, gl, lo, span, slot_ok, L, s, t, d, pfx, plog, Tm, alive, fin, estar);
         } else {
             if (G >= 2 && full)
-                dtw_body<G, RPAR, D, WL, false, (G >= 2)>(ps, it, gl, lo, span, slot_ok, L, s, t, d, pfx, Tm, alive, fin, estar);
+                dtw_body<G, RPAR, D, WL, false, (G >= 2)>(ps, it, gl, lo, span, slot_ok, L, s, t, d, pfx, plog, Tm, alive, fin, estar);
             else
-                dtw_body<G, RPAR, D, WL, false, false>(ps, it, gl, lo, span, slot_ok, L, s, t, d, pfx, Tm, alive, fin, estar);
+                dtw_body<G, RPAR, D, WL, false, false>(ps, it, gl, lo, span, slot_ok, L, s, t, d, pfx, plog, Tm, alive, fin, estar);
         }
         it += P;
         bool finished = false;
@@ -372,26 +333,7 @@ __global__ void __launch_bounds__(TPB, MINB) dtw_dp_kernel(DpArgs a, uint32_t ps
             }
             if (gl == 0) {
                 if (st) T = ld_volatile(&st->T);
-                const bool exact = completed && f <= T;
-                if (a.out_exact) {
-                    a.out_exact[pr.c] = exact ? 1 : 0;
-                    a.out_val[pr.c] = exact ? f : T;
-                }
-                if (exact) {
-                    if (st) {
-                        atomicAdd(&st->full_dp, 1ull);
-                        offer_exact(st, a.slots + (size_t)pr.q * kKMax, a.results, pr.q, f, pr.c,
-                                    false);
-                    } else if (a.results.dist) {  // fixed threshold: append only
-                        const unsigned pos = atomicAdd(a.results.count + pr.q, 1u);
-                        if (pos < a.results.cap) {
-                            a.results.dist[(size_t)pr.q * a.results.cap + pos] = f;
-                            a.results.idx[(size_t)pr.q * a.results.cap + pos] = pr.c;
-                        }
-                    }
-                } else if (st) {
-                    atomicAdd(&st->early_abandoned, 1ull);
-                }
+                finish_pair(a, st, pr, completed, f, T);
             }
             have = false;
         }
@@ -407,7 +349,7 @@ void run(const DpArgs& a, uint32_t max_pairs, cudaStream_t st) {
     constexpr int TPB = (D >= 8 || G >= 4) ? 128 : 256;
     constexpr int MINB = (D >= 8) ? 4 : (G >= 8 ? 1 : (G >= 2 ? 2 : 3));
     const int threads = TPB;
-    const uint32_t pstride = ((a.qlen + 1) + 3) & ~3u;
+    const uint32_t pstride = (std::max<uint32_t>(a.qlen + 1, kPfxBlocks + 1) + 3) & ~3u;
     const size_t smem = (size_t)(threads / WL) * pstride * sizeof(float);
     auto kern = dtw_dp_kernel<G, RPAR, D, WL, TPB, MINB>;
     if (smem > 48 * 1024)
@@ -450,6 +392,10 @@ void run_wide(const DpArgs& a, uint32_t max_pairs, int rpar, cudaStream_t st) {
 }  // namespace
 
 void launch_dtw_dp(const DpArgs& a, uint32_t max_pairs, cudaStream_t st) {
+    if (dtw4_supported(a) && !std::getenv("TSW_DTW_GENERIC")) {
+        launch_dtw4(a, max_pairs, st);
+        return;
+    }
     const uint32_t r = std::min(a.r, a.qlen - 1);
     const uint32_t need = r + 1;  // lanes x G >= r + 1
     const int rpar = (int)(r & 1u);

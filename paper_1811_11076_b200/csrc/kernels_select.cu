@@ -114,7 +114,7 @@ __global__ void seed_kernel(SeedArgs a) {
     for (uint32_t j = threadIdx.x; j < (uint32_t)kKMax; j += blockDim.x) a.slots[(size_t)q * kKMax + j] = kInf;
     for (uint32_t j = threadIdx.x; j < a.probe; j += blockDim.x) {
         const uint32_t c = (uint32_t)((uint64_t)ix[j] * a.n / a.S);
-        a.probe_q.e[(size_t)q * a.probe + j] = QEntry{q, c, 0.0};
+        a.probe_q.e[(size_t)q * a.probe + j] = QEntry{q, c, 0.0f, kNoPfx};
         a.probed[(size_t)c * a.nq + q] = 1;  // candidate-major [n][nq]
     }
     if (q == 0 && threadIdx.x == 0) {

@@ -1,9 +1,13 @@
 // Internal device-side types and helpers shared by the tswarp_b200 kernels.
 //
 // HBM layout: every series is stored in 32-point tiles, dimension-major inside a
-// tile -- element (point p, dim k) at tidx(p, k, d) = (p / 32) * 32d + 32k + p % 32 (zero
-// padding up to a whole tile).  Lanes that read 32 consecutive points of one dimension touch
-// 2 cache lines per load, and the d dimensions of a point sit at immediate offsets 32k.
+// tile -- element (point p, dim k) at tidx(p, k, d) = (p / 32) * 32d + 32k + p % 32.  Lanes that
+// read 32 consecutive points of one dimension touch 2 cache lines per load, and the d
+// dimensions of a point sit at immediate offsets 32k.  Guards: one tile before and after every
+// fp64 series (shared between neighbours) and the padding points of its last tile hold -inf
+// (store) / +inf (queries), so a banded DTW cell outside the matrix costs (+inf - -inf)^2 = +inf
+// with no index clamping or masking (kernels_dtw4.cu); tidx() of p in [-32, 0) lands in the
+// leading guard.  The fp32 copy holds 0 there (LB terms of padding are 0).
 //   store   : series c at data + off(c); a float copy `data32` (round-to-nearest, same layout)
 //             feeds the fp32 LB_Box lower bound.
 //   queries : [nq][qstride] doubles, same layout; envelope: [nq][qstride] floats of midpoints
@@ -40,7 +44,8 @@ struct StoreDev {
     const uint32_t* len;  // per-series length (ragged); nullptr if uniform
     uint32_t n, d;
     uint32_t ulen;        // uniform length (0 if ragged)
-    uint64_t ustride;     // uniform series stride in elements
+    uint64_t ustride;     // uniform series pitch in elements (tiles + one guard tile)
+    uint64_t tstride;     // uniform tiled series length in elements (no guard)
 };
 
 __host__ __device__ inline uint64_t round_even64(uint64_t x) { return (x + 1u) & ~1ull; }
@@ -60,12 +65,15 @@ __device__ __forceinline__ uint32_t series_len(const StoreDev& s, uint32_t i) {
 //    distances of distinct candidates (insertion = CAS on the current maximum slot), so T is
 //    always an upper bound of the true k-th distance; it only ever decreases (atomicMin on the
 //    bit pattern, valid for non-negative doubles).
-struct QState {
+// The threshold words and the counters sit on different 128-byte lines: every DP group reads
+// T once per body, and the per-pair counter atomics must not queue those reads behind them.
+struct alignas(128) QState {
     double T;          // current threshold, distance domain (DTW: squared-sum semantics)
     double Tsq;        // DK only: largest x with sqrt(x) <= T (sqrt monotone)
     unsigned k;        // min(k, n) if k <= kKMax (slots active), else 0 (threshold stays at seed)
     unsigned pad;
-    unsigned long long lb_pruned, full_dp, early_abandoned;
+    alignas(128) unsigned long long lb_pruned;
+    unsigned long long full_dp, early_abandoned;
 };
 
 // Result append buffer: per query `cap` slots (cap = n: a candidate is appended at most once).
@@ -76,12 +84,17 @@ struct ResultBuf {
     uint32_t cap;
 };
 
-// DP work item: query, candidate and the lower bound that admitted it (re-checked at dequeue
-// against the then-current threshold).  DTW: fp32 LB_Box; DK: max(first, last) squared cost.
+// DP work item: query, candidate, the lower bound that admitted it (re-checked at dequeue
+// against the then-current threshold; DTW: fp32 LB_Box, DK: max(first, last) squared cost,
+// rounded down to fp32) and the slot of its LB block sums in the prefix buffer (DTW, else
+// kNoPfx).
 struct QEntry {
     uint32_t q, c;
-    double key;
+    float key;
+    uint32_t ps;
 };
+constexpr uint32_t kNoPfx = 0xffffffffu;
+constexpr int kPfxBlocks = 32;  // LB block sums per pair (one per lane of the LB warp)
 
 // Work queue with two regions: "near" entries fill from the front, "far" entries from the back
 // (a 2-bucket ordering by key / threshold: likely neighbours are processed first).
@@ -187,9 +200,12 @@ void launch_envelope32(const double* q, uint32_t nq, uint32_t d, uint32_t len, u
                        uint32_t r, float err, float* lo, float* hi, cudaStream_t st);
 void launch_envelope64(const double* q, uint32_t nq, uint32_t d, uint32_t len, uint64_t qstride,
                        uint32_t r, double* lo, double* hi, cudaStream_t st);
-// row-major [nser][len][d] -> tiled [nser][stride] (zero padding)
+// row-major [nser][len][d] -> tiled series of `stride` elements at `pitch` spacing; padding
+// points and the guard tile after each series (pitch - stride elements) hold `pad`
 void launch_rowmajor_to_tiled(const double* src, uint64_t nser, uint32_t len, uint32_t d,
-                              uint64_t stride, double* dst, cudaStream_t st);
+                              uint64_t stride, uint64_t pitch, double pad, double* dst,
+                              cudaStream_t st);
+void launch_fill(double* p, uint64_t count, double v, cudaStream_t st);
 // ends[c] = (first point, last point) of every series of a store
 void launch_series_ends(const StoreDev& s, double* ends, cudaStream_t st);
 void launch_to_float(const double* src, uint64_t count, float* dst, cudaStream_t st);
@@ -238,6 +254,11 @@ struct LbCompactArgs {
     const uint8_t* probed;
     WorkQueue queue;
     float* lb_out;        // optional [nq][n] (diagnostics / tsw_lb_box_all)
+    // LB block sums of the survivors (feed the DP's cumulative abandon bound): lane l of the LB
+    // warp owns points [l*B, (l+1)*B), B = 4 * pfx_qn; pfx_qn = 0: off
+    float* pfx_out;       // [pfx_cap][kPfxBlocks]
+    unsigned* pfx_count;
+    uint32_t pfx_cap, pfx_qn;
 };
 void launch_lb_compact(const LbCompactArgs& a, cudaStream_t st);
 
@@ -274,9 +295,15 @@ struct DpArgs {
     double* out_val;
     ResultBuf results;          // exact-result append buffer (results.dist == nullptr: off)
     unsigned long long* cells;  // DP cells evaluated (global accumulator)
+    const float* pfx_blocks;    // DTW: LB block sums by QEntry::ps (nullptr: per-point, in-kernel)
+    uint32_t pfx_log;           // log2 of the block length in points
+    int guarded;                // queries and store carry the +-inf guard tiles
 };
 
 void launch_dtw_dp(const DpArgs& a, uint32_t max_pairs, cudaStream_t st);
+// guarded small-d fast path (kernels_dtw4.cu), chosen by launch_dtw_dp when supported
+bool dtw4_supported(const DpArgs& a);
+void launch_dtw4(const DpArgs& a, uint32_t max_pairs, cudaStream_t st);
 void launch_dk_dp(const DpArgs& a, uint32_t max_pairs, uint32_t max_len, cudaStream_t st);
 
 int sm_count();

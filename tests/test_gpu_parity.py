@@ -89,6 +89,32 @@ def test_dtw_all_bit_exact(tsw, port, N, L, d, r):
         assert ex2[i] == oe and val2[i] == ov, (i, ex2[i], val2[i], oe, ov)
 
 
+@pytest.mark.parametrize("variant", ["1,16", "1,32", "2,8", "2,16", "2,32", "generic"])
+def test_dtw_fast_path_variants(tsw, port, variant, monkeypatch):
+    """Every (cells per lane G, group width WL) instance of the guarded fast path
+    (kernels_dtw4.cu) and the generic kernel, d = 1..4, bands that put offset +r on either
+    lane parity, L not a multiple of the 32-point tile (padding = guard values)."""
+    import oracle
+
+    if variant == "generic":
+        monkeypatch.setenv("TSW_DTW_GENERIC", "1")
+    else:
+        monkeypatch.setenv("TSW_DTW4", variant)
+    rng = np.random.default_rng(12)
+    for d in (1, 2, 3, 4):
+        for L, r in ((1, 0), (5, 2), (37, 6), (45, 7), (70, 14), (70, 15), (100, 30), (120, 52)):
+            X = walks(rng, 24, L, d)
+            q = walks(rng, 1, L, d)[0]
+            ex, val = tsw.dist_all(tsw.Store(X), q, "dtw", r)
+            ref = port.dtw_all(q, oracle.Dataset(X), r)
+            assert ex.all() and np.array_equal(val.view(np.uint64), ref.view(np.uint64)), (d, L, r)
+            Q = np.concatenate([q[None], X[3:4] + 1e-3])
+            gi, gd, _ = tsw.knn(tsw.Dataset(X), Q, 3, "dtw", r)
+            for j in range(len(Q)):
+                oi, od, _ = port.knn(Q[j], oracle.Dataset(X), 3, "dtw", r)
+                assert_knn_equal(gi[j], gd[j], oi, od, f"{variant} d={d} L={L} r={r} q{j}")
+
+
 def test_dtw_spec_kats(tsw):
     # SPEC.md:207-210: s=((0),(0)), t=((1),(1)), r=1 -> 2 ; s=t -> 0
     ex, val = tsw.dist_all(tsw.Store(np.ones((1, 2, 1))), np.zeros((2, 1)), "dtw", 1)
