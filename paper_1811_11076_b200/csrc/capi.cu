@@ -467,6 +467,7 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
     da.qstride = p->qstride;
     da.r = (uint32_t)std::min<uint64_t>(p->r, 0xffffffffu);
     da.state = p->state.p;
+    da.nq = nq;
     da.slots = p->slots.p;
     da.margin = p->margin;
     da.cells = p->cells.p;

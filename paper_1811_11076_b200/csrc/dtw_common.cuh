@@ -108,8 +108,11 @@ __device__ __forceinline__ void setup_pfx(const DpArgs& a, const QEntry& pr, int
 
 // Report a finished pair (one lane): exact iff the DP completed with value <= T, as
 // dtw_early_abandon (dtw.cpp:82-90); exact results feed the device KBest.
+// ab_local: optional per-block shared counters of early-abandoned pairs by query (flushed at the
+// end of the kernel; one global atomic per query per block instead of one per pair).
 __device__ __forceinline__ void finish_pair(const DpArgs& a, QState* st, const QEntry& pr,
-                                            bool completed, double f, double T) {
+                                            bool completed, double f, double T,
+                                            unsigned* ab_local = nullptr) {
     const bool exact = completed && f <= T;
     if (a.out_exact) {
         a.out_exact[pr.c] = exact ? 1 : 0;
@@ -127,7 +130,8 @@ __device__ __forceinline__ void finish_pair(const DpArgs& a, QState* st, const Q
             }
         }
     } else if (st) {
-        atomicAdd(&st->early_abandoned, 1ull);
+        if (ab_local) atomicAdd(ab_local + pr.q, 1u);
+        else atomicAdd(&st->early_abandoned, 1ull);
     }
 }
 

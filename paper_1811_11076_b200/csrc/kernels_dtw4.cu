@@ -32,6 +32,7 @@ namespace tswb {
 namespace {
 
 constexpr unsigned kFull = 0xffffffffu;
+constexpr uint32_t kAbLocalMax = 4096;  // queries with block-local abandon counters
 
 // tiled element offset of point p of a series (p < 0 lands in the leading guard tile)
 template <int D>
@@ -62,6 +63,22 @@ __device__ __forceinline__ double cost(const double (&a)[D], const double (&b)[D
     }
     return acc;
 }
+
+// cp.async (global -> shared, bypassing L1) for the work staging
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+// per-group double buffer of staged work: entries, {T, Tsq} snapshots, LB block rows
+constexpr int kSB = 4;  // pairs per staged batch (small: the T snapshots stay fresh)
+struct Stage {
+    QEntry e[2][kSB];
+    double2 t[2][kSB];
+    float row[2][kSB][kPfxBlocks];
+};
 
 template <int G, int RPAR>
 struct Geo {
@@ -150,13 +167,24 @@ __device__ __forceinline__ void body(Lane<G, D>& s, const double* __restrict__ s
 
 template <int G, int D, int WL, int RPAR, int MINB>
 __global__ void __launch_bounds__(256, MINB) dtw4_kernel(DpArgs a, uint32_t pstride) {
-    extern __shared__ float smem_pfx[];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int P = Geo<G, RPAR>::P;
     constexpr int S0 = Geo<G, RPAR>::S0;
+    constexpr int NG = 256 / WL;  // groups per block
     const int lane = threadIdx.x & 31;
     const int gl = lane % WL;
     const unsigned gmask = WL == 32 ? kFull : (((1u << WL) - 1u) << (lane & ~(WL - 1)));
+    Stage* sg = reinterpret_cast<Stage*>(smem_raw) + threadIdx.x / WL;
+    float* smem_pfx = reinterpret_cast<float*>(smem_raw + NG * sizeof(Stage));
     float* pfx = smem_pfx + (size_t)(threadIdx.x / WL) * pstride;
+    // per-block early-abandon counters by query (nq <= kAbLocalMax), else global atomics
+    unsigned* ab_local = a.state && a.nq <= kAbLocalMax ? reinterpret_cast<unsigned*>(
+                                                              smem_pfx + (size_t)NG * pstride)
+                                                        : nullptr;
+    if (ab_local) {
+        for (uint32_t i = threadIdx.x; i < a.nq; i += blockDim.x) ab_local[i] = 0u;
+        __syncthreads();
+    }
     const int L = (int)a.qlen;
     const int r = (int)min(a.r, a.qlen - 1);
     const int plog = a.pfx_blocks ? (int)a.pfx_log : 0;
@@ -191,58 +219,113 @@ __global__ void __launch_bounds__(256, MINB) dtw4_kernel(DpArgs a, uint32_t pstr
     for (int e = 0; e < 2 * G; ++e) s.v[e] = kInf;
     s.qo = s.co = 0;
 
-    // Next-pair prefetch (group-uniform): stage 1 claims a queue slot, stage 2 reads the entry,
-    // stage 3 reads its threshold and LB block row.  One stage per body, so every link of the
-    // dependent chain atomic -> entry -> (T, row) gets a whole body of latency cover instead of
-    // stalling the warp at the pair switch.
-    constexpr int PER = kPfxBlocks / WL;
-    int pf = 0;
-    unsigned pslot = 0;
-    bool nx_ok = false;
-    QEntry nx{0, 0, 0.0f, kNoPfx};
-    double nxT = a.fixed_eps;
-    float nbv[PER];
+    // Work staging (group-uniform state): the group claims kSB queue slots with one atomic and
+    // copies their entries, then their thresholds and LB block rows, into its shared-memory
+    // double buffer with cp.async -- one stage per body, so the dependent chain atomic ->
+    // entries -> (T, rows) completes behind the DP instead of stalling the warp at every pair
+    // switch.  Pairs are taken from the ready buffer with no global traffic.
+    const unsigned total = nf + nbk;
+    // batch size: WL slots per claim when the queue is deep, down to 1 for short queues (the
+    // probe launch), so that every group of the grid gets work
+    const unsigned ngrid = gridDim.x * (unsigned)NG;
+    const int bsz = (int)max(1u, min((unsigned)kSB, total / (ngrid * 8u)));
+    int cb = 0, ci = 0, cnt0 = -1, cnt1 = -1;  // current buffer, next index, counts (-1: empty)
+    int sst = 0, ncnt = 0;                      // staging stage of buffer cb ^ 1
+    unsigned sbase = 0;
+    bool qdone = false;
+    auto stage_step = [&]() {
+        const int nb = cb ^ 1;
+        if (sst == 0) {
+            if (qdone || (nb ? cnt1 : cnt0) >= 0) return;
+            if (gl == 0) sbase = atomicAdd(a.queue.head, (unsigned)bsz);
+            sst = 1;
+        } else if (sst == 1) {
+            const unsigned base = __shfl_sync(gmask, sbase, 0, WL);
+            ncnt = base >= total ? 0 : (int)min((unsigned)bsz, total - base);
+            if (ncnt == 0) {
+                qdone = true;
+                sst = 0;
+                return;
+            }
+            if (gl < ncnt) {
+                const unsigned slot = base + gl;
+                const QEntry* src = slot < nf ? a.queue.e + slot : a.queue.e + (a.queue.cap - 1 - (slot - nf));
+                cp_async16(&sg->e[nb][gl], src);
+            }
+            cp_async_commit();
+            sst = 2;
+        } else if (sst == 2) {
+            cp_async_wait_all();
+            __syncwarp(gmask);
+            if (gl < ncnt) {
+                const QEntry e = sg->e[nb][gl];
+                if (a.state) cp_async16(&sg->t[nb][gl], &a.state[e.q].T);  // {T, Tsq}
+                else sg->t[nb][gl] = make_double2(a.fixed_eps, a.fixed_eps_sq);
+                float* dst = sg->row[nb][gl];
+                if (a.pfx_blocks && e.ps != kNoPfx) {
+                    const float* srow = a.pfx_blocks + (uint64_t)e.ps * kPfxBlocks;
 #pragma unroll
-    for (int i = 0; i < PER; ++i) nbv[i] = 0.0f;
-    auto advance = [&]() {
-        if (pf == 0) {
-            if (gl == 0) pslot = atomicAdd(a.queue.head, 1u);
-        } else if (pf == 1) {
-            nx_ok = queue_get(a.queue, nf, nbk, __shfl_sync(gmask, pslot, 0, WL), nx);
-        } else if (nx_ok) {
-            if (a.state && gl == 0) nxT = ld_volatile(&a.state[nx.q].T);
-            if (a.pfx_blocks) load_pfx_row<WL>(a, nx.ps, gl, nbv);
+                    for (int i = 0; i < kPfxBlocks; i += 4) cp_async16(dst + i, srow + i);
+                } else {
+#pragma unroll
+                    for (int i = 0; i < kPfxBlocks; i += 4)
+                        *reinterpret_cast<float4*>(dst + i) = make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+            }
+            cp_async_commit();
+            sst = 3;
+        } else {
+            cp_async_wait_all();
+            __syncwarp(gmask);
+            if (nb) cnt1 = ncnt; else cnt0 = ncnt;
+            sst = 0;
         }
-        ++pf;
     };
 
     for (;;) {
-        // ---- groups without a pair take the prefetched one (divergent per group) -----------
+        // ---- groups without a pair take the next staged one (divergent per group) ----------
         if (!have && !done) {
             for (;;) {
-                while (pf < 3) advance();  // finish the pipeline (stalls only if it lagged)
-                pf = 0;
-                if (!nx_ok) {
+                int idx = -1;
+                for (;;) {
+                    if (ci < (cb ? cnt1 : cnt0)) {
+                        idx = ci++;
+                        break;
+                    }
+                    if ((cb ? cnt0 : cnt1) >= 0) {  // next buffer ready: swap, free the old one
+                        if (cb) cnt1 = -1; else cnt0 = -1;
+                        cb ^= 1;
+                        ci = 0;
+                        continue;
+                    }
+                    if (qdone && sst == 0) break;
+                    stage_step();  // lagging: progress synchronously
+                }
+                if (idx < 0) {
                     done = true;
                     break;
                 }
-                pr = nx;
+                pr = sg->e[cb][idx];
                 st = a.state ? a.state + pr.q : nullptr;
-                // gl 0's read, broadcast: the dequeue decision must be group-uniform (T can drop
-                // between two lanes' reads, and a split group would deadlock on its shuffles)
-                T = st ? __shfl_sync(gmask, nxT, 0, WL) : a.fixed_eps;
+                // staged T (>= the current one): the dequeue test stays conservative
+                T = sg->t[cb][idx].x;
                 Tm = __dmul_ru(T, a.margin);
                 if (!((double)pr.key <= Tm)) {  // re-check the admitting lower bound at dequeue
                     if (gl == 0 && st) atomicAdd(&st->lb_pruned, 1ull);
                     continue;
+                }
+                if (a.pfx_blocks) {
+                    float bv[kPfxBlocks / WL];
+#pragma unroll
+                    for (int i = 0; i < kPfxBlocks / WL; ++i) bv[i] = sg->row[cb][idx][gl * (kPfxBlocks / WL) + i];
+                    scan_pfx_row<WL>(bv, gl, gmask, pfx);
                 }
                 break;
             }
             if (!done) {
                 sq = a.queries + (uint64_t)pr.q * a.qstride;
                 tc = a.store.data + series_off(a.store, pr.c);
-                if (a.pfx_blocks) scan_pfx_row<WL>(nbv, gl, gmask, pfx);
-                else setup_pfx<WL>(a, pr, gl, gmask, pfx, L, D);
+                if (!a.pfx_blocks) setup_pfx<WL>(a, pr, gl, gmask, pfx, L, D);
                 __syncwarp(gmask);
 #pragma unroll
                 for (int e = 0; e < 2 * G; ++e) s.v[e] = (gl == pstar && e == estar) ? 0.0 : kInf;
@@ -257,12 +340,11 @@ __global__ void __launch_bounds__(256, MINB) dtw4_kernel(DpArgs a, uint32_t pstr
                 it = 0;
                 fin = kInf;
                 have = true;
-                advance();  // claim the next pair's slot now: two bodies of lead for the rest
             }
         }
         __syncwarp();
         if (!__any_sync(kFull, have)) break;
-        if (have && pf < 3 && (pf < 2 || nx_ok)) advance();
+        if (have) stage_step();
 
         // ---- P iterations (phase-unrolled); abandon check on the last one ------------------
         bool alive = false;
@@ -287,13 +369,18 @@ __global__ void __launch_bounds__(256, MINB) dtw4_kernel(DpArgs a, uint32_t pstr
             }
             // T of the last check (>= the current one): a value in between is exact too and
             // only costs an append (the KBest keeps the k smallest)
-            if (gl == 0) finish_pair(a, st, pr, completed, f, T);
+            if (gl == 0) finish_pair(a, st, pr, completed, f, T, ab_local);
             have = false;
         }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) cells += __shfl_xor_sync(kFull, cells, o);
     if (lane == 0 && a.cells) atomicAdd(a.cells, cells);
+    if (ab_local) {
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < a.nq; i += blockDim.x)
+            if (ab_local[i]) atomicAdd(&a.state[i].early_abandoned, (unsigned long long)ab_local[i]);
+    }
 }
 
 template <int G, int D, int WL, int RPAR>
@@ -301,7 +388,8 @@ void run4(const DpArgs& a, uint32_t max_pairs, cudaStream_t st) {
     constexpr int TPB = 256;
     constexpr int MINB = 2;
     const uint32_t pstride = (std::max<uint32_t>(a.qlen + 1, kPfxBlocks + 1) + 3) & ~3u;
-    const size_t smem = (size_t)(TPB / WL) * pstride * sizeof(float);
+    const size_t smem = (size_t)(TPB / WL) * (sizeof(Stage) + pstride * sizeof(float)) +
+                        (a.state && a.nq <= kAbLocalMax ? a.nq * sizeof(unsigned) : 0);
     auto kern = dtw4_kernel<G, D, WL, RPAR, MINB>;
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -287,6 +287,7 @@ struct DpArgs {
     uint64_t qstride;
     WorkQueue queue;
     QState* state;              // per query (nullptr in fixed-eps mode)
+    uint32_t nq;                // queries of the plan (state has nq entries)
     double* slots;              // [nq][kKMax] threshold slots
     double fixed_eps;           // used when state == nullptr
     double fixed_eps_sq;
