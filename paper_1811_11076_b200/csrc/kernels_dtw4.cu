@@ -101,7 +101,7 @@ template <int G, int D, int WL, int RPAR, bool CHECK, int PH>
 __device__ __forceinline__ void iter(Lane<G, D>& s, const double* __restrict__ sq,
                                      const double* __restrict__ tc, int gl, int edge, int tjb,
                                      unsigned okm, const float* __restrict__ pfx, int plog, int L,
-                                     double Tm, bool& alive) {
+                                     double T, double margin, bool& alive) {
     constexpr int P = Geo<G, RPAR>::P;
     constexpr int FS = Geo<G, RPAR>::FS;
     // prefetch iteration it+1's new points into the free slots
@@ -131,6 +131,7 @@ __device__ __forceinline__ void iter(Lane<G, D>& s, const double* __restrict__ s
             if (e == FS) nv = gl == 0 ? kInf : nv;  // offset -r-1
             s.v[e] = nv;
             if (CHECK) {
+                const double Tm = __dmul_ru(T, margin);
                 const int tj = min(max(tjb - tt, 0), L - 1);
                 alive |= ((okm >> e) & 1u) && dadd(nv, (double)pfx[tj >> plog]) <= Tm;
             }
@@ -143,20 +144,19 @@ __device__ __forceinline__ void body(Lane<G, D>& s, const double* __restrict__ s
                                      const double* __restrict__ tc, int gl, int edge, int it,
                                      int tb0, unsigned okm, const float* __restrict__ pfx, int plog,
                                      int L, const QState* st, double margin, double& T,
-                                     bool& alive, double& fin, int estar) {
+                                     bool& alive, double& fin, bool ehi) {
     constexpr int P = Geo<G, RPAR>::P;
     static_assert(P <= 4, "G <= 2");
     // the threshold is read at the top and consumed by the last phase's check: the load has
     // P-1 iterations of cover (any T >= the current one is a valid abandon threshold)
     if (st) T = ld_volatile(&st->T);
-    const double Tm = __dmul_ru(T, margin);
+    // slot of offset 0: parity RPAR, +2 when ehi (G = 2)
+    constexpr int E0 = RPAR, E1 = G == 2 ? RPAR + 2 : RPAR;
 #define TSW_ITER4(PH)                                                                          \
     if constexpr (PH < P) {                                                                    \
         iter<G, D, WL, RPAR, PH == P - 1, PH>(s, sq, tc, gl, edge, tb0 - (it + PH), okm, pfx,  \
-                                              plog, L, Tm, alive);                             \
-        if (it + PH == L - 1) {                                                                \
-            _Pragma("unroll") for (int e = 0; e < 2 * G; ++e) if (e == estar) fin = s.v[e];    \
-        }                                                                                      \
+                                              plog, L, T, margin, alive);                      \
+        if (it + PH == L - 1) fin = ehi ? s.v[E1] : s.v[E0];                                   \
     }
     TSW_ITER4(0)
     TSW_ITER4(1)
@@ -165,12 +165,12 @@ __device__ __forceinline__ void body(Lane<G, D>& s, const double* __restrict__ s
 #undef TSW_ITER4
 }
 
-template <int G, int D, int WL, int RPAR, int MINB>
-__global__ void __launch_bounds__(256, MINB) dtw4_kernel(DpArgs a, uint32_t pstride) {
+template <int G, int D, int WL, int RPAR, int TPB, int MINB>
+__global__ void __launch_bounds__(TPB, MINB) dtw4_kernel(DpArgs a, uint32_t pstride) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int P = Geo<G, RPAR>::P;
     constexpr int S0 = Geo<G, RPAR>::S0;
-    constexpr int NG = 256 / WL;  // groups per block
+    constexpr int NG = TPB / WL;  // groups per block
     const int lane = threadIdx.x & 31;
     const int gl = lane % WL;
     const unsigned gmask = WL == 32 ? kFull : (((1u << WL) - 1u) << (lane & ~(WL - 1)));
@@ -350,7 +350,7 @@ __global__ void __launch_bounds__(256, MINB) dtw4_kernel(DpArgs a, uint32_t pstr
         bool alive = false;
         if (!have) s.qo = s.co = 0;  // idle group: keep its (ignored) loads inside the guards
         body<G, D, WL, RPAR>(s, sq, tc, gl, edge, it, tb0, okm, pfx, plog, L, st, a.margin, T,
-                             alive, fin, estar);
+                             alive, fin, estar >= 2);
         it += P;
         const unsigned bal = __ballot_sync(kFull, alive) & gmask;
         const bool completed = have && it >= L;
@@ -385,12 +385,13 @@ __global__ void __launch_bounds__(256, MINB) dtw4_kernel(DpArgs a, uint32_t pstr
 
 template <int G, int D, int WL, int RPAR>
 void run4(const DpArgs& a, uint32_t max_pairs, cudaStream_t st) {
-    constexpr int TPB = 256;
-    constexpr int MINB = 2;
+    // 128-thread blocks: finer occupancy steps at ~100 registers per thread
+    constexpr int TPB = 128;
+    constexpr int MINB = 4;
     const uint32_t pstride = (std::max<uint32_t>(a.qlen + 1, kPfxBlocks + 1) + 3) & ~3u;
     const size_t smem = (size_t)(TPB / WL) * (sizeof(Stage) + pstride * sizeof(float)) +
                         (a.state && a.nq <= kAbLocalMax ? a.nq * sizeof(unsigned) : 0);
-    auto kern = dtw4_kernel<G, D, WL, RPAR, MINB>;
+    auto kern = dtw4_kernel<G, D, WL, RPAR, TPB, MINB>;
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
