@@ -195,7 +195,97 @@ __global__ void __launch_bounds__(256) sample_ub_kernel(SampleArgs a) {
     }
 }
 
+// Tiled form for uniform stores whose series have the query length (every DTW store; DK when
+// the lengths agree): a block owns kUQ queries x kUC sampled candidates, stages kUP-point
+// chunks of both sides in shared memory (dimension-major, series fastest) and every thread
+// accumulates 2 x 2 pairs, so each loaded point feeds two pairs.  Same per-point costs and
+// accumulation (DTW: fl sum in any order, scaled up; DK: exact max) as sample_ub_kernel.
+constexpr int kUQ = 16, kUC = 32, kUP = 16;
+constexpr int kUQS = kUQ + 2, kUCS = kUC + 2;  // padded rows: 2-way instead of 16-way store conflicts
+
+constexpr int kUSub = 4;  // threads per pair set (interleaved points), reduced at the end
+
+template <bool DK>
+__global__ void __launch_bounds__(128 * kUSub) sample_ub_tile_kernel(SampleArgs a) {
+    extern __shared__ __align__(16) double usm[];
+    const uint32_t d = a.store.d, L = a.qlen;
+    double* qs = usm;                           // [d][kUP][kUQS]
+    double* cs = usm + (size_t)d * kUP * kUQS;  // [d][kUP][kUCS]
+    const uint32_t q0 = blockIdx.y * kUQ, j0 = blockIdx.x * kUC;
+    const int t = threadIdx.x, sub = t / 128, tp = t % 128;
+    const int tq = tp / (kUC / 2), tc = tp % (kUC / 2);
+    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    for (uint32_t p0 = 0; p0 < L; p0 += kUP) {
+        __syncthreads();
+        // chunk loads: kUP consecutive points of one dimension are contiguous in a tile
+        for (uint32_t e = t; e < (uint32_t)kUQ * d * kUP; e += blockDim.x) {
+            const uint32_t pp = e % kUP, k = (e / kUP) % d, sr = e / (kUP * d);
+            const uint32_t q = min(q0 + sr, a.nq - 1), p = min(p0 + pp, L - 1);
+            qs[(k * kUP + pp) * kUQS + sr] = a.queries[(uint64_t)q * a.qstride + tidx(p, k, d)];
+        }
+        for (uint32_t e = t; e < (uint32_t)kUC * d * kUP; e += blockDim.x) {
+            const uint32_t pp = e % kUP, k = (e / kUP) % d, sr = e / (kUP * d);
+            const uint32_t j = min(j0 + sr, a.S - 1);
+            const uint32_t c = (uint32_t)((uint64_t)j * a.store.n / a.S);
+            const uint32_t p = min(p0 + pp, L - 1);
+            cs[(k * kUP + pp) * kUCS + sr] = a.store.data[series_off(a.store, c) + tidx(p, k, d)];
+        }
+        __syncthreads();
+        const uint32_t np = min((uint32_t)kUP, L - p0);
+        for (uint32_t pp = sub; pp < np; pp += kUSub) {
+            double cst[2][2];
+            for (uint32_t k = 0; k < d; ++k) {
+                const double2 qv = *reinterpret_cast<const double2*>(qs + (k * kUP + pp) * kUQS + 2 * tq);
+                const double2 cv = *reinterpret_cast<const double2*>(cs + (k * kUP + pp) * kUCS + 2 * tc);
+                const double qa[2] = {qv.x, qv.y}, cb[2] = {cv.x, cv.y};
+#pragma unroll
+                for (int x = 0; x < 2; ++x)
+#pragma unroll
+                    for (int y = 0; y < 2; ++y) {
+                        const double e = dsub(qa[x], cb[y]);
+                        cst[x][y] = k == 0 ? dmul(e, e) : dadd(cst[x][y], dmul(e, e));
+                    }
+            }
+#pragma unroll
+            for (int x = 0; x < 2; ++x)
+#pragma unroll
+                for (int y = 0; y < 2; ++y) acc[x][y] = DK ? dmax(acc[x][y], cst[x][y]) : dadd(acc[x][y], cst[x][y]);
+        }
+    }
+    // combine the kUSub interleaved partials (DTW: fl sum in any order, covered by ub_scale)
+    __syncthreads();
+    double* red = usm;  // [kUSub][128][4]
+#pragma unroll
+    for (int x = 0; x < 2; ++x)
+#pragma unroll
+        for (int y = 0; y < 2; ++y) red[((size_t)sub * 128 + tp) * 4 + 2 * x + y] = acc[x][y];
+    __syncthreads();
+    if (sub == 0) {
+#pragma unroll
+        for (int x = 0; x < 2; ++x)
+#pragma unroll
+            for (int y = 0; y < 2; ++y) {
+                double v = acc[x][y];
+                for (int u = 1; u < kUSub; ++u) {
+                    const double w = red[((size_t)u * 128 + tp) * 4 + 2 * x + y];
+                    v = DK ? dmax(v, w) : dadd(v, w);
+                }
+                const uint32_t q = q0 + 2 * tq + x, j = j0 + 2 * tc + y;
+                if (q < a.nq && j < a.S) a.out_ub[(uint64_t)q * a.S + j] = DK ? v : __dmul_ru(v, a.ub_scale);
+            }
+    }
+}
+
 void launch_sample_ub(const SampleArgs& a, cudaStream_t st) {
+    if (a.store.ulen == a.qlen) {
+        const dim3 grid((a.S + kUC - 1) / kUC, (a.nq + kUQ - 1) / kUQ);
+        const size_t smem = std::max<size_t>((size_t)a.store.d * kUP * (kUQS + kUCS),
+                                             (size_t)kUSub * 128 * 4) * sizeof(double);
+        auto kern = a.dk ? sample_ub_tile_kernel<true> : sample_ub_tile_kernel<false>;
+        if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<grid, 128 * kUSub, smem, st>>>(a);
+        return;
+    }
     const uint64_t warps = (uint64_t)a.nq * a.S;
     const int blocks = (int)std::min<uint64_t>((warps * 32 + 255) / 256, (uint64_t)sm_count() * 16);
     sample_ub_kernel<<<std::max(blocks, 1), 256, 0, st>>>(a);
