@@ -396,9 +396,9 @@ void run4(const DpArgs& a, uint32_t max_pairs, cudaStream_t st) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TPB, smem);
+    const uint64_t full = (uint64_t)sm_count() * std::max(per_sm, 1);
     const uint64_t want = ((uint64_t)max_pairs * WL + TPB - 1) / TPB;
-    const int blocks = (int)std::max<uint64_t>(
-        1, std::min<uint64_t>(want, (uint64_t)sm_count() * std::max(per_sm, 1)));
+    const int blocks = (int)std::max<uint64_t>(1, std::min<uint64_t>(want, full));
     kern<<<blocks, TPB, smem, st>>>(a, pstride);
 }
 

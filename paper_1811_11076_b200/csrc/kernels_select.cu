@@ -59,6 +59,111 @@ __global__ void __launch_bounds__(512) select_chunk_kernel(const double* __restr
     }
 }
 
+// ---- small-P selection (P <= kKMax) ---------------------------------------------------------
+// grid (nchunks, nq), 512 threads.  Each warp sorts its 256 values 8 per lane, then extracts its
+// P smallest by P rounds of a warp argmin over the lanes' heads; warp 0 then extracts the
+// chunk's P smallest from the 16 warp lists the same way.  Same (distance, index) order and
+// output as select_chunk_kernel at a fraction of the barrier count.
+__device__ __forceinline__ void cswap(double& a, uint32_t& ia, double& b, uint32_t& ib) {
+    if (pair_less(b, ib, a, ia)) {
+        const double t = a; a = b; b = t;
+        const uint32_t u = ia; ia = ib; ib = u;
+    }
+}
+
+// warp argmin of (v, i) pairs; returns the winning lane (ties broken by the pair order, unique)
+__device__ __forceinline__ int warp_argmin(double& v, uint32_t& i) {
+    int l = (int)(threadIdx.x & 31);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+        const uint32_t oi = __shfl_xor_sync(0xffffffffu, i, o);
+        const int ol = __shfl_xor_sync(0xffffffffu, l, o);
+        if (pair_less(ov, oi, v, i) || (ov == v && oi == i && ol < l)) {
+            v = ov; i = oi; l = ol;
+        }
+    }
+    return l;
+}
+
+__global__ void __launch_bounds__(512) select_small_kernel(const double* __restrict__ in_v,
+                                                           const uint32_t* __restrict__ in_i,
+                                                           const unsigned* __restrict__ counts,
+                                                           uint32_t n_in, uint32_t P,
+                                                           double* __restrict__ out_v,
+                                                           uint32_t* __restrict__ out_i) {
+    __shared__ double wv[16][kKMax];
+    __shared__ uint32_t wi[16][kKMax];
+    const uint32_t q = blockIdx.y, chunk = blockIdx.x, nchunks = gridDim.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const size_t base = (size_t)q * n_in;
+    const uint64_t valid = counts ? (uint64_t)min(counts[q], n_in) : (uint64_t)n_in;
+    const uint64_t rest = valid > (uint64_t)chunk * kSelChunk ? valid - (uint64_t)chunk * kSelChunk : 0;
+    const uint32_t have = rest < (uint64_t)kSelChunk ? (uint32_t)rest : (uint32_t)kSelChunk;
+    double v[8];
+    uint32_t ix[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+        const uint32_t t = warp * 256 + lane + 32 * u;
+        const uint64_t g = (uint64_t)chunk * kSelChunk + t;
+        if (t < have) {
+            v[u] = in_v[base + g];
+            ix[u] = in_i ? in_i[base + g] : (uint32_t)g;
+        } else {
+            v[u] = kInf;
+            ix[u] = 0xffffffffu;
+        }
+    }
+    // insertion network: v[0..7] ascending
+#pragma unroll
+    for (int a = 1; a < 8; ++a)
+#pragma unroll
+        for (int b = a; b > 0; --b) cswap(v[b - 1], ix[b - 1], v[b], ix[b]);
+    const uint32_t wcount = have > (uint32_t)warp * 256 ? min(256u, have - warp * 256) : 0u;
+    const uint32_t wp = min(P, wcount);
+    for (uint32_t r = 0; r < wp; ++r) {
+        double bv = v[0];
+        uint32_t bi = ix[0];
+        const int bl = warp_argmin(bv, bi);
+        if (lane == 0) {
+            wv[warp][r] = bv;
+            wi[warp][r] = bi;
+        }
+        if (lane == bl) {
+#pragma unroll
+            for (int u = 0; u < 7; ++u) {
+                v[u] = v[u + 1];
+                ix[u] = ix[u + 1];
+            }
+            v[7] = kInf;
+            ix[7] = 0xffffffffu;
+        }
+    }
+    for (uint32_t r = wp + lane; r < P; r += 32) {
+        wv[warp][r] = kInf;
+        wi[warp][r] = 0xffffffffu;
+    }
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t hp = 0;  // lane l < 16: head of warp l's list
+        const size_t ob = ((size_t)q * nchunks + chunk) * P;
+        for (uint32_t r = 0; r < P; ++r) {
+            double bv = kInf;
+            uint32_t bi = 0xffffffffu;
+            if (lane < 16 && hp < P) {
+                bv = wv[lane][hp];
+                bi = wi[lane][hp];
+            }
+            const int bl = warp_argmin(bv, bi);
+            if (lane == 0) {
+                out_v[ob + r] = bv;
+                out_i[ob + r] = bi;
+            }
+            if (lane == bl) ++hp;
+        }
+    }
+}
+
 void launch_select_smallest(const double* vals, const uint32_t* idx, const unsigned* counts,
                             uint32_t nq, uint32_t n, uint32_t P,
                             double* scratch_v, uint32_t* scratch_i, double* out_v,
@@ -80,7 +185,10 @@ void launch_select_smallest(const double* vals, const uint32_t* idx, const unsig
             dv = scratch_v + ping * half;
             di = scratch_i + ping * half;
         }
-        select_chunk_kernel<<<dim3(nchunks, nq), 512, 0, st>>>(cur_v, cur_i, cur_c, cur_n, P, dv, di);
+        if (P <= (uint32_t)kKMax)
+            select_small_kernel<<<dim3(nchunks, nq), 512, 0, st>>>(cur_v, cur_i, cur_c, cur_n, P, dv, di);
+        else
+            select_chunk_kernel<<<dim3(nchunks, nq), 512, 0, st>>>(cur_v, cur_i, cur_c, cur_n, P, dv, di);
         if (launches) ++*launches;
         if (nchunks == 1) break;
         cur_v = dv;
