@@ -85,14 +85,19 @@ struct Geo {
     // shift: offset +r lands on slot 2G-1 of its lane; the forced slot S0-1 is even
     static constexpr int S0 = G == 1 ? 1 : (RPAR ? 3 : 1);
     static constexpr int FS = S0 - 1;
-    static constexpr int P = G + 2;  // register slots per point window = iterations per body
+#ifndef TSW_DTW4_PREFETCH
+#define TSW_DTW4_PREFETCH 1
+#endif
+    // register slots per point window = iterations per body: G+2 with the next iteration's
+    // points prefetched, G+1 when they are loaded at the top of their own iteration
+    static constexpr int P = TSW_DTW4_PREFETCH ? G + 2 : G + 1;
 };
 
 template <int G, int D>
 struct Lane {
     double v[2 * G];
-    double S[G + 2][D];  // query points, rotating
-    double T[G + 2][D];  // candidate points, rotating
+    double S[G + 1 + TSW_DTW4_PREFETCH][D];  // query points, rotating
+    double T[G + 1 + TSW_DTW4_PREFETCH][D];  // candidate points, rotating
     int qo, co;          // tiled offsets of the next query / candidate point to load
 };
 
@@ -104,10 +109,14 @@ __device__ __forceinline__ void iter(Lane<G, D>& s, const double* __restrict__ s
                                      double T, double margin, bool& alive) {
     constexpr int P = Geo<G, RPAR>::P;
     constexpr int FS = Geo<G, RPAR>::FS;
-    // prefetch iteration it+1's new points into the free slots
-    ldp<D>(s.S[(P - (PH + 1) % P) % P], sq, s.qo);
+    if constexpr (TSW_DTW4_PREFETCH) {  // iteration it+1's new points into the free slots
+        ldp<D>(s.S[(P - (PH + 1) % P) % P], sq, s.qo);
+        ldp<D>(s.T[(G + 1 + PH) % P], tc, s.co);
+    } else {  // this iteration's new points into the slots just freed
+        ldp<D>(s.S[(P - PH % P) % P], sq, s.qo);
+        ldp<D>(s.T[(G + PH) % P], tc, s.co);
+    }
     s.qo = prev_off<D>(s.qo);
-    ldp<D>(s.T[(G + 1 + PH) % P], tc, s.co);
     s.co = prev_off<D>(s.co);
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
@@ -331,12 +340,11 @@ __global__ void __launch_bounds__(TPB, MINB) dtw4_kernel(DpArgs a, uint32_t pstr
                 for (int e = 0; e < 2 * G; ++e) s.v[e] = (gl == pstar && e == estar) ? 0.0 : kInf;
                 // phase 0: logical window slot == physical slot
 #pragma unroll
-                for (int g = 0; g <= G; ++g) {
-                    ldp<D>(s.S[g], sq, toff<D>(sb0 + g));
-                    ldp<D>(s.T[g], tc, toff<D>(tb0 - g));
-                }
-                s.qo = toff<D>(sb0 - 1);
-                s.co = toff<D>(tb0 - G - 1);
+                for (int g = 1 - TSW_DTW4_PREFETCH; g <= G; ++g) ldp<D>(s.S[g], sq, toff<D>(sb0 + g));
+#pragma unroll
+                for (int g = 0; g < G + TSW_DTW4_PREFETCH; ++g) ldp<D>(s.T[g], tc, toff<D>(tb0 - g));
+                s.qo = toff<D>(sb0 - TSW_DTW4_PREFETCH);
+                s.co = toff<D>(tb0 - G - TSW_DTW4_PREFETCH);
                 it = 0;
                 fin = kInf;
                 have = true;

@@ -27,7 +27,8 @@ from typing import Sequence
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libtswarp_b200.so")
+# TSW_LIB: an alternative build of the same library (A/B measurements of compile-time variants)
+LIB_PATH = os.environ.get("TSW_LIB") or os.path.join(HERE, "lib", "libtswarp_b200.so")
 
 METRIC_DTW = 0
 METRIC_DK = 1
