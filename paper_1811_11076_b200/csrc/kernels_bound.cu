@@ -351,6 +351,7 @@ __global__ void __launch_bounds__(256, 2) lb_compact_kernel(LbCompactArgs a) {
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     const uint32_t total4 = (uint32_t)(a.store.tstride / 4);  // tiles only (no guard), multiple of 32d
     __shared__ QEntry stage_buf[8][2][kStage];
+    extern __shared__ float lb_stash[];  // block mode: [8 warps][32 pairs][32 lanes]
     Stage sg{stage_buf[threadIdx.x >> 5][0], stage_buf[threadIdx.x >> 5][1], 0u, 0u};
     for (uint64_t w = wid; w < ngroups * nqb; w += nw) {
         // candidate-major order: the nqb query blocks of one candidate group run on adjacent
@@ -404,17 +405,29 @@ __global__ void __launch_bounds__(256, 2) lb_compact_kernel(LbCompactArgs a) {
         } else {
             for (uint32_t f = lane; f < total4; f += 32) body(f);
         }
-        // warp reduction (round-down adds keep the lower-bound property in any order)
-        float mine = 0.0f;
+        // block mode: stash the lane's 32 partials (its block sums of the 32 pairs) for the rows
+        float* stash = lb_stash + (size_t)(threadIdx.x >> 5) * 32 * 32;
+        if (a.pfx_out) {
 #pragma unroll
-        for (int qb = 0; qb < QB; ++qb)
+            for (int j = 0; j < 32; ++j) stash[j * 32 + lane] = acc[j / CB][j % CB];
+        }
+        // transpose reduction: at each level a lane keeps half of its pairs and adds the
+        // partner's half, so lane j ends with the sum of pair j in 31 shuffles (round-down adds
+        // keep the lower-bound property in any order)
+        float v[32];
 #pragma unroll
-            for (int cb = 0; cb < CB; ++cb) {
-                float v = acc[qb][cb];
+        for (int j = 0; j < 32; ++j) v[j] = acc[j / CB][j % CB];
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) v = __fadd_rd(v, __shfl_xor_sync(0xffffffffu, v, o));
-                if (lane == (unsigned)(qb * CB + cb)) mine = v;
+        for (int o = 16; o >= 1; o >>= 1) {
+            const bool upper = (lane & o) != 0;
+#pragma unroll
+            for (int i = 0; i < o; ++i) {
+                const float send = upper ? v[i] : v[i + o];
+                const float keep = upper ? v[i + o] : v[i];
+                v[i] = __fadd_rd(keep, __shfl_xor_sync(0xffffffffu, send, o));
             }
+        }
+        const float mine = v[0];
         const uint32_t q = q0 + lane / CB, c = c0 + lane % CB;
         const bool valid = q < a.nq && c < n;
         bool take = false, near = false;
@@ -441,10 +454,11 @@ __global__ void __launch_bounds__(256, 2) lb_compact_kernel(LbCompactArgs a) {
                 base = __shfl_sync(0xffffffffu, base, 0);
                 const unsigned my = base + __popc(tm & ((1u << lane) - 1u));
                 if (take && my < a.pfx_cap) ps = my;
-#pragma unroll
-                for (int j = 0; j < 32; ++j) {
+                __syncwarp();
+                for (unsigned rem = tm; rem; rem &= rem - 1) {
+                    const int j = __ffs(rem) - 1;
                     const uint32_t pj = __shfl_sync(0xffffffffu, ps, j);
-                    if (pj != kNoPfx) a.pfx_out[(uint64_t)pj * kPfxBlocks + lane] = acc[j / CB][j % CB];
+                    if (pj != kNoPfx) a.pfx_out[(uint64_t)pj * kPfxBlocks + lane] = stash[j * 32 + lane];
                 }
             }
             enqueue(sg, a.queue, take, near, q, c, mine, ps);
@@ -460,7 +474,9 @@ void launch_lb_compact(const LbCompactArgs& a, cudaStream_t st) {
     constexpr int QB = 8, CB = 4;
     const uint64_t tiles = (uint64_t)((a.store.n + CB - 1) / CB) * ((a.nq + QB - 1) / QB);
     const int blocks = (int)std::min<uint64_t>((tiles * 32 + 255) / 256, (uint64_t)sm_count() * 8);
-    lb_compact_kernel<QB, CB><<<std::max(blocks, 1), 256, 0, st>>>(a);
+    const size_t smem = a.pfx_out ? (size_t)8 * 32 * 32 * sizeof(float) : 0;
+    if (smem) cudaFuncSetAttribute(lb_compact_kernel<QB, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    lb_compact_kernel<QB, CB><<<std::max(blocks, 1), 256, smem, st>>>(a);
 }
 
 // ---- DK: first / last cell bound fused with compaction ------------------------------------
