@@ -166,6 +166,13 @@ struct tsw_store {
     float err32 = 0.0f;      // >= max |x - fp32(x)| over the store
     std::mutex mu;
     std::unique_ptr<tsw_plan> cached_plan;
+    // candidate envelopes (fp32 midpoint / half-width, store layout) by band radius, for the
+    // reverse LB_Box filter (built once per radius, like the fp32 copy)
+    struct CEnv {
+        uint64_t r;
+        DevBuf<float> m, h;
+    };
+    std::vector<std::unique_ptr<CEnv>> cenv;
     StoreDev dev() const {
         StoreDev s{};
         s.data = data.p + guard;
@@ -184,7 +191,7 @@ struct tsw_store {
 };
 
 // counters layout of a plan
-enum { C_PFRONT = 0, C_PBACK, C_PHEAD, C_MFRONT, C_MBACK, C_MHEAD, C_PFX, C_COUNT = 8 };
+enum { C_PFRONT = 0, C_PBACK, C_PHEAD, C_MFRONT, C_MBACK, C_MHEAD, C_PFX, C_TASK, C_COUNT = 8 };
 
 struct tsw_plan {
     tsw_store* store = nullptr;
@@ -196,6 +203,11 @@ struct tsw_plan {
     DevBuf<double> q, q_rm, ub, sel_sv, sel_v, slots, top_d;
     DevBuf<float> env_lo, env_hi;
     DevBuf<float> pfx;  // DTW: survivors' LB block sums [pfx_cap][kPfxBlocks]
+    // DTW reverse LB bound: fp32 queries, their max |value|, the candidate envelope
+    DevBuf<float> q32;
+    DevBuf<double> qabsmax;
+    const float* cenv_m = nullptr;
+    const float* cenv_h = nullptr;
     uint32_t pfx_qn = 0, pfx_log = 0, pfx_cap = 0;
     DevBuf<uint32_t> sel_si, sel_i, top_i, fin_si;
     DevBuf<double> fin_sv;
@@ -328,6 +340,37 @@ std::unique_ptr<tsw_plan> make_plan(tsw_store* s, uint64_t nq_max, uint64_t qlen
         p->env_hi.alloc(nq_max * p->qstride);
         // LB block sums for the DP's cumulative bound when a lane of the LB warp covers at most
         // 2 point quads per dimension (longer series: per-point prefix computed in the DP)
+        // reverse LB bound: pays when a DP pair is expensive next to its L*d reverse terms (wide
+        // bands; measured: r = 51 -24%, r = 13 / 26 and d = 16 a loss); TSW_LB2=0/1 overrides.
+        // Skipped when the candidate envelope would not fit.
+        const char* lb2e = std::getenv("TSW_LB2");
+        const bool want_lb2 = lb2e ? std::atoi(lb2e) != 0 : r >= 32;
+        if (want_lb2) {
+            const uint64_t bytes = 2 * (s->guard + n * s->ustride) * sizeof(float);
+            size_t fr = 0, tot = 0;
+            cudaMemGetInfo(&fr, &tot);
+            tsw_store::CEnv* ce = nullptr;
+            for (auto& c : s->cenv)
+                if (c->r == r) ce = c.get();
+            if (!ce && bytes < fr / 4) {
+                auto c = std::make_unique<tsw_store::CEnv>();
+                c->r = r;
+                c->m.alloc(s->guard + n * s->ustride);
+                c->h.alloc(s->guard + n * s->ustride);
+                launch_envelope32(s->data.p + s->guard, (uint32_t)n, (uint32_t)s->d, (uint32_t)s->ulen,
+                                  s->ustride, (uint32_t)std::min<uint64_t>(r, 0xffffffffu), 0.0f,
+                                  c->m.p + s->guard, c->h.p + s->guard, p->own);
+                ck(cudaStreamSynchronize(p->own), "candidate envelope");
+                ce = c.get();
+                s->cenv.push_back(std::move(c));
+            }
+            if (ce) {
+                p->cenv_m = ce->m.p + s->guard;
+                p->cenv_h = ce->h.p + s->guard;
+                p->q32.alloc(nq_max * p->qstride);
+                p->qabsmax.alloc(1);
+            }
+        }
         const uint64_t qn = (tiled_stride(qlen, 1) + 127) / 128;
         if (qn <= 2) {
             p->pfx_qn = (uint32_t)qn;
@@ -498,6 +541,16 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
         la.pfx_out = p->pfx_qn ? p->pfx.p : nullptr;
         la.pfx_count = p->counters.p + C_PFX;
         la.pfx_cap = p->pfx_cap;
+        if (p->cenv_m) {  // fused reverse bound (queries in fp32 + their max |value| first)
+            launch_to_float(p->qg(), (uint64_t)nq * p->qstride, p->q32.p, st);
+            launch_absmax(p->qg(), (uint64_t)nq * p->qstride, p->qabsmax.p, st);
+            la.cenv_m = p->cenv_m;
+            la.cenv_h = p->cenv_h;
+            la.q32 = p->q32.p;
+            la.qabsmax = p->qabsmax.p;
+            la.task = p->counters.p + C_TASK;
+            launches += 2;
+        }
         launch_lb_compact(la, st);
     } else {
         DkCompactArgs ka{};

@@ -338,12 +338,121 @@ __device__ __forceinline__ void enqueue(Stage& sg, const WorkQueue& w, bool take
 }
 
 // ---- K2 + K3: fp32 LB_Box tile kernel fused with compaction --------------------------------
-// Tile = CB consecutive candidates x QB queries per warp; after the warp reduction lane
+// Tile = QB queries x CB consecutive candidates per warp; after the warp reduction lane
 // j = qb * CB + cb owns pair (q0 + qb, c0 + cb).
+struct TileOut {
+    float lb;
+    uint32_t q, c, ps;
+    bool take, near;
+};
+
+// One tile: lane j ends with its pair's fp32 LB_Box (rounded down), whether it survives the
+// current threshold (and was not probed), its queue region and -- block mode -- the slot of its
+// LB block-sum row, written here for every survivor.  `stash`: this warp's 32 x 32 floats.
 template <int QB, int CB>
-__global__ void __launch_bounds__(256, 2) lb_compact_kernel(LbCompactArgs a) {
+__device__ __forceinline__ TileOut lb1_tile(const LbCompactArgs& a, uint32_t c0, uint32_t q0,
+                                            float* stash, uint32_t total4) {
     static_assert(QB * CB == 32, "one pair per lane after the reduction");
     const unsigned lane = lane_id();
+    const uint32_t n = a.store.n;
+    // base pointers only (per-query / per-candidate offsets are recomputed: register budget)
+    const float4* xb = reinterpret_cast<const float4*>(a.store.data32) + (uint64_t)c0 * (a.store.ustride / 4);
+    const uint64_t xs = a.store.ustride / 4;
+    const float4* lob = reinterpret_cast<const float4*>(a.env_lo) + (uint64_t)q0 * (a.qstride / 4);
+    const float4* hib = reinterpret_cast<const float4*>(a.env_hi) + (uint64_t)q0 * (a.qstride / 4);
+    const uint64_t qs = a.qstride / 4;
+    const uint32_t cmax = n - 1 - c0, qmax = a.nq - 1 - q0;  // clamp tails to valid rows
+    float acc[QB][CB];
+#pragma unroll
+    for (int qb = 0; qb < QB; ++qb)
+#pragma unroll
+        for (int cb = 0; cb < CB; ++cb) acc[qb][cb] = 0.0f;
+    auto body = [&](uint32_t f) {
+        float4 x[CB];
+#pragma unroll
+        for (int cb = 0; cb < CB; ++cb) x[cb] = __ldg(xb + (uint64_t)min((uint32_t)cb, cmax) * xs + f);
+#pragma unroll
+        for (int qb = 0; qb < QB; ++qb) {
+            const uint64_t qo = (uint64_t)min((uint32_t)qb, qmax) * qs + f;
+            const float4 l = __ldg(lob + qo);
+            const float4 h = __ldg(hib + qo);
+#pragma unroll
+            for (int cb = 0; cb < CB; ++cb) {
+                float sacc = acc[qb][cb];
+                sacc = lb_term_rd(sacc, x[cb].x, l.x, h.x);
+                sacc = lb_term_rd(sacc, x[cb].y, l.y, h.y);
+                sacc = lb_term_rd(sacc, x[cb].z, l.z, h.z);
+                sacc = lb_term_rd(sacc, x[cb].w, l.w, h.w);
+                acc[qb][cb] = sacc;
+            }
+        }
+    };
+    if (a.pfx_qn) {
+        // block mode: lane l owns the point quads [l*qn, (l+1)*qn) of every dimension, so its
+        // partial sums are the pair's LB block sums (points [4*l*qn, 4*(l+1)*qn))
+        const uint32_t d = a.store.d, nquad = total4 / d;
+        for (uint32_t j = 0; j < a.pfx_qn; ++j) {
+            const uint32_t g = lane * a.pfx_qn + j;
+            if (g < nquad)
+                for (uint32_t k = 0; k < d; ++k) body((g >> 3) * 8 * d + 8 * k + (g & 7));
+        }
+    } else {
+        for (uint32_t f = lane; f < total4; f += 32) body(f);
+    }
+    // block mode: stash the lane's 32 partials (its block sums of the 32 pairs) for the rows
+    if (a.pfx_out) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) stash[j * 32 + lane] = acc[j / CB][j % CB];
+    }
+    // transpose reduction: at each level a lane keeps half of its pairs and adds the partner's
+    // half, so lane j ends with the sum of pair j in 31 shuffles (round-down adds keep the
+    // lower-bound property in any order)
+    float v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = acc[j / CB][j % CB];
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        const bool upper = (lane & o) != 0;
+#pragma unroll
+        for (int i = 0; i < o; ++i) {
+            const float send = upper ? v[i] : v[i + o];
+            const float keep = upper ? v[i + o] : v[i];
+            v[i] = __fadd_rd(keep, __shfl_xor_sync(0xffffffffu, send, o));
+        }
+    }
+    TileOut t{v[0], q0 + lane / CB, c0 + lane % CB, kNoPfx, false, false};
+    const bool valid = t.q < a.nq && t.c < n;
+    if (valid) {
+        const double lb = (double)t.lb;
+        if (a.lb_out) a.lb_out[(uint64_t)t.q * n + t.c] = t.lb;
+        if (a.state) {
+            const double T = a.state[t.q].T;
+            const bool probed = a.probed && a.probed[(uint64_t)t.c * a.nq + t.q];
+            t.take = !probed && lb <= __dmul_ru(T, a.margin);
+            t.near = lb <= a.near_frac * T;
+        }
+    }
+    const unsigned tm = __ballot_sync(0xffffffffu, t.take);
+    if (a.pfx_out && tm) {
+        // survivors' block sums: one slot per survivor (one atomic per warp tile), each written
+        // by the 32 lanes as one coalesced 128-byte row
+        unsigned base = 0;
+        if (lane == 0) base = atomicAdd(a.pfx_count, (unsigned)__popc(tm));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        const unsigned my = base + __popc(tm & ((1u << lane) - 1u));
+        if (t.take && my < a.pfx_cap) t.ps = my;
+        __syncwarp();
+        for (unsigned rem = tm; rem; rem &= rem - 1) {
+            const int j = __ffs(rem) - 1;
+            const uint32_t pj = __shfl_sync(0xffffffffu, t.ps, j);
+            if (pj != kNoPfx) a.pfx_out[(uint64_t)pj * kPfxBlocks + lane] = stash[j * 32 + lane];
+        }
+    }
+    return t;
+}
+
+template <int QB, int CB>
+__global__ void __launch_bounds__(256, 2) lb_compact_kernel(LbCompactArgs a) {
     const uint32_t n = a.store.n;
     const uint64_t ngroups = (n + CB - 1) / CB;
     const uint32_t nqb = (a.nq + QB - 1) / QB;
@@ -353,116 +462,16 @@ __global__ void __launch_bounds__(256, 2) lb_compact_kernel(LbCompactArgs a) {
     __shared__ QEntry stage_buf[8][2][kStage];
     extern __shared__ float lb_stash[];  // block mode: [8 warps][32 pairs][32 lanes]
     Stage sg{stage_buf[threadIdx.x >> 5][0], stage_buf[threadIdx.x >> 5][1], 0u, 0u};
+    float* stash = lb_stash + (size_t)(threadIdx.x >> 5) * 32 * 32;
     for (uint64_t w = wid; w < ngroups * nqb; w += nw) {
         // candidate-major order: the nqb query blocks of one candidate group run on adjacent
         // warps, so the group's bytes come from HBM once and are re-read from L1/L2
         const uint64_t cg = w / nqb;
         const uint32_t qbk = (uint32_t)(w - cg * nqb);
-        const uint32_t c0 = (uint32_t)cg * CB;
-        const uint32_t q0 = qbk * QB;
-        // base pointers only (per-query / per-candidate offsets are recomputed: register budget)
-        const float4* xb = reinterpret_cast<const float4*>(a.store.data32) +
-                           (uint64_t)c0 * (a.store.ustride / 4);
-        const uint64_t xs = a.store.ustride / 4;
-        const float4* lob = reinterpret_cast<const float4*>(a.env_lo) + (uint64_t)q0 * (a.qstride / 4);
-        const float4* hib = reinterpret_cast<const float4*>(a.env_hi) + (uint64_t)q0 * (a.qstride / 4);
-        const uint64_t qs = a.qstride / 4;
-        const uint32_t cmax = n - 1 - c0, qmax = a.nq - 1 - q0;  // clamp tails to valid rows
-        float acc[QB][CB];
-#pragma unroll
-        for (int qb = 0; qb < QB; ++qb)
-#pragma unroll
-            for (int cb = 0; cb < CB; ++cb) acc[qb][cb] = 0.0f;
-        auto body = [&](uint32_t f) {
-            float4 x[CB];
-#pragma unroll
-            for (int cb = 0; cb < CB; ++cb) x[cb] = __ldg(xb + (uint64_t)min((uint32_t)cb, cmax) * xs + f);
-#pragma unroll
-            for (int qb = 0; qb < QB; ++qb) {
-                const uint64_t qo = (uint64_t)min((uint32_t)qb, qmax) * qs + f;
-                const float4 l = __ldg(lob + qo);
-                const float4 h = __ldg(hib + qo);
-#pragma unroll
-                for (int cb = 0; cb < CB; ++cb) {
-                    float sacc = acc[qb][cb];
-                    sacc = lb_term_rd(sacc, x[cb].x, l.x, h.x);
-                    sacc = lb_term_rd(sacc, x[cb].y, l.y, h.y);
-                    sacc = lb_term_rd(sacc, x[cb].z, l.z, h.z);
-                    sacc = lb_term_rd(sacc, x[cb].w, l.w, h.w);
-                    acc[qb][cb] = sacc;
-                }
-            }
-        };
-        if (a.pfx_qn) {
-            // block mode: lane l owns the point quads [l*qn, (l+1)*qn) of every dimension, so its
-            // partial sums are the pair's LB block sums (points [4*l*qn, 4*(l+1)*qn))
-            const uint32_t d = a.store.d, nquad = total4 / d;
-            for (uint32_t j = 0; j < a.pfx_qn; ++j) {
-                const uint32_t g = lane * a.pfx_qn + j;
-                if (g < nquad)
-                    for (uint32_t k = 0; k < d; ++k) body((g >> 3) * 8 * d + 8 * k + (g & 7));
-            }
-        } else {
-            for (uint32_t f = lane; f < total4; f += 32) body(f);
-        }
-        // block mode: stash the lane's 32 partials (its block sums of the 32 pairs) for the rows
-        float* stash = lb_stash + (size_t)(threadIdx.x >> 5) * 32 * 32;
-        if (a.pfx_out) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j) stash[j * 32 + lane] = acc[j / CB][j % CB];
-        }
-        // transpose reduction: at each level a lane keeps half of its pairs and adds the
-        // partner's half, so lane j ends with the sum of pair j in 31 shuffles (round-down adds
-        // keep the lower-bound property in any order)
-        float v[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = acc[j / CB][j % CB];
-#pragma unroll
-        for (int o = 16; o >= 1; o >>= 1) {
-            const bool upper = (lane & o) != 0;
-#pragma unroll
-            for (int i = 0; i < o; ++i) {
-                const float send = upper ? v[i] : v[i + o];
-                const float keep = upper ? v[i + o] : v[i];
-                v[i] = __fadd_rd(keep, __shfl_xor_sync(0xffffffffu, send, o));
-            }
-        }
-        const float mine = v[0];
-        const uint32_t q = q0 + lane / CB, c = c0 + lane % CB;
-        const bool valid = q < a.nq && c < n;
-        bool take = false, near = false;
-        if (valid) {
-            const double lb = (double)mine;
-            if (a.lb_out) a.lb_out[(uint64_t)q * n + c] = mine;
-            if (a.state) {
-                const double T = a.state[q].T;
-                const bool probed = a.probed && a.probed[(uint64_t)c * a.nq + q];
-                take = !probed && lb <= __dmul_ru(T, a.margin);
-                near = lb <= a.near_frac * T;
-            }
-        }
+        const TileOut t = lb1_tile<QB, CB>(a, (uint32_t)cg * CB, qbk * QB, stash, total4);
         // pruned pairs are not counted here: the host derives lb_pruned = n - full_dp -
         // early_abandoned (every surviving pair ends in the DP as one of the two)
-        if (a.state) {
-            uint32_t ps = kNoPfx;
-            const unsigned tm = __ballot_sync(0xffffffffu, take);
-            if (a.pfx_out && tm) {
-                // survivors' block sums: one slot per survivor (one atomic per warp tile), each
-                // written by the 32 lanes as one coalesced 128-byte row
-                unsigned base = 0;
-                if (lane == 0) base = atomicAdd(a.pfx_count, (unsigned)__popc(tm));
-                base = __shfl_sync(0xffffffffu, base, 0);
-                const unsigned my = base + __popc(tm & ((1u << lane) - 1u));
-                if (take && my < a.pfx_cap) ps = my;
-                __syncwarp();
-                for (unsigned rem = tm; rem; rem &= rem - 1) {
-                    const int j = __ffs(rem) - 1;
-                    const uint32_t pj = __shfl_sync(0xffffffffu, ps, j);
-                    if (pj != kNoPfx) a.pfx_out[(uint64_t)pj * kPfxBlocks + lane] = stash[j * 32 + lane];
-                }
-            }
-            enqueue(sg, a.queue, take, near, q, c, mine, ps);
-        }
+        if (a.state) enqueue(sg, a.queue, t.take, t.near, t.q, t.c, t.lb, t.ps);
     }
     if (a.state) {
         stage_flush(sg, a.queue, true);
@@ -470,11 +479,146 @@ __global__ void __launch_bounds__(256, 2) lb_compact_kernel(LbCompactArgs a) {
     }
 }
 
+// ---- K2 + reverse LB_Box + K3 ---------------------------------------------------------------
+// A warp owns one candidate group (CB candidates) against ALL queries: the forward tiles run
+// as above, their survivors are listed in shared memory, and the list gets the reverse bound
+// (query points against the candidate's envelope, LB_Keogh's other direction) candidate by
+// candidate -- the candidate's envelope chunk is loaded into registers once and every listed
+// query of that candidate streams its fp32 row (L1-resident: all warps share the queries).
+// A pair enters the DP queue iff max(forward, reverse) <= T * margin.  Reverse term:
+// max(|q32 - m| - RU(h + eq), 0)^2 with RZ / RD rounding, eq >= |q - fp32(q)|: a rigorous lower
+// bound of dist(q, [lo, hi])^2.
+constexpr int kList = 128;  // listed survivors per warp before a reverse-bound flush
+
+template <int QB, int CB, int FCH>  // FCH: float4 per lane per envelope chunk
+__device__ __forceinline__ void lb2_flush(const LbCompactArgs& a, uint32_t c0, QEntry* list,
+                                          float* l2, int cnt, uint32_t total4, float eq, Stage& sg) {
+    const unsigned lane = lane_id();
+    __syncwarp();
+    for (int i = lane; i < cnt; i += 32) l2[i] = 0.0f;
+    __syncwarp();
+    const float4* q4 = reinterpret_cast<const float4*>(a.q32);
+    const uint32_t qs4 = (uint32_t)(a.qstride / 4);
+    for (int cb = 0; cb < CB; ++cb) {
+        const uint32_t c = c0 + cb;
+        if (c >= a.store.n) break;
+        const uint64_t co = series_off(a.store, c) / 4;
+        const float4* m4 = reinterpret_cast<const float4*>(a.cenv_m) + co;
+        const float4* h4 = reinterpret_cast<const float4*>(a.cenv_h) + co;
+        for (uint32_t f0 = 0; f0 < total4; f0 += 32 * FCH) {
+            // the candidate's envelope chunk in registers, shared by its listed queries
+            float4 mv[FCH], hv[FCH];
+#pragma unroll
+            for (int i = 0; i < FCH; ++i) {
+                const uint32_t f = f0 + lane + 32 * i;
+                if (f < total4) {
+                    mv[i] = __ldg(m4 + f);
+                    const float4 h = __ldg(h4 + f);
+                    hv[i] = make_float4(__fadd_ru(h.x, eq), __fadd_ru(h.y, eq), __fadd_ru(h.z, eq),
+                                        __fadd_ru(h.w, eq));
+                } else {  // outside the series: terms of 0
+                    mv[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    hv[i] = make_float4(kInfF, kInfF, kInfF, kInfF);
+                }
+            }
+            for (int e = 0; e < cnt; ++e) {
+                const QEntry en = list[e];
+                if (en.c != c) continue;
+                const float4* qr = q4 + (uint64_t)en.q * qs4;
+                float t = 0.0f;
+#pragma unroll
+                for (int i = 0; i < FCH; ++i) {
+                    const uint32_t f = f0 + lane + 32 * i;
+                    const float4 x = f < total4 ? __ldg(qr + f) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    t = lb_term_rd(t, x.x, mv[i].x, hv[i].x);
+                    t = lb_term_rd(t, x.y, mv[i].y, hv[i].y);
+                    t = lb_term_rd(t, x.z, mv[i].z, hv[i].z);
+                    t = lb_term_rd(t, x.w, mv[i].w, hv[i].w);
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) t = __fadd_rd(t, __shfl_xor_sync(0xffffffffu, t, o));
+                if (lane == 0) l2[e] = __fadd_rd(l2[e], t);
+            }
+        }
+    }
+    __syncwarp();
+    // decisions and staged enqueue, 32 listed pairs per round (one per lane)
+    for (int b = 0; b < cnt; b += 32) {
+        const int e = b + (int)lane;
+        bool take = false, near = false;
+        QEntry en{0, 0, 0.0f, kNoPfx};
+        if (e < cnt) {
+            en = list[e];
+            en.key = fmaxf(en.key, l2[e]);
+            const double T = a.state[en.q].T;
+            take = (double)en.key <= __dmul_ru(T, a.margin);
+            near = (double)en.key <= a.near_frac * T;
+        }
+        enqueue(sg, a.queue, take, near, en.q, en.c, en.key, en.ps);
+    }
+    __syncwarp();
+}
+
+template <int QB, int CB, int FCH>
+__global__ void __launch_bounds__(256, 2) lb12_compact_kernel(LbCompactArgs a) {
+    const unsigned lane = lane_id();
+    const uint32_t n = a.store.n;
+    const uint32_t ngroups = (n + CB - 1) / CB;
+    const uint32_t nqb = (a.nq + QB - 1) / QB;
+    const uint32_t total4 = (uint32_t)(a.store.tstride / 4);
+    __shared__ QEntry stage_buf[8][2][kStage];
+    // dynamic: survivor lists [8][kList] QEntry, their reverse bounds [8][kList] float, then
+    // (block mode) the LB block-sum stash [8 warps][32 pairs][32 lanes]
+    extern __shared__ __align__(16) unsigned char lb12_smem[];
+    const int wib = threadIdx.x >> 5;
+    Stage sg{stage_buf[wib][0], stage_buf[wib][1], 0u, 0u};
+    QEntry* list = reinterpret_cast<QEntry*>(lb12_smem) + (size_t)wib * kList;
+    float* l2 = reinterpret_cast<float*>(lb12_smem + 8 * kList * sizeof(QEntry)) + (size_t)wib * kList;
+    float* stash = reinterpret_cast<float*>(lb12_smem + 8 * kList * (sizeof(QEntry) + sizeof(float))) +
+                   (size_t)wib * 32 * 32;
+    const float eq = __double2float_ru(__dmul_ru(*a.qabsmax, 0x1p-24));
+    for (;;) {
+        unsigned cg = 0;
+        if (lane == 0) cg = atomicAdd(a.task, 1u);  // dynamic: groups' reverse work varies
+        cg = __shfl_sync(0xffffffffu, cg, 0);
+        if (cg >= ngroups) break;
+        const uint32_t c0 = cg * CB;
+        int cnt = 0;
+        for (uint32_t qbk = 0; qbk < nqb; ++qbk) {
+            const TileOut t = lb1_tile<QB, CB>(a, c0, qbk * QB, stash, total4);
+            const unsigned tm = __ballot_sync(0xffffffffu, t.take);
+            if (t.take) list[cnt + __popc(tm & ((1u << lane) - 1u))] = QEntry{t.q, t.c, t.lb, t.ps};
+            cnt += __popc(tm);
+            if (cnt > kList - 32) {
+                lb2_flush<QB, CB, FCH>(a, c0, list, l2, cnt, total4, eq, sg);
+                cnt = 0;
+            }
+        }
+        if (cnt) lb2_flush<QB, CB, FCH>(a, c0, list, l2, cnt, total4, eq, sg);
+    }
+    stage_flush(sg, a.queue, true);
+    stage_flush(sg, a.queue, false);
+}
+
 void launch_lb_compact(const LbCompactArgs& a, cudaStream_t st) {
     constexpr int QB = 8, CB = 4;
+    const size_t smem = a.pfx_out ? (size_t)8 * 32 * 32 * sizeof(float) : 0;
+    if (a.cenv_m && a.state) {
+        // fused forward + reverse bound; envelope chunk = the whole series when it fits 4
+        // float4 per lane
+        const uint32_t total4 = (uint32_t)(a.store.tstride / 4);
+        const uint32_t fpl = (total4 + 31) / 32;
+        auto kern = lb12_compact_kernel<QB, CB, 4>;
+        if (fpl <= 1) kern = lb12_compact_kernel<QB, CB, 1>;
+        else if (fpl <= 2) kern = lb12_compact_kernel<QB, CB, 2>;
+        else if (fpl <= 3) kern = lb12_compact_kernel<QB, CB, 3>;
+        const size_t smem12 = (size_t)8 * kList * (sizeof(QEntry) + sizeof(float)) + smem;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem12);
+        kern<<<sm_count() * 2, 256, smem12, st>>>(a);
+        return;
+    }
     const uint64_t tiles = (uint64_t)((a.store.n + CB - 1) / CB) * ((a.nq + QB - 1) / QB);
     const int blocks = (int)std::min<uint64_t>((tiles * 32 + 255) / 256, (uint64_t)sm_count() * 8);
-    const size_t smem = a.pfx_out ? (size_t)8 * 32 * 32 * sizeof(float) : 0;
     if (smem) cudaFuncSetAttribute(lb_compact_kernel<QB, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     lb_compact_kernel<QB, CB><<<std::max(blocks, 1), 256, smem, st>>>(a);
 }

@@ -114,12 +114,13 @@ __global__ void __launch_bounds__(512) select_small_kernel(const double* __restr
             ix[u] = 0xffffffffu;
         }
     }
-    // insertion network: v[0..7] ascending
-#pragma unroll
-    for (int a = 1; a < 8; ++a)
-#pragma unroll
-        for (int b = a; b > 0; --b) cswap(v[b - 1], ix[b - 1], v[b], ix[b]);
     const uint32_t wcount = have > (uint32_t)warp * 256 ? min(256u, have - warp * 256) : 0u;
+    if (wcount > 0) {  // insertion network: v[0..7] ascending (empty warps skip it)
+#pragma unroll
+        for (int a = 1; a < 8; ++a)
+#pragma unroll
+            for (int b = a; b > 0; --b) cswap(v[b - 1], ix[b - 1], v[b], ix[b]);
+    }
     const uint32_t wp = min(P, wcount);
     for (uint32_t r = 0; r < wp; ++r) {
         double bv = v[0];

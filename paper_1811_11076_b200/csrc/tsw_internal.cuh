@@ -26,6 +26,7 @@ constexpr int kWarp = 32;
 constexpr int kKMax = 64;       // device top-k list capacity (threshold tightening)
 constexpr int kSelChunk = 4096; // bitonic selection chunk
 constexpr double kInf = __builtin_huge_val();
+constexpr float kInfF = __builtin_huge_valf();
 constexpr uint32_t kTile = 32;  // points per layout tile
 
 // element offset of (point p, dim k) in a tiled series of dimension d
@@ -259,6 +260,13 @@ struct LbCompactArgs {
     float* pfx_out;       // [pfx_cap][kPfxBlocks]
     unsigned* pfx_count;
     uint32_t pfx_cap, pfx_qn;
+    // reverse LB_Box (query points against the CANDIDATE's envelope, LB_Keogh's other
+    // direction), fused when cenv_m is set: a pair survives iff max(forward, reverse) <= T*margin
+    const float* cenv_m;      // candidate envelope midpoints, store layout (pitch ustride)
+    const float* cenv_h;      // half-widths (rounded up; exact interval, no value error)
+    const float* q32;         // fp32 (round-to-nearest) queries, pitch qstride
+    const double* qabsmax;    // max |query value|: the fp32 conversion error is <= it * 2^-24
+    unsigned* task;           // candidate-group work counter (zeroed per execute)
 };
 void launch_lb_compact(const LbCompactArgs& a, cudaStream_t st);
 

@@ -195,6 +195,29 @@ def test_knn_random_datasets(tsw, best_oracle):
                 _check_counters(gc[q], n, metric)
 
 
+@pytest.mark.parametrize("lb2", ["0", "1"])
+def test_knn_reverse_bound_modes(tsw, best_oracle, lb2, monkeypatch):
+    """The fused forward + reverse LB_Box pass (TSW_LB2=1: query points against the candidate
+    envelope) and the forward-only pass give the reference's neighbours on the same inputs:
+    ragged tails (L not a multiple of 32), d = 1..5, LB block-sum rows on and off (L <= 256 /
+    longer), narrow and wide bands."""
+    import oracle
+
+    monkeypatch.setenv("TSW_LB2", lb2)
+    rng = np.random.default_rng(31)
+    for n, L, d, r, k in ((150, 20, 1, 3, 2), (300, 45, 3, 6, 1), (200, 97, 2, 20, 4),
+                          (120, 130, 4, 40, 3), (80, 300, 3, 33, 2), (60, 64, 5, 10, 5)):
+        X = walks(rng, n, L, d)
+        Q = walks(rng, 4, L, d)
+        Q[1] = X[7] + 1e-3 * rng.standard_normal((L, d))
+        gi, gd, gc = tsw.knn(tsw.Dataset(X), Q, k, "dtw", r)
+        ods = oracle.Dataset(X)
+        for q in range(len(Q)):
+            oi, od, _ = best_oracle.knn(Q[q], ods, k, "dtw", r)
+            assert_knn_equal(gi[q], gd[q], oi, od, f"lb2={lb2} n={n} L={L} d={d} r={r} q{q}")
+            _check_counters(gc[q], n, "dtw")
+
+
 def test_knn_ties_and_duplicates(tsw, best_oracle):
     import oracle
 
