@@ -199,6 +199,8 @@ struct tsw_plan {
     int metric = 0;
     uint64_t nq = 0;  // queries of the last set_queries
     cudaStream_t own = nullptr;
+    cudaStream_t aux = nullptr;  // DTW probe DP, overlapped with the LB pass
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     DevBuf<double> qends;  // DK compaction scratch [2d][nq_max]
     DevBuf<double> q, q_rm, ub, sel_sv, sel_v, slots, top_d;
     DevBuf<float> env_lo, env_hi;
@@ -239,6 +241,9 @@ struct tsw_plan {
         for (auto& e : ev)
             if (e) cudaEventDestroy(e);
         if (own) cudaStreamDestroy(own);
+        if (aux) cudaStreamDestroy(aux);
+        if (fork_ev) cudaEventDestroy(fork_ev);
+        if (join_ev) cudaEventDestroy(join_ev);
     }
     double* qg() const { return q.p + store->d * kTile; }  // first query (after the leading guard)
     WorkQueue probe_wq() const {
@@ -329,6 +334,9 @@ std::unique_ptr<tsw_plan> make_plan(tsw_store* s, uint64_t nq_max, uint64_t qlen
     p->probe = p->kk <= (uint64_t)kKMax ? std::min<uint64_t>({p->S, (uint64_t)kKMax, want_probe}) : 0;
     p->P = std::max<uint64_t>(1, std::min<uint64_t>(kKMax, std::max(p->kk, p->probe)));
     ck(cudaStreamCreateWithFlags(&p->own, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaStreamCreateWithFlags(&p->aux, cudaStreamNonBlocking), "cudaStreamCreate");
+    ck(cudaEventCreateWithFlags(&p->fork_ev, cudaEventDisableTiming), "cudaEventCreate");
+    ck(cudaEventCreateWithFlags(&p->join_ev, cudaEventDisableTiming), "cudaEventCreate");
     for (auto& e : p->ev) ck(cudaEventCreate(&e), "cudaEventCreate");
     p->q.alloc(kTile * s->d + nq_max * p->qstride);
     launch_fill(p->q.p, kTile * s->d, INFINITY, p->own);  // leading guard of query 0
@@ -517,13 +525,27 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
     da.results = ResultBuf{p->res_d.p, p->res_i.p, p->res_n.p, n};
     da.pfx_blocks = p->pfx_qn ? p->pfx.p : nullptr;
     da.pfx_log = p->pfx_log;
-    auto run_dp = [&](const WorkQueue& w, uint32_t max_pairs) {
+    auto run_dp = [&](const WorkQueue& w, uint32_t max_pairs, cudaStream_t on) {
         da.queue = w;
-        if (dk) launch_dk_dp(da, max_pairs, (uint32_t)s->max_len, st);
-        else launch_dtw_dp(da, max_pairs, st);
+        if (dk) launch_dk_dp(da, max_pairs, (uint32_t)s->max_len, on);
+        else launch_dtw_dp(da, max_pairs, on);
         ++launches;
     };
-    if (p->probe && sep_probe) run_dp(p->probe_wq(), nq * (uint32_t)p->probe);
+    // TSW_PROBE_OVERLAP=1 (DTW): the probe DP runs beside the LB pass on the aux stream and the
+    // pass reads the threshold as the probes tighten it (any T >= the current one is a valid
+    // pruning threshold; the DP re-checks every pair at dequeue).  Off by default: measured
+    // slower (config 2: 0.859 vs 0.836 ms) -- the pass outruns the probes and admits ~55% more
+    // pairs under the seed threshold.
+    static const bool overlap_env = std::getenv("TSW_PROBE_OVERLAP") != nullptr;
+    const bool overlap = !dk && overlap_env && p->probe && sep_probe;
+    if (overlap) {
+        ck(cudaEventRecord(p->fork_ev, st), "fork");
+        ck(cudaStreamWaitEvent(p->aux, p->fork_ev, 0), "fork");
+        run_dp(p->probe_wq(), nq * (uint32_t)p->probe, p->aux);
+        ck(cudaEventRecord(p->join_ev, p->aux), "join");
+    } else if (p->probe && sep_probe) {
+        run_dp(p->probe_wq(), nq * (uint32_t)p->probe, st);
+    }
     mark(3);
     if (!dk) {
         LbCompactArgs la{};
@@ -568,7 +590,8 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
     }
     ++launches;
     mark(4);
-    run_dp(p->main_wq(), nq * n);
+    run_dp(p->main_wq(), nq * n, st);
+    if (overlap) ck(cudaStreamWaitEvent(st, p->join_ev, 0), "join");
     // final device top-k: the kk smallest (distance, index) of every query's exact results
     if (p->kk <= (uint64_t)kKMax) {
         launch_select_smallest(p->res_d.p, p->res_i.p, p->res_n.p, nq, n, (uint32_t)p->kk,
