@@ -953,8 +953,9 @@ int tsw_plan_stats(tsw_plan* p, tsw_stats* out) {
         const bool dk = p->metric == TSW_METRIC_DK;
         out->bound_passes = dk ? 0 : 1;
         // DTW: the fp32 copy of the store is streamed once per execute (query blocks of one
-        // candidate tile are served from L1/L2);  DK bounds read 2 points per pair
-        out->bound_bytes = dk ? (uint64_t)p->nq * p->store->n * 2 * p->store->d * sizeof(double)
+        // candidate tile are served from L1/L2);  DK: the candidates' first/last points (the
+        // ends array, once per execute; each query re-reads them from L1/L2)
+        out->bound_bytes = dk ? (uint64_t)p->store->n * 2 * p->store->d * sizeof(double)
                               : p->store->bytes / 2;
         out->kernel_launches = (uint64_t)p->launches;
         if (p->timing && p->executed) {
