@@ -765,16 +765,18 @@ int tsw_store_create(const double* values, const uint64_t* lengths, uint64_t uni
         s->max_len = mx;
         s->host_len = lens;
         uint64_t elems = 0;
-        const uint64_t g = kTile * d;  // guard tile: before every series and after the last
+        // guard tiles: one before series 0, one after every series, one more after the last
+        const uint64_t g = kTile * d;
         s->guard = g;
         if (uniform) {
             // tiled series at a pitch of tiles + one guard tile (-inf)
             s->ulen = lens[0];
             s->tstride = stride_of(lens[0], d);
             s->ustride = s->tstride + g;
-            elems = g + n * s->ustride;
+            elems = g + n * s->ustride + g;  // + a second guard tile after the last series
             s->data.alloc(elems);
             launch_fill(s->data.p, g, -INFINITY, 0);
+            launch_fill(s->data.p + elems - g, g, -INFINITY, 0);
             // upload row-major through a bounded staging buffer, re-tile on the device
             const uint64_t row = lens[0] * d;
             const uint64_t batch = std::max<uint64_t>(1, std::min<uint64_t>(n, (256ull << 20) / (row * 8)));
@@ -795,7 +797,7 @@ int tsw_store_create(const double* values, const uint64_t* lengths, uint64_t uni
                 off[i] = rel;
                 rel += stride_of(lens[i], d) + g;
             }
-            elems = g + rel;
+            elems = g + rel + g;  // + a second guard tile after the last series
             std::vector<double> buf(elems, -INFINITY);
             uint64_t src = 0;
             for (uint64_t i = 0; i < n; ++i) {

@@ -65,28 +65,41 @@ struct Strip {
 };
 
 // One skewed step k: lane l computes cells (R + RPL*l + q, cstart + k - l), q < RPL.
+// tiled element offset of column j (j may be negative or past the end: guard tiles)
+__device__ __forceinline__ int toff_rt(int j, int stride) {
+    return (j >> 5) * (int)(kTile * stride) + (j & 31);
+}
+
+template <int D>
+__device__ __forceinline__ void load_pt(Pt<D>& p, const double* __restrict__ t, int j, int stride) {
+    if (D > 0) {
+        const double* tp = t + toff_rt(j, stride);
+#pragma unroll
+        for (int kk = 0; kk < (D > 0 ? D : 1); ++kk) p.x[kk] = __ldg(tp + kk * (int)kTile);
+    }
+}
+
+// One skewed step; `tv` holds column j's candidate point (loaded a step ahead) and `tn` gets
+// column j+1's.  Column indices run past [0, n) by at most 32 + 4 points: the store's guard
+// tiles (one after every series, two after the last) keep those loads inside the allocation,
+// and their cells are masked.
 template <int D, bool LIVE>
 __device__ __forceinline__ void dk_step(const Strip& S, int k, int lane, int n,
                                         const Pt<D> (&sp)[RPL], const double* const (&srow)[RPL],
                                         const double* __restrict__ t, uint32_t d,
                                         double* __restrict__ bnd, double Tsq,
                                         double (&left)[RPL], double& mine, double& up_prev,
-                                        bool& live) {
+                                        bool& live, const Pt<D>& tv, Pt<D>& tn) {
     const int stride = D > 0 ? D : (int)d;
     const int j = S.cstart + k - lane;
     const bool colok = (unsigned)(k - lane) <= (unsigned)(n - 1 - S.cstart);
     double up = __shfl_up_sync(kFull, mine, 1);  // lane l-1's last row at column j
     double dg = up_prev;                          // ... at column j-1 (previous step)
-    const int jc = min(max(j, 0), n - 1);
-    const double b = bnd[jc];  // boundary row (row R-1); only lane 0 uses it
+    const double b = bnd[j];  // boundary row (row R-1), padded by 64 each side; lane 0 uses it
     if (lane == 0) up = (!S.first && j <= S.b_hi) ? b : kInf;
     up_prev = up;
-    const double* tp = t + tidx((uint32_t)jc, 0, (uint32_t)stride);
-    Pt<D> tv;
-    if (D > 0) {
-#pragma unroll
-        for (int kk = 0; kk < (D > 0 ? D : 1); ++kk) tv.x[kk] = __ldg(tp + kk * kTile);
-    }
+    load_pt<D>(tn, t, j + 1, stride);
+    const double* tp = t + toff_rt(j, stride);  // runtime-d path
     bool lv = false;
 #pragma unroll
     for (int q = 0; q < RPL; ++q) {
@@ -109,7 +122,8 @@ template <int D>
 __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) {
     extern __shared__ double smem[];
     const int lane = threadIdx.x & 31;
-    double* bnd = smem + (size_t)(threadIdx.x >> 5) * max_len;
+    // boundary row of the warp, padded by 64 columns on both sides (out-of-range reads)
+    double* bnd = smem + (size_t)(threadIdx.x >> 5) * (max_len + 128) + 64;
     const uint32_t d = a.store.d;
     const int m = (int)a.qlen;
     const int stride = D > 0 ? D : (int)d;
@@ -165,11 +179,13 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
             const int kmax = (n - 1 - S.cstart) + last_lane;
             bool l2 = false, l3 = false, dummy = false;
             int k_done = -1;
+            Pt<D> ta, tb;  // candidate points of the current / next column (ping-pong)
+            load_pt<D>(ta, t, S.cstart - lane, stride);
             for (int k = 0; k <= kmax; k += 4) {
-                dk_step<D, false>(S, k, lane, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, dummy);
-                dk_step<D, false>(S, k + 1, lane, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, dummy);
-                dk_step<D, true>(S, k + 2, lane, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, l2);
-                dk_step<D, true>(S, k + 3, lane, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, l3);
+                dk_step<D, false>(S, k, lane, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, dummy, ta, tb);
+                dk_step<D, false>(S, k + 1, lane, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, dummy, tb, ta);
+                dk_step<D, true>(S, k + 2, lane, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, l2, ta, tb);
+                dk_step<D, true>(S, k + 3, lane, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, l3, tb, ta);
                 k_done = k + 3;
                 // dead cut: no live cell on steps k+2, k+3 and nothing live ahead of lane 0
                 if (!__any_sync(kFull, l2 || l3) && S.cstart + k + 3 > S.b_alive_hi) break;
@@ -247,7 +263,7 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
 template <int D>
 void run_dk(const DpArgs& a, uint32_t max_pairs, uint32_t max_len, cudaStream_t st) {
     const int threads = 128;
-    const size_t smem = (size_t)(threads / 32) * max_len * sizeof(double);
+    const size_t smem = (size_t)(threads / 32) * (max_len + 128) * sizeof(double);
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(dk_dp_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
