@@ -200,7 +200,17 @@ __global__ void __launch_bounds__(256) sample_ub_kernel(SampleArgs a) {
 // chunks of both sides in shared memory (dimension-major, series fastest) and every thread
 // accumulates 2 x 2 pairs, so each loaded point feeds two pairs.  Same per-point costs and
 // accumulation (DTW: fl sum in any order, scaled up; DK: exact max) as sample_ub_kernel.
-constexpr int kUQ = 16, kUC = 32, kUP = 16;
+constexpr int kUQ = 16, kUC = 32;
+// points per chunk: 16, or the power of two <= 64 / d at large d (a power of two divides the
+// 32-point tile, so a chunk never straddles tiles and its element offsets are per-thread
+// constants plus one per-chunk shift)
+__host__ __device__ inline uint32_t ub_chunk(uint32_t d) {
+    if (d <= 4) return 16u;
+    uint32_t c = 1;
+    while (c * 2 * d <= 64) c *= 2;
+    return c;
+}
+constexpr int kUElem = 8;  // chunk elements per thread: (kUQ + kUC) * d * kUP <= 3072 <= 8 * 512
 constexpr int kUQS = kUQ + 2, kUCS = kUC + 2;  // padded rows: 2-way instead of 16-way store conflicts
 
 constexpr int kUSub = 4;  // threads per pair set (interleaved points), reduced at the end
@@ -209,29 +219,49 @@ template <bool DK>
 __global__ void __launch_bounds__(128 * kUSub) sample_ub_tile_kernel(SampleArgs a) {
     extern __shared__ __align__(16) double usm[];
     const uint32_t d = a.store.d, L = a.qlen;
+    const uint32_t kUP = ub_chunk(d);
     double* qs = usm;                           // [d][kUP][kUQS]
     double* cs = usm + (size_t)d * kUP * kUQS;  // [d][kUP][kUCS]
     const uint32_t q0 = blockIdx.y * kUQ, j0 = blockIdx.x * kUC;
     const int t = threadIdx.x, sub = t / 128, tp = t % 128;
     const int tq = tp / (kUC / 2), tc = tp % (kUC / 2);
     double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-    for (uint32_t p0 = 0; p0 < L; p0 += kUP) {
-        __syncthreads();
-        // chunk loads: kUP consecutive points of one dimension are contiguous in a tile
-        for (uint32_t e = t; e < (uint32_t)kUQ * d * kUP; e += blockDim.x) {
+    // this thread's chunk elements, resolved once: element e = (series sr, dim k, point pp),
+    // pp fastest; query side [0, nqe), candidate side after.  Chunk p0 adds one uniform tile
+    // offset.  Points past L read padding / guard values, which the compute never uses.
+    const uint32_t nqe = (uint32_t)kUQ * d * kUP, nce = (uint32_t)kUC * d * kUP;
+    const double* gsrc[kUElem];
+    uint32_t sdst[kUElem];
+    int nel = 0;
+#pragma unroll
+    for (int i = 0; i < kUElem; ++i) {
+        const uint32_t e = t + i * blockDim.x;
+        gsrc[i] = a.queries;
+        sdst[i] = 0;
+        if (e < nqe) {
             const uint32_t pp = e % kUP, k = (e / kUP) % d, sr = e / (kUP * d);
-            const uint32_t q = min(q0 + sr, a.nq - 1), p = min(p0 + pp, L - 1);
-            qs[(k * kUP + pp) * kUQS + sr] = a.queries[(uint64_t)q * a.qstride + tidx(p, k, d)];
-        }
-        for (uint32_t e = t; e < (uint32_t)kUC * d * kUP; e += blockDim.x) {
-            const uint32_t pp = e % kUP, k = (e / kUP) % d, sr = e / (kUP * d);
+            const uint32_t q = min(q0 + sr, a.nq - 1);
+            gsrc[i] = a.queries + (uint64_t)q * a.qstride + k * kTile + pp;
+            sdst[i] = (k * kUP + pp) * kUQS + sr;
+            nel = i + 1;
+        } else if (e < nqe + nce) {
+            const uint32_t ec = e - nqe;
+            const uint32_t pp = ec % kUP, k = (ec / kUP) % d, sr = ec / (kUP * d);
             const uint32_t j = min(j0 + sr, a.S - 1);
             const uint32_t c = (uint32_t)((uint64_t)j * a.store.n / a.S);
-            const uint32_t p = min(p0 + pp, L - 1);
-            cs[(k * kUP + pp) * kUCS + sr] = a.store.data[series_off(a.store, c) + tidx(p, k, d)];
+            gsrc[i] = a.store.data + series_off(a.store, c) + k * kTile + pp;
+            sdst[i] = (uint32_t)(d * kUP * kUQS) + (k * kUP + pp) * kUCS + sr;
+            nel = i + 1;
         }
+    }
+    for (uint32_t p0 = 0; p0 < L; p0 += kUP) {
         __syncthreads();
-        const uint32_t np = min((uint32_t)kUP, L - p0);
+        const uint64_t coff = (uint64_t)(p0 >> 5) * kTile * d + (p0 & 31);
+#pragma unroll
+        for (int i = 0; i < kUElem; ++i)
+            if (i < nel) usm[sdst[i]] = gsrc[i][coff];
+        __syncthreads();
+        const uint32_t np = min(kUP, L - p0);
         for (uint32_t pp = sub; pp < np; pp += kUSub) {
             double cst[2][2];
             for (uint32_t k = 0; k < d; ++k) {
@@ -277,9 +307,9 @@ __global__ void __launch_bounds__(128 * kUSub) sample_ub_tile_kernel(SampleArgs 
 }
 
 void launch_sample_ub(const SampleArgs& a, cudaStream_t st) {
-    if (a.store.ulen == a.qlen) {
+    if (a.store.ulen == a.qlen && (kUQ + kUC) * a.store.d * ub_chunk(a.store.d) <= kUElem * 128 * kUSub) {
         const dim3 grid((a.S + kUC - 1) / kUC, (a.nq + kUQ - 1) / kUQ);
-        const size_t smem = std::max<size_t>((size_t)a.store.d * kUP * (kUQS + kUCS),
+        const size_t smem = std::max<size_t>((size_t)a.store.d * ub_chunk(a.store.d) * (kUQS + kUCS),
                                              (size_t)kUSub * 128 * 4) * sizeof(double);
         auto kern = a.dk ? sample_ub_tile_kernel<true> : sample_ub_tile_kernel<false>;
         if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
