@@ -190,12 +190,24 @@ __global__ void __launch_bounds__(TPB, MINB) dtw4_kernel(DpArgs a, uint32_t pstr
     unsigned* ab_local = a.state && a.nq <= kAbLocalMax ? reinterpret_cast<unsigned*>(
                                                               smem_pfx + (size_t)NG * pstride)
                                                         : nullptr;
-    if (ab_local) {
-        for (uint32_t i = threadIdx.x; i < a.nq; i += blockDim.x) ab_local[i] = 0u;
-        __syncthreads();
-    }
     const int L = (int)a.qlen;
     const int r = (int)min(a.r, a.qlen - 1);
+    // ctab[i]: in-matrix band cells of a pair that ran i iterations (the cell statistic, one
+    // shared-memory read per finished pair instead of a per-slot clamp computation)
+    uint32_t* ctab = reinterpret_cast<uint32_t*>(smem_pfx + (size_t)NG * pstride) +
+                     (a.state && a.nq <= kAbLocalMax ? a.nq : 0);
+    for (int i = threadIdx.x; i <= L; i += blockDim.x) {
+        uint32_t sum = 0;
+        for (int o = -r; o <= r; ++o) {
+            const int h = o >> 1, lo = max(h, h - o), hi = L - 1 + min(h, h - o);
+            const int c = min(i - 1, hi) - lo + 1;
+            sum += c > 0 ? (uint32_t)c : 0u;
+        }
+        ctab[i] = sum;
+    }
+    if (ab_local)
+        for (uint32_t i = threadIdx.x; i < a.nq; i += blockDim.x) ab_local[i] = 0u;
+    __syncthreads();
     const int plog = a.pfx_blocks ? (int)a.pfx_log : 0;
     // lane geometry: slot e holds offset obase + e; lanes past `edge` are idle (garbage) and
     // read `edge`'s points
@@ -365,16 +377,7 @@ __global__ void __launch_bounds__(TPB, MINB) dtw4_kernel(DpArgs a, uint32_t pstr
         const bool finished = completed || (have && bal == 0u);  // complete, or a dead cut
         const double f = __shfl_sync(kFull, fin, (lane - gl) + pstar);
         if (have && finished) {
-            const int it_end = min(it, L);
-#pragma unroll
-            for (int e = 0; e < 2 * G; ++e) {
-                if ((okm >> e) & 1u) {  // in-matrix cells of offset o: it in [lo, hi]
-                    const int o = obase + e, h = o >> 1;
-                    const int lo = max(h, h - o), hi = L - 1 + min(h, h - o);
-                    const int c = min(it_end - 1, hi) - lo + 1;
-                    cells += c > 0 ? (unsigned long long)c : 0ull;
-                }
-            }
+            if (gl == 0) cells += ctab[min(it, L)];
             // T of the last check (>= the current one): a value in between is exact too and
             // only costs an append (the KBest keeps the k smallest)
             if (gl == 0) finish_pair(a, st, pr, completed, f, T, ab_local);
@@ -398,7 +401,8 @@ void run4(const DpArgs& a, uint32_t max_pairs, cudaStream_t st) {
     constexpr int MINB = 4;
     const uint32_t pstride = (std::max<uint32_t>(a.qlen + 1, kPfxBlocks + 1) + 3) & ~3u;
     const size_t smem = (size_t)(TPB / WL) * (sizeof(Stage) + pstride * sizeof(float)) +
-                        (a.state && a.nq <= kAbLocalMax ? a.nq * sizeof(unsigned) : 0);
+                        (a.state && a.nq <= kAbLocalMax ? a.nq * sizeof(unsigned) : 0) +
+                        (a.qlen + 1) * sizeof(uint32_t);
     auto kern = dtw4_kernel<G, D, WL, RPAR, TPB, MINB>;
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
