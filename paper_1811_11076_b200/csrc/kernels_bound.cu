@@ -254,13 +254,24 @@ __global__ void __launch_bounds__(128 * kUSub) sample_ub_tile_kernel(SampleArgs 
             nel = i + 1;
         }
     }
+    // register-staged chunks: the next chunk's loads are in flight during this one's compute
+    double nxt[kUElem];
+#pragma unroll
+    for (int i = 0; i < kUElem; ++i)
+        if (i < nel) nxt[i] = gsrc[i][0];
     for (uint32_t p0 = 0; p0 < L; p0 += kUP) {
         __syncthreads();
-        const uint64_t coff = (uint64_t)(p0 >> 5) * kTile * d + (p0 & 31);
 #pragma unroll
         for (int i = 0; i < kUElem; ++i)
-            if (i < nel) usm[sdst[i]] = gsrc[i][coff];
+            if (i < nel) usm[sdst[i]] = nxt[i];
         __syncthreads();
+        if (p0 + kUP < L) {
+            const uint32_t p1 = p0 + kUP;
+            const uint64_t coff = (uint64_t)(p1 >> 5) * kTile * d + (p1 & 31);
+#pragma unroll
+            for (int i = 0; i < kUElem; ++i)
+                if (i < nel) nxt[i] = gsrc[i][coff];
+        }
         const uint32_t np = min(kUP, L - p0);
         for (uint32_t pp = sub; pp < np; pp += kUSub) {
             double cst[2][2];
