@@ -34,6 +34,8 @@ extern "C" {
 
 #define TSW_METRIC_DTW 0 /* banded DTW, squared-Euclidean point cost (dtw.hpp:8-16)        */
 #define TSW_METRIC_DK 1  /* dog-keeper / discrete Frechet, Euclidean cost (dogkeeper.hpp) */
+#define TSW_METRIC_DK_SUB 2 /* subsequence dog-keeper: best match of the query inside each
+                               candidate (sparse_dk_sub, dogkeeper.cpp:235-241)            */
 
 /* Mirrors tswarp::Neighbor (search.hpp:21-24). */
 typedef struct tsw_neighbor {
@@ -92,11 +94,14 @@ int tsw_store_info(const tsw_store* store, uint64_t* n, uint64_t* d, uint64_t* m
  * tsw_knn replaces, for nq queries at once,
  *   tswarp::knn_dtw(query, data, k, BandRadius{r}, threads)   (search.hpp:46-47, search.cpp:125-169)
  *   tswarp::knn_dk (query, data, k, threads)                   (search.hpp:56-57, search.cpp:171-214)
+ *   tswarp::knn_dk_sub(query, data, k, threads)                (search.hpp:75-76, search.cpp:250-280)
+ *     metric TSW_METRIC_DK_SUB: each candidate's distance is its best subsequence match
  * queries: nq equal-length row-major series of qlen points (d = the store's d).
  * out    : nq x min(k, n) neighbours, each query's sorted by (distance, index).
- * counters: nq entries or NULL.  `r` is ignored for DK.
+ * counters: nq entries or NULL.
  * Errors: k == 0 -> TSW_EINVAL ("knn_dtw: k must be positive"); DTW with any series length
- * != qlen -> TSW_EINVAL (check_query, search.cpp:99-115); non-finite query -> TSW_EVALIDATION. */
+ * != qlen -> TSW_EINVAL (check_query, search.cpp:99-115); non-finite query -> TSW_EVALIDATION.
+ * `r` is ignored for DK and DK_SUB; DK and DK_SUB accept any series lengths. */
 int tsw_knn(tsw_store* store, const double* queries, uint64_t nq, uint64_t qlen, int metric,
             uint64_t r, uint64_t k, tsw_neighbor* out, tsw_counters* counters);
 
@@ -143,6 +148,15 @@ int tsw_lb_box_all(tsw_store* store, const double* query, uint64_t qlen, uint64_
  * value[i] = eps.  eps = +inf gives dtw_banded / dk_full for every candidate. */
 int tsw_dist_all(tsw_store* store, const double* query, uint64_t qlen, int metric, uint64_t r,
                  double eps, int* exact, double* value);
+
+/* Subsequence DK of the query against every candidate:
+ *   sparse_dk_sub(query, data[i], eps)  (dogkeeper.cpp:235-241), which equals
+ *   sub_search_dk(query, data[i], eps)  (search.cpp:241-248; the greedy seed only tightens eps)
+ * found[i] = 1, value[i] = best match distance, end[i] = SubMatch::end_index (earliest end
+ * column on ties) when a match <= eps exists; else found[i] = 0, value[i] = +inf (nullopt).
+ * `end` may be NULL.  eps < 0 -> TSW_EINVAL. */
+int tsw_sub_dk_all(tsw_store* store, const double* query, uint64_t qlen, double eps, int* found,
+                   double* value, uint64_t* end);
 
 /* ---- diagnostics ---------------------------------------------------------------------------
  * Host<->device bytes moved by the calling thread's last tsw_knn / plan set_queries+fetch. */

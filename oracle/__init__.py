@@ -25,6 +25,8 @@ PORT_SO = os.path.join(HERE, "_build", "liborc.so")
 REF_SO = os.path.join(HERE, "_ref", "libtswarp_ref.so")
 REF_ROOT = "/root/reference/proj/core"
 
+_METRIC = {"dtw": 0, "dk": 1, "dk_sub": 2}
+
 _lock = threading.Lock()
 _cache: dict[str, "Oracle"] = {}
 
@@ -119,6 +121,9 @@ class Oracle:
                                        _dp, _up, _up]
             L.orc_dtw_all.argtypes = [_dp, _u64, _u64, _dp, _up, _u64, _u64, _dp]
             L.orc_dk_all.argtypes = [_dp, _u64, _u64, _dp, _up, _u64, _dp]
+            L.orc_knn_dk_sub.argtypes = [_dp, _u64, _u64, _dp, _up, _u64, _u64, _u64, _up, _dp,
+                                         _up, _up]
+            L.orc_dk_sub_full.argtypes = [_dp, _u64, _dp, _u64, _u64, _dp, _up]
         getattr(L, p + "envelope").argtypes = [_dp, _u64, _u64, _u64, _dp, _dp]
         getattr(L, p + "lb_box").argtypes = [_dp, _dp, _u64, _u64, _u64, _dp]
         getattr(L, p + "lb_sigma_min").argtypes = [_dp, _dp, _u64, _u64, _u64, _dp]
@@ -129,6 +134,9 @@ class Oracle:
         getattr(L, p + "gdk").argtypes = [_dp, _u64, _dp, _u64, _u64, C.c_double, _dp]
         getattr(L, p + "sparse_dk").argtypes = [_dp, _u64, _dp, _u64, _u64, C.c_double, _ip, _dp]
         getattr(L, p + "znormalize").argtypes = [_dp, _u64, _u64, _dp]
+        getattr(L, p + "gdk_sub").argtypes = [_dp, _u64, _dp, _u64, _u64, C.c_double, _dp, _up]
+        for f in ("sparse_dk_sub", "sub_search_dk"):
+            getattr(L, p + f).argtypes = [_dp, _u64, _dp, _u64, _u64, C.c_double, _ip, _dp, _up]
 
     # -- helpers --------------------------------------------------------------------------
     def _call(self, name, *args):
@@ -201,6 +209,42 @@ class Oracle:
                    C.byref(ex), _dptr(out))
         return bool(ex.value), float(out[0])
 
+    def gdk_sub(self, s, t, eps=float("inf")):
+        """-> (distance, end_index): SubMatch of gdk_sub (dogkeeper.cpp:96-111)."""
+        s, t = self._s(s), self._s(t)
+        out = np.zeros(1)
+        end = np.zeros(1, dtype=np.uint64)
+        self._call("gdk_sub", _dptr(s), s.shape[0], _dptr(t), t.shape[0], s.shape[1], eps,
+                   _dptr(out), _uptr(end))
+        return float(out[0]), int(end[0])
+
+    def _sub(self, name, s, t, eps):
+        s, t = self._s(s), self._s(t)
+        out = np.zeros(1)
+        end = np.zeros(1, dtype=np.uint64)
+        found = C.c_int(0)
+        self._call(name, _dptr(s), s.shape[0], _dptr(t), t.shape[0], s.shape[1], eps,
+                   C.byref(found), _dptr(out), _uptr(end))
+        return (float(out[0]), int(end[0])) if found.value else None
+
+    def sparse_dk_sub(self, s, t, eps):
+        """-> (distance, end_index) or None (std::nullopt), dogkeeper.cpp:235-241."""
+        return self._sub("sparse_dk_sub", s, t, eps)
+
+    def sub_search_dk(self, s, t, eps=float("inf")):
+        """-> (distance, end_index) or None, search.cpp:241-248."""
+        return self._sub("sub_search_dk", s, t, eps)
+
+    def dk_sub_full(self, s, t):
+        """Brute-force subsequence DK (port only) -> (distance, end_index)."""
+        assert self.kind == "port"
+        s, t = self._s(s), self._s(t)
+        out = np.zeros(1)
+        end = np.zeros(1, dtype=np.uint64)
+        self._call("dk_sub_full", _dptr(s), s.shape[0], _dptr(t), t.shape[0], s.shape[1],
+                   _dptr(out), _uptr(end))
+        return float(out[0]), int(end[0])
+
     def znormalize(self, s):
         s = self._s(s)
         out = np.empty_like(s)
@@ -218,12 +262,16 @@ class Oracle:
         ctr = np.zeros(5, dtype=np.uint64)
         if self.kind == "reference":
             h = data.ref_handle(self.lib)
-            self._call("knn", h, _dptr(q), q.shape[0], q.shape[1], 0 if metric == "dtw" else 1,
+            self._call("knn", h, _dptr(q), q.shape[0], q.shape[1], _METRIC[metric],
                        k, r, threads, cap, _uptr(idx), _dptr(dist), _uptr(cnt), _uptr(ctr), None)
         elif metric == "dtw":
             self._call("knn_dtw", _dptr(q), q.shape[0], q.shape[1], _dptr(data.values),
                        _uptr(data.lengths), data.n, k, r, cap, _uptr(idx), _dptr(dist),
                        _uptr(cnt), _uptr(ctr))
+        elif metric == "dk_sub":
+            self._call("knn_dk_sub", _dptr(q), q.shape[0], q.shape[1], _dptr(data.values),
+                       _uptr(data.lengths), data.n, k, cap, _uptr(idx), _dptr(dist), _uptr(cnt),
+                       _uptr(ctr))
         else:
             self._call("knn_dk", _dptr(q), q.shape[0], q.shape[1], _dptr(data.values),
                        _uptr(data.lengths), data.n, k, cap, _uptr(idx), _dptr(dist), _uptr(cnt),
@@ -244,7 +292,7 @@ class Oracle:
         ctr = np.zeros((nq, 5), dtype=np.uint64)
         h = data.ref_handle(self.lib)
         threads = threads or os.cpu_count() or 1
-        self._call("knn_batch", h, _dptr(qs), nq, L, d, 0 if metric == "dtw" else 1, k, r, threads,
+        self._call("knn_batch", h, _dptr(qs), nq, L, d, _METRIC[metric], k, r, threads,
                    cap, _uptr(idx), _dptr(dist), _uptr(cnt), _uptr(ctr))
         return idx, dist, cnt, ctr
 

@@ -97,16 +97,18 @@ void* ref_dataset_create(const double* values, const uint64_t* lengths, uint64_t
 void ref_dataset_destroy(void* ds) { delete static_cast<R::Dataset*>(ds); }
 
 // ---- k-NN / eps-NN drivers (search.cpp:125-239) ----------------------------------------------
-// metric: 0 = DTW (knn_dtw), 1 = DK (knn_dk).  counters: 5 x u64 in SearchCounters order.
+// metric: 0 = DTW (knn_dtw), 1 = DK (knn_dk), 2 = subsequence DK (knn_dk_sub).
+// counters: 5 x u64 in SearchCounters order.
 int ref_knn(void* ds, const double* q, uint64_t qlen, uint64_t d, int metric, uint64_t k,
             uint64_t r, int threads, uint64_t cap, uint64_t* idx, double* dist, uint64_t* count,
             uint64_t* counters, double* wall) {
     return guard([&] {
         const auto& data = *static_cast<const R::Dataset*>(ds);
         const R::TimeSeries query = make_series(q, qlen, d);
-        const R::SearchReport rep = metric == 0
-                                        ? R::knn_dtw(query, data, k, R::BandRadius{r}, threads)
-                                        : R::knn_dk(query, data, k, threads);
+        const R::SearchReport rep =
+            metric == 0   ? R::knn_dtw(query, data, k, R::BandRadius{r}, threads)
+            : metric == 1 ? R::knn_dk(query, data, k, threads)
+                          : R::knn_dk_sub(query, data, k, threads);
         write_report(rep, cap, idx, dist, count, counters);
         if (wall) *wall = rep.wall_time_seconds;
     });
@@ -220,6 +222,37 @@ int ref_sparse_dk(const double* s, uint64_t m, const double* t, uint64_t n, uint
         const auto td = R::sparse_dk(make_series(s, m, d), make_series(t, n, d), eps);
         *exact = td.is_exact() ? 1 : 0;
         *out = td.value;
+    });
+}
+
+// Subsequence DK (dogkeeper.cpp:96-111, 235-241; search.cpp:241-248).  found = 0 <->
+// std::nullopt; end = SubMatch::end_index.
+int ref_gdk_sub(const double* s, uint64_t m, const double* t, uint64_t n, uint64_t d, double eps,
+                double* out, uint64_t* end) {
+    return guard([&] {
+        const R::SubMatch sm = R::gdk_sub(make_series(s, m, d), make_series(t, n, d), eps);
+        *out = sm.distance;
+        *end = sm.end_index;
+    });
+}
+
+int ref_sparse_dk_sub(const double* s, uint64_t m, const double* t, uint64_t n, uint64_t d,
+                      double eps, int* found, double* out, uint64_t* end) {
+    return guard([&] {
+        const auto sm = R::sparse_dk_sub(make_series(s, m, d), make_series(t, n, d), eps);
+        *found = sm ? 1 : 0;
+        *out = sm ? sm->distance : R::kInf;
+        *end = sm ? sm->end_index : 0;
+    });
+}
+
+int ref_sub_search_dk(const double* s, uint64_t m, const double* t, uint64_t n, uint64_t d,
+                      double eps, int* found, double* out, uint64_t* end) {
+    return guard([&] {
+        const auto sm = R::sub_search_dk(make_series(s, m, d), make_series(t, n, d), eps);
+        *found = sm ? 1 : 0;
+        *out = sm ? sm->distance : R::kInf;
+        *end = sm ? sm->end_index : 0;
     });
 }
 

@@ -235,16 +235,18 @@ int orc_dk_full(const double* s, uint64_t m, const double* t, uint64_t n, uint64
     return 0;
 }
 
-/* ---- greedy_walk<false> + gdk, dogkeeper.cpp:52-94 ---------------------------------------- */
-int orc_gdk(const double* s, uint64_t m, const double* t, uint64_t n, uint64_t k, double eps,
-            double* out) {
-    size_t i = 0, j = 0;
-    double g = dist(s, t, k);
+/* ---- greedy_walk<StopAtLastRow>, dogkeeper.cpp:52-86 ---------------------------------------
+ * From (i, j) step to the cheapest of down / diag / right (strict <, tie order down > diag >
+ * right); out-of-range moves cost +inf; returns early once the running max exceeds eps.
+ * *end receives the final column (SubMatch::end_index). */
+static double greedy_walk(const double* s, uint64_t m, const double* t, uint64_t n, uint64_t k,
+                          size_t i, size_t j, double g, double eps, int stop_at_last_row,
+                          size_t* end) {
     if (g > eps) {
-        *out = g;
-        return 0;
+        *end = j;
+        return g;
     }
-    while (i != m - 1 || j != n - 1) {
+    while (stop_at_last_row ? (i != m - 1) : (i != m - 1 || j != n - 1)) {
         double d_down = ORC_INF, d_diag = ORC_INF, d_right = ORC_INF;
         if (i + 1 < m) {
             d_down = dist(s + (i + 1) * k, t + j * k, k);
@@ -268,17 +270,45 @@ int orc_gdk(const double* s, uint64_t m, const double* t, uint64_t n, uint64_t k
         g = max_d(g, step);
         if (g > eps) break;
     }
-    *out = g;
+    *end = j;
+    return g;
+}
+
+/* gdk, dogkeeper.cpp:90-94 */
+int orc_gdk(const double* s, uint64_t m, const double* t, uint64_t n, uint64_t k, double eps,
+            double* out) {
+    size_t end = 0;
+    *out = greedy_walk(s, m, t, n, k, 0, 0, dist(s, t, k), eps, 0, &end);
     return 0;
 }
 
-/* ---- sparse_engine<false> + sparse_dk, dogkeeper.cpp:120-233 ------------------------------
+/* gdk_sub, dogkeeper.cpp:96-111: start at the column closest to s_0 (lowest index on ties),
+ * walk until the last query row is aligned. */
+int orc_gdk_sub(const double* s, uint64_t m, const double* t, uint64_t n, uint64_t k, double eps,
+                double* out, uint64_t* end) {
+    size_t j0 = 0, e = 0;
+    double g0 = dist(s, t, k);
+    for (size_t j = 1; j < n; ++j) {
+        const double dd = dist(s, t + j * k, k);
+        if (dd < g0) {
+            g0 = dd;
+            j0 = j;
+        }
+    }
+    *out = greedy_walk(s, m, t, n, k, 0, j0, g0, eps, 1, &e);
+    *end = e;
+    return 0;
+}
+
+/* ---- sparse_engine<Sub>, dogkeeper.cpp:120-223 --------------------------------------------
  * Column-by-column over t with sorted active row lists; a cell is kept iff its point distance
- * and its accumulated value are both <= eps; virtual 0-predecessor only at (0,0); the scan
- * stops when the next-column frontier is empty. */
-int orc_sparse_dk(const double* s, uint64_t m, const double* t, uint64_t n, uint64_t k, double eps,
-                  int* exact, double* out) {
-    if (eps < 0) return 1;
+ * and its accumulated value are both <= eps.  Whole mode: virtual 0-predecessor only at (0,0),
+ * the scan stops when the next-column frontier is empty, the result is cell (m-1, n-1).
+ * Sub mode: row 0 has a virtual 0-predecessor in every column (and is re-activated every
+ * column), the last-row value of every column is folded into the running best (strict <, so
+ * the earliest end column wins ties). */
+static int sparse_engine(const double* s, uint64_t m, const double* t, uint64_t n, uint64_t k,
+                         double eps, int sub, double* out, uint64_t* end_out) {
     size_t* prev_idx = (size_t*)malloc(sizeof(size_t) * (m + 1));
     double* prev_val = (double*)malloc(sizeof(double) * (m + 1));
     size_t* cur_idx = (size_t*)malloc(sizeof(size_t) * (m + 1));
@@ -288,6 +318,8 @@ int orc_sparse_dk(const double* s, uint64_t m, const double* t, uint64_t n, uint
     size_t n_prev = 0, n_cur = 0, n_active = 1, n_next = 0;
     int found = 0;
     double whole = ORC_INF;
+    double best = ORC_INF;
+    size_t best_end = 0;
     active[0] = 0;
     for (size_t c = 0; c < n; ++c) {
         n_cur = 0;
@@ -306,7 +338,7 @@ int orc_sparse_dk(const double* s, uint64_t m, const double* t, uint64_t n, uint
             const double dd = dist(s + i * k, t + c * k, k);
             if (dd > eps) continue;
             double pred = ORC_INF;
-            if (i == 0 && c == 0) pred = 0.0;
+            if (i == 0 && (sub || c == 0)) pred = 0.0;
             if (pred != 0.0) {
                 if (last_row == i - 1) pred = min_d(pred, last_val);
                 while (pp < n_prev && prev_idx[pp] + 1 < i) ++pp;
@@ -325,11 +357,20 @@ int orc_sparse_dk(const double* s, uint64_t m, const double* t, uint64_t n, uint
                 if (next_active[n_next - 1] != i + 1) next_active[n_next++] = i + 1;
             }
         }
-        if (n_cur > 0 && cur_idx[n_cur - 1] == m - 1 && c == n - 1) {
-            whole = cur_val[n_cur - 1];
-            found = 1;
+        if (n_cur > 0 && cur_idx[n_cur - 1] == m - 1) {
+            const double vm = cur_val[n_cur - 1];
+            if (sub) {
+                if (vm < best) {
+                    best = vm;
+                    best_end = c;
+                    found = 1;
+                }
+            } else if (c == n - 1) {
+                whole = vm;
+                found = 1;
+            }
         }
-        if (n_next == 0) break;
+        if (!sub && n_next == 0) break;
         {
             size_t* ti = prev_idx; prev_idx = cur_idx; cur_idx = ti;
             double* tv = prev_val; prev_val = cur_val; cur_val = tv;
@@ -337,15 +378,78 @@ int orc_sparse_dk(const double* s, uint64_t m, const double* t, uint64_t n, uint
             n_prev = n_cur;
             n_active = n_next;
         }
+        if (sub && (n_active == 0 || active[0] != 0)) { /* re-activate row 0 (front insert) */
+            memmove(active + 1, active, n_active * sizeof(size_t));
+            active[0] = 0;
+            ++n_active;
+        }
     }
     free(prev_idx); free(prev_val); free(cur_idx); free(cur_val); free(active); free(next_active);
-    if (found) {
+    *out = sub ? best : whole;
+    if (end_out) *end_out = sub ? best_end : n - 1;
+    return found;
+}
+
+/* sparse_dk, dogkeeper.cpp:227-233 */
+int orc_sparse_dk(const double* s, uint64_t m, const double* t, uint64_t n, uint64_t k, double eps,
+                  int* exact, double* out) {
+    if (eps < 0) return 1;
+    double v = 0.0;
+    if (sparse_engine(s, m, t, n, k, eps, 0, &v, NULL)) {
         *exact = 1;
-        *out = whole;
+        *out = v;
     } else {
         *exact = 0;
         *out = eps;
     }
+    return 0;
+}
+
+/* sparse_dk_sub, dogkeeper.cpp:235-241: *found = 0 <-> std::nullopt. */
+int orc_sparse_dk_sub(const double* s, uint64_t m, const double* t, uint64_t n, uint64_t k,
+                      double eps, int* found, double* out, uint64_t* end) {
+    if (eps < 0) return 1;
+    double v = 0.0;
+    uint64_t e = 0;
+    *found = sparse_engine(s, m, t, n, k, eps, 1, &v, &e);
+    *out = *found ? v : ORC_INF;
+    *end = *found ? e : 0;
+    return 0;
+}
+
+/* sub_search_dk, search.cpp:241-248: gdk_sub seeds, sparse_dk_sub under min(eps, seed). */
+int orc_sub_search_dk(const double* s, uint64_t m, const double* t, uint64_t n, uint64_t k,
+                      double eps, int* found, double* out, uint64_t* end) {
+    double g = 0.0;
+    uint64_t ge = 0;
+    orc_gdk_sub(s, m, t, n, k, eps, &g, &ge);
+    return orc_sparse_dk_sub(s, m, t, n, k, g < eps ? g : eps, found, out, end);
+}
+
+/* Brute-force subsequence DK (parity oracle): full DP with a 0-predecessor for row 0 in every
+ * column; the best last-row value, earliest column on ties. */
+int orc_dk_sub_full(const double* s, uint64_t m, const double* t, uint64_t n, uint64_t k,
+                    double* out, uint64_t* end) {
+    double* prev = (double*)malloc(sizeof(double) * m);
+    double* cur = (double*)malloc(sizeof(double) * m);
+    double best = ORC_INF;
+    uint64_t be = 0;
+    for (size_t c = 0; c < n; ++c) {
+        for (size_t i = 0; i < m; ++i) {
+            double pred = 0.0; /* row 0: the virtual 0-predecessor */
+            if (i > 0) pred = c > 0 ? min_d(min_d(prev[i], prev[i - 1]), cur[i - 1]) : cur[i - 1];
+            cur[i] = max_d(dist(s + i * k, t + c * k, k), pred);
+        }
+        if (cur[m - 1] < best) {
+            best = cur[m - 1];
+            be = c;
+        }
+        double* tp = prev; prev = cur; cur = tp;
+    }
+    free(prev);
+    free(cur);
+    *out = best;
+    *end = be;
     return 0;
 }
 
@@ -494,6 +598,47 @@ int orc_knn_dk(const double* q, uint64_t qlen, uint64_t d, const double* values,
             orc_sparse_dk(q, qlen, values + off[i], lengths[i], d, eps, &exact[i - b0], &vals[i - b0]);
         for (uint64_t i = b0; i < b1; ++i) {
             if (exact[i - b0]) {
+                ++cnt[2];
+                kbest_offer(&best, i, vals[i - b0], 1);
+            } else {
+                ++cnt[3];
+            }
+        }
+    }
+    if (count) *count = best.size;
+    for (size_t j = 0; j < best.size && j < cap; ++j) {
+        idx[j] = best.e[j].index;
+        dist_out[j] = best.e[j].value;
+    }
+    if (counters) memcpy(counters, cnt, sizeof(cnt));
+    free(best.e); free(off);
+    return 0;
+}
+
+/* knn_dk_sub, search.cpp:250-280: one sub_search_dk per candidate under the block-frozen
+ * threshold; found matches are offered as exact. */
+int orc_knn_dk_sub(const double* q, uint64_t qlen, uint64_t d, const double* values,
+                   const uint64_t* lengths, uint64_t n, uint64_t k, uint64_t cap, uint64_t* idx,
+                   double* dist_out, uint64_t* count, uint64_t* counters) {
+    if (k == 0 || n == 0) return 1;
+    uint64_t* off = (uint64_t*)malloc(sizeof(uint64_t) * n);
+    offsets_of(lengths, n, d, off);
+    KBest best = {k < n ? k : n, 0, NULL};
+    best.e = (KEntry*)malloc(sizeof(KEntry) * best.k);
+    uint64_t cnt[5] = {0, 0, 0, 0, 0};
+    double vals[SCAN_BLOCK];
+    int found[SCAN_BLOCK];
+    for (uint64_t b0 = 0; b0 < n; b0 += SCAN_BLOCK) {
+        const uint64_t b1 = b0 + SCAN_BLOCK < n ? b0 + SCAN_BLOCK : n;
+        const double eps = kbest_threshold(&best);
+        for (uint64_t i = b0; i < b1; ++i) {
+            uint64_t e = 0;
+            orc_sub_search_dk(q, qlen, values + off[i], lengths[i], d, eps, &found[i - b0],
+                              &vals[i - b0], &e);
+        }
+        for (uint64_t i = b0; i < b1; ++i) {
+            ++cnt[4];
+            if (found[i - b0]) {
                 ++cnt[2];
                 kbest_offer(&best, i, vals[i - b0], 1);
             } else {

@@ -300,13 +300,16 @@ double dtw_margin(uint64_t L, uint64_t d) {
     return up_factor(2.0 * (2.0 * (double)L + (double)d + 8.0) + 8.0);
 }
 
+const char* knn_name(int metric) {
+    return metric == TSW_METRIC_DTW ? "knn_dtw" : metric == TSW_METRIC_DK ? "knn_dk" : "knn_dk_sub";
+}
+
 std::unique_ptr<tsw_plan> make_plan(tsw_store* s, uint64_t nq_max, uint64_t qlen, int metric,
                                     uint64_t r, uint64_t k) {
-    if (k == 0)
-        fail(TSW_EINVAL, metric == TSW_METRIC_DTW ? "knn_dtw: k must be positive"
-                                                  : "knn_dk: k must be positive");
+    if (metric != TSW_METRIC_DTW && metric != TSW_METRIC_DK && metric != TSW_METRIC_DK_SUB)
+        fail(TSW_EINVAL, "unknown metric");
+    if (k == 0) fail(TSW_EINVAL, std::string(knn_name(metric)) + ": k must be positive");
     if (qlen == 0) fail(TSW_EVALIDATION, "time series values must hold n >= 1 complete points");
-    if (metric != TSW_METRIC_DTW && metric != TSW_METRIC_DK) fail(TSW_EINVAL, "unknown metric");
     if (metric == TSW_METRIC_DTW && s->ulen != qlen) {
         // check_query(equal_lengths=true), search.cpp:106-113: report the first offender
         for (uint64_t i = 0; i < s->n; ++i)
@@ -446,7 +449,8 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
     tsw_store* s = p->store;
     const uint32_t n = (uint32_t)s->n, nq = (uint32_t)p->nq;
     if (nq == 0) fail(TSW_EINVAL, "no queries set on this plan");
-    const bool dk = p->metric == TSW_METRIC_DK;
+    const bool dk = p->metric != TSW_METRIC_DTW;  // DK or subsequence DK
+    const bool sub = p->metric == TSW_METRIC_DK_SUB;
     int launches = 0;
     static const bool dbg = std::getenv("TSW_DEBUG_SYNC") != nullptr;
     auto mark = [&](int i) {
@@ -525,6 +529,7 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
     da.results = ResultBuf{p->res_d.p, p->res_i.p, p->res_n.p, n};
     da.pfx_blocks = p->pfx_qn ? p->pfx.p : nullptr;
     da.pfx_log = p->pfx_log;
+    da.sub = sub ? 1 : 0;
     auto run_dp = [&](const WorkQueue& w, uint32_t max_pairs, cudaStream_t on) {
         da.queue = w;
         if (dk) launch_dk_dp(da, max_pairs, (uint32_t)s->max_len, on);
@@ -586,6 +591,7 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
         ka.state = p->state.p;
         ka.probed = p->probed.p;
         ka.queue = p->main_wq();
+        ka.sub = sub ? 1 : 0;
         launch_dk_compact(ka, st);
     }
     ++launches;
@@ -952,7 +958,7 @@ int tsw_plan_stats(tsw_plan* p, tsw_stats* out) {
         ck(cudaMemcpy(&cells, p->cells.p, sizeof(cells), cudaMemcpyDeviceToHost), "stats");
         out->dp_pairs = (uint64_t)cnt[C_PFRONT] + cnt[C_MFRONT] + cnt[C_MBACK];
         out->dp_cells = cells;
-        const bool dk = p->metric == TSW_METRIC_DK;
+        const bool dk = p->metric != TSW_METRIC_DTW;
         out->bound_passes = dk ? 0 : 1;
         // DTW: the fp32 copy of the store is streamed once per execute (query blocks of one
         // candidate tile are served from L1/L2);  DK: the candidates' first/last points (the
@@ -979,9 +985,9 @@ int tsw_knn(tsw_store* s, const double* queries, uint64_t nq, uint64_t qlen, int
             uint64_t r, uint64_t k, tsw_neighbor* out, tsw_counters* counters) {
     return guard([&] {
         if (!s) fail(TSW_EINVAL, "store is null");
-        if (k == 0)
-            fail(TSW_EINVAL, metric == TSW_METRIC_DTW ? "knn_dtw: k must be positive"
-                                                      : "knn_dk: k must be positive");
+        if (metric != TSW_METRIC_DTW && metric != TSW_METRIC_DK && metric != TSW_METRIC_DK_SUB)
+            fail(TSW_EINVAL, "unknown metric");
+        if (k == 0) fail(TSW_EINVAL, std::string(knn_name(metric)) + ": k must be positive");
         if (nq == 0) return;
         if (!queries) fail(TSW_EINVAL, "queries is null");
         check_finite(queries, nq * qlen * s->d, "query");
@@ -1067,6 +1073,56 @@ int tsw_epsnn_dk(tsw_store* s, const double* query, uint64_t qlen, double eps,
         if (count) *count = cnt;
         for (uint64_t j = 0; out && j < cnt && j < cap; ++j) out[j] = all[j];
         if (counters) *counters = tsw_counters{0, 0, cnt, n - cnt, 0};
+    });
+}
+
+int tsw_sub_dk_all(tsw_store* s, const double* query, uint64_t qlen, double eps, int* found,
+                   double* value, uint64_t* end) {
+    return guard([&] {
+        if (!s || !query || !found || !value) fail(TSW_EINVAL, "null argument");
+        if (!(eps >= 0)) fail(TSW_EINVAL, "sparse_dk_sub: eps must be nonnegative");
+        if (qlen == 0) fail(TSW_EVALIDATION, "time series values must hold n >= 1 complete points");
+        check_finite(query, qlen * s->d, "query");
+        std::lock_guard<std::mutex> lk(s->mu);
+        DeviceGuard dg(s->device);
+        const uint64_t n = s->n, d = s->d, qs = stride_of(qlen, d);
+        DevBuf<double> q(qs), val(n);
+        DevBuf<int> ex(n);
+        DevBuf<uint32_t> ed(n);
+        DevBuf<unsigned> ctr(4);
+        DevBuf<QEntry> queue(n);
+        std::vector<QEntry> hq(n);
+        for (uint64_t i = 0; i < n; ++i) hq[i] = QEntry{0, (uint32_t)i, 0.0f, kNoPfx};
+        const unsigned cnt[4] = {(unsigned)n, 0u, 0u, 0u};
+        ck(cudaMemcpy(queue.p, hq.data(), n * sizeof(QEntry), cudaMemcpyHostToDevice), "upload");
+        ck(cudaMemcpy(ctr.p, cnt, sizeof(cnt), cudaMemcpyHostToDevice), "upload");
+        {
+            const std::vector<double> tq = tiled_host(query, qlen, d);
+            ck(cudaMemcpy(q.p, tq.data(), qs * sizeof(double), cudaMemcpyHostToDevice), "upload");
+        }
+        DpArgs da{};
+        da.store = s->dev();
+        da.queries = q.p;
+        da.qlen = (uint32_t)qlen;
+        da.qstride = qs;
+        da.queue = WorkQueue{queue.p, ctr.p, ctr.p + 1, ctr.p + 2, (uint32_t)n};
+        da.fixed_eps = eps;
+        da.fixed_eps_sq = host_sq_threshold(eps);
+        da.margin = 1.0;
+        da.out_exact = ex.p;
+        da.out_val = val.p;
+        da.out_end = ed.p;
+        da.sub = 1;
+        launch_dk_dp(da, (uint32_t)n, (uint32_t)s->max_len, 0);
+        ck(cudaGetLastError(), "kernel launch");
+        std::vector<uint32_t> he(n);
+        ck(cudaMemcpy(found, ex.p, n * sizeof(int), cudaMemcpyDeviceToHost), "fetch");
+        ck(cudaMemcpy(value, val.p, n * sizeof(double), cudaMemcpyDeviceToHost), "fetch");
+        ck(cudaMemcpy(he.data(), ed.p, n * sizeof(uint32_t), cudaMemcpyDeviceToHost), "fetch");
+        for (uint64_t i = 0; i < n; ++i) {
+            if (!found[i]) value[i] = INFINITY;  // std::nullopt
+            if (end) end[i] = he[i];
+        }
     });
 }
 

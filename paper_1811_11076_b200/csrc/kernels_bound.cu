@@ -666,6 +666,8 @@ void launch_lb_compact(const LbCompactArgs& a, cudaStream_t st) {
 
 // ---- DK: first / last cell bound fused with compaction ------------------------------------
 // Both cells lie on every warping path, so max(c(0,0), c(m-1,n-1)) > Tsq  =>  dk > T (exact).
+// Subsequence mode: a match may start and end at any column, so the key is 0 (every pair that
+// was not probed enters the queue; the DP's own frontier test prunes it).
 __global__ void __launch_bounds__(256) dk_compact_kernel(DkCompactArgs a) {
     const uint32_t n = a.store.n, d = a.store.d;
     const uint64_t total = (uint64_t)a.nq * n;
@@ -687,7 +689,7 @@ __global__ void __launch_bounds__(256) dk_compact_kernel(DkCompactArgs a) {
                 // queries), candidate endpoints broadcast from the store's ends array
                 const double* e = a.store.ends + (uint64_t)c * 2 * d;  // first, last point
                 double c0 = 0.0, c1 = 0.0;
-                for (uint32_t k = 0; k < d; ++k) {
+                for (uint32_t k = 0; k < (a.sub ? 0u : d); ++k) {
                     const double e0 = dsub(a.qends[(uint64_t)k * a.nq + q], e[k]);
                     c0 = dadd(c0, dmul(e0, e0));
                     const double e1 = dsub(a.qends[(uint64_t)(d + k) * a.nq + q], e[d + k]);

@@ -83,13 +83,22 @@ __device__ __forceinline__ void load_pt(Pt<D>& p, const double* __restrict__ t, 
 // column j+1's.  Column indices run past [0, n) by at most 32 + 4 points: the store's guard
 // tiles (one after every series, two after the last) keep those loads inside the allocation,
 // and their cells are masked.
-template <int D, int RPL, bool LIVE>
+// Subsequence mode (SUB, sparse_engine<true>): row 0 has a virtual 0-predecessor in every
+// column, and in the last strip the lane holding row m-1 folds each column's last-row value
+// into (bsq, bs, bcol) = (min square, its sqrt, earliest column with that sqrt).
+struct SubFold {
+    int fl, fq;           // lane / slot of row m-1 in the last strip
+    double bsq, bs;       // running min of the squared last-row values, sqrt of it
+    int bcol;             // earliest column whose sqrt equals bs
+};
+
+template <int D, int RPL, bool LIVE, bool SUB>
 __device__ __forceinline__ void dk_step(const Strip& S, int k, int lane, int n,
                                         const Pt<D> (&sp)[RPL], const double* const (&srow)[RPL],
                                         const double* __restrict__ t, uint32_t d,
                                         double* __restrict__ bnd, double Tsq,
                                         double (&left)[RPL], double& mine, double& up_prev,
-                                        bool& live, const Pt<D>& tv, Pt<D>& tn) {
+                                        bool& live, const Pt<D>& tv, Pt<D>& tn, SubFold& sf) {
     const int stride = D > 0 ? D : (int)d;
     const int j = S.cstart + k - lane;
     const bool colok = (unsigned)(k - lane) <= (unsigned)(n - 1 - S.cstart);
@@ -101,24 +110,36 @@ __device__ __forceinline__ void dk_step(const Strip& S, int k, int lane, int n,
     load_pt<D>(tn, t, j + 1, stride);
     const double* tp = t + toff_rt(j, stride);  // runtime-d path
     bool lv = false;
+    double vlast = kInf;
 #pragma unroll
     for (int q = 0; q < RPL; ++q) {
         const bool active = colok && RPL * lane + q < S.nrows;
         const double c = D > 0 ? cost<D>(sp[q], tv) : cost_rt(srow[q], tp, d);
         double pred = dmin(dmin(left[q], up), dg);
-        if (q == 0 && S.first && lane == 0 && j == 0) pred = 0.0;  // virtual start (whole match)
+        // virtual start: (0, 0) for a whole match, (0, j) for every j in subsequence mode
+        if (q == 0 && S.first && lane == 0 && (SUB || j == 0)) pred = 0.0;
         const double v = active ? dmax(c, pred) : kInf;
         dg = left[q];           // next row's diagonal: this row at column j-1
         left[q] = active ? v : left[q];
         up = v;                 // next row's up: this row at column j
         if (LIVE) lv |= v <= Tsq;
+        if (SUB) vlast = q == sf.fq ? v : vlast;
+    }
+    if (SUB && !S.write_bnd && lane == sf.fl && vlast < sf.bsq) {
+        // strict: a column whose square ties or whose sqrt ties the best keeps the earlier end
+        sf.bsq = vlast;
+        const double r = __dsqrt_rn(vlast);
+        if (r < sf.bs) {
+            sf.bs = r;
+            sf.bcol = j;
+        }
     }
     mine = up;  // last row of this lane (inf when inactive)
     if (S.write_bnd && lane == 31 && colok) bnd[j] = mine;  // in place: lane 0 is >= 30 columns ahead
     if (LIVE) live = lv;
 }
 
-template <int D, int RPL>
+template <int D, int RPL, bool SUB>
 __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) {
     constexpr int kStrip = 32 * RPL;  // rows per strip
     extern __shared__ double smem[];
@@ -152,10 +173,16 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
 
         Strip S;
         S.b_hi = -1;
-        S.b_alive_hi = 0;  // virtual start at (0, 0)
+        S.b_alive_hi = SUB ? n - 1 : 0;  // virtual start at (0, 0) / at every (0, j)
         int b_alive_lo = 0;
         bool dead = false;
         double fin = kInf;
+        SubFold sf;
+        sf.fl = ((m - 1) % kStrip) / RPL;
+        sf.fq = ((m - 1) % kStrip) % RPL;
+        sf.bsq = kInf;
+        sf.bs = kInf;
+        sf.bcol = 0;
         for (int R = 0; R < m; R += kStrip) {
             S.R = R;
             S.nrows = min(kStrip, m - R);
@@ -183,10 +210,10 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
             Pt<D> ta, tb;  // candidate points of the current / next column (ping-pong)
             load_pt<D>(ta, t, S.cstart - lane, stride);
             for (int k = 0; k <= kmax; k += 4) {
-                dk_step<D, RPL, false>(S, k, lane, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, dummy, ta, tb);
-                dk_step<D, RPL, false>(S, k + 1, lane, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, dummy, tb, ta);
-                dk_step<D, RPL, true>(S, k + 2, lane, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, l2, ta, tb);
-                dk_step<D, RPL, true>(S, k + 3, lane, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, l3, tb, ta);
+                dk_step<D, RPL, false, SUB>(S, k, lane, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, dummy, ta, tb, sf);
+                dk_step<D, RPL, false, SUB>(S, k + 1, lane, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, dummy, tb, ta, sf);
+                dk_step<D, RPL, true, SUB>(S, k + 2, lane, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, l2, ta, tb, sf);
+                dk_step<D, RPL, true, SUB>(S, k + 3, lane, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, l3, tb, ta, sf);
                 k_done = k + 3;
                 // dead cut: no live cell on steps k+2, k+3 and nothing live ahead of lane 0
                 if (!__any_sync(kFull, l2 || l3) && S.cstart + k + 3 > S.b_alive_hi) break;
@@ -220,6 +247,11 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
                 S.b_hi = hi;
                 b_alive_lo = first;
                 S.b_alive_hi = last;
+            } else if (SUB) {
+                // final strip: the best last-row column, folded by the lane holding row m-1
+                fin = __shfl_sync(kFull, sf.bsq, sf.fl);
+                sf.bs = __shfl_sync(kFull, sf.bs, sf.fl);
+                sf.bcol = __shfl_sync(kFull, sf.bcol, sf.fl);
             } else {
                 // final strip: the lane holding row m-1 ends on column n-1 iff the sweep reached kmax
                 const int fl = (m - 1 - R) / RPL, fq = (m - 1 - R) % RPL;
@@ -234,10 +266,11 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
         if (lane == 0) {
             if (st) Tsq = ld_volatile(&st->Tsq);
             const bool exact = !dead && fin <= Tsq;
-            const double dist = __dsqrt_rn(fin);
+            const double dist = SUB ? sf.bs : __dsqrt_rn(fin);
             if (a.out_exact) {
                 a.out_exact[pr.c] = exact ? 1 : 0;
                 a.out_val[pr.c] = exact ? dist : (st ? ld_volatile(&st->T) : a.fixed_eps);
+                if (SUB && a.out_end) a.out_end[pr.c] = exact ? (uint32_t)sf.bcol : 0u;
             }
             if (exact) {
                 if (st) {
@@ -265,7 +298,7 @@ template <int D, int RPL>
 void run_dk(const DpArgs& a, uint32_t max_pairs, uint32_t max_len, cudaStream_t st) {
     const int threads = 128;
     const size_t smem = (size_t)(threads / 32) * (max_len + 128) * sizeof(double);
-    auto kern = dk_dp_kernel<D, RPL>;
+    auto kern = a.sub ? dk_dp_kernel<D, RPL, true> : dk_dp_kernel<D, RPL, false>;
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;

@@ -283,6 +283,7 @@ struct DkCompactArgs {
     unsigned long long* fixed_pruned;
     const uint8_t* probed;
     WorkQueue queue;
+    int sub;                  // subsequence DK: no endpoint bound (every column may start/end a match)
 };
 void launch_dk_compact(const DkCompactArgs& a, cudaStream_t st);
 
@@ -307,6 +308,8 @@ struct DpArgs {
     const float* pfx_blocks;    // DTW: LB block sums by QEntry::ps (nullptr: per-point, in-kernel)
     uint32_t pfx_log;           // log2 of the block length in points
     int guarded;                // queries and store carry the +-inf guard tiles
+    int sub;                    // DK: subsequence mode (sparse_engine<true>, dogkeeper.cpp:120-223)
+    uint32_t* out_end;          // DK sub, dist_all mode: SubMatch::end_index per candidate
 };
 
 void launch_dtw_dp(const DpArgs& a, uint32_t max_pairs, cudaStream_t st);

@@ -160,6 +160,46 @@ std::vector<SearchReport> knn_dk_batch(const std::vector<TimeSeries>& queries, c
     return run_knn(queries, data, k, TSW_METRIC_DK, 0, "knn_dk");
 }
 
+SearchReport knn_dk_sub(const TimeSeries& query, const Dataset& data, std::size_t k, int) {
+    return run_knn({query}, data, k, TSW_METRIC_DK_SUB, 0, "knn_dk_sub").front();
+}
+
+std::vector<SearchReport> knn_dk_sub_batch(const std::vector<TimeSeries>& queries,
+                                           const Dataset& data, std::size_t k) {
+    return run_knn(queries, data, k, TSW_METRIC_DK_SUB, 0, "knn_dk_sub");
+}
+
+std::optional<SubMatch> sparse_dk_sub(const TimeSeries& s, const TimeSeries& t, double eps) {
+    if (s.dim() != t.dim()) {
+        throw std::invalid_argument("sparse_dk_sub: dimensionality mismatch (" +
+                                    std::to_string(s.dim()) + " vs " + std::to_string(t.dim()) +
+                                    ")");
+    }
+    if (eps < 0) throw std::invalid_argument("sparse_dk_sub: eps must be nonnegative");
+    // a one-series store for the haystack (the scan over a Dataset is knn_dk_sub)
+    tsw_store* st = nullptr;
+    const uint64_t n = t.length();
+    int rc = tsw_store_create(t.flat().data(), &n, 0, 1, t.dim(), 0, &st);
+    if (rc != TSW_OK) detail::rethrow(rc);
+    int found = 0;
+    double v = 0.0;
+    uint64_t end = 0;
+    rc = tsw_sub_dk_all(st, s.flat().data(), s.length(), eps, &found, &v, &end);
+    tsw_store_destroy(st);
+    if (rc != TSW_OK) detail::rethrow(rc);
+    if (!found) return std::nullopt;
+    return SubMatch{v, static_cast<std::size_t>(end)};
+}
+
+std::optional<SubMatch> sub_search_dk(const TimeSeries& query, const TimeSeries& haystack,
+                                      double eps) {
+    if (query.dim() != haystack.dim())
+        throw std::invalid_argument("sub_search_dk: dimensionality mismatch");
+    // the reference seeds eps with gdk_sub (search.cpp:246-247); the seed only tightens the
+    // threshold, so the exact match under eps is the same
+    return sparse_dk_sub(query, haystack, eps);
+}
+
 SearchReport epsnn_dk(const TimeSeries& query, const Dataset& data, double eps, int) {
     if (eps < 0) throw std::invalid_argument("epsnn_dk: eps must be nonnegative");
     check_query(query, data, false, "epsnn_dk");

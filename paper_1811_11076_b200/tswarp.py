@@ -6,6 +6,9 @@ Same names, argument meaning and error behaviour as the reference's hot-path API
 * ``knn_dtw(query, data, k, r, threads=1)``   <-> ``tswarp::knn_dtw``   (search.cpp:125-169)
 * ``knn_dk(query, data, k, threads=1)``       <-> ``tswarp::knn_dk``    (search.cpp:171-214)
 * ``epsnn_dk(query, data, eps, threads=1)``   <-> ``tswarp::epsnn_dk``  (search.cpp:216-239)
+* ``knn_dk_sub(query, data, k, threads=1)``   <-> ``tswarp::knn_dk_sub`` (search.cpp:250-280)
+* ``sub_search_dk(query, haystack, eps)``     <-> ``tswarp::sub_search_dk`` (search.cpp:241-248)
+* ``sparse_dk_sub(s, t, eps)``                <-> ``tswarp::sparse_dk_sub`` (dogkeeper.cpp:235-241)
 * ``SearchReport`` / ``SearchCounters`` / ``Neighbor`` mirror search.hpp:13-32.
 * ``ValidationError`` mirrors tswarp::ValidationError; invalid arguments raise ``ValueError``
   (the Python spelling of std::invalid_argument).
@@ -32,6 +35,15 @@ LIB_PATH = os.environ.get("TSW_LIB") or os.path.join(HERE, "lib", "libtswarp_b20
 
 METRIC_DTW = 0
 METRIC_DK = 1
+METRIC_DK_SUB = 2
+_METRICS = {"dtw": METRIC_DTW, "dk": METRIC_DK, "dk_sub": METRIC_DK_SUB}
+
+
+def _metric(name: str) -> int:
+    try:
+        return _METRICS[name]
+    except KeyError:
+        raise ValueError(f"unknown metric {name!r} (dtw | dk | dk_sub)") from None
 
 _u64 = C.c_uint64
 _dp = C.POINTER(C.c_double)
@@ -102,6 +114,7 @@ def lib():
     L.tsw_envelope.argtypes = [_dp, _u64, _u64, _u64, _dp, _dp]
     L.tsw_lb_box_all.argtypes = [_vp, _dp, _u64, _u64, _dp, _dp]
     L.tsw_dist_all.argtypes = [_vp, _dp, _u64, C.c_int, _u64, C.c_double, _ip, _dp]
+    L.tsw_sub_dk_all.argtypes = [_vp, _dp, _u64, C.c_double, _ip, _dp, _up]
     L.tsw_last_transfer_bytes.argtypes = [_up, _up]
     L.tsw_fp64_peak.argtypes = [_dp]
     L.tsw_l2_flush.argtypes = [_vp, _u64, _vp]
@@ -284,7 +297,7 @@ def knn(data, queries, k: int, metric: str = "dtw", r: int = 0):
     kk = min(k, st.n)
     out = (Neighbor_t * max(1, nq * kk))()
     ctr = (Counters_t * max(1, nq))()
-    m = METRIC_DTW if metric == "dtw" else METRIC_DK
+    m = _metric(metric)
     _check(lib().tsw_knn(st.handle, qs.ctypes.data_as(_dp), nq, qlen, m, r, k, out, ctr))
     raw = np.frombuffer(out, dtype=np.dtype([("index", "<u8"), ("distance", "<f8")]),
                         count=nq * kk)
@@ -320,6 +333,63 @@ def knn_dk(query, data, k: int, threads: int = 1) -> SearchReport:
     t0 = time.perf_counter()
     idx, dist, c = knn(data, q[None], k, "dk")
     return _report(idx[0], dist[0], c[0], time.perf_counter() - t0)
+
+
+def knn_dk_sub(query, data, k: int, threads: int = 1) -> SearchReport:
+    """tswarp::knn_dk_sub(query, data, k, threads) -- search.hpp:75-76: the k candidates whose
+    best subsequence match of the query is closest, ranked by (match distance, index)."""
+    q = _series(query)
+    if k == 0:
+        raise ValueError("knn_dk_sub: k must be positive")
+    _check_query(q, data, False, "knn_dk_sub")
+    t0 = time.perf_counter()
+    idx, dist, c = knn(data, q[None], k, "dk_sub")
+    return _report(idx[0], dist[0], c[0], time.perf_counter() - t0)
+
+
+@dataclass
+class SubMatch:
+    """tswarp::SubMatch (dogkeeper.hpp:11-14)."""
+    distance: float
+    end_index: int
+
+
+def sub_dk_all(data, query, eps: float = float("inf")):
+    """-> (found bool[n], distance f64[n], end u64[n]): sparse_dk_sub(query, data[i], eps) for
+    every candidate (== sub_search_dk, whose greedy seed only tightens eps).  Not found:
+    distance = +inf (std::nullopt)."""
+    st = _as_store(data)
+    q = _series(query)
+    if q.shape[1] != st.dim:
+        raise ValueError("sub_search_dk: dimensionality mismatch")
+    if eps < 0:
+        raise ValueError("sparse_dk_sub: eps must be nonnegative")
+    found = np.empty(st.n, dtype=np.int32)
+    val = np.empty(st.n)
+    end = np.empty(st.n, dtype=np.uint64)
+    _check(lib().tsw_sub_dk_all(st.handle, q.ctypes.data_as(_dp), q.shape[0], float(eps),
+                                found.ctypes.data_as(_ip), val.ctypes.data_as(_dp),
+                                end.ctypes.data_as(_up)))
+    return found.astype(bool), val, end
+
+
+def sparse_dk_sub(s, t, eps: float):
+    """tswarp::sparse_dk_sub(s, t, eps) -- dogkeeper.hpp:72-73: SubMatch or None (nullopt)."""
+    s, t = _series(s), _series(t)
+    if s.shape[1] != t.shape[1]:
+        raise ValueError(f"sparse_dk_sub: dimensionality mismatch ({s.shape[1]} vs {t.shape[1]})")
+    if eps < 0:
+        raise ValueError("sparse_dk_sub: eps must be nonnegative")
+    f, v, e = sub_dk_all(Store([t]), s, eps)
+    return SubMatch(float(v[0]), int(e[0])) if f[0] else None
+
+
+def sub_search_dk(query, haystack, eps: float = float("inf")):
+    """tswarp::sub_search_dk(query, haystack, eps) -- search.hpp:68-69."""
+    q, h = _series(query), _series(haystack)
+    if q.shape[1] != h.shape[1]:
+        raise ValueError("sub_search_dk: dimensionality mismatch")
+    return sparse_dk_sub(q, h, eps)
 
 
 def epsnn_dk(query, data, eps: float, threads: int = 1) -> SearchReport:
@@ -398,8 +468,7 @@ class Plan:
         self.k = k
         self.kk = min(k, self.store.n)
         h = _vp()
-        _check(lib().tsw_plan_create(self.store.handle, nq_max, qlen,
-                                     METRIC_DTW if metric == "dtw" else METRIC_DK, r, k,
+        _check(lib().tsw_plan_create(self.store.handle, nq_max, qlen, _metric(metric), r, k,
                                      C.byref(h)))
         self._h = h
         self.nq = 0

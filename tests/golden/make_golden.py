@@ -101,5 +101,54 @@ def main():
     print(f"wrote {path} ({os.path.getsize(path) / 1024:.0f} KiB, {len(cases)} cases)")
 
 
+def main_sub():
+    """Subsequence DK fixtures: knn_dk_sub, sparse_dk_sub, sub_search_dk and
+    gdk_sub from the reference, on short queries inside longer (and ragged) haystacks."""
+    R = oracle.ref()
+    rng = np.random.default_rng(SEED + 2)
+    cases = []
+    shapes = [  # (n, haystack length range, d, query lengths, ks)
+        (40, (30, 31), 1, [6, 12], [1, 3]),
+        (50, (20, 60), 2, [5, 17], [1, 5, 50]),
+        (30, (8, 40), 3, [9, 45], [1, 4]),
+        (20, (24, 25), 16, [7], [1, 2]),
+    ]
+    for ci, (n, (lmin, lmax), d, qlens, ks) in enumerate(shapes):
+        series = [rng.standard_normal((int(rng.integers(lmin, lmax)), d)).cumsum(0) for _ in range(n)]
+        queries = [rng.standard_normal((m, d)).cumsum(0) for m in qlens]
+        if ci == 1:
+            # a query cut out of a haystack: an exact subsequence match at distance 0
+            queries[0] = series[9][3:8].copy()
+            series[21] = series[9].copy()  # duplicate haystack: tie broken by lower index
+        ds = oracle.Dataset(series)
+        case = {"name": f"sub{ci}", "d": d, "series": [hx(x) for x in series],
+                "queries": [hx(q) for q in queries], "qlens": qlens, "knn": [], "pair": []}
+        for qi, q in enumerate(queries):
+            for k in ks:
+                idx, dist, ctr = R.knn(q, ds, k, "dk_sub")
+                case["knn"].append({"q": qi, "k": k, "index": [int(i) for i in idx],
+                                    "distance": hx(dist), "counters": [int(c) for c in ctr]})
+            for si, x in enumerate(series[:10]):
+                full = R.sparse_dk_sub(q, x, float("inf"))
+                ent = {"q": qi, "i": si, "sub_inf": [full[0].hex(), full[1]],
+                       "gdk_sub": [R.gdk_sub(q, x)[0].hex(), R.gdk_sub(q, x)[1]]}
+                below = R.sparse_dk_sub(q, x, full[0] * 0.999)
+                ent["sub_below"] = None if below is None else [below[0].hex(), below[1]]
+                at = R.sub_search_dk(q, x, full[0])
+                ent["search_at"] = None if at is None else [at[0].hex(), at[1]]
+                case["pair"].append(ent)
+        cases.append(case)
+    out = {"generator": "tests/golden/make_golden.py (main_sub)",
+           "reference": "oracle/_ref/libtswarp_ref.so", "seed": SEED + 2, "cases": cases}
+    path = os.path.join(HERE, "reference_sub_vectors.json")
+    with open(path, "w") as f:
+        json.dump(out, f, separators=(",", ":"))
+    print(f"wrote {path} ({os.path.getsize(path) / 1024:.0f} KiB, {len(cases)} cases)")
+
+
 if __name__ == "__main__":
-    main()
+    if "--sub" in sys.argv:
+        main_sub()
+    else:
+        main()
+        main_sub()

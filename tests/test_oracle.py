@@ -207,3 +207,93 @@ def test_acceptance_8_search_equals_brute_force():
             order = sorted(range(n), key=lambda i: (allv[i], i))[:min(k, n)]
             idx, dist, _ = P.knn(q, ds, k, metric, r)
             assert idx.tolist() == order and dist.tolist() == [allv[i] for i in order]
+
+
+# ---- subsequence DK ----------------------------------------------------
+@pytest.fixture(scope="module")
+def golden_sub():
+    with open(os.path.join(HERE, "golden", "reference_sub_vectors.json")) as f:
+        return json.load(f)
+
+
+def sub_case_data(case):
+    d = case["d"]
+    series = [unhex(s).reshape(-1, d) for s in case["series"]]
+    queries = [unhex(q).reshape(-1, d) for q in case["queries"]]
+    return series, queries
+
+
+def _hx_match(m):
+    return None if m is None else [m[0].hex(), m[1]]
+
+
+def test_port_matches_reference_sub_golden(golden_sub):
+    P = oracle.port()
+    for case in golden_sub["cases"]:
+        series, queries = sub_case_data(case)
+        ds = oracle.Dataset(series)
+        for e in case["knn"]:
+            idx, dist, ctr = P.knn(queries[e["q"]], ds, e["k"], "dk_sub")
+            assert idx.tolist() == e["index"], (case["name"], e)
+            assert [v.hex() for v in dist.tolist()] == e["distance"], (case["name"], e)
+            assert ctr.tolist() == e["counters"], (case["name"], e)
+        for e in case["pair"]:
+            q, x = queries[e["q"]], series[e["i"]]
+            full = P.sparse_dk_sub(q, x, INF)
+            assert _hx_match(full) == e["sub_inf"]
+            assert _hx_match(P.gdk_sub(q, x)) == e["gdk_sub"]
+            assert _hx_match(P.sparse_dk_sub(q, x, full[0] * 0.999)) == e["sub_below"]
+            assert _hx_match(P.sub_search_dk(q, x, full[0])) == e["search_at"]
+            assert P.dk_sub_full(q, x) == full  # brute force: same value and end column
+
+
+def test_port_sub_matches_live_reference():
+    if not (oracle.ref_available() or os.path.isdir(oracle.REF_ROOT)):
+        pytest.skip("reference library not available")
+    P, R = oracle.port(), oracle.ref()
+    rng = np.random.default_rng(12)
+    for it in range(600):
+        d = int(rng.integers(1, 5))
+        m, n = int(rng.integers(1, 20)), int(rng.integers(1, 40))
+        s = rng.standard_normal((m, d)).cumsum(0)
+        t = rng.standard_normal((n, d)).cumsum(0)
+        if it % 7 == 0:  # integer grids: many exact ties between end columns
+            s, t = np.round(s), np.round(t)
+        eps = float(rng.random() * 4)
+        assert P.sparse_dk_sub(s, t, eps) == R.sparse_dk_sub(s, t, eps)
+        assert P.sub_search_dk(s, t, eps) == R.sub_search_dk(s, t, eps)
+        assert P.gdk_sub(s, t, eps) == R.gdk_sub(s, t, eps)
+    for _ in range(20):
+        d = int(rng.integers(1, 4))
+        n = int(rng.integers(1, 80))
+        X = [rng.standard_normal((int(rng.integers(1, 50)), d)).cumsum(0) for _ in range(n)]
+        q = rng.standard_normal((int(rng.integers(1, 15)), d)).cumsum(0)
+        k = int(rng.integers(1, 8))
+        ds = oracle.Dataset(X)
+        a, b = P.knn(q, ds, k, "dk_sub"), R.knn(q, ds, k, "dk_sub")
+        assert all(np.array_equal(x, y) for x, y in zip(a, b))
+
+
+def test_sub_properties():
+    """sub <= whole DK (the whole path is one subsequence path), the sparse engine equals the
+    brute-force DP, and knn_dk_sub equals the brute-force (distance, index) top-k."""
+    P = oracle.port()
+    rng = np.random.default_rng(13)
+    for _ in range(300):
+        d = int(rng.integers(1, 4))
+        s = rng.standard_normal((int(rng.integers(1, 25)), d))
+        t = rng.standard_normal((int(rng.integers(1, 40)), d))
+        full = P.dk_sub_full(s, t)
+        assert P.sparse_dk_sub(s, t, INF) == full
+        assert full[0] <= P.dk_full(s, t)
+        g, _ = P.gdk_sub(s, t)
+        assert g >= full[0]
+    X = [rng.standard_normal((int(rng.integers(5, 60)), 2)).cumsum(0) for _ in range(120)]
+    ds = oracle.Dataset(X)
+    for _ in range(5):
+        q = rng.standard_normal((int(rng.integers(2, 12)), 2)).cumsum(0)
+        allv = [P.dk_sub_full(q, x)[0] for x in X]
+        order = sorted(range(len(X)), key=lambda i: (allv[i], i))[:4]
+        idx, dist, ctr = P.knn(q, ds, 4, "dk_sub")
+        assert idx.tolist() == order and dist.tolist() == [allv[i] for i in order]
+        assert ctr[4] == len(X) and ctr[2] + ctr[3] == len(X)
