@@ -385,8 +385,9 @@ def main():
         roof_lb = {"bound": "hbm", "kernel": lb_kernel, **hbm_view,
                    "traffic": (load_traffic(a.config, metric) or {}).get("bound"),
                    "share_of_step": lb_ms / ph["ms_total"] if ph["ms_total"] else None}
-    dp_kernel = ("dtw4_kernel" if (d <= 4 and r <= 52) else "dtw_dp_kernel") if metric == "dtw" \
-        else "dk_dp_kernel"
+    dp_kernel = ("dtw4_kernel" if (d <= 4 and r <= 52) else
+                 "dtwt_kernel" if (d >= 5 and min(r, L - 1) <= 31) else "dtw_dp_kernel") \
+        if metric == "dtw" else "dk_dp_kernel"
     roof_dp = {"bound": "fp64", "kernel": dp_kernel,
                "achieved": dp_tflops, "peak": fp64_tflops, "unit": "TFLOP/s",
                "frac": (dp_tflops / fp64_tflops) if dp_tflops and fp64_tflops else None,

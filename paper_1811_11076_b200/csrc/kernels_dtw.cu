@@ -396,6 +396,10 @@ void launch_dtw_dp(const DpArgs& a, uint32_t max_pairs, cudaStream_t st) {
         launch_dtw4(a, max_pairs, st);
         return;
     }
+    if (dtwt_supported(a) && !std::getenv("TSW_DTW_GENERIC")) {
+        launch_dtwt(a, max_pairs, st);
+        return;
+    }
     const uint32_t r = std::min(a.r, a.qlen - 1);
     const uint32_t need = r + 1;  // lanes x G >= r + 1
     const int rpar = (int)(r & 1u);

@@ -316,6 +316,9 @@ void launch_dtw_dp(const DpArgs& a, uint32_t max_pairs, cudaStream_t st);
 // guarded small-d fast path (kernels_dtw4.cu), chosen by launch_dtw_dp when supported
 bool dtw4_supported(const DpArgs& a);
 void launch_dtw4(const DpArgs& a, uint32_t max_pairs, cudaStream_t st);
+// tiled-cost large-d path (kernels_dtwt.cu), chosen by launch_dtw_dp when supported
+bool dtwt_supported(const DpArgs& a);
+void launch_dtwt(const DpArgs& a, uint32_t max_pairs, cudaStream_t st);
 void launch_dk_dp(const DpArgs& a, uint32_t max_pairs, uint32_t max_len, cudaStream_t st);
 
 int sm_count();

@@ -115,6 +115,38 @@ def test_dtw_fast_path_variants(tsw, port, variant, monkeypatch):
                 assert_knn_equal(gi[j], gd[j], oi, od, f"{variant} d={d} L={L} r={r} q{j}")
 
 
+@pytest.mark.parametrize("variant", ["tiled", "generic"])
+def test_dtw_tiled_large_d(tsw, port, variant, monkeypatch):
+    """The tiled-cost large-d path (kernels_dtwt.cu, d >= 5, r <= 31) against the oracle and the
+    generic kernel: tiny L (tiles reaching into both guard tiles), L not a multiple of 4 or 32,
+    both band parities, r = 0 and r = 31 (the widest band of one warp), thresholds that abandon
+    in the first and in later cost phases, and the k-NN pipeline with the cumulative bound."""
+    import oracle
+
+    if variant == "generic":
+        monkeypatch.setenv("TSW_DTW_GENERIC", "1")
+    rng = np.random.default_rng(21)
+    for d, L, r in ((5, 1, 0), (6, 2, 1), (5, 3, 2), (5, 37, 5), (7, 64, 31), (16, 256, 26),
+                    (16, 130, 13), (24, 100, 30), (16, 50, 0), (9, 300, 12), (16, 45, 44)):
+        X = walks(rng, 40, L, d)
+        q = walks(rng, 1, L, d)[0]
+        st = tsw.Store(X)
+        ex, val = tsw.dist_all(st, q, "dtw", r)
+        ref = port.dtw_all(q, oracle.Dataset(X), r)
+        assert ex.all() and np.array_equal(val.view(np.uint64), ref.view(np.uint64)), (d, L, r)
+        for eps in (float(np.quantile(ref, 0.05)), float(np.median(ref)), float(ref.min()) * 0.5):
+            ex2, val2 = tsw.dist_all(st, q, "dtw", r, eps)
+            for i in range(len(X)):
+                oe, ov = port.dtw_early_abandon(q, X[i], r, eps)
+                assert ex2[i] == oe and val2[i] == ov, (d, L, r, eps, i, ex2[i], val2[i], oe, ov)
+        Q = np.concatenate([q[None], X[3:4] + 1e-3, walks(rng, 2, L, d)])
+        gi, gd, gc = tsw.knn(tsw.Dataset(X), Q, 3, "dtw", r)
+        for j in range(len(Q)):
+            oi, od, _ = port.knn(Q[j], oracle.Dataset(X), 3, "dtw", r)
+            assert_knn_equal(gi[j], gd[j], oi, od, f"{variant} d={d} L={L} r={r} q{j}")
+            assert gc[j][0] == 40 and gc[j][1] + gc[j][2] + gc[j][3] == 40
+
+
 def test_dtw_spec_kats(tsw):
     # SPEC.md:207-210: s=((0),(0)), t=((1),(1)), r=1 -> 2 ; s=t -> 0
     ex, val = tsw.dist_all(tsw.Store(np.ones((1, 2, 1))), np.zeros((2, 1)), "dtw", 1)
