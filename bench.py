@@ -47,7 +47,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
-    ap.add_argument("--metric", default=None, choices=["dtw", "dk"])
+    ap.add_argument("--metric", default=None, choices=["dtw", "dk", "dk_sub"])
+    ap.add_argument("--sub-len", type=int, default=64,
+                    help="dk_sub: query window length (the middle of each config query)")
     ap.add_argument("--seed", type=int, default=SEED)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0,
@@ -56,7 +58,17 @@ def parse():
     return ap.parse_args()
 
 
-def workload(cfg: int, metric: str, sh: dict, nq: int) -> dict:
+def workload(cfg: int, metric: str, sh: dict, nq: int, qlen: int | None = None) -> dict:
+    if metric == "dk_sub":
+        return {
+            "workload": f"config{cfg} store: {sh['k']}-NN subsequence DK (knn_dk_sub) of "
+                        f"{qlen}-point query windows, N={sh['count']}, d={sh['d']}, "
+                        f"L={sh['len']}, {nq} queries/step",
+            "config_id": cfg, "n": sh["count"], "d": sh["d"], "L": sh["len"], "k": sh["k"],
+            "r": None, "queries_per_step": nq, "query_len": qlen, "metric": metric,
+            "queries": "the middle qlen points of each of the config's seeded queries",
+            "l2": "flushed between timed steps (256 MiB device write)",
+        }
     return {
         "workload": f"config{cfg}: {sh['k']}-NN {metric.upper()}"
                     + (f" r={sh['r']} + LB_Box" if metric == "dtw" else " (dog-keeper)")
@@ -187,6 +199,16 @@ def _cpu_model():
     return None
 
 
+def sub_windows(qs: np.ndarray, metric: str, sub_len: int) -> np.ndarray:
+    """dk_sub: the middle `sub_len` points of every query (a subsequence to find)."""
+    if metric != "dk_sub":
+        return qs
+    L = qs.shape[1]
+    w = max(1, min(sub_len, L))
+    o = (L - w) // 2
+    return np.ascontiguousarray(qs[:, o:o + w])
+
+
 def run_reference_arm(a, sh, metric):
     ws, rank, _ = dist_init()
     if rank != 0:
@@ -195,6 +217,7 @@ def run_reference_arm(a, sh, metric):
 
     db, _ = t.synth(a.config, 0, a.seed)
     qs, _ = t.synth(a.config, 1, a.seed)
+    qs = sub_windows(qs, metric, a.sub_len)
     per_step = max(3.0, min(a.cpu_seconds, 60.0))
     rates, info = cpu_reference(a.config, metric, sh, db, qs, per_step, steps=a.steps,
                                 warmup=a.warmup)
@@ -204,7 +227,7 @@ def run_reference_arm(a, sh, metric):
             "ms_per_step": 1000.0 * info["seconds_per_step"],
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded random walks, BASELINE.json shapes)",
-            "config": workload(a.config, metric, sh, len(qs)),
+            "config": workload(a.config, metric, sh, len(qs), qs.shape[1]),
             "cpu_baseline": {"value": v, "unit": "queries/s", **info},
             "e2e": {"value": v, "unit": "queries/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
@@ -252,6 +275,7 @@ def main():
 
     db, _ = t.synth(a.config, 0, a.seed)
     qs, _ = t.synth(a.config, 1, a.seed + rank)
+    qs = sub_windows(qs, metric, a.sub_len)
     nq, L, d = qs.shape
     k, r = sh["k"], sh["r"]
     store = t.Store(db, device=dev)
@@ -401,7 +425,7 @@ def main():
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": total_ms / a.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded random walks, BASELINE.json shapes; no public dataset)",
-            "config": _mode(workload(a.config, metric, sh, nq), use_graph),
+            "config": _mode(workload(a.config, metric, sh, nq, L), use_graph),
             "e2e": {"value": e2e_value, "unit": "queries/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,
                     "api": "tsw_knn (C ABI) with host query/result buffers"},

@@ -58,6 +58,15 @@ __device__ __forceinline__ double cost_rt(const double* __restrict__ srow,
     return acc;
 }
 
+// query point 0 (compile-time d), for the subsequence row-0 scan
+template <int D>
+__device__ __forceinline__ Pt<D> sp0_of(const double* __restrict__ s, int stride) {
+    Pt<D> p;
+#pragma unroll
+    for (int kk = 0; kk < D; ++kk) p.x[kk] = __ldg(s + kk * (int)kTile);
+    return p;
+}
+
 struct Strip {
     int R, cstart, b_hi, b_alive_hi;
     int nrows;  // rows of this strip (<= kStrip)
@@ -173,7 +182,7 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
 
         Strip S;
         S.b_hi = -1;
-        S.b_alive_hi = SUB ? n - 1 : 0;  // virtual start at (0, 0) / at every (0, j)
+        S.b_alive_hi = 0;  // virtual start at (0, 0) (subsequence mode: row-0 columns, scanned)
         int b_alive_lo = 0;
         bool dead = false;
         double fin = kInf;
@@ -200,37 +209,99 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
                 }
             }
             double left[RPL];
-#pragma unroll
-            for (int q = 0; q < RPL; ++q) left[q] = kInf;
-            double mine = kInf, up_prev = kInf;
+            double mine, up_prev;
             const int last_lane = (S.nrows - 1) / RPL;
-            const int kmax = (n - 1 - S.cstart) + last_lane;
-            bool l2 = false, l3 = false, dummy = false;
-            int k_done = -1;
-            Pt<D> ta, tb;  // candidate points of the current / next column (ping-pong)
-            load_pt<D>(ta, t, S.cstart - lane, stride);
-            for (int k = 0; k <= kmax; k += 4) {
-                dk_step<D, RPL, false, SUB>(S, k, lane, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, dummy, ta, tb, sf);
-                dk_step<D, RPL, false, SUB>(S, k + 1, lane, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, dummy, tb, ta, sf);
-                dk_step<D, RPL, true, SUB>(S, k + 2, lane, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, l2, ta, tb, sf);
-                dk_step<D, RPL, true, SUB>(S, k + 3, lane, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, l3, tb, ta, sf);
-                k_done = k + 3;
-                // dead cut: no live cell on steps k+2, k+3 and nothing live ahead of lane 0
-                if (!__any_sync(kFull, l2 || l3) && S.cstart + k + 3 > S.b_alive_hi) break;
-                if (st && (k & 60) == 60) Tsq = ld_volatile(&st->Tsq);
-            }
-            const int k_last = min(k_done, kmax);  // last step whose cells were computed
-            {   // cells computed by this lane in this strip (analytic count)
-                const int rows = min(RPL, max(0, S.nrows - RPL * lane));
-                const int c = min(k_last - lane, n - 1 - S.cstart) + 1;
-                cells += (c > 0 ? (unsigned long long)c : 0ull) * (unsigned long long)rows;
+            const int strip_lo = S.cstart;
+            bool reached_end = false;
+            int k_last = -1;
+            double dg0 = kInf;  // lane 0's diagonal predecessor at a segment start (boundary row)
+            // Segments: the sweep stops at a dead cut (two skewed steps without a live cell); if
+            // a live boundary cell lies ahead (the previous strip's boundary row, or in
+            // subsequence mode a row-0 column with c(0, j) <= T: every column may start a match)
+            // it restarts there with a fresh front.  Every cell in between is > T: its paths
+            // cross the dead cut or start at a dead boundary cell.
+            for (;;) {
+#pragma unroll
+                for (int q = 0; q < RPL; ++q) left[q] = kInf;
+                mine = kInf;
+                up_prev = dg0;
+                const int kmax = (n - 1 - S.cstart) + last_lane;
+                bool l2 = false, l3 = false, dummy = false, cut = false;
+                int k_done = -1;
+                Pt<D> ta, tb;  // candidate points of the current / next column (ping-pong)
+                load_pt<D>(ta, t, S.cstart - lane, stride);
+                for (int k = 0; k <= kmax; k += 4) {
+                    dk_step<D, RPL, false, SUB>(S, k, lane, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, dummy, ta, tb, sf);
+                    dk_step<D, RPL, false, SUB>(S, k + 1, lane, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, dummy, tb, ta, sf);
+                    dk_step<D, RPL, true, SUB>(S, k + 2, lane, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, l2, ta, tb, sf);
+                    dk_step<D, RPL, true, SUB>(S, k + 3, lane, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, l3, tb, ta, sf);
+                    k_done = k + 3;
+                    if (!__any_sync(kFull, l2 || l3)) {  // dead cut
+                        cut = true;
+                        break;
+                    }
+                    if (st && (k & 60) == 60) Tsq = ld_volatile(&st->Tsq);
+                }
+                k_last = min(k_done, kmax);  // last step whose cells were computed
+                {   // cells computed by this lane in this segment (analytic count)
+                    const int rows = min(RPL, max(0, S.nrows - RPL * lane));
+                    const int c = min(k_last - lane, n - 1 - S.cstart) + 1;
+                    cells += (c > 0 ? (unsigned long long)c : 0ull) * (unsigned long long)rows;
+                }
+                if (!cut || k_last >= kmax) {
+                    reached_end = true;
+                    break;
+                }
+                // next live boundary column right of lane 0's front (column cstart + k_last).  A
+                // live boundary cell AT the front column still starts paths diagonally into
+                // column `from`, so the boundary-row scan starts one column earlier.
+                const int from = S.cstart + k_last + 1;
+                const bool row0 = SUB && S.first;
+                const int lim = row0 ? n - 1 : min(S.b_hi, S.b_alive_hi);
+                int J = -1;
+                for (int j0 = row0 ? from : from - 1; j0 <= lim; j0 += 32) {
+                    const int j = j0 + lane;
+                    bool lv = false;
+                    if (j <= lim) {
+                        if (row0) {
+                            double c0;
+                            if constexpr (D > 0) {
+                                Pt<D> tj;
+                                load_pt<D>(tj, t, j, stride);
+                                c0 = cost<D>(sp0_of<D>(s, stride), tj);
+                            } else {
+                                c0 = cost_rt(s, t + toff_rt(j, stride), d);
+                            }
+                            lv = c0 <= Tsq;
+                        } else {
+                            lv = bnd[j] <= Tsq;
+                        }
+                    }
+                    const unsigned bm = __ballot_sync(kFull, lv);
+                    if (bm) {
+                        J = j0 + __ffs(bm) - 1;
+                        break;
+                    }
+                }
+                if (J < 0) break;
+                J = max(J, from);
+                // the boundary cell diagonal to (R, J): consumed by lane 0 on the last step when
+                // J == from, possibly live (its own cell may be dead); read before the gap fill
+                dg0 = (!S.first && J - 1 <= S.b_hi) ? bnd[J - 1] : kInf;
+                if (S.write_bnd) {  // lane 31 wrote [cstart, cstart + k_last - 31]; the gap is > T
+                    __syncwarp();
+                    for (int j = max(S.cstart, S.cstart + k_last - 30) + lane; j < J; j += 32) bnd[j] = kInf;
+                    __syncwarp();
+                }
+                S.cstart = J;
             }
             if (S.write_bnd) {
                 __syncwarp();
-                // next boundary row = lane 31's last row, written on [cstart, min(n-1, cstart+k_last-31)]
+                // next boundary row = lane 31's last row, written on [strip_lo, cstart + k_last - 31]
+                // (gaps between segments hold +inf)
                 const int hi = min(n - 1, S.cstart + k_last - 31);
                 int first = -1, last = -1;
-                for (int j0 = S.cstart; j0 <= hi; j0 += 32) {
+                for (int j0 = strip_lo; j0 <= hi; j0 += 32) {
                     const int j = j0 + lane;
                     const bool lv = j <= hi && bnd[j] <= Tsq;
                     const unsigned bm = __ballot_sync(kFull, lv);
@@ -260,7 +331,7 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
                 for (int q = 0; q < RPL; ++q)
                     if (q == fq) mv = left[q];
                 const double lv = __shfl_sync(kFull, mv, fl);
-                if (k_last >= kmax) fin = lv;
+                if (reached_end) fin = lv;
             }
         }
         if (lane == 0) {

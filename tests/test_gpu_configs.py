@@ -81,3 +81,21 @@ def test_config3_label_accuracy(tsw):
         idx, _, _ = tsw.knn(ds, qs, 5, metric, 26)
         acc = float(np.mean(dbl[idx[:, 0].astype(np.int64)] == labels))
         assert acc >= 0.95, (metric, acc)
+
+
+@pytest.mark.parametrize("cfg", [1, 3])
+def test_dk_topk_equals_gpu_brute_force_all_queries(tsw, cfg):
+    """Every query of the DK configs: the pruned pipeline's (distance, index) top-k equals the
+    unpruned GPU brute force (tsw_dist_all, eps = +inf: dk_full for every candidate), and two
+    executions agree (the thresholds evolve differently run to run)."""
+    db, qs, labels, ds = data(tsw, cfg)
+    sh = tsw.synth_shape(cfg, 0)
+    k = sh["k"]
+    idx, dist, _ = tsw.knn(ds, qs, k, "dk")
+    idx2, dist2, _ = tsw.knn(ds, qs, k, "dk")
+    assert np.array_equal(idx, idx2) and np.array_equal(dist, dist2)
+    for q in range(len(qs)):
+        ex, val = tsw.dist_all(ds.store, qs[q], "dk")
+        order = np.lexsort((np.arange(len(val)), val))[:k]
+        assert idx[q].tolist() == order.tolist(), (q, idx[q], order)
+        assert np.array_equal(dist[q].view(np.uint64), val[order].view(np.uint64))

@@ -179,6 +179,26 @@ def test_dk_all_bit_exact(tsw, port, N, L, d):
             assert ex2[i] == oe and val2[i] == ov, (eps, i, ex2[i], val2[i], oe, ov)
 
 
+@pytest.mark.parametrize("L,d,m", [(200, 2, 200), (300, 3, 150), (130, 1, 260), (257, 2, 129)])
+def test_dk_thresholds_multi_strip(tsw, port, L, d, m):
+    """Thresholded DK over queries spanning several 64/128-row strips, at 12 thresholds: the
+    strip sweep restarts at live boundary cells after dead cuts (a live boundary cell at the
+    cut column still reaches the next column diagonally); Exact/Exceeds and values must equal
+    sparse_dk (dogkeeper.cpp:227-233) for every candidate."""
+    rng = np.random.default_rng(L * 7 + d)
+    X = walks(rng, 120, L, d) * 0.3
+    q = walks(rng, 1, m, d)[0] * 0.3
+    X[5, : min(L, m)] = q[: min(L, m)] + 0.05 * rng.standard_normal((min(L, m), d))
+    st = tsw.Store(X)
+    ex, full = tsw.dist_all(st, q, "dk")
+    assert ex.all()
+    for eps in np.quantile(full, np.linspace(0.0, 0.9, 12)):
+        ex2, val2 = tsw.dist_all(st, q, "dk", 0, float(eps))
+        for i in range(len(X)):
+            oe, ov = port.sparse_dk(q, X[i], float(eps))
+            assert ex2[i] == oe and val2[i] == ov, (eps, i, ex2[i], val2[i], oe, ov)
+
+
 def test_dk_ragged_lengths(tsw, port):
     series = [RNG.standard_normal((int(RNG.integers(1, 90)), 3)).cumsum(0) for _ in range(150)]
     q = RNG.standard_normal((57, 3)).cumsum(0)
