@@ -31,6 +31,8 @@ extern "C" {
 #define TSW_ENOMEM 2      /* device / host allocation failed                    */
 #define TSW_ECUDA 3       /* CUDA error or no usable device                     */
 #define TSW_EVALIDATION 4 /* tswarp::ValidationError in the reference           */
+#define TSW_EPARSE 5      /* tswarp::ParseError in the reference (dataset files) */
+#define TSW_EIO 6         /* tswarp::IoError in the reference (dataset files)    */
 
 #define TSW_METRIC_DTW 0 /* banded DTW, squared-Euclidean point cost (dtw.hpp:8-16)        */
 #define TSW_METRIC_DK 1  /* dog-keeper / discrete Frechet, Euclidean cost (dogkeeper.hpp) */
@@ -157,6 +159,33 @@ int tsw_dist_all(tsw_store* store, const double* query, uint64_t qlen, int metri
  * `end` may be NULL.  eps < 0 -> TSW_EINVAL. */
 int tsw_sub_dk_all(tsw_store* store, const double* query, uint64_t qlen, double eps, int* found,
                    double* value, uint64_t* end);
+
+/* ---- dataset files ----------------------------------------------------------
+ * tsw_dataset_load_json replaces tswarp::load_dataset (dataset_io.hpp:20, dataset_io.cpp:45-112):
+ * the JSON format of dataset_io.hpp:9-19, {"dim": k, "meta": {...}, "series": [{"label": "A",
+ * "points": [[...], ...]}, ...]}, parsed and validated on the host with the reference's checks,
+ * order and messages: TSW_EIO (cannot open), TSW_EPARSE (syntax / structure), TSW_EVALIDATION
+ * (component counts, non-finite values, empty series list, mixed labels).  The result is a host
+ * dataset; tsw_dataset_to_store uploads it into a device store (tsw_store_create).
+ * tsw_dataset_save_json replaces tswarp::save_dataset (dataset_io.cpp:114-140): numbers in the
+ * shortest round-trip form, so load(save(x)) reproduces x bit for bit.  labels / meta may be
+ * NULL (unlabeled / no meta). */
+typedef struct tsw_dataset tsw_dataset;
+int tsw_dataset_load_json(const char* path, tsw_dataset** out);
+void tsw_dataset_free(tsw_dataset* ds);
+int tsw_dataset_info(const tsw_dataset* ds, uint64_t* n, uint64_t* d, uint64_t* total_points,
+                     int* labeled, uint64_t* n_meta);
+/* concatenated row-major values (total_points * d) and per-series lengths (n), owned by ds */
+const double* tsw_dataset_values(const tsw_dataset* ds);
+const uint64_t* tsw_dataset_lengths(const tsw_dataset* ds);
+/* label of series i (NULL when unlabeled); meta entry i in key order */
+const char* tsw_dataset_label(const tsw_dataset* ds, uint64_t i);
+int tsw_dataset_meta(const tsw_dataset* ds, uint64_t i, const char** key, const char** value);
+int tsw_dataset_to_store(const tsw_dataset* ds, int device, tsw_store** out);
+int tsw_dataset_save_json(const char* path, const double* values, const uint64_t* lengths,
+                          uint64_t n, uint64_t d, const char* const* labels,
+                          const char* const* meta_keys, const char* const* meta_values,
+                          uint64_t n_meta);
 
 /* ---- diagnostics ---------------------------------------------------------------------------
  * Host<->device bytes moved by the calling thread's last tsw_knn / plan set_queries+fetch. */

@@ -23,6 +23,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 PORT_SO = os.path.join(HERE, "_build", "liborc.so")
 REF_SO = os.path.join(HERE, "_ref", "libtswarp_ref.so")
+REF_IO_SO = os.path.join(HERE, "_ref", "libtswarp_ref_io.so")
 REF_ROOT = "/root/reference/proj/core"
 
 _METRIC = {"dtw": 0, "dk": 1, "dk_sub": 2}
@@ -40,7 +41,7 @@ def build(ref: bool | None = None) -> None:
     """Build the port (always) and the reference library (when /root/reference exists)."""
     targets = ["port"]
     if ref or (ref is None and os.path.isdir(REF_ROOT)):
-        targets.append("ref")
+        targets += ["ref", "ref_io"]
     subprocess.run(["make", "-s", "-C", HERE] + targets, check=True)
 
 
@@ -350,3 +351,80 @@ def ref() -> Oracle:
                 build(ref=True)
             _cache["ref"] = Oracle(REF_SO, "reference")
         return _cache["ref"]
+
+
+class RefIO:
+    """The reference's own load_dataset / save_dataset (oracle/_ref/libtswarp_ref_io.so, built
+    against nlohmann/json 3.11.3).  load() -> (values f64[total*d], lengths u64[n], d, labels |
+    None, meta dict) or raises (kind, message) as RefIOError."""
+
+    ERR = {1: "invalid_argument", 3: "runtime_error", 4: "ValidationError", 5: "ParseError",
+           6: "IoError"}
+
+    def __init__(self, path: str):
+        L = self.lib = C.CDLL(path)
+        L.refio_last_error.restype = C.c_char_p
+        L.refio_load.restype = C.c_void_p
+        L.refio_load.argtypes = [C.c_char_p, _ip]
+        L.refio_free.argtypes = [C.c_void_p]
+        L.refio_shape.argtypes = [C.c_void_p, _up, _up, _up, _ip, _up]
+        L.refio_copy.argtypes = [C.c_void_p, _dp, _up]
+        L.refio_label.argtypes = [C.c_void_p, _u64]
+        L.refio_label.restype = C.c_char_p
+        L.refio_meta.argtypes = [C.c_void_p, _u64, C.POINTER(C.c_char_p), C.POINTER(C.c_char_p)]
+        L.refio_save.argtypes = [C.c_void_p, C.c_char_p]
+
+    def _open(self, path):
+        rc = C.c_int(0)
+        h = self.lib.refio_load(os.fsencode(path), C.byref(rc))
+        if not h:
+            raise RefIOError(self.ERR.get(rc.value, str(rc.value)),
+                             self.lib.refio_last_error().decode("utf-8", "replace"))
+        return h
+
+    def load(self, path):
+        h = self._open(path)
+        try:
+            n, d, tot, nm = (np.zeros(1, dtype=np.uint64) for _ in range(4))
+            lab = C.c_int(0)
+            self.lib.refio_shape(h, _uptr(n), _uptr(d), _uptr(tot), C.byref(lab), _uptr(nm))
+            n, d, tot, nm = int(n[0]), int(d[0]), int(tot[0]), int(nm[0])
+            vals = np.zeros(tot * d)
+            lens = np.zeros(n, dtype=np.uint64)
+            self.lib.refio_copy(h, _dptr(vals), _uptr(lens))
+            labels = [self.lib.refio_label(h, i).decode("utf-8") for i in range(n)] if lab.value else None
+            meta = {}
+            for i in range(nm):
+                k, v = C.c_char_p(), C.c_char_p()
+                self.lib.refio_meta(h, i, C.byref(k), C.byref(v))
+                meta[k.value.decode("utf-8")] = v.value.decode("utf-8")
+            return vals, lens, d, labels, meta
+        finally:
+            self.lib.refio_free(h)
+
+    def resave(self, src, dst):
+        """load_dataset(src) then save_dataset(dst) through the reference."""
+        h = self._open(src)
+        try:
+            if self.lib.refio_save(h, os.fsencode(dst)) != 0:
+                raise RefIOError("save", self.lib.refio_last_error().decode())
+        finally:
+            self.lib.refio_free(h)
+
+
+class RefIOError(Exception):
+    def __init__(self, kind, message):
+        super().__init__(f"{kind}: {message}")
+        self.kind, self.message = kind, message
+
+
+def ref_io() -> RefIO:
+    with _lock:
+        if "ref_io" not in _cache:
+            if not os.path.exists(REF_IO_SO):
+                if os.path.isdir(REF_ROOT):
+                    subprocess.run(["make", "-s", "-C", HERE, "ref_io"], check=True)
+                if not os.path.exists(REF_IO_SO):
+                    raise OracleError("oracle/_ref/libtswarp_ref_io.so unavailable")
+            _cache["ref_io"] = RefIO(REF_IO_SO)
+        return _cache["ref_io"]

@@ -137,6 +137,8 @@ double up_factor(double c) { return std::nextafter(1.0 + c * 0x1p-53, INFINITY);
 
 }  // namespace
 
+void tswb::set_last_error(const std::string& msg) { g_err = msg; }
+
 int tswb::sm_count() {
     static int cached[64] = {0};
     int dev = 0;

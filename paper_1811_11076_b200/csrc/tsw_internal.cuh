@@ -18,6 +18,7 @@
 #pragma once
 
 #include <cstdint>
+#include <string>
 #include <cuda_runtime.h>
 
 namespace tswb {
@@ -322,5 +323,6 @@ void launch_dtwt(const DpArgs& a, uint32_t max_pairs, cudaStream_t st);
 void launch_dk_dp(const DpArgs& a, uint32_t max_pairs, uint32_t max_len, cudaStream_t st);
 
 int sm_count();
+void set_last_error(const std::string& msg);
 
 }  // namespace tswb

@@ -4,6 +4,7 @@
 #include "tswarp_b200.hpp"
 
 #include <chrono>
+#include <memory>
 #include <mutex>
 
 #include "tswarp_b200.h"
@@ -23,6 +24,8 @@ struct DeviceStore {
     switch (rc) {
         case TSW_EINVAL: throw std::invalid_argument(msg);
         case TSW_EVALIDATION: throw ValidationError(msg);
+        case TSW_EPARSE: throw ParseError(msg);
+        case TSW_EIO: throw IoError(msg);
         default: throw std::runtime_error("tswarp_b200: " + msg);
     }
 }
@@ -218,6 +221,55 @@ SearchReport epsnn_dk(const TimeSeries& query, const Dataset& data, double eps, 
     rep.counters = {c.lb_computed, c.lb_pruned, c.full_dp, c.early_abandoned, c.gdk_calls};
     rep.wall_time_seconds = std::chrono::duration<double>(Clock::now() - start).count();
     return rep;
+}
+
+Dataset load_dataset(const std::string& path) {
+    tsw_dataset* h = nullptr;
+    const int rc = tsw_dataset_load_json(path.c_str(), &h);
+    if (rc != TSW_OK) detail::rethrow(rc);
+    std::unique_ptr<tsw_dataset, void (*)(tsw_dataset*)> guard(h, tsw_dataset_free);
+    uint64_t n = 0, d = 0, nm = 0;
+    int labeled = 0;
+    tsw_dataset_info(h, &n, &d, nullptr, &labeled, &nm);
+    const double* v = tsw_dataset_values(h);
+    const uint64_t* len = tsw_dataset_lengths(h);
+    std::vector<TimeSeries> series;
+    series.reserve(n);
+    uint64_t off = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+        std::optional<std::string> label;
+        if (labeled) label = tsw_dataset_label(h, i);
+        series.emplace_back(std::vector<double>(v + off, v + off + len[i] * d), d, std::move(label));
+        off += len[i] * d;
+    }
+    std::map<std::string, std::string> meta;
+    for (uint64_t i = 0; i < nm; ++i) {
+        const char* k = nullptr;
+        const char* val = nullptr;
+        tsw_dataset_meta(h, i, &k, &val);
+        meta.emplace(k, val);
+    }
+    return Dataset(std::move(series), std::move(meta));
+}
+
+void save_dataset(const Dataset& ds, const std::string& path) {
+    std::vector<double> values;
+    std::vector<uint64_t> lengths;
+    std::vector<const char*> labels;
+    for (const auto& s : ds.series()) {
+        values.insert(values.end(), s.flat().begin(), s.flat().end());
+        lengths.push_back(s.length());
+        if (s.label()) labels.push_back(s.label()->c_str());
+    }
+    std::vector<const char*> keys, vals;
+    for (const auto& [k, v] : ds.meta()) {
+        keys.push_back(k.c_str());
+        vals.push_back(v.c_str());
+    }
+    const int rc = tsw_dataset_save_json(path.c_str(), values.data(), lengths.data(), ds.size(),
+                                         ds.dim(), ds.labeled() ? labels.data() : nullptr,
+                                         keys.data(), vals.data(), keys.size());
+    if (rc != TSW_OK) detail::rethrow(rc);
 }
 
 }  // namespace tswarp

@@ -60,6 +60,14 @@ class TswError(RuntimeError):
     pass
 
 
+class ParseError(RuntimeError):
+    """tswarp::ParseError (types.hpp:19-22): malformed dataset files."""
+
+
+class IoError(RuntimeError):
+    """tswarp::IoError (types.hpp:31-34): dataset files that cannot be read or written."""
+
+
 class Neighbor_t(C.Structure):
     _fields_ = [("index", C.c_uint64), ("distance", C.c_double)]
 
@@ -118,6 +126,20 @@ def lib():
     L.tsw_last_transfer_bytes.argtypes = [_up, _up]
     L.tsw_fp64_peak.argtypes = [_dp]
     L.tsw_l2_flush.argtypes = [_vp, _u64, _vp]
+    L.tsw_dataset_load_json.argtypes = [C.c_char_p, C.POINTER(_vp)]
+    L.tsw_dataset_free.argtypes = [_vp]
+    L.tsw_dataset_free.restype = None
+    L.tsw_dataset_info.argtypes = [_vp, _up, _up, _up, _ip, _up]
+    L.tsw_dataset_values.argtypes = [_vp]
+    L.tsw_dataset_values.restype = _dp
+    L.tsw_dataset_lengths.argtypes = [_vp]
+    L.tsw_dataset_lengths.restype = _up
+    L.tsw_dataset_label.argtypes = [_vp, _u64]
+    L.tsw_dataset_label.restype = C.c_char_p
+    L.tsw_dataset_meta.argtypes = [_vp, _u64, C.POINTER(C.c_char_p), C.POINTER(C.c_char_p)]
+    L.tsw_dataset_to_store.argtypes = [_vp, C.c_int, C.POINTER(_vp)]
+    L.tsw_dataset_save_json.argtypes = [C.c_char_p, _dp, _up, _u64, _u64, C.POINTER(C.c_char_p),
+                                        C.POINTER(C.c_char_p), C.POINTER(C.c_char_p), _u64]
     L.tsw_synth_shape.argtypes = [C.c_int, C.c_int, _up, _up, _up, _up, _up]
     L.tsw_synth_generate.argtypes = [C.c_int, C.c_int, _u64, _dp, C.POINTER(C.c_int32)]
     _lib = L
@@ -134,6 +156,10 @@ def _check(rc: int) -> None:
         raise ValidationError(msg)
     if rc == 2:
         raise MemoryError(msg)
+    if rc == 5:
+        raise ParseError(msg)
+    if rc == 6:
+        raise IoError(msg)
     raise TswError(msg)
 
 
@@ -247,7 +273,7 @@ class Store:
 class Dataset:
     """Mirror of tswarp::Dataset: validated series plus a lazily uploaded device store."""
 
-    def __init__(self, series, labels: Sequence[str] | None = None):
+    def __init__(self, series, labels: Sequence[str] | None = None, meta: dict | None = None):
         if isinstance(series, np.ndarray) and series.ndim == 3:
             self._arr = np.ascontiguousarray(series, dtype=np.float64)
             self._list = None
@@ -261,6 +287,7 @@ class Dataset:
         if self.n == 0:
             raise ValidationError("dataset must contain at least one series")
         self.labels = list(labels) if labels is not None else None
+        self.meta = dict(meta) if meta else {}
         self._store: Store | None = None
 
     def __len__(self):
@@ -274,6 +301,57 @@ class Dataset:
         if self._store is None:
             self._store = Store(self._arr if self._arr is not None else self._list)
         return self._store
+
+
+def series(self, i: int) -> np.ndarray:
+    return self._arr[i] if self._arr is not None else self._list[i]
+
+
+Dataset.series = series
+
+
+# ---- dataset files (dataset_io.hpp:9-23) ---------------------------------------------------
+def load_dataset(path) -> Dataset:
+    """tswarp::load_dataset(path) -- dataset_io.cpp:45-112: ParseError / ValidationError /
+    IoError as the reference raises them."""
+    L = lib()
+    h = _vp()
+    _check(L.tsw_dataset_load_json(os.fsencode(path), C.byref(h)))
+    try:
+        n, d, tot, nm = _u64(), _u64(), _u64(), _u64()
+        lab = C.c_int()
+        _check(L.tsw_dataset_info(h, C.byref(n), C.byref(d), C.byref(tot), C.byref(lab), C.byref(nm)))
+        vals = np.ctypeslib.as_array(L.tsw_dataset_values(h), shape=(tot.value * d.value,)).copy()
+        lens = np.ctypeslib.as_array(L.tsw_dataset_lengths(h), shape=(n.value,)).copy()
+        labels = [L.tsw_dataset_label(h, i).decode("utf-8") for i in range(n.value)] if lab.value else None
+        meta = {}
+        for i in range(nm.value):
+            k, v = C.c_char_p(), C.c_char_p()
+            _check(L.tsw_dataset_meta(h, i, C.byref(k), C.byref(v)))
+            meta[k.value.decode("utf-8")] = v.value.decode("utf-8")
+    finally:
+        L.tsw_dataset_free(h)
+    offs = np.concatenate([[0], np.cumsum(lens * d.value)]).astype(np.int64)
+    sers = [vals[offs[i]:offs[i + 1]].reshape(-1, d.value) for i in range(n.value)]
+    if len(set(lens.tolist())) == 1:
+        return Dataset(np.stack(sers), labels, meta)
+    return Dataset(sers, labels, meta)
+
+
+def save_dataset(ds: Dataset, path) -> None:
+    """tswarp::save_dataset(ds, path) -- dataset_io.cpp:114-140 (round-trip exact numbers)."""
+    sers = [np.ascontiguousarray(ds.series(i), dtype=np.float64) for i in range(ds.n)]
+    vals = np.concatenate([x.reshape(-1) for x in sers])
+    lens = np.array([x.shape[0] for x in sers], dtype=np.uint64)
+    labels = None
+    if ds.labels is not None:
+        labels = (C.c_char_p * ds.n)(*[str(x).encode("utf-8") for x in ds.labels])
+    keys = sorted(ds.meta)
+    kk = (C.c_char_p * max(1, len(keys)))(*[k.encode("utf-8") for k in keys])
+    vv = (C.c_char_p * max(1, len(keys)))(*[str(ds.meta[k]).encode("utf-8") for k in keys])
+    _check(lib().tsw_dataset_save_json(os.fsencode(path), vals.ctypes.data_as(_dp),
+                                       lens.ctypes.data_as(_up), ds.n, ds.dim, labels, kk, vv,
+                                       len(keys)))
 
 
 def _as_store(data) -> Store:

@@ -146,9 +146,101 @@ def main_sub():
     print(f"wrote {path} ({os.path.getsize(path) / 1024:.0f} KiB, {len(cases)} cases)")
 
 
+IO_DOCS = [  # (name, document bytes): valid files, number/strings edge cases, every error path
+    ("basic", b'{"dim": 2, "meta": {"src": "unit", "a": "b"}, "series": [{"label": "A", "points": [[1, 2], [3.5, -4e-3]]}, {"label": "B", "points": [[0.1, 0.2]]}]}'),
+    ("unlabeled_ragged", b'{"dim":1,"series":[{"points":[[1],[2],[3]]},{"points":[[4]]}]}'),
+    ("no_meta_ws", b' \r\n\t{ "series" : [ { "points" : [ [ 7 ] ] } ] , "dim" : 1 } \n'),
+    ("bom", b'\xef\xbb\xbf{"dim":1,"series":[{"points":[[1]]}]}'),
+    ("numbers", b'{"dim":1,"series":[{"points":[[-0],[-0.0],[0.1],[1e400],[1E5],[123456789012345678901234567890],[-9223372036854775809],[18446744073709551615],[18446744073709551616],[9007199254740993],[1.7976931348623157e308],[4.9e-324],[1e-400],[2.2250738585072011e-308],[0.30000000000000004],[-1.5e+2]]}]}'),
+    ("numbers_finite", b'{"dim":1,"series":[{"points":[[-0],[-0.0],[0.1],[1E5],[123456789012345678901234567890],[-9223372036854775809],[18446744073709551615],[18446744073709551616],[9007199254740993],[1.7976931348623157e308],[4.9e-324],[1e-400],[2.2250738585072011e-308],[0.30000000000000004],[-1.5e+2]]}]}'),
+    ("strings", b'{"dim":1,"meta":{"k\\u00e9y":"v\\n\\t\\"q\\"","emoji":"\\ud83d\\ude00","raw":"\xc3\xa9\xe2\x82\xac"},"series":[{"label":"\\u0041\\/b","points":[[1]]}]}'),
+    ("dup_keys", b'{"dim":3,"dim":1,"series":[{"points":[[1]]}],"meta":{"a":"1","a":"2"}}'),
+    ("extra_keys", b'{"dim":1,"x":[1,{"y":null}],"series":[{"points":[[1]],"other":true}]}'),
+    ("empty", b''),
+    ("not_object", b'[1,2]'),
+    ("missing_series", b'{"dim":1}'),
+    ("missing_dim", b'{"series":[{"points":[[1]]}]}'),
+    ("dim_zero", b'{"dim":0,"series":[{"points":[[1]]}]}'),
+    ("dim_negative", b'{"dim":-1,"series":[{"points":[[1]]}]}'),
+    ("dim_float", b'{"dim":1.0,"series":[{"points":[[1]]}]}'),
+    ("dim_string", b'{"dim":"1","series":[{"points":[[1]]}]}'),
+    ("meta_not_object", b'{"dim":1,"meta":[],"series":[{"points":[[1]]}]}'),
+    ("meta_value", b'{"dim":1,"meta":{"a":"x","b":2},"series":[{"points":[[1]]}]}'),
+    ("series_empty", b'{"dim":1,"series":[]}'),
+    ("series_not_array", b'{"dim":1,"series":{"points":[[1]]}}'),
+    ("series_item", b'{"dim":1,"series":[{"points":[[1]]},[1]]}'),
+    ("series_no_points", b'{"dim":1,"series":[{"label":"a"}]}'),
+    ("label_type", b'{"dim":1,"series":[{"label":1,"points":[[1]]}]}'),
+    ("points_empty", b'{"dim":1,"series":[{"points":[]}]}'),
+    ("points_type", b'{"dim":1,"series":[{"points":5}]}'),
+    ("point_type", b'{"dim":1,"series":[{"points":[[1],2]}]}'),
+    ("point_size", b'{"dim":2,"series":[{"points":[[1,2],[3]]}]}'),
+    ("component_string", b'{"dim":2,"series":[{"points":[[1,"2"]]}]}'),
+    ("component_null", b'{"dim":1,"series":[{"points":[[null]]}]}'),
+    ("component_bool", b'{"dim":1,"series":[{"points":[[true]]}]}'),
+    ("nonfinite", b'{"dim":2,"series":[{"points":[[1,2]]},{"points":[[1,2],[3,-1e999]]}]}'),
+    ("labels_mixed", b'{"dim":1,"series":[{"label":"a","points":[[1]]},{"points":[[2]]}]}'),
+    ("labels_mixed2", b'{"dim":1,"series":[{"points":[[1]]},{"label":"b","points":[[2]]}]}'),
+    ("size_before_label_mix", b'{"dim":1,"series":[{"label":"a","points":[[1]]},{"points":[[2,3]]}]}'),
+    ("trailing_comma", b'{"dim":1,"series":[{"points":[[1],]}]}'),
+    ("trailing_garbage", b'{"dim":1,"series":[{"points":[[1]]}]} x'),
+    ("two_docs", b'{"dim":1,"series":[{"points":[[1]]}]}{}'),
+    ("leading_zero", b'{"dim":1,"series":[{"points":[[01]]}]}'),
+    ("plus", b'{"dim":1,"series":[{"points":[[+1]]}]}'),
+    ("dot", b'{"dim":1,"series":[{"points":[[.5]]}]}'),
+    ("nan", b'{"dim":1,"series":[{"points":[[NaN]]}]}'),
+    ("infinity", b'{"dim":1,"series":[{"points":[[Infinity]]}]}'),
+    ("frac_missing", b'{"dim":1,"series":[{"points":[[1.]]}]}'),
+    ("exp_missing", b'{"dim":1,"series":[{"points":[[1e]]}]}'),
+    ("single_quote", b"{'dim':1}"),
+    ("control_char", b'{"dim":1,"series":[{"label":"a\tb","points":[[1]]}]}'),
+    ("bad_escape", b'{"dim":1,"series":[{"label":"a\\x","points":[[1]]}]}'),
+    ("lone_surrogate", b'{"dim":1,"series":[{"label":"\\udc00","points":[[1]]}]}'),
+    ("high_surrogate_alone", b'{"dim":1,"series":[{"label":"\\ud800x","points":[[1]]}]}'),
+    ("bad_utf8", b'{"dim":1,"series":[{"label":"\xff","points":[[1]]}]}'),
+    ("overlong_utf8", b'{"dim":1,"series":[{"label":"\xc0\xaf","points":[[1]]}]}'),
+    ("unterminated", b'{"dim":1,"series":[{"points":[[1]]}]'),
+    ("bad_literal", b'{"dim":1,"series":[{"points":[[1]]}],"x":tru}'),
+]
+
+
+def main_io():
+    """Dataset-file fixtures: every IO_DOCS document through the reference's
+    own load_dataset (oracle/_ref/libtswarp_ref_io.so, nlohmann/json 3.11.3), recording the
+    exception kind + message (with the file path replaced by {path}) or the loaded dataset."""
+    import base64
+    import tempfile
+
+    RIO = oracle.ref_io()
+    out = []
+    with tempfile.TemporaryDirectory() as td:
+        path = os.path.join(td, "doc.json")
+        for name, doc in IO_DOCS:
+            with open(path, "wb") as f:
+                f.write(doc)
+            ent = {"name": name, "doc_b64": base64.b64encode(doc).decode()}
+            try:
+                vals, lens, d, labels, meta = RIO.load(path)
+                ent["ok"] = {"d": d, "values": hx(vals), "lengths": [int(x) for x in lens],
+                             "labels": labels, "meta": meta}
+            except oracle.RefIOError as e:
+                ent["error"] = {"kind": e.kind, "message": e.message.replace(path, "{path}")}
+            out.append(ent)
+    res = {"generator": "tests/golden/make_golden.py (main_io)",
+           "reference": "oracle/_ref/libtswarp_ref_io.so (dataset_io.cpp + nlohmann/json 3.11.3)",
+           "cases": out}
+    p = os.path.join(HERE, "dataset_io_vectors.json")
+    with open(p, "w") as f:
+        json.dump(res, f, indent=0)
+    print(f"wrote {p} ({len(out)} cases)")
+
+
 if __name__ == "__main__":
     if "--sub" in sys.argv:
         main_sub()
+    elif "--io" in sys.argv:
+        main_io()
     else:
         main()
         main_sub()
+        main_io()
