@@ -13,3 +13,9 @@ $C5K > gpurun_out/prof_plain4.log 2>&1 && \
 C5T="python bench.py --config 5 --metric dtw --steps 1 --warmup 3 --no-cpu-baseline"
 $C5T > gpurun_out/prof_plain5.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:lb12_compact_kernel -s 0 -c 1 -f -o gpurun_out/prof_lb12_c5 $C5T > gpurun_out/prof_f4.log 2>&1; echo "lb12 full $?"
+C4T="python bench.py --config 4 --metric dtw --steps 1 --warmup 3 --no-cpu-baseline"
+$C4T > gpurun_out/prof_plain6.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:dtwt_kernel -s 1 -c 1 -f -o gpurun_out/prof_dtwt_c4 $C4T > gpurun_out/prof_f5.log 2>&1; echo "dtwt full $?"
+C3S="python bench.py --config 3 --metric dk_sub --steps 1 --warmup 3 --no-cpu-baseline"
+$C3S > gpurun_out/prof_plain7.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:dk_dp_kernel -s 1 -c 1 -f -o gpurun_out/prof_dk_sub_c3 $C3S > gpurun_out/prof_f6.log 2>&1; echo "dk sub full $?"

@@ -64,7 +64,7 @@ def _worker(rank, world, port, X, Q, k, metric, r, out):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("metric,k", [("dtw", 1), ("dtw", 5), ("dk", 3)])
+@pytest.mark.parametrize("metric,k", [("dtw", 1), ("dtw", 5), ("dk", 3), ("dk_sub", 4)])
 def test_sharded_knn_gloo_world2(metric, k):
     import oracle
 
