@@ -8,13 +8,14 @@ C++ drop-in header (include/tswarp_b200.hpp) and this Python mirror (tswarp.py).
 from .tswarp import (  # noqa: F401
     Dataset, IoError, Neighbor, ParseError, Plan, SearchCounters, SearchReport, Store, SubMatch,
     TswError, ValidationError, device_count, dist_all, envelope, epsnn_dk, fp64_peak, knn, knn_dk,
-    load_dataset, save_dataset,
+    load_dataset, loo_accuracy, pruning_power, save_dataset, speedup,
     knn_dk_sub, knn_dtw, l2_flush, last_transfer_bytes, lb_box_all, lib, sparse_dk_sub,
     sub_dk_all, sub_search_dk, synth, synth_shape,
 )
 
 __all__ = [
-    "Dataset", "IoError", "Neighbor", "ParseError", "Plan", "load_dataset", "save_dataset", "SearchCounters", "SearchReport", "Store", "SubMatch",
+    "Dataset", "IoError", "Neighbor", "ParseError", "Plan", "load_dataset", "save_dataset",
+    "loo_accuracy", "pruning_power", "speedup", "SearchCounters", "SearchReport", "Store", "SubMatch",
     "TswError", "ValidationError", "device_count", "dist_all", "envelope", "epsnn_dk",
     "fp64_peak", "knn", "knn_dk", "knn_dk_sub", "knn_dtw", "l2_flush", "last_transfer_bytes",
     "lb_box_all", "lib", "sparse_dk_sub", "sub_dk_all", "sub_search_dk", "synth", "synth_shape",

@@ -3,6 +3,7 @@
 // and search.cpp:99-115,127,172,217 (std::invalid_argument).
 #include "tswarp_b200.hpp"
 
+#include <algorithm>
 #include <chrono>
 #include <memory>
 #include <mutex>
@@ -221,6 +222,73 @@ SearchReport epsnn_dk(const TimeSeries& query, const Dataset& data, double eps, 
     rep.counters = {c.lb_computed, c.lb_pruned, c.full_dp, c.early_abandoned, c.gdk_calls};
     rep.wall_time_seconds = std::chrono::duration<double>(Clock::now() - start).count();
     return rep;
+}
+
+namespace {
+
+// knn over queries of any lengths: one batched device pass per query length
+std::vector<SearchReport> knn_any(const std::vector<TimeSeries>& queries, const Dataset& data,
+                                  std::size_t k, int metric, std::size_t r, const char* op) {
+    std::map<std::size_t, std::vector<std::size_t>> by_len;
+    for (std::size_t i = 0; i < queries.size(); ++i) by_len[queries[i].length()].push_back(i);
+    std::vector<SearchReport> out(queries.size());
+    for (const auto& [len, ids] : by_len) {
+        std::vector<TimeSeries> group;
+        group.reserve(ids.size());
+        for (std::size_t i : ids) group.push_back(queries[i]);
+        auto reps = run_knn(group, data, k, metric, r, op);
+        for (std::size_t j = 0; j < ids.size(); ++j) out[ids[j]] = std::move(reps[j]);
+    }
+    return out;
+}
+
+}  // namespace
+
+double pruning_power(const Dataset& queries, const Dataset& data, BandRadius r) {
+    const auto reps = knn_any(queries.series(), data, 1, TSW_METRIC_DTW, r.value, "knn_dtw");
+    double pruned = 0.0, computed = 0.0;
+    for (const auto& rep : reps) {
+        pruned += static_cast<double>(rep.counters.lb_pruned);
+        computed += static_cast<double>(rep.counters.lb_computed);
+    }
+    return computed > 0.0 ? pruned / computed : 0.0;
+}
+
+double loo_accuracy(const Dataset& data, MetricKind metric, BandRadius r) {
+    if (!data.labeled()) throw std::invalid_argument("loo_accuracy: the dataset has no labels");
+    if (data.size() < 2) throw std::invalid_argument("loo_accuracy: needs at least two series");
+    // 2-NN of every series against the whole dataset: the first neighbour that is not the
+    // series itself is its leave-one-out 1-NN under the (distance, index) rule
+    const int m = metric == MetricKind::Dtw ? TSW_METRIC_DTW : TSW_METRIC_DK;
+    const auto reps = knn_any(data.series(), data, 2, m, r.value,
+                              metric == MetricKind::Dtw ? "knn_dtw" : "knn_dk");
+    std::size_t correct = 0;
+    for (std::size_t i = 0; i < data.size(); ++i) {
+        for (const auto& nb : reps[i].neighbors) {
+            if (nb.index == i) continue;
+            if (*data[nb.index].label() == *data[i].label()) ++correct;
+            break;
+        }
+    }
+    return static_cast<double>(correct) / static_cast<double>(data.size());
+}
+
+double speedup(const Dataset& queries, const Dataset& data, BandRadius r, int repetitions, int) {
+    if (repetitions < 1) throw std::invalid_argument("speedup: repetitions must be positive");
+    auto timed = [&](int metric) {
+        (void)knn_any(queries.series(), data, 1, metric, r.value, "knn");  // warm-up
+        std::vector<double> ts;
+        for (int i = 0; i < repetitions; ++i) {
+            const auto t0 = Clock::now();
+            (void)knn_any(queries.series(), data, 1, metric, r.value, "knn");
+            ts.push_back(std::chrono::duration<double>(Clock::now() - t0).count());
+        }
+        std::sort(ts.begin(), ts.end());
+        return ts[ts.size() / 2];
+    };
+    const double t_dtw = timed(TSW_METRIC_DTW);
+    const double t_dk = timed(TSW_METRIC_DK);
+    return t_dk > 0.0 ? t_dtw / t_dk : 0.0;
 }
 
 Dataset load_dataset(const std::string& path) {

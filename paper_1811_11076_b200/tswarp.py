@@ -354,6 +354,59 @@ def save_dataset(ds: Dataset, path) -> None:
                                        len(keys)))
 
 
+# ---- experiment drivers (metrics.hpp:56-72) ---------------------------------------------
+def _by_length(data: Dataset):
+    groups: dict[int, list[int]] = {}
+    for i in range(data.n):
+        groups.setdefault(data.length(i), []).append(i)
+    return groups
+
+
+def pruning_power(queries: Dataset, data, r: int) -> float:
+    """Fraction of candidate DTW computations skipped by LB_Box over 1-NN DTW scans of every
+    query: sum(lb_pruned) / sum(lb_computed) (this engine's threshold schedule)."""
+    pruned = computed = 0
+    for L, ids in _by_length(queries).items():
+        qs = np.stack([queries.series(i) for i in ids])
+        _, _, c = knn(data, qs, 1, "dtw", r)
+        pruned += int(c[:, 1].sum())
+        computed += int(c[:, 0].sum())
+    return pruned / computed if computed else 0.0
+
+
+def loo_accuracy(data: Dataset, metric: str = "dtw", r: int = 0) -> float:
+    """Leave-one-out 1-NN accuracy (ties to the lowest index); labels required."""
+    if data.labels is None:
+        raise ValueError("loo_accuracy: the dataset has no labels")
+    if data.n < 2:
+        raise ValueError("loo_accuracy: needs at least two series")
+    correct = 0
+    for L, ids in _by_length(data).items():
+        qs = np.stack([data.series(i) for i in ids])
+        idx, _, _ = knn(data, qs, 2, metric, r)
+        for row, i in enumerate(ids):
+            j = next(int(x) for x in idx[row] if int(x) != i)
+            correct += data.labels[j] == data.labels[i]
+    return correct / data.n
+
+
+def speedup(queries: Dataset, data, r: int, repetitions: int = 3) -> float:
+    """Median wall time of the DTW + LB_Box 1-NN scan over that of the dog-keeper scan."""
+    def timed(metric):
+        def run():
+            for L, ids in _by_length(queries).items():
+                knn(data, np.stack([queries.series(i) for i in ids]), 1, metric, r)
+        run()
+        ts = []
+        for _ in range(repetitions):
+            t0 = time.perf_counter()
+            run()
+            ts.append(time.perf_counter() - t0)
+        return sorted(ts)[len(ts) // 2]
+    t_dtw, t_dk = timed("dtw"), timed("dk")
+    return t_dtw / t_dk if t_dk > 0 else 0.0
+
+
 def _as_store(data) -> Store:
     return data.store if isinstance(data, Dataset) else data
 
