@@ -887,42 +887,47 @@ int tsw_plan_set_queries_device(tsw_plan* p, const double* q, uint64_t nq, void*
     });
 }
 
+// One pipeline execution, as a CUDA graph launch when the plan has graphs on (after a warm
+// eager run), else eager launches.
+static void execute_graph_or_eager(tsw_plan* p, cudaStream_t st) {
+    if (!p->use_graph || p->timing || std::getenv("TSW_DEBUG_SYNC") || !p->graph_warm) {
+        execute_impl(p, st);  // the first execution also runs the one-time kernel setup
+        p->graph_warm = true;
+        return;
+    }
+    // CUDA graph of the whole (host-sync-free) pipeline, re-captured when the query count
+    // or the stream changes: one launch instead of ~10 per execution
+    if (!p->graph || p->graph_nq != p->nq || p->graph_stream != st) {
+        if (p->graph) {
+            cudaGraphExecDestroy(p->graph);
+            p->graph = nullptr;
+        }
+        cudaGraph_t g = nullptr;
+        ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "graph capture");
+        try {
+            execute_impl(p, st);
+        } catch (...) {
+            cudaStreamEndCapture(st, &g);
+            if (g) cudaGraphDestroy(g);
+            throw;
+        }
+        ck(cudaStreamEndCapture(st, &g), "graph capture");
+        ck(cudaGraphInstantiate(&p->graph, g, 0), "graph instantiate");
+        cudaGraphDestroy(g);
+        p->graph_nq = p->nq;
+        p->graph_stream = st;
+        p->graph_launches = p->launches;
+    }
+    ck(cudaGraphLaunch(p->graph, st), "graph launch");
+    p->launches = p->graph_launches;
+    p->executed = true;
+}
+
 int tsw_plan_execute(tsw_plan* p, void* stream) {
     return guard([&] {
         if (!p) fail(TSW_EINVAL, "null plan");
         DeviceGuard dg(p->store->device);
-        cudaStream_t st = pick(p, stream);
-        if (!p->use_graph || p->timing || std::getenv("TSW_DEBUG_SYNC") || !p->graph_warm) {
-            execute_impl(p, st);  // the first execution also runs the one-time kernel setup
-            p->graph_warm = true;
-            return;
-        }
-        // CUDA graph of the whole (host-sync-free) pipeline, re-captured when the query count
-        // or the stream changes: one launch instead of ~10 per execution
-        if (!p->graph || p->graph_nq != p->nq || p->graph_stream != st) {
-            if (p->graph) {
-                cudaGraphExecDestroy(p->graph);
-                p->graph = nullptr;
-            }
-            cudaGraph_t g = nullptr;
-            ck(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "graph capture");
-            try {
-                execute_impl(p, st);
-            } catch (...) {
-                cudaStreamEndCapture(st, &g);
-                if (g) cudaGraphDestroy(g);
-                throw;
-            }
-            ck(cudaStreamEndCapture(st, &g), "graph capture");
-            ck(cudaGraphInstantiate(&p->graph, g, 0), "graph instantiate");
-            cudaGraphDestroy(g);
-            p->graph_nq = p->nq;
-            p->graph_stream = st;
-            p->graph_launches = p->launches;
-        }
-        ck(cudaGraphLaunch(p->graph, st), "graph launch");
-        p->launches = p->graph_launches;
-        p->executed = true;
+        execute_graph_or_eager(p, pick(p, stream));
     });
 }
 
@@ -996,12 +1001,13 @@ int tsw_knn(tsw_store* s, const double* queries, uint64_t nq, uint64_t qlen, int
         std::lock_guard<std::mutex> lk(s->mu);
         DeviceGuard dg(s->device);
         tsw_plan* p = cached_plan(s, nq, qlen, metric, r, k);
+        p->use_graph = true;  // repeated calls replay the captured pipeline (one launch)
         const uint64_t kk = p->kk;
         uint64_t h2d = 0, d2h = 0;
         for (uint64_t q0 = 0; q0 < nq; q0 += p->nq_max) {
             const uint64_t nb = std::min(p->nq_max, nq - q0);
             set_queries_impl(p, queries + q0 * qlen * s->d, nb, false, p->own);
-            execute_impl(p, p->own);
+            execute_graph_or_eager(p, p->own);
             fetch_impl(p, out ? out + q0 * kk : nullptr, counters ? counters + q0 : nullptr, p->own);
             h2d += g_h2d;
             d2h += g_d2h;
