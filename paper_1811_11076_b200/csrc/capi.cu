@@ -570,7 +570,10 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
         la.pfx_out = p->pfx_qn ? p->pfx.p : nullptr;
         la.pfx_count = p->counters.p + C_PFX;
         la.pfx_cap = p->pfx_cap;
-        if (p->cenv_m) {  // fused reverse bound (queries in fp32 + their max |value| first)
+        // fused reverse bound (queries in fp32 + their max |value| first); 1-3 queries stream
+        // the store with the forward bound only (measured: the reverse pass costs more than
+        // the DP pairs it removes there)
+        if (p->cenv_m && nq >= 4) {
             launch_to_float(p->qg(), (uint64_t)nq * p->qstride, p->q32.p, st);
             launch_absmax(p->qg(), (uint64_t)nq * p->qstride, p->qabsmax.p, st);
             la.cenv_m = p->cenv_m;

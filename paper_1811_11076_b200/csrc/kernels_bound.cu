@@ -492,6 +492,89 @@ __device__ __forceinline__ TileOut lb1_tile(const LbCompactArgs& a, uint32_t c0,
     return t;
 }
 
+// ---- K2 for 1-3 queries (the reference's single-query call shape) -----------------------------
+// The tile kernel amortises one candidate read over 8 query rows; with fewer queries it would
+// compute duplicated rows.  Here a warp takes one candidate at a time and streams it once for
+// all NQ queries: lane l owns the same point quads as in the tile kernel (block mode: points
+// [l*B, (l+1)*B), so its partial sums are the pair's LB block sums), a warp reduction (RD
+// adds) gives the bound, lane 0 decides, and the lanes write the block-sum row of a survivor.
+// Few registers, high occupancy: the pass streams the fp32 store at HBM rate.
+template <int NQ>
+__global__ void __launch_bounds__(256, 3) lb_few_kernel(LbCompactArgs a) {
+    const unsigned lane = lane_id();
+    const uint32_t n = a.store.n, d = a.store.d;
+    const uint32_t total4 = (uint32_t)(a.store.tstride / 4);
+    const uint64_t w0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    __shared__ QEntry stage_buf[8][2][kStage];
+    Stage sg{stage_buf[threadIdx.x >> 5][0], stage_buf[threadIdx.x >> 5][1], 0u, 0u};
+    const float4* lob = reinterpret_cast<const float4*>(a.env_lo);
+    const float4* hib = reinterpret_cast<const float4*>(a.env_hi);
+    const uint64_t qs = a.qstride / 4;
+    double T[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) T[q] = a.state ? a.state[q].T : kInf;
+    for (uint64_t c = w0; c < n; c += nw) {
+        const float4* xb = reinterpret_cast<const float4*>(a.store.data32) + c * (a.store.ustride / 4);
+        float acc[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) acc[q] = 0.0f;
+        auto body = [&](uint32_t f) {
+            const float4 x = __ldg(xb + f);
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                const float4 l = __ldg(lob + q * qs + f);
+                const float4 h = __ldg(hib + q * qs + f);
+                float sacc = acc[q];
+                sacc = lb_term_rd(sacc, x.x, l.x, h.x);
+                sacc = lb_term_rd(sacc, x.y, l.y, h.y);
+                sacc = lb_term_rd(sacc, x.z, l.z, h.z);
+                sacc = lb_term_rd(sacc, x.w, l.w, h.w);
+                acc[q] = sacc;
+            }
+        };
+        if (a.pfx_qn) {
+            const uint32_t nquad = total4 / d;
+            for (uint32_t j = 0; j < a.pfx_qn; ++j) {
+                const uint32_t g = lane * a.pfx_qn + j;
+                if (g < nquad)
+                    for (uint32_t k = 0; k < d; ++k) body((g >> 3) * 8 * d + 8 * k + (g & 7));
+            }
+        } else {
+            for (uint32_t f = lane; f < total4; f += 32) body(f);
+        }
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            if (q >= (int)a.nq) break;
+            float lb = acc[q];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) lb = __fadd_rd(lb, __shfl_xor_sync(0xffffffffu, lb, o));
+            bool take = false, near = false;
+            if (a.lb_out && lane == 0) a.lb_out[(uint64_t)q * n + c] = lb;
+            if (a.state) {
+                const bool probed = a.probed && a.probed[c * a.nq + q];
+                take = !probed && (double)lb <= __dmul_ru(T[q], a.margin);
+                near = (double)lb <= a.near_frac * T[q];
+            }
+            uint32_t ps = kNoPfx;
+            if (take && a.pfx_out) {  // warp-uniform: every lane holds the same decision
+                unsigned base = 0;
+                if (lane == 0) base = atomicAdd(a.pfx_count, 1u);
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (base < a.pfx_cap) {
+                    ps = base;
+                    a.pfx_out[(uint64_t)base * kPfxBlocks + lane] = acc[q];
+                }
+            }
+            if (a.state) enqueue(sg, a.queue, take && lane == 0, near, (uint32_t)q, (uint32_t)c, lb, ps);
+        }
+    }
+    if (a.state) {
+        stage_flush(sg, a.queue, true);
+        stage_flush(sg, a.queue, false);
+    }
+}
+
 template <int QB, int CB>
 __global__ void __launch_bounds__(256, 2) lb_compact_kernel(LbCompactArgs a) {
     const uint32_t n = a.store.n;
@@ -656,6 +739,14 @@ void launch_lb_compact(const LbCompactArgs& a, cudaStream_t st) {
         const size_t smem12 = (size_t)8 * kList * (sizeof(QEntry) + sizeof(float)) + smem;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem12);
         kern<<<sm_count() * 2, 256, smem12, st>>>(a);
+        return;
+    }
+    if (a.nq <= 3) {  // the reference's call shape: stream the store once, no duplicated rows
+        const int blocks = (int)std::min<uint64_t>(((uint64_t)a.store.n * 32 + 255) / 256,
+                                                   (uint64_t)sm_count() * 8);
+        if (a.nq == 1) lb_few_kernel<1><<<std::max(blocks, 1), 256, 0, st>>>(a);
+        else if (a.nq == 2) lb_few_kernel<2><<<std::max(blocks, 1), 256, 0, st>>>(a);
+        else lb_few_kernel<3><<<std::max(blocks, 1), 256, 0, st>>>(a);
         return;
     }
     const uint64_t tiles = (uint64_t)((a.store.n + CB - 1) / CB) * ((a.nq + QB - 1) / QB);
