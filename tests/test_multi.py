@@ -83,3 +83,48 @@ def test_sharded_knn_gloo_world2(metric, k):
         gi, gd = out[rank]
         for q in range(len(Q)):
             assert gi[q] == ref[q][0].tolist() and gd[q] == ref[q][1].tolist(), (rank, q)
+
+
+def _gpu_worker(rank, world, port, X, Q, k, metric, r, out):
+    import torch.distributed as dist
+
+    import paper_1811_11076_b200 as tsw
+    from paper_1811_11076_b200.dist import shard_range, sharded_knn
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    lo, hi = shard_range(X.shape[0], world, rank)
+    # each rank's shard in its own device store; the ranks' kernels never wait on each other
+    # (the only exchange is the host-side all-gather of the local top-k lists)
+    shard = tsw.Dataset(X[lo:hi]) if hi > lo else None
+
+    def local(queries, kq):
+        i, d, _ = tsw.knn(shard, queries, kq, metric, r)
+        return i, d
+
+    gi, gd = sharded_knn(local, Q, k, X.shape[0])
+    out[rank] = (gi.tolist(), gd.tolist())
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("metric,k", [("dtw", 3), ("dk", 2), ("dk_sub", 2)])
+def test_sharded_knn_gpu_shards(metric, k):
+    """The sharded path with the GPU pipeline as the per-shard search (two shard stores on
+    cuda:0, gloo for the exchange): equals the oracle on the whole dataset."""
+    import oracle
+
+    rng = np.random.default_rng(13)
+    X = rng.standard_normal((301, 40, 3)).cumsum(1)
+    X[250] = X[10]  # cross-shard duplicate: the tie goes to index 10
+    Q = np.stack([X[10] + 0.001, rng.standard_normal((40, 3)).cumsum(0)])
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_gpu_worker, args=(2, _free_port(), X, Q, k, metric, 4, out), nprocs=2, join=True)
+    P = oracle.port()
+    for rank in range(2):
+        gi, gd = out[rank]
+        for q in range(len(Q)):
+            oi, od, _ = P.knn(Q[q], oracle.Dataset(X), k, metric, 4)
+            assert gi[q] == oi.tolist() and gd[q] == od.tolist(), (rank, q)
