@@ -110,11 +110,13 @@ __device__ __forceinline__ void dk_step(const Strip& S, int k, int lane, int n,
                                         bool& live, const Pt<D>& tv, Pt<D>& tn, SubFold& sf) {
     const int stride = D > 0 ? D : (int)d;
     const int j = S.cstart + k - lane;
-    const bool colok = (unsigned)(k - lane) <= (unsigned)(n - 1 - S.cstart);
     double up = __shfl_up_sync(kFull, mine, 1);  // lane l-1's last row at column j
     double dg = up_prev;                          // ... at column j-1 (previous step)
-    const double b = bnd[j];  // boundary row (row R-1), padded by 64 each side; lane 0 uses it
-    if (lane == 0) up = (!S.first && j <= S.b_hi) ? b : kInf;
+    // boundary row (row R-1, padded by 64 each side); filled so that lane 0 can take it as is:
+    // +inf right of the live range, and 0 on the first strip in subsequence mode (the virtual
+    // 0-predecessor of every row-0 cell)
+    const double b = bnd[j];
+    if (lane == 0) up = b;
     up_prev = up;
     load_pt<D>(tn, t, j + 1, stride);
     const double* tp = t + toff_rt(j, stride);  // runtime-d path
@@ -122,14 +124,15 @@ __device__ __forceinline__ void dk_step(const Strip& S, int k, int lane, int n,
     double vlast = kInf;
 #pragma unroll
     for (int q = 0; q < RPL; ++q) {
-        const bool active = colok && RPL * lane + q < S.nrows;
+        // No masks (compile-time d): a lane's cells left of the segment start see only +inf
+        // predecessors, columns past n - 1 read the store's -inf guard points and rows past
+        // m - 1 hold +inf query points, so all of them come out +inf.
         const double c = D > 0 ? cost<D>(sp[q], tv) : cost_rt(srow[q], tp, d);
-        double pred = dmin(dmin(left[q], up), dg);
-        // virtual start: (0, 0) for a whole match, (0, j) for every j in subsequence mode
-        if (q == 0 && S.first && lane == 0 && (SUB || j == 0)) pred = 0.0;
-        const double v = active ? dmax(c, pred) : kInf;
+        const double pred = dmin(dmin(left[q], up), dg);
+        double v = dmax(c, pred);
+        if (D == 0) v = RPL * lane + q < S.nrows ? v : kInf;  // runtime d: clamped rows
         dg = left[q];           // next row's diagonal: this row at column j-1
-        left[q] = active ? v : left[q];
+        left[q] = v;
         up = v;                 // next row's up: this row at column j
         if (LIVE) lv |= v <= Tsq;
         if (SUB) vlast = q == sf.fq ? v : vlast;
@@ -143,8 +146,10 @@ __device__ __forceinline__ void dk_step(const Strip& S, int k, int lane, int n,
             sf.bcol = j;
         }
     }
-    mine = up;  // last row of this lane (inf when inactive)
-    if (S.write_bnd && lane == 31 && colok) bnd[j] = mine;  // in place: lane 0 is >= 30 columns ahead
+    mine = up;  // last row of this lane
+    // in place (lane 0 is >= 31 columns ahead); columns left of the segment start get +inf,
+    // which they are (> T) for the next strip; columns past n - 1 never reach lane 31
+    if (S.write_bnd && lane == 31) bnd[j] = mine;
     if (LIVE) live = lv;
 }
 
@@ -203,10 +208,16 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
 #pragma unroll
             for (int q = 0; q < RPL; ++q) {
                 srow[q] = s + tidx((uint32_t)min(R + RPL * lane + q, m - 1), 0, (uint32_t)stride);
-                if (D > 0) {
+                if (D > 0) {  // rows past m - 1: +inf points (their cells come out +inf)
+                    const bool rok = R + RPL * lane + q < m;
 #pragma unroll
-                    for (int kk = 0; kk < (D > 0 ? D : 1); ++kk) sp[q].x[kk] = __ldg(srow[q] + kk * kTile);
+                    for (int kk = 0; kk < (D > 0 ? D : 1); ++kk)
+                        sp[q].x[kk] = rok ? __ldg(srow[q] + kk * kTile) : kInf;
                 }
+            }
+            if (S.first) {  // lane 0's row above row 0: 0 (subsequence) or +inf everywhere
+                for (int j = lane; j < n + 32; j += 32) bnd[j] = SUB ? 0.0 : kInf;
+                __syncwarp();
             }
             double left[RPL];
             double mine, up_prev;
@@ -214,7 +225,9 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
             const int strip_lo = S.cstart;
             bool reached_end = false;
             int k_last = -1;
-            double dg0 = kInf;  // lane 0's diagonal predecessor at a segment start (boundary row)
+            // lane 0's diagonal predecessor at a segment start (boundary row); the virtual start
+            // of a whole match is a 0-predecessor of cell (0, 0)
+            double dg0 = (S.first && !SUB) ? 0.0 : kInf;
             // Segments: the sweep stops at a dead cut (two skewed steps without a live cell); if
             // a live boundary cell lies ahead (the previous strip's boundary row, or in
             // subsequence mode a row-0 column with c(0, j) <= T: every column may start a match)
@@ -224,13 +237,18 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
 #pragma unroll
                 for (int q = 0; q < RPL; ++q) left[q] = kInf;
                 mine = kInf;
-                up_prev = dg0;
+                up_prev = lane == 0 ? dg0 : kInf;
                 const int kmax = (n - 1 - S.cstart) + last_lane;
                 bool l2 = false, l3 = false, dummy = false, cut = false;
                 int k_done = -1;
                 Pt<D> ta, tb;  // candidate points of the current / next column (ping-pong)
                 load_pt<D>(ta, t, S.cstart - lane, stride);
-                for (int k = 0; k <= kmax; k += 4) {
+                // Whole groups of 4 steps, then 0-3 single steps up to kmax exactly: lane
+                // last_lane (the lane holding the strip's last row) never passes column n - 1, so
+                // its `left` ends on the final cell, and lanes never read past column n + 31
+                // (inside the store's guard points).
+                int k = 0;
+                for (; k + 3 <= kmax; k += 4) {
                     dk_step<D, RPL, false, SUB>(S, k, lane, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, dummy, ta, tb, sf);
                     dk_step<D, RPL, false, SUB>(S, k + 1, lane, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, dummy, tb, ta, sf);
                     dk_step<D, RPL, true, SUB>(S, k + 2, lane, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, l2, ta, tb, sf);
@@ -241,6 +259,15 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
                         break;
                     }
                     if (st && (k & 60) == 60) Tsq = ld_volatile(&st->Tsq);
+                }
+                if (!cut && k <= kmax) {
+                    dk_step<D, RPL, false, SUB>(S, k, lane, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, dummy, ta, tb, sf);
+                    if (k + 1 <= kmax) {
+                        dk_step<D, RPL, false, SUB>(S, k + 1, lane, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, dummy, tb, ta, sf);
+                        if (k + 2 <= kmax)
+                            dk_step<D, RPL, false, SUB>(S, k + 2, lane, n, sp, srow, t, d, bnd, Tsq, left, mine, up_prev, dummy, ta, tb, sf);
+                    }
+                    k_done = kmax;
                 }
                 k_last = min(k_done, kmax);  // last step whose cells were computed
                 {   // cells computed by this lane in this segment (analytic count)
@@ -310,6 +337,8 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
                         last = j0 + 31 - __clz(bm);
                     }
                 }
+                if (first >= 0)  // lane 0 of the next strip reads the row as is: +inf past hi
+                    for (int j = hi + 1 + lane; j < n + 32; j += 32) bnd[j] = kInf;
                 __syncwarp();
                 if (first < 0) {
                     dead = true;
