@@ -67,6 +67,22 @@ __device__ __forceinline__ Pt<D> sp0_of(const double* __restrict__ s, int stride
     return p;
 }
 
+// first set bit at column >= from of a per-warp liveness bitmap of W words (-1: none)
+__device__ __forceinline__ int next_live(const unsigned* __restrict__ mk, int W, int from, int lane) {
+    for (int w0 = from >> 5; w0 < W; w0 += 32) {
+        const int w = w0 + lane;
+        unsigned bits = w < W ? mk[w] : 0u;
+        if (w == (from >> 5)) bits &= ~0u << (from & 31);
+        const unsigned bm = __ballot_sync(kFull, bits != 0u);
+        if (bm) {
+            const int src = __ffs(bm) - 1;
+            const unsigned b = __shfl_sync(kFull, bits, src);
+            return (w0 + src) * 32 + __ffs(b) - 1;
+        }
+    }
+    return -1;
+}
+
 struct Strip {
     int R, cstart, b_hi, b_alive_hi;
     int nrows;  // rows of this strip (<= kStrip)
@@ -113,10 +129,10 @@ __device__ __forceinline__ void dk_step(const Strip& S, int k, int lane, int n,
     double up = __shfl_up_sync(kFull, mine, 1);  // lane l-1's last row at column j
     double dg = up_prev;                          // ... at column j-1 (previous step)
     // boundary row (row R-1, padded by 64 each side); filled so that lane 0 can take it as is:
-    // +inf right of the live range, and 0 on the first strip in subsequence mode (the virtual
-    // 0-predecessor of every row-0 cell)
+    // +inf right of the live range, and +inf on the first strip of a whole match.  In
+    // subsequence mode row 0 has the virtual 0-predecessor in every column.
     const double b = bnd[j];
-    if (lane == 0) up = b;
+    if (lane == 0) up = (SUB && S.first) ? 0.0 : b;
     up_prev = up;
     load_pt<D>(tn, t, j + 1, stride);
     const double* tp = t + toff_rt(j, stride);  // runtime-d path
@@ -160,15 +176,31 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
     const int lane = threadIdx.x & 31;
     // boundary row of the warp, padded by 64 columns on both sides (out-of-range reads)
     double* bnd = smem + (size_t)(threadIdx.x >> 5) * (max_len + 128) + 64;
+    // subsequence mode: row-0 liveness bits (c(0, j) <= Tsq), one word per 32 columns
+    const int wmax = (int)(max_len + 31) / 32;
+    unsigned* r0m = reinterpret_cast<unsigned*>(smem + (size_t)(blockDim.x >> 5) * (max_len + 128)) +
+                    (size_t)(threadIdx.x >> 5) * wmax;
     const uint32_t d = a.store.d;
     const int m = (int)a.qlen;
     const int stride = D > 0 ? D : (int)d;
     unsigned long long cells = 0;
     const unsigned nf = *a.queue.front, nbk = *a.queue.back;
+    // subsequence mode: queue claims of bsz slots per atomic when the queue is deep (every
+    // (query, series) pair is queued, most die within a few columns, and one same-address atomic
+    // per pair was a bottleneck); whole matches claim single slots (the batch state costs the
+    // long DP sweeps 12 registers)
+    const unsigned total = nf + nbk;
+    const unsigned nwarps = gridDim.x * (blockDim.x >> 5);
+    const unsigned bsz = SUB ? max(1u, min(8u, total / (nwarps * 16u))) : 1u;
+    unsigned cur = 0, cend = 0;  // claimed slots [cur, cend)
     for (;;) {
-        unsigned slot = 0;
-        if (lane == 0) slot = atomicAdd(a.queue.head, 1u);
-        slot = __shfl_sync(kFull, slot, 0);
+        if (cur == cend) {
+            unsigned base = 0;
+            if (lane == 0) base = atomicAdd(a.queue.head, bsz);
+            cur = __shfl_sync(kFull, base, 0);
+            cend = cur >= total ? cur + 1 : min(cur + bsz, total);  // past the end: one failing get
+        }
+        const unsigned slot = cur++;
         QEntry pr;
         if (!queue_get(a.queue, nf, nbk, slot, pr)) break;
         QState* st = a.state ? a.state + pr.q : nullptr;
@@ -187,9 +219,34 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
 
         Strip S;
         S.b_hi = -1;
-        S.b_alive_hi = 0;  // virtual start at (0, 0) (subsequence mode: row-0 columns, scanned)
+        S.b_alive_hi = 0;  // virtual start at (0, 0) (subsequence mode: live row-0 columns)
         int b_alive_lo = 0;
         bool dead = false;
+        if constexpr (SUB && D > 0) {
+            // every row-0 cell may start a match; its value is c(0, j).  Liveness bits for the
+            // whole row, all loads in flight together (Tsq only decreases: stale bits are a
+            // superset, which is safe).  Columns past n - 1 read guard points and are masked.
+            const Pt<D> p0 = sp0_of<D>(s, stride);
+            const int W = (n + 31) >> 5;
+            for (int w0 = 0; w0 < W; w0 += 4) {
+                bool lv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int j = (w0 + u) * 32 + lane;
+                    Pt<D> tj;
+                    load_pt<D>(tj, t, min(j, n + 31), stride);
+                    lv[u] = j < n && cost<D>(p0, tj) <= Tsq;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const unsigned bm = __ballot_sync(kFull, lv[u]);
+                    if (lane == 0 && w0 + u < W) r0m[w0 + u] = bm;
+                }
+            }
+            __syncwarp();
+            b_alive_lo = next_live(r0m, W, 0, lane);
+            dead = b_alive_lo < 0;
+        }
         double fin = kInf;
         SubFold sf;
         sf.fl = ((m - 1) % kStrip) / RPL;
@@ -197,7 +254,7 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
         sf.bsq = kInf;
         sf.bs = kInf;
         sf.bcol = 0;
-        for (int R = 0; R < m; R += kStrip) {
+        for (int R = 0; R < m && !dead; R += kStrip) {
             S.R = R;
             S.nrows = min(kStrip, m - R);
             S.first = R == 0;
@@ -215,8 +272,8 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
                         sp[q].x[kk] = rok ? __ldg(srow[q] + kk * kTile) : kInf;
                 }
             }
-            if (S.first) {  // lane 0's row above row 0: 0 (subsequence) or +inf everywhere
-                for (int j = lane; j < n + 32; j += 32) bnd[j] = SUB ? 0.0 : kInf;
+            if (!SUB && S.first) {  // lane 0's row above row 0
+                for (int j = lane; j < n + 32; j += 32) bnd[j] = kInf;
                 __syncwarp();
             }
             double left[RPL];
@@ -286,28 +343,24 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
                 const bool row0 = SUB && S.first;
                 const int lim = row0 ? n - 1 : min(S.b_hi, S.b_alive_hi);
                 int J = -1;
-                for (int j0 = row0 ? from : from - 1; j0 <= lim; j0 += 32) {
-                    const int j = j0 + lane;
-                    bool lv = false;
-                    if (j <= lim) {
-                        if (row0) {
-                            double c0;
-                            if constexpr (D > 0) {
-                                Pt<D> tj;
-                                load_pt<D>(tj, t, j, stride);
-                                c0 = cost<D>(sp0_of<D>(s, stride), tj);
+                if (row0 && D > 0) {
+                    J = from <= lim ? next_live(r0m, (n + 31) >> 5, from, lane) : -1;
+                } else {
+                    for (int j0 = row0 ? from : from - 1; j0 <= lim; j0 += 32) {
+                        const int j = j0 + lane;
+                        bool lv = false;
+                        if (j <= lim) {
+                            if (row0) {
+                                lv = cost_rt(s, t + toff_rt(j, stride), d) <= Tsq;
                             } else {
-                                c0 = cost_rt(s, t + toff_rt(j, stride), d);
+                                lv = bnd[j] <= Tsq;
                             }
-                            lv = c0 <= Tsq;
-                        } else {
-                            lv = bnd[j] <= Tsq;
                         }
-                    }
-                    const unsigned bm = __ballot_sync(kFull, lv);
-                    if (bm) {
-                        J = j0 + __ffs(bm) - 1;
-                        break;
+                        const unsigned bm = __ballot_sync(kFull, lv);
+                        if (bm) {
+                            J = j0 + __ffs(bm) - 1;
+                            break;
+                        }
                     }
                 }
                 if (J < 0) break;
@@ -397,7 +450,8 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
 template <int D, int RPL>
 void run_dk(const DpArgs& a, uint32_t max_pairs, uint32_t max_len, cudaStream_t st) {
     const int threads = 128;
-    const size_t smem = (size_t)(threads / 32) * (max_len + 128) * sizeof(double);
+    const size_t smem = (size_t)(threads / 32) * ((max_len + 128) * sizeof(double) +
+                                                  (max_len + 31) / 32 * sizeof(unsigned));
     auto kern = a.sub ? dk_dp_kernel<D, RPL, true> : dk_dp_kernel<D, RPL, false>;
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
