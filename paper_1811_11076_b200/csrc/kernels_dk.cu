@@ -20,6 +20,7 @@
 // step (2 or 4), so one candidate-point load, one shuffle and the loop overhead are shared by
 // RPL cells.
 #include <algorithm>
+#include <cstdlib>
 
 #include "tsw_internal.cuh"
 
@@ -466,6 +467,16 @@ void run_dk(const DpArgs& a, uint32_t max_pairs, uint32_t max_len, cudaStream_t 
 template <int D>
 void run_dk_r(const DpArgs& a, uint32_t max_pairs, uint32_t max_len, cudaStream_t st) {
     // measured: 4 rows per lane -16% at L = 1024 and -6% at d = 16, +20% at L = 256, d = 2
+    // (TSW_DK_RPL=2|4 overrides, for measurements)
+    static const int rpl_env = [] {
+        const char* e = std::getenv("TSW_DK_RPL");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (rpl_env == 2 || rpl_env == 4) {
+        if (rpl_env == 4) run_dk<D, 4>(a, max_pairs, max_len, st);
+        else run_dk<D, 2>(a, max_pairs, max_len, st);
+        return;
+    }
     if (a.qlen >= 512 || a.store.d >= 8) run_dk<D, 4>(a, max_pairs, max_len, st);
     else run_dk<D, 2>(a, max_pairs, max_len, st);
 }
