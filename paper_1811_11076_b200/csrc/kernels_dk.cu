@@ -105,6 +105,42 @@ __device__ __forceinline__ void load_pt(Pt<D>& p, const double* __restrict__ t, 
     }
 }
 
+// Subsequence mode, a claim of cnt > 1 consecutive queue slots that all hold the same series
+// (the queue is candidate-major): the row-0 liveness bits of every claimed pair in ONE pass
+// over the series -- each column point is loaded once for all cnt queries (per-pair passes
+// re-read the series for every query).  Each pair's bits use its threshold at claim time (a
+// superset of the live cells later: safe).  Returns false (nothing written) otherwise.
+constexpr int kSubB = 8;  // max slots per claim
+template <int D>
+__device__ bool sub_claim_masks(const DpArgs& a, int cnt, bool ok, uint32_t eq, uint32_t ec,
+                                double tsq, unsigned* __restrict__ r0m, int wmax, int lane,
+                                int stride) {
+    // lane i < cnt holds claimed entry i (ok, eq, ec) and its threshold tsq
+    const unsigned c0 = __shfl_sync(kFull, ec, 0);
+    if (!__all_sync(kFull, lane >= cnt || (ok && ec == c0))) return false;
+    Pt<D> p0;  // lane i < cnt: point 0 of query i
+    if (lane < cnt) p0 = sp0_of<D>(a.queries + (uint64_t)eq * a.qstride, stride);
+    const double* t = a.store.data + series_off(a.store, c0);
+    const int n = (int)series_len(a.store, c0);
+    const int W = (n + 31) >> 5;
+#pragma unroll 2
+    for (int w = 0; w < W; ++w) {
+        const int j = w * 32 + lane;
+        Pt<D> tj;
+        load_pt<D>(tj, t, min(j, n + 31), stride);
+        for (int i = 0; i < cnt; ++i) {
+            Pt<D> pi;
+#pragma unroll
+            for (int kk = 0; kk < D; ++kk) pi.x[kk] = __shfl_sync(kFull, p0.x[kk], i);
+            const double ti = __shfl_sync(kFull, tsq, i);
+            const unsigned bm = __ballot_sync(kFull, j < n && cost<D>(pi, tj) <= ti);
+            if (lane == 0) r0m[i * wmax + w] = bm;
+        }
+    }
+    __syncwarp();
+    return true;
+}
+
 // One skewed step; `tv` holds column j's candidate point (loaded a step ahead) and `tn` gets
 // column j+1's.  Column indices run past [0, n) by at most 32 + 4 points: the store's guard
 // tiles (one after every series, two after the last) keep those loads inside the allocation,
@@ -180,7 +216,7 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
     // subsequence mode: row-0 liveness bits (c(0, j) <= Tsq), one word per 32 columns
     const int wmax = (int)(max_len + 31) / 32;
     unsigned* r0m = reinterpret_cast<unsigned*>(smem + (size_t)(blockDim.x >> 5) * (max_len + 128)) +
-                    (size_t)(threadIdx.x >> 5) * wmax;
+                    (size_t)(threadIdx.x >> 5) * wmax * (SUB ? kSubB : 1);
     const uint32_t d = a.store.d;
     const int m = (int)a.qlen;
     const int stride = D > 0 ? D : (int)d;
@@ -192,24 +228,58 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
     // long DP sweeps 12 registers)
     const unsigned total = nf + nbk;
     const unsigned nwarps = gridDim.x * (blockDim.x >> 5);
-    const unsigned bsz = SUB ? max(1u, min(8u, total / (nwarps * 16u))) : 1u;
-    unsigned cur = 0, cend = 0;  // claimed slots [cur, cend)
+    const unsigned bsz = SUB ? max(1u, min((unsigned)kSubB, total / (nwarps * 16u))) : 1u;
+    unsigned cur = 0, cend = 0, cbase = 0;  // claimed slots [cur, cend) of [cbase, cend)
+    bool premask = false;                   // row-0 bits of the whole claim computed at once
+    // subsequence mode: lane i holds claimed entry i and its threshold, loaded together at the
+    // claim (per-pair queue and threshold reads were two serial global latencies per pair)
+    bool cok = false;
+    uint32_t cq = 0, cc = 0;
+    float ckey = 0.0f;
+    double ctsq = 0.0;
     for (;;) {
         if (cur == cend) {
             unsigned base = 0;
             if (lane == 0) base = atomicAdd(a.queue.head, bsz);
             cur = __shfl_sync(kFull, base, 0);
             cend = cur >= total ? cur + 1 : min(cur + bsz, total);  // past the end: one failing get
+            cbase = cur;
+            premask = false;
+            if constexpr (SUB) {
+                const int cnt = (int)(cend - cur);
+                QEntry e{0, 0, 0.0f, 0};
+                cok = lane < cnt && queue_get(a.queue, nf, nbk, cur + lane, e);
+                cq = e.q;
+                cc = e.c;
+                ckey = e.key;
+                ctsq = a.fixed_eps_sq;
+                if (cok && a.state) ctsq = ld_volatile(&a.state[e.q].Tsq);
+                if constexpr (D > 0) {
+                    if (cnt > 1)
+                        premask = sub_claim_masks<D>(a, cnt, cok, cq, cc, ctsq, r0m, wmax, lane, stride);
+                }
+            }
         }
         const unsigned slot = cur++;
         QEntry pr;
-        if (!queue_get(a.queue, nf, nbk, slot, pr)) break;
+        double Tsq = a.fixed_eps_sq;
+        if constexpr (SUB) {  // the claim-time entry and threshold (>= the current one: safe)
+            const int ix = (int)(slot - cbase);
+            if (!__shfl_sync(kFull, cok, ix)) break;
+            pr.q = __shfl_sync(kFull, cq, ix);
+            pr.c = __shfl_sync(kFull, cc, ix);
+            pr.key = __shfl_sync(kFull, ckey, ix);
+            Tsq = __shfl_sync(kFull, ctsq, ix);
+        } else {
+            if (!queue_get(a.queue, nf, nbk, slot, pr)) break;
+        }
         QState* st = a.state ? a.state + pr.q : nullptr;
         // one read per warp: the dequeue decision must be warp-uniform (Tsq can drop between
         // two lanes' reads, and a split warp would deadlock on the next shuffle)
-        double Tsq = a.fixed_eps_sq;
-        if (st && lane == 0) Tsq = ld_volatile(&st->Tsq);
-        if (st) Tsq = __shfl_sync(kFull, Tsq, 0);
+        if (!SUB && st) {
+            if (lane == 0) Tsq = ld_volatile(&st->Tsq);
+            Tsq = __shfl_sync(kFull, Tsq, 0);
+        }
         if (!(pr.key <= Tsq)) {  // re-check the admitting first/last-cell bound at dequeue
             if (lane == 0 && st) atomicAdd(&st->early_abandoned, 1ull);
             continue;
@@ -223,7 +293,11 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
         S.b_alive_hi = 0;  // virtual start at (0, 0) (subsequence mode: live row-0 columns)
         int b_alive_lo = 0;
         bool dead = false;
+        unsigned* mk = r0m;  // this pair's row-0 liveness bits (subsequence mode)
         if constexpr (SUB && D > 0) {
+          if (premask) {
+            mk = r0m + (slot - cbase) * wmax;
+          } else {
             // every row-0 cell may start a match; its value is c(0, j).  Liveness bits for the
             // whole row, all loads in flight together (Tsq only decreases: stale bits are a
             // superset, which is safe).  Columns past n - 1 read guard points and are masked.
@@ -245,7 +319,8 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
                 }
             }
             __syncwarp();
-            b_alive_lo = next_live(r0m, W, 0, lane);
+          }
+            b_alive_lo = next_live(mk, (n + 31) >> 5, 0, lane);
             dead = b_alive_lo < 0;
         }
         double fin = kInf;
@@ -345,7 +420,7 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
                 const int lim = row0 ? n - 1 : min(S.b_hi, S.b_alive_hi);
                 int J = -1;
                 if (row0 && D > 0) {
-                    J = from <= lim ? next_live(r0m, (n + 31) >> 5, from, lane) : -1;
+                    J = from <= lim ? next_live(mk, (n + 31) >> 5, from, lane) : -1;
                 } else {
                     for (int j0 = row0 ? from : from - 1; j0 <= lim; j0 += 32) {
                         const int j = j0 + lane;
@@ -451,8 +526,9 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
 template <int D, int RPL>
 void run_dk(const DpArgs& a, uint32_t max_pairs, uint32_t max_len, cudaStream_t st) {
     const int threads = 128;
-    const size_t smem = (size_t)(threads / 32) * ((max_len + 128) * sizeof(double) +
-                                                  (max_len + 31) / 32 * sizeof(unsigned));
+    const size_t smem = (size_t)(threads / 32) *
+                        ((max_len + 128) * sizeof(double) +
+                         (a.sub ? (max_len + 31) / 32 * kSubB * sizeof(unsigned) : 0));
     auto kern = a.sub ? dk_dp_kernel<D, RPL, true> : dk_dp_kernel<D, RPL, false>;
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
