@@ -7,6 +7,7 @@
 // stays exact.  One warp owns a tile of CB consecutive candidates x QB queries: each 128-bit
 // candidate load is reused for QB queries and each envelope load for CB candidates.
 #include <algorithm>
+#include <cstdlib>
 
 #include "tsw_internal.cuh"
 
@@ -390,18 +391,21 @@ struct TileOut {
 // One tile: lane j ends with its pair's fp32 LB_Box (rounded down), whether it survives the
 // current threshold (and was not probed), its queue region and -- block mode -- the slot of its
 // LB block-sum row, written here for every survivor.  `stash`: this warp's 32 x 32 floats.
-template <int QB, int CB>
+// SENV: the QB queries' envelopes are staged in shared memory ([QB][total4] float4 each, rows
+// past the last query duplicate it) instead of read through L1.
+template <int QB, int CB, bool SENV = false>
 __device__ __forceinline__ TileOut lb1_tile(const LbCompactArgs& a, uint32_t c0, uint32_t q0,
-                                            float* stash, uint32_t total4) {
+                                            float* stash, uint32_t total4,
+                                            const float4* slo = nullptr, const float4* shi = nullptr) {
     static_assert(QB * CB == 32, "one pair per lane after the reduction");
     const unsigned lane = lane_id();
     const uint32_t n = a.store.n;
     // base pointers only (per-query / per-candidate offsets are recomputed: register budget)
     const float4* xb = reinterpret_cast<const float4*>(a.store.data32) + (uint64_t)c0 * (a.store.ustride / 4);
     const uint64_t xs = a.store.ustride / 4;
-    const float4* lob = reinterpret_cast<const float4*>(a.env_lo) + (uint64_t)q0 * (a.qstride / 4);
-    const float4* hib = reinterpret_cast<const float4*>(a.env_hi) + (uint64_t)q0 * (a.qstride / 4);
-    const uint64_t qs = a.qstride / 4;
+    const float4* lob = SENV ? slo : reinterpret_cast<const float4*>(a.env_lo) + (uint64_t)q0 * (a.qstride / 4);
+    const float4* hib = SENV ? shi : reinterpret_cast<const float4*>(a.env_hi) + (uint64_t)q0 * (a.qstride / 4);
+    const uint64_t qs = SENV ? total4 : a.qstride / 4;
     const uint32_t cmax = n - 1 - c0, qmax = a.nq - 1 - q0;  // clamp tails to valid rows
     float acc[QB][CB];
 #pragma unroll
@@ -415,8 +419,8 @@ __device__ __forceinline__ TileOut lb1_tile(const LbCompactArgs& a, uint32_t c0,
 #pragma unroll
         for (int qb = 0; qb < QB; ++qb) {
             const uint64_t qo = (uint64_t)min((uint32_t)qb, qmax) * qs + f;
-            const float4 l = __ldg(lob + qo);
-            const float4 h = __ldg(hib + qo);
+            const float4 l = SENV ? lob[qo] : __ldg(lob + qo);
+            const float4 h = SENV ? hib[qo] : __ldg(hib + qo);
 #pragma unroll
             for (int cb = 0; cb < CB; ++cb) {
                 float sacc = acc[qb][cb];
@@ -603,6 +607,57 @@ __global__ void __launch_bounds__(256, 2) lb_compact_kernel(LbCompactArgs a) {
     }
 }
 
+// ---- K2 with the envelopes in shared memory (short series) ----------------------------------
+// lb_compact_kernel re-reads each warp's 8 query envelopes through L1 for every candidate
+// group; with all queries in flight the envelopes miss L1 (hit rate 35%) and the pass waits on
+// L2.  Here a block owns one query block at a time: its QB envelopes are staged once in shared
+// memory and the block's warps stream the candidate groups of a chunk against them.  Work
+// items are (chunk, query block), query block fastest, and the grid is a multiple of the
+// number of query blocks, so a block keeps its query block (one staging) while the blocks
+// running at the same time cover the same candidate chunks (their bytes come from L2).
+template <int QB, int CB>
+__global__ void __launch_bounds__(256, 2) lb_env_kernel(LbCompactArgs a, uint32_t chunk) {
+    const uint32_t n = a.store.n;
+    const uint32_t ngroups = (n + CB - 1) / CB;
+    const uint32_t nqb = (a.nq + QB - 1) / QB;
+    const uint32_t nchunks = (ngroups + chunk - 1) / chunk;
+    const uint32_t total4 = (uint32_t)(a.store.tstride / 4);
+    const uint32_t warp = threadIdx.x >> 5;
+    __shared__ QEntry stage_buf[8][2][kStage];
+    extern __shared__ float4 lbe_smem[];  // lo [QB][total4], hi [QB][total4], stash (block mode)
+    float4* elo = lbe_smem;
+    float4* ehi = lbe_smem + (size_t)QB * total4;
+    float* stash = reinterpret_cast<float*>(lbe_smem + (size_t)2 * QB * total4) + (size_t)warp * 32 * 32;
+    Stage sg{stage_buf[warp][0], stage_buf[warp][1], 0u, 0u};
+    uint32_t have_qb = 0xffffffffu;
+    const uint64_t items = (uint64_t)nchunks * nqb;
+    for (uint64_t it = blockIdx.x; it < items; it += gridDim.x) {
+        const uint32_t qbk = (uint32_t)(it % nqb), ch = (uint32_t)(it / nqb);
+        if (qbk != have_qb) {  // block-uniform
+            __syncthreads();
+            const float4* glo = reinterpret_cast<const float4*>(a.env_lo);
+            const float4* ghi = reinterpret_cast<const float4*>(a.env_hi);
+            for (uint32_t i = threadIdx.x; i < QB * total4; i += blockDim.x) {
+                const uint32_t qb = i / total4, f = i - qb * total4;
+                const uint64_t qo = (uint64_t)min(qbk * QB + qb, a.nq - 1) * (a.qstride / 4) + f;
+                elo[i] = __ldg(glo + qo);
+                ehi[i] = __ldg(ghi + qo);
+            }
+            __syncthreads();
+            have_qb = qbk;
+        }
+        const uint32_t gend = min((ch + 1) * chunk, ngroups);
+        for (uint32_t g = ch * chunk + warp; g < gend; g += 8) {
+            const TileOut t = lb1_tile<QB, CB, true>(a, g * CB, qbk * QB, stash, total4, elo, ehi);
+            if (a.state) enqueue(sg, a.queue, t.take, t.near, t.q, t.c, t.lb, t.ps);
+        }
+    }
+    if (a.state) {
+        stage_flush(sg, a.queue, true);
+        stage_flush(sg, a.queue, false);
+    }
+}
+
 // ---- K2 + reverse LB_Box + K3 ---------------------------------------------------------------
 // A warp owns one candidate group (CB candidates) against ALL queries: the forward tiles run
 // as above, their survivors are listed in shared memory, and the list gets the reverse bound
@@ -747,6 +802,31 @@ void launch_lb_compact(const LbCompactArgs& a, cudaStream_t st) {
         if (a.nq == 1) lb_few_kernel<1><<<std::max(blocks, 1), 256, 0, st>>>(a);
         else if (a.nq == 2) lb_few_kernel<2><<<std::max(blocks, 1), 256, 0, st>>>(a);
         else lb_few_kernel<3><<<std::max(blocks, 1), 256, 0, st>>>(a);
+        return;
+    }
+    const uint32_t total4 = (uint32_t)(a.store.tstride / 4);
+    const size_t esmem = (size_t)2 * QB * total4 * sizeof(float4);
+    static const int env_mode = [] {  // TSW_LB_ENV=0 forces the L1 path (A/B)
+        const char* e = std::getenv("TSW_LB_ENV");
+        return e ? std::atoi(e) : 1;
+    }();
+    if (env_mode && esmem <= 48 * 1024) {
+        const uint32_t nqb = (a.nq + QB - 1) / QB;
+        const uint32_t slots = (uint32_t)sm_count() * 2;  // resident blocks (256 threads, 2 / SM)
+        const uint32_t grid = nqb <= slots ? slots / nqb * nqb : slots;
+        const uint32_t ngroups = (uint32_t)((a.store.n + CB - 1) / CB);
+        // chunk = one candidate group per warp: the blocks running together then cover a
+        // narrow candidate range, which keeps the DP queue close to candidate-major (DP cache
+        // reuse); TSW_LB_CHUNK overrides (A/B)
+        static const uint32_t chunk_env = [] {
+            const char* e = std::getenv("TSW_LB_CHUNK");
+            return e ? (uint32_t)std::atoi(e) : 0u;
+        }();
+        const uint32_t chunk = chunk_env ? chunk_env : 8u;
+        (void)ngroups;
+        const size_t sm = esmem + smem;
+        cudaFuncSetAttribute(lb_env_kernel<QB, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        lb_env_kernel<QB, CB><<<grid, 256, sm, st>>>(a, chunk);
         return;
     }
     const uint64_t tiles = (uint64_t)((a.store.n + CB - 1) / CB) * ((a.nq + QB - 1) / QB);
