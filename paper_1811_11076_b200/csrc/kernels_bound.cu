@@ -806,10 +806,8 @@ void launch_lb_compact(const LbCompactArgs& a, cudaStream_t st) {
     }
     const uint32_t total4 = (uint32_t)(a.store.tstride / 4);
     const size_t esmem = (size_t)2 * QB * total4 * sizeof(float4);
-    static const int env_mode = [] {  // TSW_LB_ENV=0 forces the L1 path (A/B)
-        const char* e = std::getenv("TSW_LB_ENV");
-        return e ? std::atoi(e) : 1;
-    }();
+    const char* env_e = std::getenv("TSW_LB_ENV");  // TSW_LB_ENV=0: the L1 path (A/B, tests)
+    const int env_mode = env_e ? std::atoi(env_e) : 1;
     if (env_mode && esmem <= 48 * 1024) {
         const uint32_t nqb = (a.nq + QB - 1) / QB;
         const uint32_t slots = (uint32_t)sm_count() * 2;  // resident blocks (256 threads, 2 / SM)
@@ -818,10 +816,8 @@ void launch_lb_compact(const LbCompactArgs& a, cudaStream_t st) {
         // chunk = one candidate group per warp: the blocks running together then cover a
         // narrow candidate range, which keeps the DP queue close to candidate-major (DP cache
         // reuse); TSW_LB_CHUNK overrides (A/B)
-        static const uint32_t chunk_env = [] {
-            const char* e = std::getenv("TSW_LB_CHUNK");
-            return e ? (uint32_t)std::atoi(e) : 0u;
-        }();
+        const char* chunk_e = std::getenv("TSW_LB_CHUNK");
+        const uint32_t chunk_env = chunk_e ? (uint32_t)std::atoi(chunk_e) : 0u;
         const uint32_t chunk = chunk_env ? chunk_env : 8u;
         (void)ngroups;
         const size_t sm = esmem + smem;

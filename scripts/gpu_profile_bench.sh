@@ -6,7 +6,7 @@ $CMD > gpurun_out/prof_plain.log 2>&1 && \
 $CMD > gpurun_out/prof_plain2.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:dtw4_kernel -s 1 -c 1 -f -o gpurun_out/prof_dtw_dp_c2 $CMD > gpurun_out/prof_f1.log 2>&1; echo "dtw full $?"
 $CMD > gpurun_out/prof_plain3.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:lb_compact_kernel -s 0 -c 1 -f -o gpurun_out/prof_lb_c2 $CMD > gpurun_out/prof_f2.log 2>&1; echo "lb full $?"
+  ncu --set full --clock-control none --import-source on -k regex:"lb_(env|compact)_kernel" -s 0 -c 1 -f -o gpurun_out/prof_lb_c2 $CMD > gpurun_out/prof_f2.log 2>&1; echo "lb full $?"
 C5K="python bench.py --config 5 --metric dk --steps 1 --warmup 3 --no-cpu-baseline"
 $C5K > gpurun_out/prof_plain4.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:dk_dp_kernel -s 1 -c 1 -f -o gpurun_out/prof_dk_dp_c5 $C5K > gpurun_out/prof_f3.log 2>&1; echo "dk full $?"

@@ -389,3 +389,27 @@ def test_plan_cuda_graph_matches_eager(tsw):
             assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
             for c in b[2]:
                 assert c[2] + c[3] + (c[1] if metric == "dtw" else 0) == 700
+
+
+@pytest.mark.parametrize("env", ["1", "0"])
+def test_knn_lb_envelope_paths(tsw, best_oracle, env, monkeypatch):
+    """K2 with the query envelopes staged in shared memory (lb_env_kernel, TSW_LB_ENV=1, the
+    default for L*d <= 768) and the L1 tile kernel (TSW_LB_ENV=0) give the reference's
+    neighbours: query counts that are not multiples of the 8-query block, candidate counts that
+    are not multiples of the 4-candidate group, lengths that are not multiples of 32, block-sum
+    rows on (L <= 256), and a store long enough for several candidate chunks per block."""
+    import oracle
+
+    monkeypatch.setenv("TSW_LB_ENV", env)
+    rng = np.random.default_rng(77)
+    for n, L, d, r, k, nq in ((1001, 40, 3, 4, 1, 9), (333, 128, 3, 13, 3, 17),
+                              (2050, 96, 2, 9, 2, 5), (517, 190, 4, 19, 1, 12)):
+        X = walks(rng, n, L, d)
+        Q = walks(rng, nq, L, d)
+        Q[2] = X[11] + 1e-3 * rng.standard_normal((L, d))
+        gi, gd, gc = tsw.knn(tsw.Dataset(X), Q, k, "dtw", r)
+        ods = oracle.Dataset(X)
+        for q in range(nq):
+            oi, od, _ = best_oracle.knn(Q[q], ods, k, "dtw", r)
+            assert_knn_equal(gi[q], gd[q], oi, od, f"env={env} n={n} L={L} d={d} r={r} q{q}")
+            _check_counters(gc[q], n, "dtw")
