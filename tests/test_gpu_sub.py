@@ -146,3 +146,24 @@ def test_sub_errors_mirror_reference(tsw):
         tsw.sub_search_dk(np.zeros((3, 3)), X[0])
     with pytest.raises(ValueError, match="eps must be nonnegative"):
         tsw.sparse_dk_sub(X[0][:3], X[1], -1.0)
+
+
+def test_knn_dk_sub_deep_queue_claims(tsw, best_oracle):
+    """A queue deep enough (64 queries x 6000 series = 384k pairs) that the DP warps claim 8
+    slots per atomic and compute the row-0 liveness bits of a claim's pairs in one pass over
+    the shared series (claims that straddle two series take the per-pair path): the neighbours
+    of a sample of queries equal the reference's, bit for bit."""
+    import oracle
+
+    rng = np.random.default_rng(4242)
+    n, L, m, d, k = 6000, 64, 16, 2, 3
+    X = list(rng.standard_normal((n, L, d)).cumsum(1))
+    Q = rng.standard_normal((64, m, d)).cumsum(1)
+    Q[5] = X[123][10:10 + m] + 1e-3 * rng.standard_normal((m, d))
+    gi, gd, gc = tsw.knn(tsw.Dataset(X), Q, k, "dk_sub")
+    ods = oracle.Dataset(X)
+    for q in (0, 5, 17, 31, 40, 63):
+        oi, od, _ = best_oracle.knn(Q[q], ods, k, "dk_sub")
+        assert np.array_equal(gi[q], oi), (q, gi[q], oi)
+        assert np.array_equal(_bits(gd[q]), _bits(od)), (q, gd[q], od)
+        assert gc[q][4] == n and gc[q][2] + gc[q][3] == n
