@@ -118,6 +118,14 @@ __device__ __forceinline__ void iter(Lane<G, D>& s, const double* __restrict__ s
     }
     s.qo = prev_off<D>(s.qo);
     s.co = prev_off<D>(s.co);
+    // cumulative bound of the cut, one value per lane: pfx is non-decreasing in the candidate
+    // point, so the lane's smallest candidate index (largest window slot tt) gives a lower
+    // bound of every slot's own term (abandoning on it is conservative)
+    double Rmin = 0.0;
+    if (CHECK) {
+        constexpr int TTMAX = (2 * G - 1) - ((2 * G - 1 + RPAR) >> 1);
+        Rmin = (double)pfx[min(max(tjb - TTMAX, 0), L - 1) >> plog];
+    }
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
         const int par = half == 0 ? RPAR : 1 - RPAR;
@@ -141,8 +149,7 @@ __device__ __forceinline__ void iter(Lane<G, D>& s, const double* __restrict__ s
             s.v[e] = nv;
             if (CHECK) {
                 const double Tm = __dmul_ru(T, margin);
-                const int tj = min(max(tjb - tt, 0), L - 1);
-                alive |= ((okm >> e) & 1u) && dadd(nv, (double)pfx[tj >> plog]) <= Tm;
+                alive |= ((okm >> e) & 1u) && dadd(nv, Rmin) <= Tm;
             }
         }
     }
