@@ -413,3 +413,22 @@ def test_knn_lb_envelope_paths(tsw, best_oracle, env, monkeypatch):
             oi, od, _ = best_oracle.knn(Q[q], ods, k, "dtw", r)
             assert_knn_equal(gi[q], gd[q], oi, od, f"env={env} n={n} L={L} d={d} r={r} q{q}")
             _check_counters(gc[q], n, "dtw")
+
+
+def test_knn_lb_envelope_many_query_blocks(tsw, best_oracle):
+    """More 8-query blocks (313) than resident LB blocks (2 per SM): the blocks of the
+    shared-memory-envelope K2 then change query block from one work item to the next and
+    re-stage the envelopes; sampled queries equal the reference's neighbours."""
+    import oracle
+
+    rng = np.random.default_rng(2500)
+    n, L, d, r, k, nq = 300, 32, 2, 3, 2, 2500
+    X = walks(rng, n, L, d)
+    Q = walks(rng, nq, L, d)
+    Q[1234] = X[42] + 1e-3 * rng.standard_normal((L, d))
+    gi, gd, gc = tsw.knn(tsw.Dataset(X), Q, k, "dtw", r)
+    ods = oracle.Dataset(X)
+    for q in (0, 1, 7, 8, 1234, 2367, 2368, 2499):
+        oi, od, _ = best_oracle.knn(Q[q], ods, k, "dtw", r)
+        assert_knn_equal(gi[q], gd[q], oi, od, f"q{q}")
+        _check_counters(gc[q], n, "dtw")
