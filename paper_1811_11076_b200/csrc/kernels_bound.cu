@@ -11,6 +11,8 @@
 
 #include "tsw_internal.cuh"
 
+
+
 namespace tswb {
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
@@ -393,7 +395,10 @@ struct TileOut {
 // LB block-sum row, written here for every survivor.  `stash`: this warp's 32 x 32 floats.
 // SENV: the QB queries' envelopes are staged in shared memory ([QB][total4] float4 each, rows
 // past the last query duplicate it) instead of read through L1.
-template <int QB, int CB, bool SENV = false>
+// PACK: the terms' subtractions as packed FP32x2 (lb_term2_rd): -8% / -7% / -4% on the K2
+// pass at C2 / C3 / C4; the fused wide-band kernel keeps the scalar form (the packed one
+// spills there and is 8% slower at C5).
+template <int QB, int CB, bool SENV = false, bool PACK = true>
 __device__ __forceinline__ TileOut lb1_tile(const LbCompactArgs& a, uint32_t c0, uint32_t q0,
                                             float* stash, uint32_t total4,
                                             const float4* slo = nullptr, const float4* shi = nullptr) {
@@ -423,12 +428,22 @@ __device__ __forceinline__ TileOut lb1_tile(const LbCompactArgs& a, uint32_t c0,
             const float4 h = SENV ? hib[qo] : __ldg(hib + qo);
 #pragma unroll
             for (int cb = 0; cb < CB; ++cb) {
-                float sacc = acc[qb][cb];
-                sacc = lb_term_rd(sacc, x[cb].x, l.x, h.x);
-                sacc = lb_term_rd(sacc, x[cb].y, l.y, h.y);
-                sacc = lb_term_rd(sacc, x[cb].z, l.z, h.z);
-                sacc = lb_term_rd(sacc, x[cb].w, l.w, h.w);
-                acc[qb][cb] = sacc;
+                if constexpr (PACK) {
+                    // sum of the (x, z) terms and of the (y, w) terms, then one RD add: RD
+                    // adds in any order keep the lower-bound property (and the per-lane sums
+                    // are still the pair's block sums)
+                    float s0 = acc[qb][cb], s1 = 0.0f;
+                    lb_term2_rd(s0, s1, x[cb].x, x[cb].y, l.x, l.y, h.x, h.y);
+                    lb_term2_rd(s0, s1, x[cb].z, x[cb].w, l.z, l.w, h.z, h.w);
+                    acc[qb][cb] = __fadd_rd(s0, s1);
+                } else {
+                    float sacc = acc[qb][cb];
+                    sacc = lb_term_rd(sacc, x[cb].x, l.x, h.x);
+                    sacc = lb_term_rd(sacc, x[cb].y, l.y, h.y);
+                    sacc = lb_term_rd(sacc, x[cb].z, l.z, h.z);
+                    sacc = lb_term_rd(sacc, x[cb].w, l.w, h.w);
+                    acc[qb][cb] = sacc;
+                }
             }
         }
     };
@@ -764,7 +779,7 @@ __global__ void __launch_bounds__(256, 2) lb12_compact_kernel(LbCompactArgs a) {
         const uint32_t c0 = cg * CB;
         int cnt = 0;
         for (uint32_t qbk = 0; qbk < nqb; ++qbk) {
-            const TileOut t = lb1_tile<QB, CB>(a, c0, qbk * QB, stash, total4);
+            const TileOut t = lb1_tile<QB, CB, false, false>(a, c0, qbk * QB, stash, total4);
             const unsigned tm = __ballot_sync(0xffffffffu, t.take);
             if (t.take) list[cnt + __popc(tm & ((1u << lane) - 1u))] = QEntry{t.q, t.c, t.lb, t.ps};
             cnt += __popc(tm);

@@ -159,6 +159,29 @@ __device__ __forceinline__ float lb_term_rd(float acc, float x, float m, float h
     return __fmaf_rd(e, e, acc);
 }
 
+// Two LB terms (adjacent elements of one float4) with the subtractions done as packed FP32x2
+// (FADD2.RZ, then FADD2.RM with the |.| operand modifier), the max and the RD square-accumulate
+// per element: 6 instructions for 2 terms instead of 8.  Same roundings per element as
+// lb_term_rd, so each accumulator gets exactly the value lb_term_rd would give it.
+__device__ __forceinline__ void lb_term2_rd(float& acc0, float& acc1, float x0, float x1, float m0,
+                                            float m1, float h0, float h1) {
+    unsigned long long x, m, h, d, e;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(x) : "f"(x0), "f"(x1));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(m) : "f"(m0), "f"(m1));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(h) : "f"(h0), "f"(h1));
+    asm("sub.rz.f32x2 %0, %1, %2;" : "=l"(d) : "l"(x), "l"(m));
+    float d0, d1;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(d0), "=f"(d1) : "l"(d));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(fabsf(d0)), "f"(fabsf(d1)));
+    asm("sub.rm.f32x2 %0, %1, %2;" : "=l"(e) : "l"(d), "l"(h));
+    float e0, e1;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(e0), "=f"(e1) : "l"(e));
+    e0 = fmaxf(e0, 0.0f);
+    e1 = fmaxf(e1, 0.0f);
+    acc0 = __fmaf_rd(e0, e0, acc0);
+    acc1 = __fmaf_rd(e1, e1, acc1);
+}
+
 __device__ __forceinline__ void atomic_min_pos(double* p, double v) {
     atomicMin(reinterpret_cast<unsigned long long*>(p), (unsigned long long)__double_as_longlong(v));
 }
