@@ -93,7 +93,8 @@ def test_dtw_all_bit_exact(tsw, port, N, L, d, r):
 def test_dtw_fast_path_variants(tsw, port, variant, monkeypatch):
     """Every (cells per lane G, group width WL) instance of the guarded fast path
     (kernels_dtw4.cu) and the generic kernel, d = 1..4, bands that put offset +r on either
-    lane parity, L not a multiple of the 32-point tile (padding = guard values)."""
+    lane parity and every band radius mod 4, L not a multiple of the 32-point tile (padding =
+    guard values)."""
     import oracle
 
     if variant == "generic":
@@ -102,7 +103,8 @@ def test_dtw_fast_path_variants(tsw, port, variant, monkeypatch):
         monkeypatch.setenv("TSW_DTW4", variant)
     rng = np.random.default_rng(12)
     for d in (1, 2, 3, 4):
-        for L, r in ((1, 0), (5, 2), (37, 6), (45, 7), (70, 14), (70, 15), (100, 30), (120, 52)):
+        for L, r in ((1, 0), (5, 2), (37, 6), (45, 7), (60, 9), (70, 14), (70, 15), (90, 13),
+                     (80, 25), (100, 27), (100, 30), (120, 52)):
             X = walks(rng, 24, L, d)
             q = walks(rng, 1, L, d)[0]
             ex, val = tsw.dist_all(tsw.Store(X), q, "dtw", r)
