@@ -339,7 +339,7 @@ std::unique_ptr<tsw_plan> make_plan(tsw_store* s, uint64_t nq_max, uint64_t qlen
     // probes are cheap (banded, abandoning) and feed the LB compaction: 2k (>= 8).  A DK probe
     // runs a near-full L^2 DP under the loose seed, so DK probes only k.
     uint64_t want_probe = metric == TSW_METRIC_DTW ? std::max<uint64_t>(8, 2 * p->kk) : p->kk;
-    if (const char* pe = std::getenv("TSW_PROBE")) want_probe = std::max<long long>(1, std::atoll(pe));
+    if (const char* pe = std::getenv("TSW_PROBE"); pe && *pe) want_probe = std::max<long long>(1, std::atoll(pe));
     p->probe = p->kk <= (uint64_t)kKMax ? std::min<uint64_t>({p->S, (uint64_t)kKMax, want_probe}) : 0;
     p->P = std::max<uint64_t>(1, std::min<uint64_t>(kKMax, std::max(p->kk, p->probe)));
     ck(cudaStreamCreateWithFlags(&p->own, cudaStreamNonBlocking), "cudaStreamCreate");

@@ -822,7 +822,7 @@ void launch_lb_compact(const LbCompactArgs& a, cudaStream_t st) {
     const uint32_t total4 = (uint32_t)(a.store.tstride / 4);
     const size_t esmem = (size_t)2 * QB * total4 * sizeof(float4);
     const char* env_e = std::getenv("TSW_LB_ENV");  // TSW_LB_ENV=0: the L1 path (A/B, tests)
-    const int env_mode = env_e ? std::atoi(env_e) : 1;
+    const int env_mode = env_e && *env_e ? std::atoi(env_e) : 1;
     if (env_mode && esmem <= 48 * 1024) {
         const uint32_t nqb = (a.nq + QB - 1) / QB;
         const uint32_t slots = (uint32_t)sm_count() * 2;  // resident blocks (256 threads, 2 / SM)
