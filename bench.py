@@ -395,9 +395,9 @@ def main():
                 "frac": (lb_gbs / peaks["hbm_gbs"]) if lb_gbs else None,
                 "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json copy rate)",
                 "algorithmic_bytes_per_launch": ph["bound_bytes"] / max(1.0, ph["bound_passes"])}
-    # short series (L*d <= 768): envelopes staged in shared memory (lb_env_kernel) unless
+    # short series (tiled L*d <= 768): envelopes staged in shared memory (lb_env_kernel) unless
     # TSW_LB_ENV=0 (kernels_bound.cu launch_lb_compact)
-    lb_short = L * d <= 768 and os.environ.get("TSW_LB_ENV", "1") != "0"
+    lb_short = (L + 31) // 32 * 32 * d <= 768 and os.environ.get("TSW_LB_ENV", "1") != "0"
     lb_kernel = ("lb12_compact_kernel" if (r >= 32) else
                  "lb_env_kernel" if lb_short else "lb_compact_kernel") if metric == "dtw" \
         else "dk_compact_kernel"
