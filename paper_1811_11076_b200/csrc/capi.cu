@@ -204,7 +204,7 @@ struct tsw_plan {
     cudaStream_t aux = nullptr;  // DTW probe DP, overlapped with the LB pass
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     DevBuf<double> qends;  // DK compaction scratch [2d][nq_max]
-    DevBuf<double> q, q_rm, ub, sel_sv, sel_v, slots, top_d;
+    DevBuf<double> q, q_rm, ub, ub_part, sel_sv, sel_v, slots, top_d;
     DevBuf<float> env_lo, env_hi;
     DevBuf<float> pfx;  // DTW: survivors' LB block sums [pfx_cap][kPfxBlocks]
     // DTW reverse LB bound: fp32 queries, their max |value|, the candidate envelope
@@ -397,6 +397,9 @@ std::unique_ptr<tsw_plan> make_plan(tsw_store* s, uint64_t nq_max, uint64_t qlen
         }
     }
     p->ub.alloc(nq_max * p->S);
+    // point-range splits of the sampled bounds when the (query, sample) tiles cannot fill the
+    // GPU (few queries): up to 8 partial rows per pair
+    if (nq_max * p->S <= (1u << 20)) p->ub_part.alloc(8 * nq_max * p->S);
     const uint64_t chunks = (p->S + kSelChunk - 1) / kSelChunk;
     p->sel_sv.alloc(2 * nq_max * chunks * p->P);
     p->sel_si.alloc(2 * nq_max * chunks * p->P);
@@ -491,8 +494,9 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
     sa.ub_scale = p->ub_scale;
     sa.dk = dk;
     sa.out_ub = p->ub.p;
-    launch_sample_ub(sa, st);
-    ++launches;
+    sa.part = p->ub_part.p;
+    sa.part_cap = p->ub_part.n;
+    launches += launch_sample_ub(sa, st);
     launch_select_smallest(p->ub.p, nullptr, nullptr, nq, (uint32_t)p->S, (uint32_t)p->P,
                            p->sel_sv.p, p->sel_si.p, p->sel_v.p, p->sel_i.p, st, &launches);
     SeedArgs se{};

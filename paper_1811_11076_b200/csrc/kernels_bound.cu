@@ -219,7 +219,7 @@ constexpr int kUQS = kUQ + 2, kUCS = kUC + 2;  // padded rows: 2-way instead of 
 constexpr int kUSub = 4;  // threads per pair set (interleaved points), reduced at the end
 
 template <bool DK>
-__global__ void __launch_bounds__(128 * kUSub) sample_ub_tile_kernel(SampleArgs a) {
+__global__ void __launch_bounds__(128 * kUSub, 2) sample_ub_tile_kernel(SampleArgs a) {
     extern __shared__ __align__(16) double usm[];
     const uint32_t d = a.store.d, L = a.qlen;
     const uint32_t kUP = ub_chunk(d);
@@ -229,6 +229,9 @@ __global__ void __launch_bounds__(128 * kUSub) sample_ub_tile_kernel(SampleArgs 
     const int t = threadIdx.x, sub = t / 128, tp = t % 128;
     const int tq = tp / (kUC / 2), tc = tp % (kUC / 2);
     double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    // point range of this block: the chunks of split blockIdx.z (gridDim.z = 1: all of them)
+    const uint32_t nch = (L + kUP - 1) / kUP, cps = (nch + gridDim.z - 1) / gridDim.z;
+    const uint32_t p_lo = min(nch, blockIdx.z * cps) * kUP, p_hi = min(L, min(nch, (blockIdx.z + 1) * cps) * kUP);
     // this thread's chunk elements, resolved once: element e = (series sr, dim k, point pp),
     // pp fastest; query side [0, nqe), candidate side after.  Chunk p0 adds one uniform tile
     // offset.  Points past L read padding / guard values, which the compute never uses.
@@ -259,16 +262,19 @@ __global__ void __launch_bounds__(128 * kUSub) sample_ub_tile_kernel(SampleArgs 
     }
     // register-staged chunks: the next chunk's loads are in flight during this one's compute
     double nxt[kUElem];
+    {
+        const uint64_t coff = (uint64_t)(p_lo >> 5) * kTile * d + (p_lo & 31);
 #pragma unroll
-    for (int i = 0; i < kUElem; ++i)
-        if (i < nel) nxt[i] = gsrc[i][0];
-    for (uint32_t p0 = 0; p0 < L; p0 += kUP) {
+        for (int i = 0; i < kUElem; ++i)
+            if (i < nel && p_lo < p_hi) nxt[i] = gsrc[i][coff];
+    }
+    for (uint32_t p0 = p_lo; p0 < p_hi; p0 += kUP) {
         __syncthreads();
 #pragma unroll
         for (int i = 0; i < kUElem; ++i)
             if (i < nel) usm[sdst[i]] = nxt[i];
         __syncthreads();
-        if (p0 + kUP < L) {
+        if (p0 + kUP < p_hi) {
             const uint32_t p1 = p0 + kUP;
             const uint64_t coff = (uint64_t)(p1 >> 5) * kTile * d + (p1 & 31);
 #pragma unroll
@@ -315,24 +321,53 @@ __global__ void __launch_bounds__(128 * kUSub) sample_ub_tile_kernel(SampleArgs 
                     v = DK ? dmax(v, w) : dadd(v, w);
                 }
                 const uint32_t q = q0 + 2 * tq + x, j = j0 + 2 * tc + y;
-                if (q < a.nq && j < a.S) a.out_ub[(uint64_t)q * a.S + j] = DK ? v : __dmul_ru(v, a.ub_scale);
+                if (q < a.nq && j < a.S) {
+                    if (gridDim.z == 1) a.out_ub[(uint64_t)q * a.S + j] = DK ? v : __dmul_ru(v, a.ub_scale);
+                    else a.part[((uint64_t)blockIdx.z * a.nq + q) * a.S + j] = v;  // raw partial
+                }
             }
     }
 }
 
-void launch_sample_ub(const SampleArgs& a, cudaStream_t st) {
+// Point-range splits: DK partial maxima max-combine exactly; DTW partial sums are another
+// any-order summation of the same costs, so the one ub_scale rounding after the combine still
+// bounds the suffix-ordered fl sum.
+template <bool DK>
+__global__ void sample_ub_combine_kernel(SampleArgs a, uint32_t nsplit) {
+    const uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x, m = (uint64_t)a.nq * a.S;
+    if (i >= m) return;
+    double v = a.part[i];
+    for (uint32_t z = 1; z < nsplit; ++z) v = DK ? dmax(v, a.part[z * m + i]) : dadd(v, a.part[z * m + i]);
+    a.out_ub[i] = DK ? v : __dmul_ru(v, a.ub_scale);
+}
+
+int launch_sample_ub(const SampleArgs& a, cudaStream_t st) {
     if (a.store.ulen == a.qlen && (kUQ + kUC) * a.store.d * ub_chunk(a.store.d) <= kUElem * 128 * kUSub) {
-        const dim3 grid((a.S + kUC - 1) / kUC, (a.nq + kUQ - 1) / kUQ);
+        dim3 grid((a.S + kUC - 1) / kUC, (a.nq + kUQ - 1) / kUQ);
+        // few queries: split the point range so that the grid fills the resident slots (2
+        // blocks per SM)
+        const uint64_t blocks = (uint64_t)grid.x * grid.y, m = (uint64_t)a.nq * a.S;
+        const uint32_t nch = (a.qlen + ub_chunk(a.store.d) - 1) / ub_chunk(a.store.d);
+        uint32_t nsplit = (uint32_t)std::min<uint64_t>({(2ull * sm_count() + blocks - 1) / blocks, nch, 8ull});
+        if (!a.part || (uint64_t)nsplit * m > a.part_cap) nsplit = 1;
+        grid.z = nsplit;
         const size_t smem = std::max<size_t>((size_t)a.store.d * ub_chunk(a.store.d) * (kUQS + kUCS),
                                              (size_t)kUSub * 128 * 4) * sizeof(double);
         auto kern = a.dk ? sample_ub_tile_kernel<true> : sample_ub_tile_kernel<false>;
         if (smem > 48 * 1024) cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         kern<<<grid, 128 * kUSub, smem, st>>>(a);
-        return;
+        if (nsplit > 1) {
+            const int cb = (int)((m + 255) / 256);
+            if (a.dk) sample_ub_combine_kernel<true><<<cb, 256, 0, st>>>(a, nsplit);
+            else sample_ub_combine_kernel<false><<<cb, 256, 0, st>>>(a, nsplit);
+            return 2;
+        }
+        return 1;
     }
     const uint64_t warps = (uint64_t)a.nq * a.S;
     const int blocks = (int)std::min<uint64_t>((warps * 32 + 255) / 256, (uint64_t)sm_count() * 16);
     sample_ub_kernel<<<std::max(blocks, 1), 256, 0, st>>>(a);
+    return 1;
 }
 
 // ---- warp-staged enqueue into the two-region work queue --------------------------------------

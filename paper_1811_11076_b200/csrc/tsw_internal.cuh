@@ -245,8 +245,10 @@ struct SampleArgs {
     double ub_scale;      // DTW: diagonal-sum inflation factor (rounded up)
     int dk;
     double* out_ub;       // [nq][S]  DTW: diagonal upper bound; DK: diagonal-path max sq
+    double* part;         // optional scratch for point-range splits ([split][nq][S]), nullable
+    uint64_t part_cap;    // doubles in `part`
 };
-void launch_sample_ub(const SampleArgs& a, cudaStream_t st);
+int launch_sample_ub(const SampleArgs& a, cudaStream_t st);  // returns the kernels launched
 
 // selection: the P smallest (value, index) pairs per query of `n` values per query.
 // counts: optional per-query number of valid values (the rest count as +inf).
