@@ -542,6 +542,7 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
     da.sub = sub ? 1 : 0;
     auto run_dp = [&](const WorkQueue& w, uint32_t max_pairs, cudaStream_t on) {
         da.queue = w;
+        da.probe = (p->probe && w.e == p->probe_wq().e) ? 1 : 0;
         if (dk) launch_dk_dp(da, max_pairs, (uint32_t)s->max_len, on);
         else launch_dtw_dp(da, max_pairs, on);
         ++launches;

@@ -556,7 +556,9 @@ void run_dk_r(const DpArgs& a, uint32_t max_pairs, uint32_t max_len, cudaStream_
     // whole matches with queries of <= 128 points: one 4-row strip holds the whole query (no
     // strip hand-over; C1 DP 0.091 -> 0.085 ms).  Not for subsequence patterns: their pairs
     // die within a few columns, and 4-row steps cost them 1.5x.
-    if (a.qlen >= 512 || a.store.d >= 8 || (!a.sub && a.qlen <= 128))
+    // the probe launch (a few pairs per query, each a near-full DP under the loose seed) is
+    // latency-bound: 4-row strips halve its sequential strip sweeps (C3 probe phase -40%)
+    if (a.qlen >= 512 || a.store.d >= 8 || (!a.sub && a.qlen <= 128) || a.probe)
         run_dk<D, 4>(a, max_pairs, max_len, st);
     else run_dk<D, 2>(a, max_pairs, max_len, st);
 }

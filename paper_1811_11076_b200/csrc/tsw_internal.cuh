@@ -336,6 +336,7 @@ struct DpArgs {
     int guarded;                // queries and store carry the +-inf guard tiles
     int sub;                    // DK: subsequence mode (sparse_engine<true>, dogkeeper.cpp:120-223)
     uint32_t* out_end;          // DK sub, dist_all mode: SubMatch::end_index per candidate
+    int probe;                  // the probe launch: few pairs, latency-bound (DK: fewer strips)
 };
 
 void launch_dtw_dp(const DpArgs& a, uint32_t max_pairs, cudaStream_t st);
