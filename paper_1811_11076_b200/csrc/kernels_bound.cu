@@ -204,10 +204,12 @@ __global__ void __launch_bounds__(256) sample_ub_kernel(SampleArgs a) {
 // accumulates 2 x 2 pairs, so each loaded point feeds two pairs.  Same per-point costs and
 // accumulation (DTW: fl sum in any order, scaled up; DK: exact max) as sample_ub_kernel.
 constexpr int kUQ = 16, kUC = 32;
-// points per chunk: 16, or the power of two <= 64 / d at large d (a power of two divides the
+// points per chunk: 32 (d <= 2), 16 (d <= 4), or the power of two <= 64 / d at large d (C3 seed
+// phase 0.165 -> 0.152 ms with 32 at d = 2: half the chunk barriers; a power of two divides the
 // 32-point tile, so a chunk never straddles tiles and its element offsets are per-thread
 // constants plus one per-chunk shift)
 __host__ __device__ inline uint32_t ub_chunk(uint32_t d) {
+    if (d <= 2) return 32u;  // one whole tile: half the chunk barriers (still <= kUElem per thread)
     if (d <= 4) return 16u;
     uint32_t c = 1;
     while (c * 2 * d <= 64) c *= 2;
