@@ -93,7 +93,7 @@ struct Strip {
 // One skewed step k: lane l computes cells (R + RPL*l + q, cstart + k - l), q < RPL.
 // tiled element offset of column j (j may be negative or past the end: guard tiles)
 __device__ __forceinline__ int toff_rt(int j, int stride) {
-    return (j >> 5) * (int)(kTile * stride) + (j & 31);
+    return j + (j >> 5) * (int)(kTile * stride - kTile);  // == (j >> 5) * 32 * stride + (j & 31)
 }
 
 template <int D>

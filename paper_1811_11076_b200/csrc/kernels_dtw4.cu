@@ -121,10 +121,13 @@ __device__ __forceinline__ void iter(Lane<G, D>& s, const double* __restrict__ s
     // cumulative bound of the cut, one value per lane: pfx is non-decreasing in the candidate
     // point, so the lane's smallest candidate index (largest window slot tt) gives a lower
     // bound of every slot's own term (abandoning on it is conservative)
-    double Rmin = 0.0;
+    // alive iff some cut cell has nv <= RU(T * M - Rmin): nv > that implies nv + Rmin > T * M in
+    // real arithmetic (one subtraction per lane instead of an add per slot)
+    double Tlim = 0.0;
     if (CHECK) {
         constexpr int TTMAX = (2 * G - 1) - ((2 * G - 1 + RPAR) >> 1);
-        Rmin = (double)pfx[min(max(tjb - TTMAX, 0), L - 1) >> plog];
+        const double Rmin = (double)pfx[min(max(tjb - TTMAX, 0), L - 1) >> plog];
+        Tlim = __dsub_ru(__dmul_ru(T, margin), Rmin);
     }
 #pragma unroll
     for (int half = 0; half < 2; ++half) {
@@ -147,10 +150,7 @@ __device__ __forceinline__ void iter(Lane<G, D>& s, const double* __restrict__ s
             double nv = dadd(c, dmin(dmin(left, down), s.v[e]));
             if (e == FS) nv = gl == 0 ? kInf : nv;  // offset -r-1
             s.v[e] = nv;
-            if (CHECK) {
-                const double Tm = __dmul_ru(T, margin);
-                alive |= ((okm >> e) & 1u) && dadd(nv, Rmin) <= Tm;
-            }
+            if (CHECK) alive |= ((okm >> e) & 1u) && nv <= Tlim;
         }
     }
 }
