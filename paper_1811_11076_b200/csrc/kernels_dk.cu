@@ -174,6 +174,7 @@ __device__ __forceinline__ void dk_step(const Strip& S, int k, int lane, int n,
     load_pt<D>(tn, t, j + 1, stride);
     const double* tp = t + toff_rt(j, stride);  // runtime-d path
     bool lv = false;
+    const int tsq_hi = __double2hiint(Tsq);
     double vlast = kInf;
 #pragma unroll
     for (int q = 0; q < RPL; ++q) {
@@ -187,7 +188,10 @@ __device__ __forceinline__ void dk_step(const Strip& S, int k, int lane, int n,
         dg = left[q];           // next row's diagonal: this row at column j-1
         left[q] = v;
         up = v;                 // next row's up: this row at column j
-        if (LIVE) lv |= v <= Tsq;
+        // liveness on the high words (ALU instead of the FP64 pipe): for non-negative doubles
+        // hi(v) <= hi(Tsq) holds for every v <= Tsq, so the live set is a superset and a cut is
+        // only ever taken later (cell values are never altered)
+        if (LIVE) lv |= __double2hiint(v) <= tsq_hi;
         if (SUB) vlast = q == sf.fq ? v : vlast;
     }
     if (SUB && !S.write_bnd && lane == sf.fl && vlast < sf.bsq) {
