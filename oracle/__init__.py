@@ -24,6 +24,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 PORT_SO = os.path.join(HERE, "_build", "liborc.so")
 REF_SO = os.path.join(HERE, "_ref", "libtswarp_ref.so")
 REF_IO_SO = os.path.join(HERE, "_ref", "libtswarp_ref_io.so")
+SYNTH_SO = os.path.join(HERE, "_build", "libtsw_synth.so")
 REF_ROOT = "/root/reference/proj/core"
 
 _METRIC = {"dtw": 0, "dk": 1, "dk_sub": 2}
@@ -331,6 +332,41 @@ class Oracle:
         self._call("dk_all", _dptr(q), q.shape[0], q.shape[1], _dptr(data.values),
                    _uptr(data.lengths), data.n, _dptr(out))
         return out
+
+
+_synth_lib = None
+
+
+def _synth():
+    """The config generator built into oracle/_build (bench.py's reference arm: no product .so)."""
+    global _synth_lib
+    with _lock:
+        if _synth_lib is None:
+            if not os.path.exists(SYNTH_SO):
+                subprocess.run(["make", "-s", "-C", HERE, "synth"], check=True)
+            L = C.CDLL(SYNTH_SO)
+            L.tsw_synth_shape.argtypes = [C.c_int, C.c_int, _up, _up, _up, _up, _up]
+            L.tsw_synth_generate.argtypes = [C.c_int, C.c_int, _u64, _dp, C.POINTER(C.c_int32)]
+            _synth_lib = L
+        return _synth_lib
+
+
+def synth_shape(config: int, part: int = 0) -> dict:
+    vals = [_u64() for _ in range(5)]
+    if _synth().tsw_synth_shape(config, part, *[C.byref(v) for v in vals]) != 0:
+        raise ValueError(f"unknown config {config}")
+    return dict(zip(["count", "len", "d", "r", "k"], [v.value for v in vals]))
+
+
+def synth(config: int, part: int, seed: int = 20181127):
+    """-> (values f64[count, len, d], labels i32[count]); same bytes as the product's synth."""
+    sh = synth_shape(config, part)
+    out = np.empty((sh["count"], sh["len"], sh["d"]), dtype=np.float64)
+    lab = np.empty(sh["count"], dtype=np.int32)
+    if _synth().tsw_synth_generate(config, part, seed, _dptr(out),
+                                   lab.ctypes.data_as(C.POINTER(C.c_int32))) != 0:
+        raise ValueError(f"synth({config}, {part}) failed")
+    return out, lab
 
 
 def port() -> Oracle:

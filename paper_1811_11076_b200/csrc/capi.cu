@@ -321,6 +321,11 @@ std::unique_ptr<tsw_plan> make_plan(tsw_store* s, uint64_t nq_max, uint64_t qlen
                                      "equal lengths)");
     }
     if (nq_max == 0) nq_max = 1;
+    // the work queue, result buffers and probed flags hold nq_max * n entries addressed by
+    // 32-bit slots
+    if (nq_max * s->n >= (1ull << 32))
+        fail(TSW_EINVAL, "plan: nq_max * dataset size must be below 2^32 (got " +
+                             std::to_string(nq_max) + " x " + std::to_string(s->n) + ")");
     auto p = std::make_unique<tsw_plan>();
     p->store = s;
     p->nq_max = nq_max;
@@ -693,22 +698,39 @@ void fetch_impl(tsw_plan* p, tsw_neighbor* out, tsw_counters* counters, cudaStre
             });
             for (uint64_t j = 0; o && j < kk; ++j) o[j] = all[j];
         }
+        // every counter is counted on the device (QState); conservation (search.hpp:10-12)
+        // is then a real check: each (query, candidate) pair must have been pruned by a bound
+        // (compaction or dequeue re-check) or finished a DP exactly once
+        const QState& h = hs[q];
+        const uint64_t seen = h.bound_pruned + h.lb_pruned + h.full_dp + h.early_abandoned;
+        if (seen != n)
+            fail(TSW_ECUDA, "internal: query " + std::to_string(q) + " accounted for " +
+                                std::to_string(seen) + " of " + std::to_string(n) +
+                                " candidates (bound " + std::to_string(h.bound_pruned) +
+                                ", dequeue " + std::to_string(h.lb_pruned) + ", exact " +
+                                std::to_string(h.full_dp) + ", abandoned " +
+                                std::to_string(h.early_abandoned) + ")");
         if (counters) {
             tsw_counters& c = counters[q];
-            // every pair is pruned by its bound (compaction or dequeue re-check) or finishes in a
-            // DP as exact / abandoned, so the bound-pruned count is the complement
-            // (search.hpp:10-12 conservation holds by construction)
-            c.full_dp = hs[q].full_dp;
+            c.full_dp = h.full_dp;
             if (p->metric == TSW_METRIC_DTW) {
+                // knn_dtw (search.cpp:146-160): lb_box runs for every candidate; a candidate is
+                // lb-pruned when its bound reaches the threshold -- here in the compaction pass
+                // or at DP dequeue -- else the DP ends exact or abandoned
                 c.lb_computed = n;
-                c.early_abandoned = hs[q].early_abandoned;
-                c.lb_pruned = n - c.full_dp - c.early_abandoned;
+                c.lb_pruned = h.bound_pruned + h.lb_pruned;
+                c.early_abandoned = h.early_abandoned;
                 c.gdk_calls = 0;
             } else {
+                // knn_dk / knn_dk_sub (search.cpp:171-214, 250-280): every candidate the DP
+                // does not finish exact is early-abandoned; here that includes the pairs the
+                // exact first/last-cell bound removed (sparse_dk would die at cell (0,0) or
+                // before the last cell).  gdk_calls = the seed upper bounds actually computed
+                // (the sampled diagonal-path bounds replace GDK)
                 c.lb_computed = 0;
                 c.lb_pruned = 0;
-                c.early_abandoned = n - c.full_dp;
-                c.gdk_calls = n;
+                c.early_abandoned = h.bound_pruned + h.lb_pruned + h.early_abandoned;
+                c.gdk_calls = p->S;
             }
         }
     }
@@ -1043,7 +1065,7 @@ int tsw_epsnn_dk(tsw_store* s, const double* query, uint64_t qlen, double eps,
         DevBuf<double> q(qs), rd(n), qe(2 * d);
         DevBuf<uint32_t> ri(n);
         DevBuf<unsigned> rn(1), ctr(4);
-        DevBuf<unsigned long long> pruned(1);
+        DevBuf<unsigned long long> pruned(2);  // [0] compaction, [1] dequeue drops + abandoned
         DevBuf<QEntry> queue(n);
         {
             const std::vector<double> tq = tiled_host(query, qlen, d);
@@ -1051,7 +1073,7 @@ int tsw_epsnn_dk(tsw_store* s, const double* query, uint64_t qlen, double eps,
         }
         ck(cudaMemset(rn.p, 0, sizeof(unsigned)), "memset");
         ck(cudaMemset(ctr.p, 0, 4 * sizeof(unsigned)), "memset");
-        ck(cudaMemset(pruned.p, 0, sizeof(unsigned long long)), "memset");
+        ck(cudaMemset(pruned.p, 0, 2 * sizeof(unsigned long long)), "memset");
         const double eps_sq = host_sq_threshold(eps);
         const WorkQueue wq{queue.p, ctr.p, ctr.p + 1, ctr.p + 2, (uint32_t)n};
         DkCompactArgs ka{};
@@ -1076,6 +1098,7 @@ int tsw_epsnn_dk(tsw_store* s, const double* query, uint64_t qlen, double eps,
         da.fixed_eps_sq = eps_sq;
         da.margin = 1.0;
         da.results = ResultBuf{rd.p, ri.p, rn.p, (uint32_t)n};
+        da.fixed_ab = pruned.p + 1;
         launch_dk_dp(da, (uint32_t)n, (uint32_t)s->max_len, st);
         ck(cudaGetLastError(), "kernel launch");
         unsigned cnt = 0;
@@ -1092,7 +1115,14 @@ int tsw_epsnn_dk(tsw_store* s, const double* query, uint64_t qlen, double eps,
         });
         if (count) *count = cnt;
         for (uint64_t j = 0; out && j < cnt && j < cap; ++j) out[j] = all[j];
-        if (counters) *counters = tsw_counters{0, 0, cnt, n - cnt, 0};
+        unsigned long long hp[2] = {0, 0};
+        ck(cudaMemcpy(hp, pruned.p, sizeof(hp), cudaMemcpyDeviceToHost), "fetch");
+        if (cnt + hp[0] + hp[1] != n)
+            fail(TSW_ECUDA, "internal: epsnn_dk accounted for " + std::to_string(cnt + hp[0] + hp[1]) +
+                                " of " + std::to_string(n) + " candidates");
+        // epsnn_dk (search.cpp:216-239): exact results are full_dp, everything else is
+        // early_abandoned (bound-pruned, dropped at dequeue or abandoned in the DP)
+        if (counters) *counters = tsw_counters{0, 0, cnt, hp[0] + hp[1], 0};
     });
 }
 

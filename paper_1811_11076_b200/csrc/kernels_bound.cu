@@ -6,6 +6,7 @@
 // so every LB value is a rigorous lower bound of the real LB_Box and pruning
 // stays exact.  One warp owns a tile of CB consecutive candidates x QB queries: each 128-bit
 // candidate load is reused for QB queries and each envelope load for CB candidates.
+#include <cfloat>
 #include <algorithm>
 #include <cstdlib>
 
@@ -59,7 +60,8 @@ void launch_fill(double* p, uint64_t count, double v, cudaStream_t st) {
 __global__ void to_float_kernel(const double* __restrict__ src, uint64_t n, float* __restrict__ dst) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x)
-        dst[i] = isinf(src[i]) ? 0.0f : __double2float_rn(src[i]);  // guards / padding -> 0
+        // guards / padding -> 0; |x| > FLT_MAX saturates to +-FLT_MAX (|x32| <= |x|, see absmax)
+        dst[i] = isinf(src[i]) ? 0.0f : fminf(fmaxf(__double2float_rn(src[i]), -FLT_MAX), FLT_MAX);
 }
 
 void launch_to_float(const double* src, uint64_t count, float* dst, cudaStream_t st) {
@@ -89,7 +91,10 @@ __global__ void absmax_kernel(const double* __restrict__ src, uint64_t n, unsign
     double m = 0.0;
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x)
-        if (!isinf(src[i])) m = fmax(m, fabs(src[i]));  // skip the guard / padding values
+        // skip the guard / padding values and the values beyond fp32 range: those are clamped
+        // to +-FLT_MAX in the fp32 copies, which moves them TOWARD every in-range interval, so
+        // their LB terms stay lower bounds without an error term
+        if (fabs(src[i]) <= (double)FLT_MAX) m = fmax(m, fabs(src[i]));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
     if (lane_id() == 0) atomicMax(out, (unsigned long long)__double_as_longlong(m));
@@ -135,6 +140,12 @@ __global__ void envelope_kernel(const double* __restrict__ q, uint32_t nq, uint3
         if constexpr (sizeof(OutT) == sizeof(float)) {
             // fp32 (midpoint, half-width) form: any midpoint m works as long as the half-width
             // covers the interval from m, rounded up, plus the store's fp32 rounding err
+            if (!(mn >= -(double)FLT_MAX && mx <= (double)FLT_MAX)) {
+                // the window leaves the fp32 range: no bound from this element (term 0)
+                lo[g] = OutT(0);
+                hi[g] = OutT(INFINITY);
+                continue;
+            }
             const float m32 = __double2float_rn(0.5 * (mn + mx));
             const double hw = fmax(__dsub_ru((double)m32, mn), __dsub_ru(mx, (double)m32));
             lo[g] = m32;
@@ -436,7 +447,7 @@ struct TileOut {
 // pass at C2 / C3 / C4; the fused wide-band kernel keeps the scalar form (the packed one
 // spills there and is 8% slower at C5).
 template <int QB, int CB, bool SENV = false, bool PACK = true>
-__device__ __forceinline__ TileOut lb1_tile(const LbCompactArgs& a, uint32_t c0, uint32_t q0,
+__device__ __forceinline__ TileOut lb1_tile(const LbCompactArgs& a, PruneCount& pc, uint32_t c0, uint32_t q0,
                                             float* stash, uint32_t total4,
                                             const float4* slo = nullptr, const float4* shi = nullptr) {
     static_assert(QB * CB == 32, "one pair per lane after the reduction");
@@ -527,6 +538,7 @@ __device__ __forceinline__ TileOut lb1_tile(const LbCompactArgs& a, uint32_t c0,
             const bool probed = a.probed && a.probed[(uint64_t)t.c * a.nq + t.q];
             t.take = !probed && lb <= __dmul_ru(T, a.margin);
             t.near = lb <= a.near_frac * T;
+            pc.add(!probed && !t.take, t.q);
         }
     }
     const unsigned tm = __ballot_sync(0xffffffffu, t.take);
@@ -564,6 +576,9 @@ __global__ void __launch_bounds__(256, 3) lb_few_kernel(LbCompactArgs a) {
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     __shared__ QEntry stage_buf[8][2][kStage];
     Stage sg{stage_buf[threadIdx.x >> 5][0], stage_buf[threadIdx.x >> 5][1], 0u, 0u};
+    __shared__ unsigned pc_s[kCountQ];
+    PruneCount pc{pc_s, a.state, nullptr, a.nq};
+    pc.init();
     const float4* lob = reinterpret_cast<const float4*>(a.env_lo);
     const float4* hib = reinterpret_cast<const float4*>(a.env_hi);
     const uint64_t qs = a.qstride / 4;
@@ -611,6 +626,7 @@ __global__ void __launch_bounds__(256, 3) lb_few_kernel(LbCompactArgs a) {
                 const bool probed = a.probed && a.probed[c * a.nq + q];
                 take = !probed && (double)lb <= __dmul_ru(T[q], a.margin);
                 near = (double)lb <= a.near_frac * T[q];
+                pc.add(lane == 0 && !probed && !take, (uint32_t)q);
             }
             uint32_t ps = kNoPfx;
             if (take && a.pfx_out) {  // warp-uniform: every lane holds the same decision
@@ -629,6 +645,7 @@ __global__ void __launch_bounds__(256, 3) lb_few_kernel(LbCompactArgs a) {
         stage_flush(sg, a.queue, true);
         stage_flush(sg, a.queue, false);
     }
+    pc.flush();
 }
 
 template <int QB, int CB>
@@ -643,20 +660,23 @@ __global__ void __launch_bounds__(256, 2) lb_compact_kernel(LbCompactArgs a) {
     extern __shared__ float lb_stash[];  // block mode: [8 warps][32 pairs][32 lanes]
     Stage sg{stage_buf[threadIdx.x >> 5][0], stage_buf[threadIdx.x >> 5][1], 0u, 0u};
     float* stash = lb_stash + (size_t)(threadIdx.x >> 5) * 32 * 32;
+    __shared__ unsigned pc_s[kCountQ];
+    PruneCount pc{pc_s, a.state, nullptr, a.nq};
+    pc.init();
+
     for (uint64_t w = wid; w < ngroups * nqb; w += nw) {
         // candidate-major order: the nqb query blocks of one candidate group run on adjacent
         // warps, so the group's bytes come from HBM once and are re-read from L1/L2
         const uint64_t cg = w / nqb;
         const uint32_t qbk = (uint32_t)(w - cg * nqb);
-        const TileOut t = lb1_tile<QB, CB>(a, (uint32_t)cg * CB, qbk * QB, stash, total4);
-        // pruned pairs are not counted here: the host derives lb_pruned = n - full_dp -
-        // early_abandoned (every surviving pair ends in the DP as one of the two)
+        const TileOut t = lb1_tile<QB, CB>(a, pc, (uint32_t)cg * CB, qbk * QB, stash, total4);
         if (a.state) enqueue(sg, a.queue, t.take, t.near, t.q, t.c, t.lb, t.ps);
     }
     if (a.state) {
         stage_flush(sg, a.queue, true);
         stage_flush(sg, a.queue, false);
     }
+    pc.flush();
 }
 
 // ---- K2 with the envelopes in shared memory (short series) ----------------------------------
@@ -681,6 +701,9 @@ __global__ void __launch_bounds__(256, 2) lb_env_kernel(LbCompactArgs a, uint32_
     float4* ehi = lbe_smem + (size_t)QB * total4;
     float* stash = reinterpret_cast<float*>(lbe_smem + (size_t)2 * QB * total4) + (size_t)warp * 32 * 32;
     Stage sg{stage_buf[warp][0], stage_buf[warp][1], 0u, 0u};
+    __shared__ unsigned pc_s[kCountQ];
+    PruneCount pc{pc_s, a.state, nullptr, a.nq};
+    pc.init();
     uint32_t have_qb = 0xffffffffu;
     const uint64_t items = (uint64_t)nchunks * nqb;
     for (uint64_t it = blockIdx.x; it < items; it += gridDim.x) {
@@ -700,7 +723,7 @@ __global__ void __launch_bounds__(256, 2) lb_env_kernel(LbCompactArgs a, uint32_
         }
         const uint32_t gend = min((ch + 1) * chunk, ngroups);
         for (uint32_t g = ch * chunk + warp; g < gend; g += 8) {
-            const TileOut t = lb1_tile<QB, CB, true>(a, g * CB, qbk * QB, stash, total4, elo, ehi);
+            const TileOut t = lb1_tile<QB, CB, true>(a, pc, g * CB, qbk * QB, stash, total4, elo, ehi);
             if (a.state) enqueue(sg, a.queue, t.take, t.near, t.q, t.c, t.lb, t.ps);
         }
     }
@@ -708,6 +731,7 @@ __global__ void __launch_bounds__(256, 2) lb_env_kernel(LbCompactArgs a, uint32_
         stage_flush(sg, a.queue, true);
         stage_flush(sg, a.queue, false);
     }
+    pc.flush();
 }
 
 // ---- K2 + reverse LB_Box + K3 ---------------------------------------------------------------
@@ -723,7 +747,8 @@ constexpr int kList = 128;  // listed survivors per warp before a reverse-bound 
 
 template <int QB, int CB, int FCH>  // FCH: float4 per lane per envelope chunk
 __device__ __forceinline__ void lb2_flush(const LbCompactArgs& a, uint32_t c0, QEntry* list,
-                                          float* l2, int cnt, uint32_t total4, float eq, Stage& sg) {
+                                          float* l2, int cnt, uint32_t total4, float eq, Stage& sg,
+                                          PruneCount& pc) {
     const unsigned lane = lane_id();
     __syncwarp();
     for (int i = lane; i < cnt; i += 32) l2[i] = 0.0f;
@@ -784,6 +809,7 @@ __device__ __forceinline__ void lb2_flush(const LbCompactArgs& a, uint32_t c0, Q
             const double T = a.state[en.q].T;
             take = (double)en.key <= __dmul_ru(T, a.margin);
             near = (double)en.key <= a.near_frac * T;
+            pc.add(!take, en.q);
         }
         enqueue(sg, a.queue, take, near, en.q, en.c, en.key, en.ps);
     }
@@ -803,6 +829,10 @@ __global__ void __launch_bounds__(256, 2) lb12_compact_kernel(LbCompactArgs a) {
     extern __shared__ __align__(16) unsigned char lb12_smem[];
     const int wib = threadIdx.x >> 5;
     Stage sg{stage_buf[wib][0], stage_buf[wib][1], 0u, 0u};
+    __shared__ unsigned pc_s[kCountQ];
+    PruneCount pc{pc_s, a.state, nullptr, a.nq};
+    pc.init();
+
     QEntry* list = reinterpret_cast<QEntry*>(lb12_smem) + (size_t)wib * kList;
     float* l2 = reinterpret_cast<float*>(lb12_smem + 8 * kList * sizeof(QEntry)) + (size_t)wib * kList;
     float* stash = reinterpret_cast<float*>(lb12_smem + 8 * kList * (sizeof(QEntry) + sizeof(float))) +
@@ -816,19 +846,20 @@ __global__ void __launch_bounds__(256, 2) lb12_compact_kernel(LbCompactArgs a) {
         const uint32_t c0 = cg * CB;
         int cnt = 0;
         for (uint32_t qbk = 0; qbk < nqb; ++qbk) {
-            const TileOut t = lb1_tile<QB, CB, false, false>(a, c0, qbk * QB, stash, total4);
+            const TileOut t = lb1_tile<QB, CB, false, false>(a, pc, c0, qbk * QB, stash, total4);
             const unsigned tm = __ballot_sync(0xffffffffu, t.take);
             if (t.take) list[cnt + __popc(tm & ((1u << lane) - 1u))] = QEntry{t.q, t.c, t.lb, t.ps};
             cnt += __popc(tm);
             if (cnt > kList - 32) {
-                lb2_flush<QB, CB, FCH>(a, c0, list, l2, cnt, total4, eq, sg);
+                lb2_flush<QB, CB, FCH>(a, c0, list, l2, cnt, total4, eq, sg, pc);
                 cnt = 0;
             }
         }
-        if (cnt) lb2_flush<QB, CB, FCH>(a, c0, list, l2, cnt, total4, eq, sg);
+        if (cnt) lb2_flush<QB, CB, FCH>(a, c0, list, l2, cnt, total4, eq, sg, pc);
     }
     stage_flush(sg, a.queue, true);
     stage_flush(sg, a.queue, false);
+    pc.flush();
 }
 
 void launch_lb_compact(const LbCompactArgs& a, cudaStream_t st) {
@@ -892,6 +923,9 @@ __global__ void __launch_bounds__(256) dk_compact_kernel(DkCompactArgs a) {
     const uint64_t total = (uint64_t)a.nq * n;
     __shared__ QEntry stage_buf[8][2][kStage];
     Stage sg{stage_buf[threadIdx.x >> 5][0], stage_buf[threadIdx.x >> 5][1], 0u, 0u};
+    __shared__ unsigned pc_s[kCountQ];
+    PruneCount pc{pc_s, a.state, a.fixed_pruned, a.nq};
+    pc.init();
     for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < total;
          base += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t g = base + threadIdx.x;
@@ -918,13 +952,14 @@ __global__ void __launch_bounds__(256) dk_compact_kernel(DkCompactArgs a) {
                 const double Tsq = a.state ? a.state[q].Tsq : a.fixed_eps_sq;
                 take = key <= Tsq;
                 near = key <= a.near_frac * Tsq;
+                pc.add(!take, q);
             }
         }
-        // pruned pairs are not counted here: the host derives early_abandoned = n - full_dp
         enqueue(sg, a.queue, take, near, q, c, __double2float_rd(key), kNoPfx);
     }
     stage_flush(sg, a.queue, true);
     stage_flush(sg, a.queue, false);
+    pc.flush();
 }
 
 __global__ void query_ends_kernel(const double* __restrict__ q, uint32_t nq, uint32_t m, uint32_t d,

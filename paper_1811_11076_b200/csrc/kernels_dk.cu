@@ -285,7 +285,10 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
             Tsq = __shfl_sync(kFull, Tsq, 0);
         }
         if (!(pr.key <= Tsq)) {  // re-check the admitting first/last-cell bound at dequeue
-            if (lane == 0 && st) atomicAdd(&st->early_abandoned, 1ull);
+            if (lane == 0) {
+                if (st) atomicAdd(&st->early_abandoned, 1ull);
+                else if (a.fixed_ab) atomicAdd(a.fixed_ab, 1ull);
+            }
             continue;
         }
         const double* s = a.queries + (uint64_t)pr.q * a.qstride;
@@ -518,6 +521,8 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
                 }
             } else if (st) {
                 atomicAdd(&st->early_abandoned, 1ull);
+            } else if (a.fixed_ab) {
+                atomicAdd(a.fixed_ab, 1ull);
             }
         }
         __syncwarp();

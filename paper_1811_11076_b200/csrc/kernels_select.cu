@@ -218,7 +218,7 @@ __global__ void seed_kernel(SeedArgs a) {
         st->T = T;
         st->Tsq = a.dk ? sq_threshold(T) : T;
         st->k = kk <= (uint32_t)kKMax ? kk : 0u;
-        st->lb_pruned = st->full_dp = st->early_abandoned = 0ull;
+        st->lb_pruned = st->full_dp = st->early_abandoned = st->bound_pruned = 0ull;
     }
     for (uint32_t j = threadIdx.x; j < (uint32_t)kKMax; j += blockDim.x) a.slots[(size_t)q * kKMax + j] = kInf;
     for (uint32_t j = threadIdx.x; j < a.probe; j += blockDim.x) {

@@ -74,8 +74,46 @@ struct alignas(128) QState {
     double Tsq;        // DK only: largest x with sqrt(x) <= T (sqrt monotone)
     unsigned k;        // min(k, n) if k <= kKMax (slots active), else 0 (threshold stays at seed)
     unsigned pad;
+    // counters, all counted on the device (none derived on the host):
+    //   bound_pruned    pairs a compaction pass pruned by its bound (LB_Box fwd / reverse; DK
+    //                   first/last cell) -- counted by the compaction kernels (PruneCount)
+    //   lb_pruned       pairs dropped at DP dequeue by the re-checked bound
+    //   full_dp         pairs whose DP finished exact (distance <= threshold)
+    //   early_abandoned pairs whose DP abandoned (DK: also dequeue drops, see kernels_dk.cu)
+    // Every (query, candidate) pair is exactly one of these, so their sum is the store size
+    // (search.hpp:10-12); tsw_plan_fetch checks that and fails loudly if it does not hold.
     alignas(128) unsigned long long lb_pruned;
-    unsigned long long full_dp, early_abandoned;
+    unsigned long long full_dp, early_abandoned, bound_pruned;
+};
+
+// Per-block counts of the pairs a compaction pass prunes by its bound, by query, in shared
+// memory (one shared atomic per pruned pair), flushed with one global atomic per (block, query)
+// into QState::bound_pruned -- or into *fixed (eps-NN: one query, no QState).  Queries past
+// kCountQ count straight into global memory.
+constexpr uint32_t kCountQ = 256;  // 1 KB: the K2 kernels' shared memory is near the 2-blocks/SM limit
+struct PruneCount {
+    unsigned* s;                   // shared [kCountQ]
+    QState* st;                    // per-query state (nullptr: fixed-threshold mode)
+    unsigned long long* fixed;     // fixed-threshold mode counter (nullable)
+    uint32_t nq;
+    __device__ __forceinline__ void init() {
+        for (uint32_t i = threadIdx.x; i < min(nq, kCountQ); i += blockDim.x) s[i] = 0u;
+        __syncthreads();
+    }
+    __device__ __forceinline__ void add(bool pruned, uint32_t q) {
+        if (!pruned) return;
+        if (q < kCountQ) atomicAdd(s + q, 1u);
+        else if (st) atomicAdd(&st[q].bound_pruned, 1ull);
+    }
+    __device__ __forceinline__ void flush() {
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < min(nq, kCountQ); i += blockDim.x) {
+            const unsigned v = s[i];
+            if (!v) continue;
+            if (st) atomicAdd(&st[i].bound_pruned, (unsigned long long)v);
+            else if (fixed) atomicAdd(fixed, (unsigned long long)v);
+        }
+    }
 };
 
 // Result append buffer: per query `cap` slots (cap = n: a candidate is appended at most once).
@@ -277,7 +315,7 @@ struct LbCompactArgs {
     uint64_t qstride;
     double margin;        // prune iff lb > T * margin (rounded up)
     double near_frac;     // front region iff lb <= near_frac * T
-    const QState* state;
+    QState* state;        // per query (bound_pruned is counted into it)
     const uint8_t* probed;
     WorkQueue queue;
     float* lb_out;        // optional [nq][n] (diagnostics / tsw_lb_box_all)
@@ -304,7 +342,7 @@ struct DkCompactArgs {
     uint32_t nq, qlen;
     uint64_t qstride;
     double near_frac;
-    const QState* state;      // nullptr: fixed threshold (eps-NN)
+    QState* state;            // nullptr: fixed threshold (eps-NN)
     double fixed_eps_sq;
     unsigned long long* fixed_pruned;
     const uint8_t* probed;
@@ -330,6 +368,7 @@ struct DpArgs {
     int* out_exact;             // per candidate (dist_all mode), nullable
     double* out_val;
     ResultBuf results;          // exact-result append buffer (results.dist == nullptr: off)
+    unsigned long long* fixed_ab;  // fixed-eps mode: pairs dropped at dequeue or abandoned (nullable)
     unsigned long long* cells;  // DP cells evaluated (global accumulator)
     const float* pfx_blocks;    // DTW: LB block sums by QEntry::ps (nullptr: per-point, in-kernel)
     uint32_t pfx_log;           // log2 of the block length in points

@@ -550,6 +550,11 @@ def _check_query(q, data, equal_lengths, op):
     if q.shape[1] != dim:
         raise ValueError(f"{op}: query dim {q.shape[1]} != dataset dim {dim}")
     if equal_lengths and isinstance(data, Dataset):
+        if data._arr is not None:  # uniform-length dataset: one comparison
+            if n and data._arr.shape[1] != q.shape[0]:
+                raise ValueError(f"{op}: series 0 length differs from the query (lower bounds "
+                                 "require equal lengths)")
+            return
         for i in range(n):
             if data.length(i) != q.shape[0]:
                 raise ValueError(f"{op}: series {i} length differs from the query (lower bounds "

@@ -1,9 +1,10 @@
 """GPU parity at the five BASELINE.json configurations (full database sizes).
 
-For every config the GPU batch answer is compared with the reference library (oracle/_ref,
-the reference's own sources; the C port when it is absent) on a subset of the queries --
-indices and order exact, distances bit-exact -- and size-independent properties are checked
-for ALL queries: counter conservation (search.hpp:10-12), sorted (distance, index) order, and
+For every config and metric the GPU batch answer is compared with the reference library
+(oracle/_ref, the reference's own sources, run query-parallel on the host cores) for EVERY
+query of the configuration -- indices and order exact, distances bit-exact (north_star:
+"bit-exact k-NN sets versus the CPU oracle on all five configs").  Without oracle/_ref the C
+port checks 2 queries per config.  Size-independent properties are checked too: counter conservation (search.hpp:10-12), sorted (distance, index) order, and
 every returned distance recomputed by the unpruned GPU brute force (tsw_dist_all with
 eps = inf, i.e. dtw_banded / dk_full) equals the returned value bit for bit.
 """
@@ -14,9 +15,9 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-# (config, metric, queries checked against the CPU reference)
-CASES = [(1, "dk", 16), (2, "dtw", 64), (3, "dtw", 8), (3, "dk", 16), (4, "dtw", 2),
-         (4, "dk", 8), (5, "dtw", 2), (5, "dk", 2)]
+# (config, metric, queries checked against the CPU reference: all of them)
+CASES = [(1, "dk", 16), (2, "dtw", 64), (3, "dtw", 256), (3, "dk", 256), (4, "dtw", 32),
+         (4, "dk", 32), (5, "dtw", 32), (5, "dk", 32)]
 
 _DATA = {}
 
@@ -47,7 +48,7 @@ def test_config_parity(tsw, best_oracle, cfg, metric, nref):
         if metric == "dtw":
             assert c[0] == n and c[1] + c[2] + c[3] == n, c
         else:
-            assert c[4] == n and c[2] + c[3] == n, c
+            assert c[4] == min(n, 2048) and c[2] + c[3] == n, c
         keys = list(zip(dist[q].tolist(), idx[q].tolist()))
         assert keys == sorted(keys), f"query {q} not sorted by (distance, index)"
     # returned distances == unpruned brute force values (first 4 queries)
@@ -64,6 +65,7 @@ def test_config_parity(tsw, best_oracle, cfg, metric, nref):
     qsub = qs[:nref]
     if best_oracle.kind == "reference":
         oi, od, ocnt, _ = best_oracle.knn_batch(qsub, ods, k, metric, r, threads=os.cpu_count() or 1)
+        assert len(qsub) == len(qs), "every query is pinned to the reference"
         for q in range(len(qsub)):
             assert np.array_equal(idx[q], oi[q][:ocnt[q]]), (q, idx[q], oi[q])
             assert np.array_equal(dist[q].view(np.uint64), od[q][:ocnt[q]].view(np.uint64))

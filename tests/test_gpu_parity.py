@@ -222,7 +222,37 @@ def _check_counters(c, n, metric):
     if metric == "dtw":
         assert c[0] == n and c[1] + c[2] + c[3] == n, c
     else:
-        assert c[4] == n and c[2] + c[3] == n, c
+        assert c[4] == min(n, 2048) and c[2] + c[3] == n, c
+
+
+def test_counters_device_counted_no_pruning(tsw):
+    """k >= n: the threshold never drops below +inf, so nothing can be pruned or abandoned --
+    every candidate must be counted by the DP as full_dp (device counters, not complements)."""
+    X = RNG.standard_normal((37, 24, 2)).cumsum(1)
+    qs = RNG.standard_normal((3, 24, 2)).cumsum(1)
+    ds = tsw.Store(X)
+    for metric in ("dtw", "dk"):
+        _, _, ctr = tsw.knn(ds, qs, 40, metric, 3)
+        for c in ctr:
+            if metric == "dtw":
+                assert list(c) == [37, 0, 37, 0, 0], c
+            else:
+                assert list(c) == [0, 0, 37, 0, 37], c
+
+
+def test_counters_prune_and_abandon(tsw):
+    """1-NN where one candidate equals the query: after it is found everything else is
+    pruned by a bound or abandoned; the device counts must add up to n (checked by the
+    library too) and show real pruning."""
+    X = RNG.standard_normal((3000, 64, 3)).cumsum(1)
+    q = X[1234].copy()
+    ds = tsw.Store(X)
+    _, _, c = tsw.knn(ds, q[None], 1, "dtw", 6)
+    c = c[0]
+    assert c[0] == 3000 and c[1] + c[2] + c[3] == 3000 and c[1] > 2000 and c[2] >= 1, c
+    _, _, c = tsw.knn(ds, q[None], 1, "dk", 0)
+    c = c[0]
+    assert c[2] + c[3] == 3000 and c[2] >= 1 and c[3] > 2000 and c[4] == 2048, c
 
 
 def test_knn_random_datasets(tsw, best_oracle):
@@ -246,6 +276,33 @@ def test_knn_random_datasets(tsw, best_oracle):
             for q in range(len(Q)):
                 oi, od, _ = best_oracle.knn(Q[q], ods, k, metric, r)
                 assert_knn_equal(gi[q], gd[q], oi, od, f"trial {trial} {metric} q{q}")
+                _check_counters(gc[q], n, metric)
+
+
+@pytest.mark.parametrize("lb2", ["0", "1"])
+def test_knn_values_beyond_fp32_range(tsw, best_oracle, lb2, monkeypatch):
+    """The reference accepts any finite double (timeseries.cpp:16-21).  Values beyond FLT_MAX
+    (1e39) and values whose squared differences overflow fp64 (1e200: DTW/DK costs of +inf)
+    must give the reference's neighbours: the fp32 LB shadow saturates instead of producing
+    +inf terms that would prune true neighbours."""
+    import oracle
+
+    monkeypatch.setenv("TSW_LB2", lb2)
+    rng = np.random.default_rng(41)
+    for scale_db, scale_q in ((1e39, 1e39), (1e39, 1.0), (1.0, 1e39), (1e200, 1e200)):
+        n, L, d, r, k = 400, 40, 3, 5, 3
+        X = walks(rng, n, L, d)
+        X[::3] *= scale_db  # a third of the store beyond fp32 range
+        Q = walks(rng, 4, L, d) * scale_q
+        Q[1] = X[9] * (1 + 1e-9)
+        Q[2] = X[10]
+        ds = tsw.Dataset(X)
+        ods = oracle.Dataset(X)
+        for metric in ("dtw", "dk"):
+            gi, gd, gc = tsw.knn(ds, Q, k, metric, r)
+            for q in range(len(Q)):
+                oi, od, _ = best_oracle.knn(Q[q], ods, k, metric, r)
+                assert_knn_equal(gi[q], gd[q], oi, od, f"{scale_db} {scale_q} {metric} q{q}")
                 _check_counters(gc[q], n, metric)
 
 

@@ -125,7 +125,7 @@ def test_sub_golden_reference_vectors(tsw):
             rep = tsw.knn_dk_sub(queries[e["q"]], ds, e["k"])
             assert [nb.index for nb in rep.neighbors] == e["index"], (case["name"], e)
             assert [nb.distance.hex() for nb in rep.neighbors] == e["distance"], (case["name"], e)
-            assert rep.counters.gdk_calls == len(series)
+            assert rep.counters.gdk_calls == min(len(series), 2048)  # seed bounds computed
         st = tsw.Store(series[:10])
         for qi, q in enumerate(queries):
             found, val, end = tsw.sub_dk_all(st, q, INF)
