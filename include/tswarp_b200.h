@@ -45,6 +45,13 @@ typedef struct tsw_neighbor {
     double distance;
 } tsw_neighbor;
 
+/* Index of an unused tail entry of a query's neighbour row: the reference can return fewer
+ * than min(k, n) neighbours -- knn_dtw prunes on `lb >= eps` with eps = +inf while its KBest
+ * is not full, so candidates whose serially summed LB_Box overflows to +inf never enter it
+ * (search.cpp:147; only for values near the fp64 range limit).  Such a row ends with entries
+ * {TSW_NO_NEIGHBOR, +inf}; the C++ and Python layers drop them. */
+#define TSW_NO_NEIGHBOR UINT64_MAX
+
 /* Mirrors tswarp::SearchCounters (search.hpp:13-19).  Conservation (search.hpp:10-12):
  * DTW: lb_pruned + early_abandoned + full_dp == n;  DK: early_abandoned + full_dp == n. */
 typedef struct tsw_counters {
@@ -99,7 +106,8 @@ int tsw_store_info(const tsw_store* store, uint64_t* n, uint64_t* d, uint64_t* m
  *   tswarp::knn_dk_sub(query, data, k, threads)                (search.hpp:75-76, search.cpp:250-280)
  *     metric TSW_METRIC_DK_SUB: each candidate's distance is its best subsequence match
  * queries: nq equal-length row-major series of qlen points (d = the store's d).
- * out    : nq x min(k, n) neighbours, each query's sorted by (distance, index).
+ * out    : nq x min(k, n) neighbours, each query's sorted by (distance, index); a row with fewer
+ *          neighbours (see TSW_NO_NEIGHBOR) is padded with {TSW_NO_NEIGHBOR, +inf}.
  * counters: nq entries or NULL.
  * Errors: k == 0 -> TSW_EINVAL ("knn_dtw: k must be positive"); DTW with any series length
  * != qlen -> TSW_EINVAL (check_query, search.cpp:99-115); non-finite query -> TSW_EVALIDATION.

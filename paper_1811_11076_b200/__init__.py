@@ -6,7 +6,7 @@ re-built as hand-written sm_100a CUDA kernels behind a C ABI (include/tswarp_b20
 C++ drop-in header (include/tswarp_b200.hpp) and this Python mirror (tswarp.py).
 """
 from .tswarp import (  # noqa: F401
-    Dataset, IoError, Neighbor, ParseError, Plan, SearchCounters, SearchReport, Store, SubMatch,
+    NO_NEIGHBOR, Dataset, IoError, Neighbor, ParseError, Plan, SearchCounters, SearchReport, Store, SubMatch,
     TswError, ValidationError, device_count, dist_all, envelope, epsnn_dk, fp64_peak, knn, knn_dk,
     load_dataset, loo_accuracy, pruning_power, save_dataset, speedup,
     knn_dk_sub, knn_dtw, l2_flush, last_transfer_bytes, lb_box_all, lib, sparse_dk_sub,
@@ -14,7 +14,7 @@ from .tswarp import (  # noqa: F401
 )
 
 __all__ = [
-    "Dataset", "IoError", "Neighbor", "ParseError", "Plan", "load_dataset", "save_dataset",
+    "NO_NEIGHBOR", "Dataset", "IoError", "Neighbor", "ParseError", "Plan", "load_dataset", "save_dataset",
     "loo_accuracy", "pruning_power", "speedup", "SearchCounters", "SearchReport", "Store", "SubMatch",
     "TswError", "ValidationError", "device_count", "dist_all", "envelope", "epsnn_dk",
     "fp64_peak", "knn", "knn_dk", "knn_dk_sub", "knn_dtw", "l2_flush", "last_transfer_bytes",

@@ -139,6 +139,22 @@ double up_factor(double c) { return std::nextafter(1.0 + c * 0x1p-53, INFINITY);
 
 void tswb::set_last_error(const std::string& msg) { g_err = msg; }
 
+size_t tswb::smem_optin() {
+    static size_t cached[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!cached[dev]) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+        cached[dev] = v > 0 ? (size_t)v : 48 * 1024;
+    }
+    // TSW_SMEM_LIMIT: a lower limit (tests exercise the spill mode with short series)
+    const char* e = std::getenv("TSW_SMEM_LIMIT");
+    const size_t lim = e && std::atoll(e) > 0 ? (size_t)std::atoll(e) : (size_t)0;
+    return lim ? std::min(lim, cached[dev]) : cached[dev];
+}
+
 int tswb::sm_count() {
     static int cached[64] = {0};
     int dev = 0;
@@ -166,8 +182,12 @@ struct tsw_store {
     std::vector<uint32_t> host_len;
     uint64_t bytes = 0;      // fp64 store bytes
     float err32 = 0.0f;      // >= max |x - fp32(x)| over the store
-    std::mutex mu;
-    std::unique_ptr<tsw_plan> cached_plan;
+    std::mutex mu;  // guards the plan pool, the candidate-envelope cache and the diagnostics
+    // idle plans of tsw_knn calls: a call takes a compatible plan (or builds one) under `mu`,
+    // executes on the plan's own stream WITHOUT holding `mu`, and returns it -- concurrent
+    // tsw_knn calls on one store run concurrently (the reference functions are reentrant,
+    // search.hpp:41-44)
+    std::vector<std::unique_ptr<tsw_plan>> plan_pool;
     // candidate envelopes (fp32 midpoint / half-width, store layout) by band radius, for the
     // reverse LB_Box filter (built once per radius, like the fp32 copy)
     struct CEnv {
@@ -205,6 +225,7 @@ struct tsw_plan {
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     DevBuf<double> qends;  // DK compaction scratch [2d][nq_max]
     DevBuf<double> q, q_rm, ub, ub_part, sel_sv, sel_v, slots, top_d;
+    DevBuf<double> qinf;  // DTW: one all-+inf guarded query (the fast path's idle lanes)
     DevBuf<float> env_lo, env_hi;
     DevBuf<float> pfx;  // DTW: survivors' LB block sums [pfx_cap][kPfxBlocks]
     // DTW reverse LB bound: fp32 queries, their max |value|, the candidate envelope
@@ -258,7 +279,7 @@ struct tsw_plan {
     }
 };
 
-tsw_store::~tsw_store() { cached_plan.reset(); }
+tsw_store::~tsw_store() { plan_pool.clear(); }
 
 namespace {
 
@@ -358,6 +379,9 @@ std::unique_ptr<tsw_plan> make_plan(tsw_store* s, uint64_t nq_max, uint64_t qlen
     p->q_rm.alloc(nq_max * qlen * s->d);
     p->qends.alloc(2 * s->d * nq_max);
     if (metric == TSW_METRIC_DTW) {
+        p->qinf.alloc(kTile * s->d + p->qstride);
+        launch_fill(p->qinf.p, kTile * s->d + p->qstride, INFINITY, p->own);
+        ck(cudaStreamSynchronize(p->own), "plan init");
         p->env_lo.alloc(nq_max * p->qstride);
         p->env_hi.alloc(nq_max * p->qstride);
         // LB block sums for the DP's cumulative bound when a lane of the LB warp covers at most
@@ -527,10 +551,26 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
     ++launches;
     mark(2);
 
+    // DTW with the candidate envelopes (r >= 32): the queries in fp32 and their max |value|,
+    // for the reverse LB_Box pass and the DP's reverse cumulative bound
+    const char* rev_e = std::getenv("TSW_REVCB");  // TSW_REVCB=0: off (A/B, tests)
+    const bool rev_cb = rev_e == nullptr || std::atoi(rev_e) != 0;
+    if (!dk && p->cenv_m) {
+        launch_to_float(p->qg(), (uint64_t)nq * p->qstride, p->q32.p, st);
+        launch_absmax(p->qg(), (uint64_t)nq * p->qstride, p->qabsmax.p, st);
+        launches += 2;
+    }
     DpArgs da{};
     da.store = s->dev();
     da.queries = p->qg();
     da.guarded = 1;
+    da.inf_query = p->qinf.p ? p->qinf.p + s->d * kTile : nullptr;
+    if (!dk && p->cenv_m && rev_cb) {
+        da.q32 = p->q32.p;
+        da.cenv_m = p->cenv_m;
+        da.cenv_h = p->cenv_h;
+        da.qabsmax = p->qabsmax.p;
+    }
     da.env_lo = p->env_lo.p;
     da.env_hi = p->env_hi.p;
     da.qlen = (uint32_t)p->qlen;
@@ -588,14 +628,11 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
         // the store with the forward bound only (measured: the reverse pass costs more than
         // the DP pairs it removes there)
         if (p->cenv_m && nq >= 4) {
-            launch_to_float(p->qg(), (uint64_t)nq * p->qstride, p->q32.p, st);
-            launch_absmax(p->qg(), (uint64_t)nq * p->qstride, p->qabsmax.p, st);
             la.cenv_m = p->cenv_m;
             la.cenv_h = p->cenv_h;
             la.q32 = p->q32.p;
             la.qabsmax = p->qabsmax.p;
             la.task = p->counters.p + C_TASK;
-            launches += 2;
         }
         launch_lb_compact(la, st);
     } else {
@@ -675,12 +712,17 @@ void fetch_impl(tsw_plan* p, tsw_neighbor* out, tsw_counters* counters, cudaStre
             (kk <= (uint64_t)kKMax ? nq * kk * (sizeof(double) + sizeof(uint32_t)) : 0);
     for (uint64_t q = 0; q < nq; ++q) {
         tsw_neighbor* o = out ? out + q * kk : nullptr;
-        if (p->h_res_n.p[q] < kk || p->h_res_n.p[q] > n)
+        // every exact DP result is appended once and counted once (full_dp)
+        if (p->h_res_n.p[q] != hs[q].full_dp || p->h_res_n.p[q] > n)
             fail(TSW_ECUDA, "internal: " + std::to_string(p->h_res_n.p[q]) +
-                                " exact results for query " + std::to_string(q));
+                                " exact results for query " + std::to_string(q) + " (full_dp " +
+                                std::to_string(hs[q].full_dp) + ")");
+        // fewer than kk results: the reference's KBest ends short too (TSW_NO_NEIGHBOR)
+        const uint64_t have = std::min<uint64_t>(kk, p->h_res_n.p[q]);
         if (kk <= (uint64_t)kKMax) {
             for (uint64_t j = 0; o && j < kk; ++j)
-                o[j] = {p->h_top_i.p[q * kk + j], p->h_top_d.p[q * kk + j]};
+                o[j] = j < have ? tsw_neighbor{p->h_top_i.p[q * kk + j], p->h_top_d.p[q * kk + j]}
+                                : tsw_neighbor{TSW_NO_NEIGHBOR, INFINITY};
         } else {
             // k > kKMax: sort the (rare, large-k) exact-result buffer on the host
             const unsigned cnt = p->h_res_n.p[q];
@@ -696,7 +738,8 @@ void fetch_impl(tsw_plan* p, tsw_neighbor* out, tsw_counters* counters, cudaStre
             std::sort(all.begin(), all.end(), [](const tsw_neighbor& a, const tsw_neighbor& b) {
                 return a.distance < b.distance || (a.distance == b.distance && a.index < b.index);
             });
-            for (uint64_t j = 0; o && j < kk; ++j) o[j] = all[j];
+            for (uint64_t j = 0; o && j < kk; ++j)
+                o[j] = j < have ? all[j] : tsw_neighbor{TSW_NO_NEIGHBOR, INFINITY};
         }
         // every counter is counted on the device (QState); conservation (search.hpp:10-12)
         // is then a real check: each (query, candidate) pair must have been pruned by a bound
@@ -736,18 +779,32 @@ void fetch_impl(tsw_plan* p, tsw_neighbor* out, tsw_counters* counters, cudaStre
     }
 }
 
-tsw_plan* cached_plan(tsw_store* s, uint64_t nq, uint64_t qlen, int metric, uint64_t r,
-                      uint64_t k) {
+constexpr size_t kPlanPoolMax = 8;  // idle plans kept per store
+
+// Takes a pooled plan for (qlen, metric, r, k) holding >= min(nq, cap) queries, or builds one.
+// Called with s->mu held.
+std::unique_ptr<tsw_plan> acquire_plan(tsw_store* s, uint64_t nq, uint64_t qlen, int metric,
+                                       uint64_t r, uint64_t k) {
     const uint64_t per_q = s->n * (8 + 8 + 8 + 1) + 4096;
     const uint64_t budget = 12ull << 30;
-    const uint64_t nq_max = std::max<uint64_t>(1, std::min<uint64_t>({nq, 1024, budget / per_q}));
-    tsw_plan* p = s->cached_plan.get();
-    if (!p || p->qlen != qlen || p->metric != metric || p->r != r || p->k != k || p->nq_max < nq_max) {
-        s->cached_plan.reset();
-        s->cached_plan = make_plan(s, nq_max, qlen, metric, r, k);
-        p = s->cached_plan.get();
+    const uint64_t nq_max = std::max<uint64_t>(
+        1, std::min<uint64_t>({nq, 1024, budget / per_q, ((1ull << 32) - 1) / std::max<uint64_t>(1, s->n)}));
+    auto& pool = s->plan_pool;
+    for (size_t i = pool.size(); i-- > 0;) {
+        tsw_plan* p = pool[i].get();
+        if (p->qlen == qlen && p->metric == metric && p->r == r && p->k == k && p->nq_max >= nq_max) {
+            std::unique_ptr<tsw_plan> out = std::move(pool[i]);
+            pool.erase(pool.begin() + (long)i);
+            return out;
+        }
     }
-    return p;
+    return make_plan(s, nq_max, qlen, metric, r, k);
+}
+
+void release_plan(tsw_store* s, std::unique_ptr<tsw_plan> p) {
+    std::lock_guard<std::mutex> lk(s->mu);
+    s->plan_pool.push_back(std::move(p));
+    if (s->plan_pool.size() > kPlanPoolMax) s->plan_pool.erase(s->plan_pool.begin());
 }
 
 }  // namespace
@@ -1032,9 +1089,22 @@ int tsw_knn(tsw_store* s, const double* queries, uint64_t nq, uint64_t qlen, int
         if (nq == 0) return;
         if (!queries) fail(TSW_EINVAL, "queries is null");
         check_finite(queries, nq * qlen * s->d, "query");
-        std::lock_guard<std::mutex> lk(s->mu);
         DeviceGuard dg(s->device);
-        tsw_plan* p = cached_plan(s, nq, qlen, metric, r, k);
+        std::unique_ptr<tsw_plan> held;
+        {
+            std::lock_guard<std::mutex> lk(s->mu);
+            held = acquire_plan(s, nq, qlen, metric, r, k);
+        }
+        // back to the pool on every exit (an error leaves the plan reusable: each execute
+        // resets its state)
+        struct Return {
+            tsw_store* s;
+            std::unique_ptr<tsw_plan>& p;
+            ~Return() {
+                if (p) release_plan(s, std::move(p));
+            }
+        } ret{s, held};
+        tsw_plan* p = held.get();
         p->use_graph = true;  // repeated calls replay the captured pipeline (one launch)
         const uint64_t kk = p->kk;
         uint64_t h2d = 0, d2h = 0;
@@ -1058,7 +1128,8 @@ int tsw_epsnn_dk(tsw_store* s, const double* query, uint64_t qlen, double eps,
         if (!(eps >= 0)) fail(TSW_EINVAL, "epsnn_dk: eps must be nonnegative");
         if (qlen == 0) fail(TSW_EVALIDATION, "time series values must hold n >= 1 complete points");
         check_finite(query, qlen * s->d, "query");
-        std::lock_guard<std::mutex> lk(s->mu);
+        // no store lock: the store is read-only and every buffer below is this call's own
+        
         DeviceGuard dg(s->device);
         const uint64_t n = s->n, d = s->d, qs = stride_of(qlen, d);
         cudaStream_t st = 0;

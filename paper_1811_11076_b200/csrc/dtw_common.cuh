@@ -53,6 +53,58 @@ __device__ __forceinline__ void scan_pfx_row(float (&bv)[kPfxBlocks / WL], int g
     for (int i = 0; i < PER; ++i) pfx[1 + gl * PER + i] = __fadd_rd(base, bv[i]);
 }
 
+// Exclusive round-down prefix over points of the fp32 LB terms lb_term_rd(x, m, h + hadd):
+// out[p] <= sum of the terms of points < p (all dimensions), p = 0..L.  Lanes own 4 consecutive
+// points (one float4 per dimension in the tiled layout); RD adds in any order keep every
+// prefix a lower bound.
+template <int WL, bool HADD>
+__device__ __forceinline__ void prefix_terms(const float* x32, const float* em, const float* eh,
+                                             float hadd, int gl, unsigned gmask, float* out, int L,
+                                             int stride) {
+    float carry = 0.0f;
+    if (gl == 0) out[0] = 0.0f;
+    for (int j0 = 0; j0 < L; j0 += 4 * WL) {
+        const int p0 = j0 + 4 * gl;
+        float t0 = 0.0f, t1 = 0.0f, t2 = 0.0f, t3 = 0.0f;
+        if (p0 < L) {
+            for (int k = 0; k < stride; ++k) {
+                const uint64_t o = tidx((uint32_t)p0, (uint32_t)k, (uint32_t)stride);
+                const float4 x = __ldg(reinterpret_cast<const float4*>(x32 + o));
+                const float4 l = __ldg(reinterpret_cast<const float4*>(em + o));
+                float4 hh = __ldg(reinterpret_cast<const float4*>(eh + o));
+                if (HADD) {
+                    hh.x = __fadd_ru(hh.x, hadd);
+                    hh.y = __fadd_ru(hh.y, hadd);
+                    hh.z = __fadd_ru(hh.z, hadd);
+                    hh.w = __fadd_ru(hh.w, hadd);
+                }
+                t0 = lb_term_rd(t0, x.x, l.x, hh.x);
+                t1 = lb_term_rd(t1, x.y, l.y, hh.y);
+                t2 = lb_term_rd(t2, x.z, l.z, hh.z);
+                t3 = lb_term_rd(t3, x.w, l.w, hh.w);
+            }
+        }
+        // local inclusive scan, then a group scan of the lane totals
+        t1 = __fadd_rd(t1, t0);
+        t2 = __fadd_rd(t2, t1);
+        t3 = __fadd_rd(t3, t2);
+        float inc = t3;
+#pragma unroll
+        for (int o = 1; o < WL; o <<= 1) {
+            const float y = __shfl_up_sync(gmask, inc, o, WL);
+            if (gl >= o) inc = __fadd_rd(inc, y);
+        }
+        float base = __shfl_up_sync(gmask, inc, 1, WL);
+        if (gl == 0) base = 0.0f;
+        base = __fadd_rd(base, carry);
+        if (p0 + 1 <= L) out[p0 + 1] = __fadd_rd(base, t0);
+        if (p0 + 2 <= L) out[p0 + 2] = __fadd_rd(base, t1);
+        if (p0 + 3 <= L) out[p0 + 3] = __fadd_rd(base, t2);
+        if (p0 + 4 <= L) out[p0 + 4] = __fadd_rd(base, t3);
+        carry = __fadd_rd(carry, __shfl_sync(gmask, inc, WL - 1, WL));
+    }
+}
+
 template <int WL>
 __device__ __forceinline__ void setup_pfx(const DpArgs& a, const QEntry& pr, int gl, unsigned gmask,
                                           float* pfx, int L, int stride) {
@@ -61,49 +113,72 @@ __device__ __forceinline__ void setup_pfx(const DpArgs& a, const QEntry& pr, int
         load_pfx_row<WL>(a, pr.ps, gl, bv);
         scan_pfx_row<WL>(bv, gl, gmask, pfx);
     } else if (a.env_lo) {
-        const float* x32 = a.store.data32 + series_off(a.store, pr.c);
-        const float* el = a.env_lo + (uint64_t)pr.q * a.qstride;
-        const float* eh = a.env_hi + (uint64_t)pr.q * a.qstride;
-        float carry = 0.0f;
-        if (gl == 0) pfx[0] = 0.0f;
-        for (int j0 = 0; j0 < L; j0 += 4 * WL) {
-            const int p0 = j0 + 4 * gl;
-            float t0 = 0.0f, t1 = 0.0f, t2 = 0.0f, t3 = 0.0f;
-            if (p0 < L) {
-                for (int k = 0; k < stride; ++k) {
-                    const uint64_t o = tidx((uint32_t)p0, (uint32_t)k, (uint32_t)stride);
-                    const float4 x = __ldg(reinterpret_cast<const float4*>(x32 + o));
-                    const float4 l = __ldg(reinterpret_cast<const float4*>(el + o));
-                    const float4 hh = __ldg(reinterpret_cast<const float4*>(eh + o));
-                    t0 = lb_term_rd(t0, x.x, l.x, hh.x);
-                    t1 = lb_term_rd(t1, x.y, l.y, hh.y);
-                    t2 = lb_term_rd(t2, x.z, l.z, hh.z);
-                    t3 = lb_term_rd(t3, x.w, l.w, hh.w);
-                }
-            }
-            // local inclusive scan, then a group scan of the lane totals (RD adds
-            // in any order keep every prefix a lower bound)
-            t1 = __fadd_rd(t1, t0);
-            t2 = __fadd_rd(t2, t1);
-            t3 = __fadd_rd(t3, t2);
-            float inc = t3;
-#pragma unroll
-            for (int o = 1; o < WL; o <<= 1) {
-                const float y = __shfl_up_sync(gmask, inc, o, WL);
-                if (gl >= o) inc = __fadd_rd(inc, y);
-            }
-            float base = __shfl_up_sync(gmask, inc, 1, WL);
-            if (gl == 0) base = 0.0f;
-            base = __fadd_rd(base, carry);
-            if (p0 + 1 <= L) pfx[p0 + 1] = __fadd_rd(base, t0);
-            if (p0 + 2 <= L) pfx[p0 + 2] = __fadd_rd(base, t1);
-            if (p0 + 3 <= L) pfx[p0 + 3] = __fadd_rd(base, t2);
-            if (p0 + 4 <= L) pfx[p0 + 4] = __fadd_rd(base, t3);
-            carry = __fadd_rd(carry, __shfl_sync(gmask, inc, WL - 1, WL));
-        }
+        prefix_terms<WL, false>(a.store.data32 + series_off(a.store, pr.c),
+                                a.env_lo + (uint64_t)pr.q * a.qstride,
+                                a.env_hi + (uint64_t)pr.q * a.qstride, 0.0f, gl, gmask, pfx, L,
+                                stride);
     } else {
         for (int j = gl; j <= L; j += WL) pfx[j] = 0.0f;
     }
+}
+
+// Reverse cumulative bound (LB_Keogh's other direction, the query points against the
+// CANDIDATE's envelope): pfq[i] <= sum over query points < i of dist(q_i, env_c(i))^2.  Every
+// warping path matches each remaining query point with a candidate point inside the band,
+// i.e. inside the candidate's envelope at that index, so a cut cell (i', j') completes to at
+// least v + max(pfx[j'], pfq[i']).  fp32 terms as in the reverse LB pass (kernels_bound.cu
+// lb2_flush): RN query copy, half-width + eq >= |q - fp32(q)|, rounded up.
+template <int WL>
+__device__ __forceinline__ void setup_pfq(const DpArgs& a, const QEntry& pr, int gl, unsigned gmask,
+                                          float* pfq, int L, int stride, float eq) {
+    const uint64_t co = series_off(a.store, pr.c);
+    prefix_terms<WL, true>(a.q32 + (uint64_t)pr.q * a.qstride, a.cenv_m + co, a.cenv_h + co, eq,
+                           gl, gmask, pfq, L, stride);
+}
+
+// The reference prunes on `lb >= eps` with its serially summed fp64 LB_Box (search.cpp:147,
+// lower_bounds.cpp:34-44).  While its KBest is not full, eps = +inf, so exactly the candidates
+// whose serial sum overflows to +inf are pruned -- and those have a DTW of +inf as well (the
+// bound is a lower bound).  So an exact +inf result is the only one that can differ from the
+// reference: such a pair is dropped iff this restatement of box_bound (window min / max per
+// point and dimension, terms (lo - x)^2 / (x - hi)^2 without FMA, summed serially in flat
+// order) overflows.  Group-cooperative (all WL lanes of the group call it, same result on
+// every lane); only reached for +inf distances, i.e. inputs near the fp64 range limit.
+template <int WL>
+__device__ bool ref_lb_overflows(const DpArgs& a, const QEntry& pr, int gl, unsigned gmask, int L) {
+    const uint32_t d = a.store.d;
+    const int r = (int)min(a.r, (uint32_t)(L - 1));
+    const double* q = a.queries + (uint64_t)pr.q * a.qstride;
+    const double* x = a.store.data + series_off(a.store, pr.c);
+    const uint32_t n = (uint32_t)L * d;
+    double acc = 0.0;
+    for (uint32_t f0 = 0; f0 < n; f0 += WL) {
+        const uint32_t f = f0 + (uint32_t)gl;
+        double term = 0.0;
+        if (f < n) {
+            const uint32_t p = f / d, k = f - p * d;
+            const int w0 = max((int)p - r, 0), w1 = min((int)p + r, L - 1);
+            double lo = q[tidx((uint32_t)w0, k, d)], hi = lo;
+            for (int w = w0 + 1; w <= w1; ++w) {
+                const double v = q[tidx((uint32_t)w, k, d)];
+                lo = v < lo ? v : lo;
+                hi = v > hi ? v : hi;
+            }
+            const double xv = x[tidx(p, k, d)];
+            if (xv < lo) {
+                const double e = dsub(lo, xv);
+                term = dmul(e, e);
+            } else if (xv > hi) {
+                const double e = dsub(xv, hi);
+                term = dmul(e, e);
+            }
+        }
+        for (int j = 0; j < WL; ++j) {
+            const double tj = __shfl_sync(gmask, term, j, WL);
+            if (f0 + (uint32_t)j < n) acc = dadd(acc, tj);
+        }
+    }
+    return !(acc < kInf);
 }
 
 // Report a finished pair (one lane): exact iff the DP completed with value <= T, as

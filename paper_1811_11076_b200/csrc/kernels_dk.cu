@@ -213,7 +213,10 @@ __device__ __forceinline__ void dk_step(const Strip& S, int k, int lane, int n,
 template <int D, int RPL, bool SUB>
 __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) {
     constexpr int kStrip = 32 * RPL;  // rows per strip
-    extern __shared__ double smem[];
+    extern __shared__ double smem_dk[];
+    // shared memory, or this block's global scratch for very long series (a.spill)
+    double* smem = a.spill ? reinterpret_cast<double*>(a.spill + (size_t)blockIdx.x * a.spill_block)
+                           : smem_dk;
     const int lane = threadIdx.x & 31;
     // boundary row of the warp, padded by 64 columns on both sides (out-of-range reads)
     double* bnd = smem + (size_t)(threadIdx.x >> 5) * (max_len + 128) + 64;
@@ -535,9 +538,11 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
 template <int D, int RPL>
 void run_dk(const DpArgs& a, uint32_t max_pairs, uint32_t max_len, cudaStream_t st) {
     const int threads = 128;
-    const size_t smem = (size_t)(threads / 32) *
-                        ((max_len + 128) * sizeof(double) +
-                         (a.sub ? (max_len + 31) / 32 * kSubB * sizeof(unsigned) : 0));
+    const size_t big = (size_t)(threads / 32) *
+                       ((max_len + 128) * sizeof(double) +
+                        (a.sub ? (max_len + 31) / 32 * kSubB * sizeof(unsigned) : 0));
+    const bool spill = big > smem_optin();
+    const size_t smem = spill ? 0 : big;
     auto kern = a.sub ? dk_dp_kernel<D, RPL, true> : dk_dp_kernel<D, RPL, false>;
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -546,7 +551,11 @@ void run_dk(const DpArgs& a, uint32_t max_pairs, uint32_t max_len, cudaStream_t 
     const uint64_t want = ((uint64_t)max_pairs * 32 + threads - 1) / threads;
     const int blocks = (int)std::max<uint64_t>(
         1, std::min<uint64_t>(want, (uint64_t)sm_count() * std::max(per_sm, 1)));
-    kern<<<blocks, threads, smem, st>>>(a, max_len);
+    DpArgs b = a;
+    SpillScratch sp(spill ? blocks * big : 0, st);
+    b.spill = static_cast<unsigned char*>(sp.p);
+    b.spill_block = big;
+    kern<<<blocks, threads, smem, st>>>(b, max_len);
 }
 
 template <int D>

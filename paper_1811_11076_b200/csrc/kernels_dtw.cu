@@ -193,7 +193,9 @@ __global__ void __launch_bounds__(TPB, MINB) dtw_dp_kernel(DpArgs a, uint32_t ps
     const int lane = threadIdx.x & 31;
     const int gl = lane % WL;
     const unsigned gmask = WL == 32 ? kFull : (0xffffu << (lane & 16));
-    float* pfx = smem_pfx + (size_t)(threadIdx.x / WL) * pstride;
+    float* pbase = a.spill ? reinterpret_cast<float*>(a.spill + (size_t)blockIdx.x * a.spill_block)
+                           : smem_pfx;
+    float* pfx = pbase + (size_t)(threadIdx.x / WL) * pstride;
     const uint32_t d = a.store.d;
     const int L = (int)a.qlen;
     const int r = (int)min(a.r, a.qlen - 1);  // a band wider than the matrix is the full band
@@ -331,9 +333,13 @@ __global__ void __launch_bounds__(TPB, MINB) dtw_dp_kernel(DpArgs a, uint32_t ps
                     cells += c > 0 ? (unsigned long long)c : 0ull;
                 }
             }
+            // an exact +inf result the reference would have pruned (dtw_common.cuh)
+            const bool drop = a.state && completed && !(f < kInf) &&
+                              ref_lb_overflows<WL>(a, pr, gl, gmask, L);
             if (gl == 0) {
                 if (st) T = ld_volatile(&st->T);
-                finish_pair(a, st, pr, completed, f, T);
+                if (drop) atomicAdd(&st->lb_pruned, 1ull);
+                else finish_pair(a, st, pr, completed, f, T);
             }
             have = false;
         }
@@ -350,7 +356,9 @@ void run(const DpArgs& a, uint32_t max_pairs, cudaStream_t st) {
     constexpr int MINB = (D >= 8) ? 4 : (G >= 8 ? 1 : (G >= 2 ? 2 : 3));
     const int threads = TPB;
     const uint32_t pstride = (std::max<uint32_t>(a.qlen + 1, kPfxBlocks + 1) + 3) & ~3u;
-    const size_t smem = (size_t)(threads / WL) * pstride * sizeof(float);
+    const size_t big = (size_t)(threads / WL) * pstride * sizeof(float);
+    const bool spill = big > smem_optin();
+    const size_t smem = spill ? 0 : big;
     auto kern = dtw_dp_kernel<G, RPAR, D, WL, TPB, MINB>;
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -359,7 +367,11 @@ void run(const DpArgs& a, uint32_t max_pairs, cudaStream_t st) {
     const uint64_t want = ((uint64_t)max_pairs * WL + threads - 1) / threads;
     const int blocks = (int)std::max<uint64_t>(
         1, std::min<uint64_t>(want, (uint64_t)sm_count() * std::max(per_sm, 1)));
-    kern<<<blocks, threads, smem, st>>>(a, pstride);
+    DpArgs b = a;
+    SpillScratch sp(spill ? blocks * big : 0, st);
+    b.spill = static_cast<unsigned char*>(sp.p);
+    b.spill_block = big;
+    kern<<<blocks, threads, smem, st>>>(b, pstride);
 }
 
 template <int G, int RPAR, int WL>

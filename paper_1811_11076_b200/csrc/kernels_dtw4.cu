@@ -102,11 +102,12 @@ struct Lane {
 };
 
 // One iteration `it` (phase PH = it % P): anti-diagonals 2it (offsets of parity 0) and 2it+1.
-template <int G, int D, int WL, int RPAR, bool CHECK, int PH>
+template <int G, int D, int WL, int RPAR, bool IDLE, bool CHECK, int PH>
 __device__ __forceinline__ void iter(Lane<G, D>& s, const double* __restrict__ sq,
                                      const double* __restrict__ tc, int gl, int edge, int tjb,
-                                     unsigned okm, const float* __restrict__ pfx, int plog, int L,
-                                     double T, double margin, bool& alive) {
+                                     int sjb, unsigned okm, const float* __restrict__ pfx,
+                                     const float* __restrict__ pfq, int plog, int L, double T,
+                                     double margin, bool& alive) {
     constexpr int P = Geo<G, RPAR>::P;
     constexpr int FS = Geo<G, RPAR>::FS;
     if constexpr (TSW_DTW4_PREFETCH) {  // iteration it+1's new points into the free slots
@@ -126,7 +127,12 @@ __device__ __forceinline__ void iter(Lane<G, D>& s, const double* __restrict__ s
     double Tlim = 0.0;
     if (CHECK) {
         constexpr int TTMAX = (2 * G - 1) - ((2 * G - 1 + RPAR) >> 1);
-        const double Rmin = (double)pfx[min(max(tjb - TTMAX, 0), L - 1) >> plog];
+        // forward (candidate columns ahead) and reverse (query rows ahead, pfq) cumulative
+        // bounds at the lane's smallest candidate / query index: both lower-bound every slot's
+        // own (pfq == pfx when the reverse bound is off: max of equal values)
+        const float rc = pfx[min(max(tjb - TTMAX, 0), L - 1) >> plog];
+        const float rq = pfq == pfx ? rc : pfq[min(max(sjb, 0), L - 1)];
+        const double Rmin = (double)fmaxf(rc, rq);
         Tlim = __dsub_ru(__dmul_ru(T, margin), Rmin);
     }
 #pragma unroll
@@ -137,7 +143,9 @@ __device__ __forceinline__ void iter(Lane<G, D>& s, const double* __restrict__ s
             nb = __shfl_up_sync(kFull, s.v[2 * G - 1], 1, WL);  // lane 0: slot 0 is never read
         } else {
             nb = __shfl_down_sync(kFull, s.v[0], 1, WL);
-            if (gl == edge) nb = kInf;                          // below offset +r
+            // below offset +r: the idle lane above `edge` runs on the +inf query (IDLE), so its
+            // values are +inf already; else force it
+            if (!IDLE && gl == edge) nb = kInf;
         }
 #pragma unroll
         for (int h = 0; h < G; ++h) {
@@ -147,7 +155,17 @@ __device__ __forceinline__ void iter(Lane<G, D>& s, const double* __restrict__ s
             const double left = (e == 0) ? nb : s.v[(e + 2 * G - 1) % (2 * G)];
             const double down = (e == 2 * G - 1) ? nb : s.v[(e + 1) % (2 * G)];
             const double c = cost<D>(s.S[((ss - PH) % P + P) % P], s.T[(tt + PH) % P]);
-            double nv = dadd(c, dmin(dmin(left, down), s.v[e]));
+            // the shuffled neighbour enters the min LAST: the other two come from earlier
+            // half-iterations, so only one DSETP/FSEL pair follows the shuffle on the
+            // lane-to-lane dependency chain (min is exact: any order gives the same value)
+            double m;
+#ifndef TSW_DTW4_REORDER
+#define TSW_DTW4_REORDER 1
+#endif
+            if (TSW_DTW4_REORDER && e == 0) m = dmin(dmin(down, s.v[e]), left);
+            else if (TSW_DTW4_REORDER && e == 2 * G - 1) m = dmin(dmin(left, s.v[e]), down);
+            else m = dmin(dmin(left, down), s.v[e]);
+            double nv = dadd(c, m);
             if (e == FS) nv = gl == 0 ? kInf : nv;  // offset -r-1
             s.v[e] = nv;
             if (CHECK) alive |= ((okm >> e) & 1u) && nv <= Tlim;
@@ -155,12 +173,13 @@ __device__ __forceinline__ void iter(Lane<G, D>& s, const double* __restrict__ s
     }
 }
 
-template <int G, int D, int WL, int RPAR>
+template <int G, int D, int WL, int RPAR, bool IDLE, bool FIN>
 __device__ __forceinline__ void body(Lane<G, D>& s, const double* __restrict__ sq,
                                      const double* __restrict__ tc, int gl, int edge, int it,
-                                     int tb0, unsigned okm, const float* __restrict__ pfx, int plog,
-                                     int L, const QState* st, double margin, double& T,
-                                     bool& alive, double& fin, bool ehi) {
+                                     int tb0, int sb0, unsigned okm, const float* __restrict__ pfx,
+                                     const float* __restrict__ pfq, int plog, int L,
+                                     const QState* st, double margin, double& T, bool& alive,
+                                     double& fin, bool ehi) {
     constexpr int P = Geo<G, RPAR>::P;
     static_assert(P <= 4, "G <= 2");
     // the threshold is read at the top and consumed by the last phase's check: the load has
@@ -170,9 +189,10 @@ __device__ __forceinline__ void body(Lane<G, D>& s, const double* __restrict__ s
     constexpr int E0 = RPAR, E1 = G == 2 ? RPAR + 2 : RPAR;
 #define TSW_ITER4(PH)                                                                          \
     if constexpr (PH < P) {                                                                    \
-        iter<G, D, WL, RPAR, PH == P - 1, PH>(s, sq, tc, gl, edge, tb0 - (it + PH), okm, pfx,  \
-                                              plog, L, T, margin, alive);                      \
-        if (it + PH == L - 1) fin = ehi ? s.v[E1] : s.v[E0];                                   \
+        iter<G, D, WL, RPAR, IDLE, PH == P - 1, PH>(s, sq, tc, gl, edge, tb0 - (it + PH),      \
+                                                    sb0 - (it + PH), okm, pfx, pfq, plog, L, T,\
+                                                    margin, alive);                            \
+        if (FIN && it + PH == L - 1) fin = ehi ? s.v[E1] : s.v[E0];                            \
     }
     TSW_ITER4(0)
     TSW_ITER4(1)
@@ -181,7 +201,9 @@ __device__ __forceinline__ void body(Lane<G, D>& s, const double* __restrict__ s
 #undef TSW_ITER4
 }
 
-template <int G, int D, int WL, int RPAR, int TPB, int MINB>
+// IDLE: the group has a lane above `edge`; it runs on an all-+inf query (a.inf_query), so the
+// shuffle below offset +r delivers +inf without a select
+template <int G, int D, int WL, int RPAR, bool IDLE, int TPB, int MINB>
 __global__ void __launch_bounds__(TPB, MINB) dtw4_kernel(DpArgs a, uint32_t pstride) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int P = Geo<G, RPAR>::P;
@@ -190,19 +212,25 @@ __global__ void __launch_bounds__(TPB, MINB) dtw4_kernel(DpArgs a, uint32_t pstr
     const int lane = threadIdx.x & 31;
     const int gl = lane % WL;
     const unsigned gmask = WL == 32 ? kFull : (((1u << WL) - 1u) << (lane & ~(WL - 1)));
+    // shared: [NG Stage][ab_local: nq counters (nq <= kAbLocalMax)][pfx: NG x pstride][ctab]
+    // with the last two in global memory (a.spill, per block) for very long series
     Stage* sg = reinterpret_cast<Stage*>(smem_raw) + threadIdx.x / WL;
-    float* smem_pfx = reinterpret_cast<float*>(smem_raw + NG * sizeof(Stage));
-    float* pfx = smem_pfx + (size_t)(threadIdx.x / WL) * pstride;
+    const bool abl = a.state && a.nq <= kAbLocalMax;
     // per-block early-abandon counters by query (nq <= kAbLocalMax), else global atomics
-    unsigned* ab_local = a.state && a.nq <= kAbLocalMax ? reinterpret_cast<unsigned*>(
-                                                              smem_pfx + (size_t)NG * pstride)
-                                                        : nullptr;
+    unsigned* ab_local = abl ? reinterpret_cast<unsigned*>(smem_raw + NG * sizeof(Stage)) : nullptr;
+    float* big = a.spill ? reinterpret_cast<float*>(a.spill + (size_t)blockIdx.x * a.spill_block)
+                         : reinterpret_cast<float*>(smem_raw + NG * sizeof(Stage) +
+                                                    (abl ? ((a.nq + 3) & ~3u) * sizeof(unsigned) : 0));
+    float* pfx = big + (size_t)(threadIdx.x / WL) * pstride;
+    // reverse cumulative bound (a.cenv_m set): the group's pfq row after the pfx rows
+    const bool rev = a.cenv_m != nullptr;
+    float* pfq = rev ? big + (size_t)NG * pstride + (size_t)(threadIdx.x / WL) * pstride : pfx;
+    const float eq = rev ? __double2float_ru(__dmul_ru(*a.qabsmax, 0x1p-24)) : 0.0f;
     const int L = (int)a.qlen;
     const int r = (int)min(a.r, a.qlen - 1);
     // ctab[i]: in-matrix band cells of a pair that ran i iterations (the cell statistic, one
     // shared-memory read per finished pair instead of a per-slot clamp computation)
-    uint32_t* ctab = reinterpret_cast<uint32_t*>(smem_pfx + (size_t)NG * pstride) +
-                     (a.state && a.nq <= kAbLocalMax ? a.nq : 0);
+    uint32_t* ctab = reinterpret_cast<uint32_t*>(big + (size_t)(rev ? 2 : 1) * NG * pstride);
     for (int i = threadIdx.x; i <= L; i += blockDim.x) {
         uint32_t sum = 0;
         for (int o = -r; o <= r; ++o) {
@@ -351,9 +379,10 @@ __global__ void __launch_bounds__(TPB, MINB) dtw4_kernel(DpArgs a, uint32_t pstr
                 break;
             }
             if (!done) {
-                sq = a.queries + (uint64_t)pr.q * a.qstride;
+                sq = (IDLE && gl > edge) ? a.inf_query : a.queries + (uint64_t)pr.q * a.qstride;
                 tc = a.store.data + series_off(a.store, pr.c);
                 if (!a.pfx_blocks) setup_pfx<WL>(a, pr, gl, gmask, pfx, L, D);
+                if (rev) setup_pfq<WL>(a, pr, gl, gmask, pfq, L, D, eq);
                 __syncwarp(gmask);
 #pragma unroll
                 for (int e = 0; e < 2 * G; ++e) s.v[e] = (gl == pstar && e == estar) ? 0.0 : kInf;
@@ -376,8 +405,16 @@ __global__ void __launch_bounds__(TPB, MINB) dtw4_kernel(DpArgs a, uint32_t pstr
         // ---- P iterations (phase-unrolled); abandon check on the last one ------------------
         bool alive = false;
         if (!have) s.qo = s.co = 0;  // idle group: keep its (ignored) loads inside the guards
-        body<G, D, WL, RPAR>(s, sq, tc, gl, edge, it, tb0, okm, pfx, plog, L, st, a.margin, T,
-                             alive, fin, estar >= 2);
+        // the final cell is captured only in a pair's last body (warp-uniform variant choice)
+#ifndef TSW_DTW4_FINVAR
+#define TSW_DTW4_FINVAR 1
+#endif
+        if (!TSW_DTW4_FINVAR || __any_sync(kFull, have && it + P >= L))
+            body<G, D, WL, RPAR, IDLE, true>(s, sq, tc, gl, edge, it, tb0, sb0, okm, pfx, pfq,
+                                             plog, L, st, a.margin, T, alive, fin, estar >= 2);
+        else
+            body<G, D, WL, RPAR, IDLE, false>(s, sq, tc, gl, edge, it, tb0, sb0, okm, pfx, pfq,
+                                              plog, L, st, a.margin, T, alive, fin, estar >= 2);
         it += P;
         const unsigned bal = __ballot_sync(kFull, alive) & gmask;
         const bool completed = have && it >= L;
@@ -387,7 +424,13 @@ __global__ void __launch_bounds__(TPB, MINB) dtw4_kernel(DpArgs a, uint32_t pstr
             if (gl == 0) cells += ctab[min(it, L)];
             // T of the last check (>= the current one): a value in between is exact too and
             // only costs an append (the KBest keeps the k smallest)
-            if (gl == 0) finish_pair(a, st, pr, completed, f, T, ab_local);
+            // an exact +inf result the reference would have pruned (dtw_common.cuh)
+            const bool drop = a.state && completed && !(f < kInf) &&
+                              ref_lb_overflows<WL>(a, pr, gl, gmask, L);
+            if (gl == 0) {
+                if (drop) atomicAdd(&st->lb_pruned, 1ull);
+                else finish_pair(a, st, pr, completed, f, T, ab_local);
+            }
             have = false;
         }
     }
@@ -401,16 +444,19 @@ __global__ void __launch_bounds__(TPB, MINB) dtw4_kernel(DpArgs a, uint32_t pstr
     }
 }
 
-template <int G, int D, int WL, int RPAR>
+template <int G, int D, int WL, int RPAR, bool IDLE>
 void run4(const DpArgs& a, uint32_t max_pairs, cudaStream_t st) {
     // 128-thread blocks: finer occupancy steps at ~100 registers per thread
     constexpr int TPB = 128;
     constexpr int MINB = 4;
     const uint32_t pstride = (std::max<uint32_t>(a.qlen + 1, kPfxBlocks + 1) + 3) & ~3u;
-    const size_t smem = (size_t)(TPB / WL) * (sizeof(Stage) + pstride * sizeof(float)) +
-                        (a.state && a.nq <= kAbLocalMax ? a.nq * sizeof(unsigned) : 0) +
-                        (a.qlen + 1) * sizeof(uint32_t);
-    auto kern = dtw4_kernel<G, D, WL, RPAR, TPB, MINB>;
+    const size_t fixed = (size_t)(TPB / WL) * sizeof(Stage) +
+                         (a.state && a.nq <= kAbLocalMax ? ((a.nq + 3) & ~3u) * sizeof(unsigned) : 0);
+    const size_t big = (size_t)(TPB / WL) * pstride * sizeof(float) * (a.cenv_m ? 2 : 1) +
+                       ((a.qlen + 1 + 3) & ~3u) * sizeof(uint32_t);
+    const bool spill = fixed + big > smem_optin();
+    const size_t smem = spill ? fixed : fixed + big;
+    auto kern = dtw4_kernel<G, D, WL, RPAR, IDLE, TPB, MINB>;
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
@@ -418,23 +464,34 @@ void run4(const DpArgs& a, uint32_t max_pairs, cudaStream_t st) {
     const uint64_t full = (uint64_t)sm_count() * std::max(per_sm, 1);
     const uint64_t want = ((uint64_t)max_pairs * WL + TPB - 1) / TPB;
     const int blocks = (int)std::max<uint64_t>(1, std::min<uint64_t>(want, full));
-    kern<<<blocks, TPB, smem, st>>>(a, pstride);
+    DpArgs b = a;
+    SpillScratch sp(spill ? blocks * big : 0, st);
+    b.spill = static_cast<unsigned char*>(sp.p);
+    b.spill_block = big;
+    kern<<<blocks, TPB, smem, st>>>(b, pstride);
 }
 
-template <int G, int WL, int RPAR>
+template <int G, int WL, int RPAR, bool IDLE>
 void run4_d(const DpArgs& a, uint32_t max_pairs, cudaStream_t st) {
     switch (a.store.d) {
-        case 1: run4<G, 1, WL, RPAR>(a, max_pairs, st); break;
-        case 2: run4<G, 2, WL, RPAR>(a, max_pairs, st); break;
-        case 3: run4<G, 3, WL, RPAR>(a, max_pairs, st); break;
-        default: run4<G, 4, WL, RPAR>(a, max_pairs, st); break;
+        case 1: run4<G, 1, WL, RPAR, IDLE>(a, max_pairs, st); break;
+        case 2: run4<G, 2, WL, RPAR, IDLE>(a, max_pairs, st); break;
+        case 3: run4<G, 3, WL, RPAR, IDLE>(a, max_pairs, st); break;
+        default: run4<G, 4, WL, RPAR, IDLE>(a, max_pairs, st); break;
     }
 }
 
 template <int G, int WL>
-void run4_p(const DpArgs& a, uint32_t max_pairs, int rpar, cudaStream_t st) {
-    if (rpar) run4_d<G, WL, 1>(a, max_pairs, st);
-    else run4_d<G, WL, 0>(a, max_pairs, st);
+void run4_p(const DpArgs& a, uint32_t max_pairs, int rpar, bool idle, cudaStream_t st) {
+    if constexpr (G == 2) {
+        if (idle) {
+            if (rpar) run4_d<G, WL, 1, true>(a, max_pairs, st);
+            else run4_d<G, WL, 0, true>(a, max_pairs, st);
+            return;
+        }
+    }
+    if (rpar) run4_d<G, WL, 1, false>(a, max_pairs, st);
+    else run4_d<G, WL, 0, false>(a, max_pairs, st);
 }
 
 // lanes needed at G cells per anti-diagonal: offsets -r-S0 .. r packed 2G per lane
@@ -468,13 +525,15 @@ void launch_dtw4(const DpArgs& a, uint32_t max_pairs, cudaStream_t st) {
     const int need = lanes_needed(r, G, rpar);
     WL = std::max(WL, 8);
     while (WL < need) WL *= 2;
+    // a lane above the band edge exists: it runs on the +inf query (IDLE variant)
+    const bool idle = a.inf_query && std::getenv("TSW_DTW4_NOIDLE") == nullptr;  // (A/B)
     if (G == 1) {
-        if (WL <= 16) run4_p<1, 16>(a, max_pairs, rpar, st);
-        else run4_p<1, 32>(a, max_pairs, rpar, st);
+        if (WL <= 16) run4_p<1, 16>(a, max_pairs, rpar, false, st);
+        else run4_p<1, 32>(a, max_pairs, rpar, false, st);
     } else {
-        if (WL <= 8) run4_p<2, 8>(a, max_pairs, rpar, st);
-        else if (WL <= 16) run4_p<2, 16>(a, max_pairs, rpar, st);
-        else run4_p<2, 32>(a, max_pairs, rpar, st);
+        if (WL <= 8) run4_p<2, 8>(a, max_pairs, rpar, idle && need < 8, st);
+        else if (WL <= 16) run4_p<2, 16>(a, max_pairs, rpar, idle && need < 16, st);
+        else run4_p<2, 32>(a, max_pairs, rpar, idle && need < 32, st);
     }
 }
 

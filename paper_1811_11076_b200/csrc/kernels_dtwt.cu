@@ -67,7 +67,8 @@ __global__ void __launch_bounds__(TPB, MINB) dtwt_kernel(DpArgs a, uint32_t pstr
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     double* ring = smem_t + (size_t)wib * (kRing * kRP);
-    float* pfx = reinterpret_cast<float*>(smem_t + (size_t)(TPB / 32) * (kRing * kRP)) +
+    float* pfx = (a.spill ? reinterpret_cast<float*>(a.spill + (size_t)blockIdx.x * a.spill_block)
+                          : reinterpret_cast<float*>(smem_t + (size_t)(TPB / 32) * (kRing * kRP))) +
                  (size_t)wib * pstride;
     const int d = (int)a.store.d;
     const int s32d = 32 * d;
@@ -260,9 +261,13 @@ __global__ void __launch_bounds__(TPB, MINB) dtwt_kernel(DpArgs a, uint32_t pstr
                 cells += c > 0 ? (unsigned long long)c : 0ull;
             }
         }
+        // an exact +inf result the reference would have pruned (dtw_common.cuh)
+        const bool drop = a.state && completed && !(f < kInf) &&
+                          ref_lb_overflows<32>(a, pr, lane, kFull, L);
         if (lane == 0) {
             if (st) T = ld_volatile(&st->T);
-            finish_pair(a, st, pr, completed, f, T);
+            if (drop) atomicAdd(&st->lb_pruned, 1ull);
+            else finish_pair(a, st, pr, completed, f, T);
         }
         __syncwarp();
     }
@@ -285,7 +290,10 @@ void launch_dtwt(const DpArgs& a, uint32_t max_pairs, cudaStream_t st) {
     // spills the pipelined k loop and is slower; fewer blocks scale down linearly)
     constexpr int TPB = 128, MINB = 4;
     const uint32_t pstride = (std::max<uint32_t>(a.qlen + 1, kPfxBlocks + 1) + 3) & ~3u;
-    const size_t smem = (size_t)(TPB / 32) * (kRing * kRP * sizeof(double) + pstride * sizeof(float));
+    const size_t fixed = (size_t)(TPB / 32) * kRing * kRP * sizeof(double);
+    const size_t big = (size_t)(TPB / 32) * pstride * sizeof(float);
+    const bool spill = fixed + big > smem_optin();
+    const size_t smem = spill ? fixed : fixed + big;
     const uint32_t r = std::min(a.r, a.qlen - 1);
     const bool vec = a.qlen % 4 == 0;
     auto kern = (r & 1) ? (vec ? dtwt_kernel<1, true, TPB, MINB> : dtwt_kernel<1, false, TPB, MINB>)
@@ -297,7 +305,11 @@ void launch_dtwt(const DpArgs& a, uint32_t max_pairs, cudaStream_t st) {
     const uint64_t want = ((uint64_t)max_pairs * 32 + TPB - 1) / TPB;
     const int blocks = (int)std::max<uint64_t>(
         1, std::min<uint64_t>(want, (uint64_t)sm_count() * std::max(per_sm, 1)));
-    kern<<<blocks, TPB, smem, st>>>(a, pstride);
+    DpArgs b = a;
+    SpillScratch sp(spill ? blocks * big : 0, st);
+    b.spill = static_cast<unsigned char*>(sp.p);
+    b.spill_block = big;
+    kern<<<blocks, TPB, smem, st>>>(b, pstride);
 }
 
 }  // namespace tswb

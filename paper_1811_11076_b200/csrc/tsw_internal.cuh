@@ -376,6 +376,34 @@ struct DpArgs {
     int sub;                    // DK: subsequence mode (sparse_engine<true>, dogkeeper.cpp:120-223)
     uint32_t* out_end;          // DK sub, dist_all mode: SubMatch::end_index per candidate
     int probe;                  // the probe launch: few pairs, latency-bound (DK: fewer strips)
+    const double* inf_query;    // DTW fast path: an all-+inf guarded query (idle lanes; nullable)
+    // DTW reverse cumulative bound (nullable: off): fp32 RN queries (pitch qstride), the
+    // candidates' fp32 envelopes (midpoint, half-width; store layout) and max |query value|
+    const float* q32;
+    const float* cenv_m;
+    const float* cenv_h;
+    const double* qabsmax;
+    // long series: the per-block arrays that grow with the series length (DTW prefix bounds,
+    // DK boundary rows) live in this global scratch instead of shared memory when they would
+    // exceed the opt-in shared-memory limit (set by the launchers, see SpillScratch)
+    unsigned char* spill;
+    size_t spill_block;         // bytes per block
+};
+
+// Host: the per-block opt-in shared-memory limit, and a stream-ordered global scratch for the
+// launchers' spill mode (allocated before the launch, freed after it on the same stream).
+size_t smem_optin();
+struct SpillScratch {
+    void* p = nullptr;
+    cudaStream_t st = nullptr;
+    SpillScratch(size_t bytes, cudaStream_t s) : st(s) {
+        if (bytes && cudaMallocAsync(&p, bytes, s) != cudaSuccess) p = nullptr;
+    }
+    ~SpillScratch() {
+        if (p) cudaFreeAsync(p, st);
+    }
+    SpillScratch(const SpillScratch&) = delete;
+    SpillScratch& operator=(const SpillScratch&) = delete;
 };
 
 void launch_dtw_dp(const DpArgs& a, uint32_t max_pairs, cudaStream_t st);

@@ -134,9 +134,12 @@ std::vector<SearchReport> run_knn(const std::vector<TimeSeries>& queries, const 
     const double wall = std::chrono::duration<double>(Clock::now() - start).count();
     for (std::size_t q = 0; q < queries.size(); ++q) {
         auto& rep = reps[q];
-        rep.neighbors.resize(kk);
+        rep.neighbors.clear();
+        rep.neighbors.reserve(kk);
         for (std::size_t j = 0; j < kk; ++j)
-            rep.neighbors[j] = {static_cast<std::size_t>(out[q * kk + j].index), out[q * kk + j].distance};
+            if (out[q * kk + j].index != TSW_NO_NEIGHBOR)
+                rep.neighbors.push_back({static_cast<std::size_t>(out[q * kk + j].index),
+                                         out[q * kk + j].distance});
         rep.counters = {ctr[q].lb_computed, ctr[q].lb_pruned, ctr[q].full_dp, ctr[q].early_abandoned,
                         ctr[q].gdk_calls};
         rep.wall_time_seconds = wall / static_cast<double>(queries.size());

@@ -414,7 +414,8 @@ def _as_store(data) -> Store:
 # ---- batched k-NN -----------------------------------------------------------------------
 def knn(data, queries, k: int, metric: str = "dtw", r: int = 0):
     """Batched k-NN: queries [nq, L, d] -> (indices u64[nq, kk], distances f64[nq, kk],
-    counters u64[nq, 5]) with kk = min(k, n)."""
+    counters u64[nq, 5]) with kk = min(k, n).  A query with fewer neighbours (the reference's
+    KBest can end short, see TSW_NO_NEIGHBOR) has its row padded with (NO_NEIGHBOR, +inf)."""
     qs = np.ascontiguousarray(queries, dtype=np.float64)
     if qs.ndim == 2:
         qs = qs[None]
@@ -438,8 +439,11 @@ def knn(data, queries, k: int, metric: str = "dtw", r: int = 0):
     return idx, dist, c
 
 
+NO_NEIGHBOR = np.iinfo(np.uint64).max  # TSW_NO_NEIGHBOR: unused tail entry of a short row
+
+
 def _report(idx, dist, c, wall) -> SearchReport:
-    return SearchReport([Neighbor(int(i), float(v)) for i, v in zip(idx, dist)],
+    return SearchReport([Neighbor(int(i), float(v)) for i, v in zip(idx, dist) if i != NO_NEIGHBOR],
                         SearchCounters(*[int(x) for x in c]), wall)
 
 

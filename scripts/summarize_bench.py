@@ -19,3 +19,7 @@ for f in sorted(glob.glob(sys.argv[1] if len(sys.argv) > 1 else "gpurun_out/benc
           f"dp={ph['ms_dp']:.3f} | GCUPS={rdp['gcups'] or 0:7.1f} fp64frac={rdp['frac'] or 0:.3f} "
           f"LB GB/s={rlb['achieved'] or 0:7.1f} pairs={d['dp_pairs_per_step']:.0f} "
           f"cpu={d.get('cpu_baseline', {}).get('value')} clk={d['clocks'].get('sm_mhz')}")
+    for m, lg in d.get("legs", {}).items():
+        print(f"{'  leg ' + m:22s} q/s={lg['value']:10.1f} ms/step={lg['ms_per_step']:8.3f} "
+              f"e2e={lg['e2e']['value']:10.1f} dp={lg['phases_ms']['ms_dp']:.3f} "
+              f"fp64frac={lg['roofline_dp']['frac'] or 0:.3f} cpu={lg.get('cpu_baseline', {}).get('value')}")
