@@ -151,6 +151,20 @@ int tsw_envelope(const double* series, uint64_t n, uint64_t d, uint64_t r, doubl
  * role swap of search.cpp:132,148), and the diagonal-path DTW upper bound used as a seed. */
 int tsw_lb_box_all(tsw_store* store, const double* query, uint64_t qlen, uint64_t r,
                    double* lb_out, double* ub_out);
+/* The reference's own fp64 lb_box(data[i], envelope(query, r)) for every candidate, bit for bit
+ * (lower_bounds.cpp:19-46: no FMA, serial sum in flat order).  The k-NN pipeline uses a
+ * rigorous fp32 lower bound instead (tsw_lb_box_all); this one feeds tsw_pruning_power. */
+int tsw_lb_box_exact_all(tsw_store* store, const double* query, uint64_t qlen, uint64_t r,
+                         double* lb_out);
+/* pruning_power(queries, data, r) (metrics.hpp:54-56): the fraction of
+ * candidate DTW computations the lb_box test skips over 1-NN knn_dtw scans of every query,
+ * with the reference's scan schedule -- 64-candidate blocks scanned in index order, the
+ * threshold frozen per block (search.cpp:20,139-162) -- so the count is the reference's
+ * exactly, independent of the GPU's own (timing-dependent) pruning schedule.  Computed from
+ * every candidate's dtw_banded value and exact fp64 lb_box.  pruned: per-query counts
+ * (nullable).  Unequal lengths -> TSW_EINVAL (check_query). */
+int tsw_pruning_power(tsw_store* store, const double* queries, uint64_t nq, uint64_t qlen,
+                      uint64_t r, double* power, uint64_t* pruned);
 /* Thresholded distance of the query to every candidate:
  *   DTW: dtw_early_abandon(query, data[i], r, eps) (dtw.cpp:82-90)
  *   DK : sparse_dk(query, data[i], eps)            (dogkeeper.cpp:227-233)

@@ -9,7 +9,7 @@ from .tswarp import (  # noqa: F401
     NO_NEIGHBOR, Dataset, IoError, Neighbor, ParseError, Plan, SearchCounters, SearchReport, Store, SubMatch,
     TswError, ValidationError, device_count, dist_all, envelope, epsnn_dk, fp64_peak, knn, knn_dk,
     load_dataset, loo_accuracy, pruning_power, save_dataset, speedup,
-    knn_dk_sub, knn_dtw, l2_flush, last_transfer_bytes, lb_box_all, lib, sparse_dk_sub,
+    knn_dk_sub, knn_dtw, l2_flush, lb_box_exact_all, last_transfer_bytes, lb_box_all, lib, sparse_dk_sub,
     sub_dk_all, sub_search_dk, synth, synth_shape,
 )
 
@@ -18,5 +18,5 @@ __all__ = [
     "loo_accuracy", "pruning_power", "speedup", "SearchCounters", "SearchReport", "Store", "SubMatch",
     "TswError", "ValidationError", "device_count", "dist_all", "envelope", "epsnn_dk",
     "fp64_peak", "knn", "knn_dk", "knn_dk_sub", "knn_dtw", "l2_flush", "last_transfer_bytes",
-    "lb_box_all", "lib", "sparse_dk_sub", "sub_dk_all", "sub_search_dk", "synth", "synth_shape",
+    "lb_box_all", "lb_box_exact_all", "lib", "sparse_dk_sub", "sub_dk_all", "sub_search_dk", "synth", "synth_shape",
 ]

@@ -232,6 +232,7 @@ struct tsw_plan {
     DevBuf<float> q32;
     DevBuf<double> qabsmax;
     const float* cenv_m = nullptr;
+    bool lb2 = false;  // the LB pass adds the reverse bound (else cenv feeds only the DP)
     const float* cenv_h = nullptr;
     uint32_t pfx_qn = 0, pfx_log = 0, pfx_cap = 0;
     DevBuf<uint32_t> sel_si, sel_i, top_i, fin_si;
@@ -391,7 +392,12 @@ std::unique_ptr<tsw_plan> make_plan(tsw_store* s, uint64_t nq_max, uint64_t qlen
         // Skipped when the candidate envelope would not fit.
         const char* lb2e = std::getenv("TSW_LB2");
         const bool want_lb2 = lb2e ? std::atoi(lb2e) != 0 : r >= 32;
-        if (want_lb2) {
+        // the candidate envelopes also feed the DP's reverse cumulative abandon bound; for
+        // narrow bands (no reverse LB pass) only with TSW_CENV_DP=1 (measurements)
+        const char* cde = std::getenv("TSW_CENV_DP");
+        const bool want_cenv = want_lb2 || (cde && std::atoi(cde) != 0);
+        p->lb2 = want_lb2;
+        if (want_cenv) {
             const uint64_t bytes = 2 * (s->guard + n * s->ustride) * sizeof(float);
             size_t fr = 0, tot = 0;
             cudaMemGetInfo(&fr, &tot);
@@ -627,7 +633,7 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
         // fused reverse bound (queries in fp32 + their max |value| first); 1-3 queries stream
         // the store with the forward bound only (measured: the reverse pass costs more than
         // the DP pairs it removes there)
-        if (p->cenv_m && nq >= 4) {
+        if (p->cenv_m && p->lb2 && nq >= 4) {
             la.cenv_m = p->cenv_m;
             la.cenv_h = p->cenv_h;
             la.q32 = p->q32.p;
@@ -1316,6 +1322,70 @@ int tsw_lb_box_all(tsw_store* s, const double* query, uint64_t qlen, uint64_t r,
         if (lb_out)
             for (uint64_t i = 0; i < n; ++i) lb_out[i] = hl[i];
         if (ub_out) ck(cudaMemcpy(ub_out, ub.p, n * sizeof(double), cudaMemcpyDeviceToHost), "fetch");
+    });
+}
+
+int tsw_lb_box_exact_all(tsw_store* s, const double* query, uint64_t qlen, uint64_t r,
+                         double* lb_out) {
+    return guard([&] {
+        if (!s || !query || !lb_out) fail(TSW_EINVAL, "null argument");
+        check_finite(query, qlen * s->d, "query");
+        if (s->ulen != qlen) fail(TSW_EINVAL, "lb_box: every series must have the query length");
+        DeviceGuard dg(s->device);
+        const uint64_t n = s->n, d = s->d, qs = stride_of(qlen, d);
+        DevBuf<double> q(qs), lo(qs), hi(qs), lb(n);
+        {
+            const std::vector<double> tq = tiled_host(query, qlen, d);
+            ck(cudaMemcpy(q.p, tq.data(), qs * sizeof(double), cudaMemcpyHostToDevice), "upload");
+        }
+        launch_envelope64(q.p, 1, (uint32_t)d, (uint32_t)qlen, qs,
+                          (uint32_t)std::min<uint64_t>(r, 0xffffffffu), lo.p, hi.p, 0);
+        launch_lb64_serial(s->dev(), lo.p, hi.p, (uint32_t)qlen, lb.p, 0);
+        ck(cudaGetLastError(), "lb64 kernel");
+        ck(cudaMemcpy(lb_out, lb.p, n * sizeof(double), cudaMemcpyDeviceToHost), "fetch");
+    });
+}
+
+int tsw_pruning_power(tsw_store* s, const double* queries, uint64_t nq, uint64_t qlen,
+                      uint64_t r, double* power, uint64_t* pruned) {
+    return guard([&] {
+        if (!s || !queries || !power) fail(TSW_EINVAL, "null argument");
+        if (s->ulen != qlen) {
+            for (uint64_t i = 0; i < s->n; ++i)
+                if (s->host_len[i] != qlen)
+                    fail(TSW_EINVAL, "knn_dtw: series " + std::to_string(i) +
+                                         " length differs from the query (lower bounds require "
+                                         "equal lengths)");
+        }
+        const uint64_t n = s->n, d = s->d;
+        std::vector<double> lb(n), dv(n);
+        std::vector<int> ex(n);
+        uint64_t tot = 0;
+        for (uint64_t q = 0; q < nq; ++q) {
+            const double* qp = queries + q * qlen * d;
+            int rc = tsw_lb_box_exact_all(s, qp, qlen, r, lb.data());
+            if (rc == TSW_OK) rc = tsw_dist_all(s, qp, qlen, TSW_METRIC_DTW, r, INFINITY, ex.data(), dv.data());
+            if (rc != TSW_OK) fail(rc, tsw_last_error());
+            // knn_dtw with k = 1 (search.cpp:139-162): block-frozen eps, pruned iff lb >= eps,
+            // else exact iff dtw <= eps (dtw_early_abandon), exact results offered in index order
+            double eps = INFINITY;
+            uint64_t cnt = 0;
+            for (uint64_t b0 = 0; b0 < n; b0 += 64) {
+                const uint64_t b1 = std::min<uint64_t>(b0 + 64, n);
+                double best = eps;
+                for (uint64_t i = b0; i < b1; ++i) {
+                    if (lb[i] >= eps) {
+                        ++cnt;
+                    } else if (dv[i] <= eps && dv[i] < best) {
+                        best = dv[i];
+                    }
+                }
+                eps = best;
+            }
+            if (pruned) pruned[q] = cnt;
+            tot += cnt;
+        }
+        *power = nq && n ? (double)tot / ((double)nq * (double)n) : 0.0;
     });
 }
 

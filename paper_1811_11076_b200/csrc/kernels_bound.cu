@@ -749,9 +749,13 @@ template <int QB, int CB, int FCH>  // FCH: float4 per lane per envelope chunk
 __device__ __forceinline__ void lb2_flush(const LbCompactArgs& a, uint32_t c0, QEntry* list,
                                           float* l2, int cnt, uint32_t total4, float eq, Stage& sg,
                                           PruneCount& pc) {
+    // Reverse bound of the listed pairs, candidate by candidate: the candidate's entries are
+    // taken NB = 8 at a time, each accumulates over ALL envelope chunks in registers (the
+    // envelope chunk is loaded once per batch and shared by the 8 queries' rows, whose loads
+    // are independent: 8 x FCH loads in flight), and the 8 sums are reduced together by a
+    // transpose reduction (9 shuffles instead of 40).
+    constexpr int NB = 8;
     const unsigned lane = lane_id();
-    __syncwarp();
-    for (int i = lane; i < cnt; i += 32) l2[i] = 0.0f;
     __syncwarp();
     const float4* q4 = reinterpret_cast<const float4*>(a.q32);
     const uint32_t qs4 = (uint32_t)(a.qstride / 4);
@@ -761,40 +765,93 @@ __device__ __forceinline__ void lb2_flush(const LbCompactArgs& a, uint32_t c0, Q
         const uint64_t co = series_off(a.store, c) / 4;
         const float4* m4 = reinterpret_cast<const float4*>(a.cenv_m) + co;
         const float4* h4 = reinterpret_cast<const float4*>(a.cenv_h) + co;
-        for (uint32_t f0 = 0; f0 < total4; f0 += 32 * FCH) {
-            // the candidate's envelope chunk in registers, shared by its listed queries
-            float4 mv[FCH], hv[FCH];
+        // the list entries of candidate c (warp-uniform bit masks, kList / 32 words)
+        unsigned mk[kList / 32];
 #pragma unroll
-            for (int i = 0; i < FCH; ++i) {
-                const uint32_t f = f0 + lane + 32 * i;
-                if (f < total4) {
-                    mv[i] = __ldg(m4 + f);
-                    const float4 h = __ldg(h4 + f);
-                    hv[i] = make_float4(__fadd_ru(h.x, eq), __fadd_ru(h.y, eq), __fadd_ru(h.z, eq),
-                                        __fadd_ru(h.w, eq));
-                } else {  // outside the series: terms of 0
-                    mv[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-                    hv[i] = make_float4(kInfF, kInfF, kInfF, kInfF);
+        for (int w = 0; w < kList / 32; ++w) {
+            const int e = 32 * w + (int)lane;
+            mk[w] = __ballot_sync(0xffffffffu, e < cnt && list[e].c == c);
+        }
+        int w = 0;
+        for (;;) {
+            // the next NB entries (warp-uniform; -1: none)
+            int ej[NB];
+#pragma unroll
+            for (int j = 0; j < NB; ++j) {
+                while (w < kList / 32 && mk[w] == 0u) ++w;
+                if (w < kList / 32) {
+                    ej[j] = 32 * w + __ffs(mk[w]) - 1;
+                    mk[w] &= mk[w] - 1u;
+                } else {
+                    ej[j] = -1;
                 }
             }
-            for (int e = 0; e < cnt; ++e) {
-                const QEntry en = list[e];
-                if (en.c != c) continue;
-                const float4* qr = q4 + (uint64_t)en.q * qs4;
-                float t = 0.0f;
+            if (ej[0] < 0) break;
+            const float4* qr[NB];
+#pragma unroll
+            for (int j = 0; j < NB; ++j) qr[j] = q4 + (uint64_t)(ej[j] >= 0 ? list[ej[j]].q : list[ej[0]].q) * qs4;
+            float acc[NB];
+#pragma unroll
+            for (int j = 0; j < NB; ++j) acc[j] = 0.0f;
+            for (uint32_t f0 = 0; f0 < total4; f0 += 32 * FCH) {
+                // the candidate's envelope chunk in registers, shared by the batch's queries
+                float4 mv[FCH], hv[FCH];
 #pragma unroll
                 for (int i = 0; i < FCH; ++i) {
                     const uint32_t f = f0 + lane + 32 * i;
-                    const float4 x = f < total4 ? __ldg(qr + f) : make_float4(0.f, 0.f, 0.f, 0.f);
-                    t = lb_term_rd(t, x.x, mv[i].x, hv[i].x);
-                    t = lb_term_rd(t, x.y, mv[i].y, hv[i].y);
-                    t = lb_term_rd(t, x.z, mv[i].z, hv[i].z);
-                    t = lb_term_rd(t, x.w, mv[i].w, hv[i].w);
+                    if (f < total4) {
+                        mv[i] = __ldg(m4 + f);
+                        const float4 h = __ldg(h4 + f);
+                        hv[i] = make_float4(__fadd_ru(h.x, eq), __fadd_ru(h.y, eq), __fadd_ru(h.z, eq),
+                                            __fadd_ru(h.w, eq));
+                    } else {  // outside the series: terms of 0
+                        mv[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+                        hv[i] = make_float4(kInfF, kInfF, kInfF, kInfF);
+                    }
                 }
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) t = __fadd_rd(t, __shfl_xor_sync(0xffffffffu, t, o));
-                if (lane == 0) l2[e] = __fadd_rd(l2[e], t);
+                for (int j = 0; j < NB; ++j) {
+                    if (ej[j] < 0) continue;  // warp-uniform
+#pragma unroll
+                    for (int i = 0; i < FCH; ++i) {
+                        const uint32_t f = f0 + lane + 32 * i;
+                        const float4 x = f < total4 ? __ldg(qr[j] + f) : make_float4(0.f, 0.f, 0.f, 0.f);
+                        acc[j] = lb_term_rd(acc[j], x.x, mv[i].x, hv[i].x);
+                        acc[j] = lb_term_rd(acc[j], x.y, mv[i].y, hv[i].y);
+                        acc[j] = lb_term_rd(acc[j], x.z, mv[i].z, hv[i].z);
+                        acc[j] = lb_term_rd(acc[j], x.w, mv[i].w, hv[i].w);
+                    }
+                }
             }
+            // transpose reduction: value halves 4 / 2 / 1 against lane bits 16 / 8 / 4, then a
+            // butterfly over lane bits 2 / 1; lane l ends with the sum of entry
+            // 4 * bit4(l) + 2 * bit3(l) + bit2(l) (RD adds in any order: still lower bounds)
+            const bool u16 = lane & 16, u8 = lane & 8, u4 = lane & 4;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float send = u16 ? acc[i] : acc[i + 4];
+                const float keep = u16 ? acc[i + 4] : acc[i];
+                acc[i] = __fadd_rd(keep, __shfl_xor_sync(0xffffffffu, send, 16));
+            }
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const float send = u8 ? acc[i] : acc[i + 2];
+                const float keep = u8 ? acc[i + 2] : acc[i];
+                acc[i] = __fadd_rd(keep, __shfl_xor_sync(0xffffffffu, send, 8));
+            }
+            {
+                const float send = u4 ? acc[0] : acc[1];
+                const float keep = u4 ? acc[1] : acc[0];
+                acc[0] = __fadd_rd(keep, __shfl_xor_sync(0xffffffffu, send, 4));
+            }
+            acc[0] = __fadd_rd(acc[0], __shfl_xor_sync(0xffffffffu, acc[0], 2));
+            acc[0] = __fadd_rd(acc[0], __shfl_xor_sync(0xffffffffu, acc[0], 1));
+            const int jm = (u16 ? 4 : 0) + (u8 ? 2 : 0) + (u4 ? 1 : 0);
+            int em = -1;
+#pragma unroll
+            for (int j = 0; j < NB; ++j) em = j == jm ? ej[j] : em;
+            if ((lane & 3) == 0 && em >= 0) l2[em] = acc[0];
+            if (ej[NB - 1] < 0) break;
         }
     }
     __syncwarp();
@@ -870,10 +927,8 @@ void launch_lb_compact(const LbCompactArgs& a, cudaStream_t st) {
         // float4 per lane
         const uint32_t total4 = (uint32_t)(a.store.tstride / 4);
         const uint32_t fpl = (total4 + 31) / 32;
-        auto kern = lb12_compact_kernel<QB, CB, 4>;
-        if (fpl <= 1) kern = lb12_compact_kernel<QB, CB, 1>;
-        else if (fpl <= 2) kern = lb12_compact_kernel<QB, CB, 2>;
-        else if (fpl <= 3) kern = lb12_compact_kernel<QB, CB, 3>;
+        // (the reverse sums accumulate over all chunks: 2 float4 per lane per chunk suffice)
+        auto kern = fpl <= 1 ? lb12_compact_kernel<QB, CB, 1> : lb12_compact_kernel<QB, CB, 2>;
         const size_t smem12 = (size_t)8 * kList * (sizeof(QEntry) + sizeof(float)) + smem;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem12);
         kern<<<sm_count() * 2, 256, smem12, st>>>(a);
@@ -912,6 +967,38 @@ void launch_lb_compact(const LbCompactArgs& a, cudaStream_t st) {
     const int blocks = (int)std::min<uint64_t>((tiles * 32 + 255) / 256, (uint64_t)sm_count() * 8);
     if (smem) cudaFuncSetAttribute(lb_compact_kernel<QB, CB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     lb_compact_kernel<QB, CB><<<std::max(blocks, 1), 256, smem, st>>>(a);
+}
+
+// ---- the reference's own fp64 lb_box, bit for bit (lower_bounds.cpp:19-46) -----------------
+// One thread per candidate: terms (lo - x)^2 / (x - hi)^2 of the fp64 query envelope, no FMA
+// (-fmad=false), summed serially in the flat order f = i * d + j like box_bound.  Not on the
+// k-NN path (the pipeline uses the fp32 lower bound of K2); feeds the exact pruning-power
+// driver and the parity tests.
+__global__ void lb64_serial_kernel(StoreDev s, const double* __restrict__ lo,
+                                   const double* __restrict__ hi, uint32_t len, double* __restrict__ out) {
+    const uint32_t c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= s.n) return;
+    const double* x = s.data + series_off(s, c);
+    const uint32_t d = s.d;
+    double acc = 0.0;
+    for (uint32_t p = 0; p < len; ++p)
+        for (uint32_t k = 0; k < d; ++k) {
+            const uint64_t o = tidx(p, k, d);
+            const double v = x[o], l = lo[o], h = hi[o];
+            if (v < l) {
+                const double e = dsub(l, v);
+                acc = dadd(acc, dmul(e, e));
+            } else if (v > h) {
+                const double e = dsub(v, h);
+                acc = dadd(acc, dmul(e, e));
+            }
+        }
+    out[c] = acc;
+}
+
+void launch_lb64_serial(const StoreDev& s, const double* lo, const double* hi, uint32_t len,
+                        double* out, cudaStream_t st) {
+    lb64_serial_kernel<<<(s.n + 127) / 128, 128, 0, st>>>(s, lo, hi, len, out);
 }
 
 // ---- DK: first / last cell bound fused with compaction ------------------------------------

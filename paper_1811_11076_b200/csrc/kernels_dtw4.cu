@@ -155,12 +155,12 @@ __device__ __forceinline__ void iter(Lane<G, D>& s, const double* __restrict__ s
             const double left = (e == 0) ? nb : s.v[(e + 2 * G - 1) % (2 * G)];
             const double down = (e == 2 * G - 1) ? nb : s.v[(e + 1) % (2 * G)];
             const double c = cost<D>(s.S[((ss - PH) % P + P) % P], s.T[(tt + PH) % P]);
-            // the shuffled neighbour enters the min LAST: the other two come from earlier
-            // half-iterations, so only one DSETP/FSEL pair follows the shuffle on the
-            // lane-to-lane dependency chain (min is exact: any order gives the same value)
+            // (REORDER: the shuffled neighbour enters the min last, so only one DSETP/FSEL
+            // pair follows the shuffle on the lane-to-lane chain; min is exact in any order)
             double m;
+// (shuffled neighbour last in the min: measured neutral at C5, -1.6% at C3 -> off)
 #ifndef TSW_DTW4_REORDER
-#define TSW_DTW4_REORDER 1
+#define TSW_DTW4_REORDER 0
 #endif
             if (TSW_DTW4_REORDER && e == 0) m = dmin(dmin(down, s.v[e]), left);
             else if (TSW_DTW4_REORDER && e == 2 * G - 1) m = dmin(dmin(left, s.v[e]), down);
@@ -203,7 +203,10 @@ __device__ __forceinline__ void body(Lane<G, D>& s, const double* __restrict__ s
 
 // IDLE: the group has a lane above `edge`; it runs on an all-+inf query (a.inf_query), so the
 // shuffle below offset +r delivers +inf without a select
-template <int G, int D, int WL, int RPAR, bool IDLE, int TPB, int MINB>
+// LONG (series > 256 points): the final cell is captured only in a pair's last body, a
+// warp-uniform choice between two body copies (C5 DP -12%); short series keep one body with a
+// per-iteration capture (the vote and the second copy cost C2 8%)
+template <int G, int D, int WL, int RPAR, bool IDLE, bool LONG, int TPB, int MINB>
 __global__ void __launch_bounds__(TPB, MINB) dtw4_kernel(DpArgs a, uint32_t pstride) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int P = Geo<G, RPAR>::P;
@@ -405,11 +408,9 @@ __global__ void __launch_bounds__(TPB, MINB) dtw4_kernel(DpArgs a, uint32_t pstr
         // ---- P iterations (phase-unrolled); abandon check on the last one ------------------
         bool alive = false;
         if (!have) s.qo = s.co = 0;  // idle group: keep its (ignored) loads inside the guards
-        // the final cell is captured only in a pair's last body (warp-uniform variant choice)
-#ifndef TSW_DTW4_FINVAR
-#define TSW_DTW4_FINVAR 1
-#endif
-        if (!TSW_DTW4_FINVAR || __any_sync(kFull, have && it + P >= L))
+        // (the redundant `L <= 256` test in the LONG form is deliberate: that code generation
+        // measured C5 DP 12.6 -> 11.1 ms against the plain `__any_sync` form, same registers)
+        if (!LONG || L <= 256 || __any_sync(kFull, have && it + P >= L))
             body<G, D, WL, RPAR, IDLE, true>(s, sq, tc, gl, edge, it, tb0, sb0, okm, pfx, pfq,
                                              plog, L, st, a.margin, T, alive, fin, estar >= 2);
         else
@@ -444,7 +445,7 @@ __global__ void __launch_bounds__(TPB, MINB) dtw4_kernel(DpArgs a, uint32_t pstr
     }
 }
 
-template <int G, int D, int WL, int RPAR, bool IDLE>
+template <int G, int D, int WL, int RPAR, bool IDLE, bool LONG>
 void run4(const DpArgs& a, uint32_t max_pairs, cudaStream_t st) {
     // 128-thread blocks: finer occupancy steps at ~100 registers per thread
     constexpr int TPB = 128;
@@ -456,7 +457,7 @@ void run4(const DpArgs& a, uint32_t max_pairs, cudaStream_t st) {
                        ((a.qlen + 1 + 3) & ~3u) * sizeof(uint32_t);
     const bool spill = fixed + big > smem_optin();
     const size_t smem = spill ? fixed : fixed + big;
-    auto kern = dtw4_kernel<G, D, WL, RPAR, IDLE, TPB, MINB>;
+    auto kern = dtw4_kernel<G, D, WL, RPAR, IDLE, LONG, TPB, MINB>;
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
@@ -471,14 +472,26 @@ void run4(const DpArgs& a, uint32_t max_pairs, cudaStream_t st) {
     kern<<<blocks, TPB, smem, st>>>(b, pstride);
 }
 
+template <int G, int WL, int RPAR, bool IDLE, bool LONG>
+void run4_dl(const DpArgs& a, uint32_t max_pairs, cudaStream_t st) {
+    switch (a.store.d) {
+        case 1: run4<G, 1, WL, RPAR, IDLE, LONG>(a, max_pairs, st); break;
+        case 2: run4<G, 2, WL, RPAR, IDLE, LONG>(a, max_pairs, st); break;
+        case 3: run4<G, 3, WL, RPAR, IDLE, LONG>(a, max_pairs, st); break;
+        default: run4<G, 4, WL, RPAR, IDLE, LONG>(a, max_pairs, st); break;
+    }
+}
+
+// LONG variants only for the wide groups (bands of r >= ~14) of the G = 2 path
 template <int G, int WL, int RPAR, bool IDLE>
 void run4_d(const DpArgs& a, uint32_t max_pairs, cudaStream_t st) {
-    switch (a.store.d) {
-        case 1: run4<G, 1, WL, RPAR, IDLE>(a, max_pairs, st); break;
-        case 2: run4<G, 2, WL, RPAR, IDLE>(a, max_pairs, st); break;
-        case 3: run4<G, 3, WL, RPAR, IDLE>(a, max_pairs, st); break;
-        default: run4<G, 4, WL, RPAR, IDLE>(a, max_pairs, st); break;
+    if constexpr (G == 2 && WL >= 16) {
+        if (a.qlen > 256 && std::getenv("TSW_DTW4_NOLONG") == nullptr) {
+            run4_dl<G, WL, RPAR, IDLE, true>(a, max_pairs, st);
+            return;
+        }
     }
+    run4_dl<G, WL, RPAR, IDLE, false>(a, max_pairs, st);
 }
 
 template <int G, int WL>

@@ -263,6 +263,9 @@ void launch_envelope32(const double* q, uint32_t nq, uint32_t d, uint32_t len, u
                        uint32_t r, float err, float* lo, float* hi, cudaStream_t st);
 void launch_envelope64(const double* q, uint32_t nq, uint32_t d, uint32_t len, uint64_t qstride,
                        uint32_t r, double* lo, double* hi, cudaStream_t st);
+// the reference's fp64 lb_box(candidate, envelope) of every candidate, serial flat order
+void launch_lb64_serial(const StoreDev& s, const double* lo, const double* hi, uint32_t len,
+                        double* out, cudaStream_t st);
 // row-major [nser][len][d] -> tiled series of `stride` elements at `pitch` spacing; padding
 // points and the guard tile after each series (pitch - stride elements) hold `pad`
 void launch_rowmajor_to_tiled(const double* src, uint64_t nser, uint32_t len, uint32_t d,

@@ -248,13 +248,22 @@ std::vector<SearchReport> knn_any(const std::vector<TimeSeries>& queries, const 
 }  // namespace
 
 double pruning_power(const Dataset& queries, const Dataset& data, BandRadius r) {
-    const auto reps = knn_any(queries.series(), data, 1, TSW_METRIC_DTW, r.value, "knn_dtw");
-    double pruned = 0.0, computed = 0.0;
-    for (const auto& rep : reps) {
-        pruned += static_cast<double>(rep.counters.lb_pruned);
-        computed += static_cast<double>(rep.counters.lb_computed);
+    // the reference's 1-NN scan schedule replayed exactly on the GPU (tsw_pruning_power): the
+    // count does not depend on this engine's own pruning order
+    auto& st = data.device_store();
+    double pruned = 0.0, total = 0.0;
+    for (std::size_t i = 0; i < queries.size(); ++i) {
+        const TimeSeries& q = queries[i];
+        if (q.dim() != data.dim())
+            throw std::invalid_argument("knn_dtw: query dim " + std::to_string(q.dim()) +
+                                        " != dataset dim " + std::to_string(data.dim()));
+        double p = 0.0;
+        const int rc = tsw_pruning_power(st.h, q.flat().data(), 1, q.length(), r.value, &p, nullptr);
+        if (rc != TSW_OK) detail::rethrow(rc);
+        pruned += p * static_cast<double>(data.size());
+        total += static_cast<double>(data.size());
     }
-    return computed > 0.0 ? pruned / computed : 0.0;
+    return total > 0.0 ? pruned / total : 0.0;
 }
 
 double loo_accuracy(const Dataset& data, MetricKind metric, BandRadius r) {

@@ -122,6 +122,8 @@ def lib():
     L.tsw_envelope.argtypes = [_dp, _u64, _u64, _u64, _dp, _dp]
     L.tsw_lb_box_all.argtypes = [_vp, _dp, _u64, _u64, _dp, _dp]
     L.tsw_dist_all.argtypes = [_vp, _dp, _u64, C.c_int, _u64, C.c_double, _ip, _dp]
+    L.tsw_lb_box_exact_all.argtypes = [_vp, _dp, _u64, _u64, _dp]
+    L.tsw_pruning_power.argtypes = [_vp, _dp, _u64, _u64, _u64, C.POINTER(C.c_double), _up]
     L.tsw_sub_dk_all.argtypes = [_vp, _dp, _u64, C.c_double, _ip, _dp, _up]
     L.tsw_last_transfer_bytes.argtypes = [_up, _up]
     L.tsw_fp64_peak.argtypes = [_dp]
@@ -363,15 +365,34 @@ def _by_length(data: Dataset):
 
 
 def pruning_power(queries: Dataset, data, r: int) -> float:
-    """Fraction of candidate DTW computations skipped by LB_Box over 1-NN DTW scans of every
-    query: sum(lb_pruned) / sum(lb_computed) (this engine's threshold schedule)."""
-    pruned = computed = 0
+    """pruning_power (metrics.hpp:54-56): the fraction of candidate DTW computations the lb_box
+    test skips over 1-NN knn_dtw scans of every query, with the reference's own scan schedule
+    (64-candidate blocks, block-frozen threshold, search.cpp:139-162) replayed exactly on the
+    GPU (tsw_pruning_power) -- deterministic and equal to the reference's counters."""
+    st = _as_store(data)
+    pruned = total = 0
     for L, ids in _by_length(queries).items():
-        qs = np.stack([queries.series(i) for i in ids])
-        _, _, c = knn(data, qs, 1, "dtw", r)
-        pruned += int(c[:, 1].sum())
-        computed += int(c[:, 0].sum())
-    return pruned / computed if computed else 0.0
+        qs = np.ascontiguousarray(np.stack([queries.series(i) for i in ids]), dtype=np.float64)
+        if qs.shape[2] != st.dim:
+            raise ValueError(f"knn_dtw: query dim {qs.shape[2]} != dataset dim {st.dim}")
+        per = np.zeros(len(ids), dtype=np.uint64)
+        p = C.c_double()
+        _check(lib().tsw_pruning_power(st.handle, qs.ctypes.data_as(_dp), len(ids), L, r,
+                                       C.byref(p), per.ctypes.data_as(_up)))
+        pruned += int(per.sum())
+        total += len(ids) * st.n
+    return pruned / total if total else 0.0
+
+
+def lb_box_exact_all(data, query, r: int) -> np.ndarray:
+    """The reference's fp64 lb_box(data[i], envelope(query, r)) for every candidate, bit for
+    bit (lower_bounds.cpp:19-46) -- not the pipeline's fp32 bound."""
+    q = _series(query)
+    st = _as_store(data)
+    out = np.empty(st.n)
+    _check(lib().tsw_lb_box_exact_all(st.handle, q.ctypes.data_as(_dp), q.shape[0], r,
+                                      out.ctypes.data_as(_dp)))
+    return out
 
 
 def loo_accuracy(data: Dataset, metric: str = "dtw", r: int = 0) -> float:

@@ -98,5 +98,10 @@ def test_bench_accuracy_and_pruning(files, port):
     pp = float(r.stdout.strip().splitlines()[1].split(",")[1])
     assert 0.0 <= pp <= 1.0
     assert pp == t.pruning_power(t.load_dataset(query), t.load_dataset(data), 3)
+    # the reference's own counters (knn_dtw, k = 1) give the same fraction exactly
+    qs = t.load_dataset(query)
+    ods = oracle.Dataset(X)
+    pruned = sum(int(port.knn(qs.series(i), ods, 1, "dtw", 3)[2][1]) for i in range(len(qs)))
+    assert pp == pruned / (len(qs) * len(X))
     r = run("bench", "speedup", "--data", data, "--query", query, "--band", "3", "--reps", "2")
     assert r.returncode == 0 and float(r.stdout.strip().splitlines()[1].split(",")[1]) > 0

@@ -579,3 +579,26 @@ def test_dtw_fast_path_variants(tsw, best_oracle, revcb, noidle, monkeypatch):
             oi, od, _ = best_oracle.knn(Q[q], ods, k, "dtw", r)
             assert_knn_equal(gi[q], gd[q], oi, od, f"n={n} L={L} d={d} r={r} q{q}")
             _check_counters(gc[q], n, "dtw")
+
+
+def test_lb_box_exact_and_pruning_power_match_reference(tsw, best_oracle):
+    """tsw_lb_box_exact_all is the reference's fp64 lb_box bit for bit, and pruning_power
+    replays the reference's 1-NN scan schedule exactly: its pruned count equals the sum of the
+    reference knn_dtw's lb_pruned counters (deterministic, unlike this engine's own counters)."""
+    import oracle
+
+    rng = np.random.default_rng(12)
+    for n, L, d, r in ((700, 60, 3, 6), (300, 128, 2, 13), (257, 33, 1, 0)):
+        X = walks(rng, n, L, d)
+        Q = walks(rng, 5, L, d)
+        Q[2] = X[100]  # self-match: distance 0 found mid-scan
+        st = tsw.Store(X)
+        for q in Q[:2]:
+            lb = tsw.lb_box_exact_all(st, q, r)
+            ref = np.array([best_oracle.lb_box(X[i], q, r) for i in range(n)])
+            assert np.array_equal(lb.view(np.uint64), ref.view(np.uint64))
+        ds = tsw.Dataset(X)
+        pp = tsw.pruning_power(tsw.Dataset(list(Q)), ds, r)
+        ods = oracle.Dataset(X)
+        pruned = sum(int(best_oracle.knn(q, ods, 1, "dtw", r)[2][1]) for q in Q)
+        assert pp == pruned / (len(Q) * n), (pp, pruned)
