@@ -744,6 +744,9 @@ __global__ void __launch_bounds__(256, 2) lb_env_kernel(LbCompactArgs a, uint32_
 // max(|q32 - m| - RU(h + eq), 0)^2 with RZ / RD rounding, eq >= |q - fp32(q)|: a rigorous lower
 // bound of dist(q, [lo, hi])^2.
 constexpr int kList = 128;  // listed survivors per warp before a reverse-bound flush
+#ifndef TSW_LB12_PACK
+#define TSW_LB12_PACK false  // packed FP32x2 forward terms: spill here (C5 pass 5.7 -> 7.7 ms)
+#endif
 
 template <int QB, int CB, int FCH>  // FCH: float4 per lane per envelope chunk
 __device__ __forceinline__ void lb2_flush(const LbCompactArgs& a, uint32_t c0, QEntry* list,
@@ -903,7 +906,7 @@ __global__ void __launch_bounds__(256, 2) lb12_compact_kernel(LbCompactArgs a) {
         const uint32_t c0 = cg * CB;
         int cnt = 0;
         for (uint32_t qbk = 0; qbk < nqb; ++qbk) {
-            const TileOut t = lb1_tile<QB, CB, false, false>(a, pc, c0, qbk * QB, stash, total4);
+            const TileOut t = lb1_tile<QB, CB, false, TSW_LB12_PACK>(a, pc, c0, qbk * QB, stash, total4);
             const unsigned tm = __ballot_sync(0xffffffffu, t.take);
             if (t.take) list[cnt + __popc(tm & ((1u << lane) - 1u))] = QEntry{t.q, t.c, t.lb, t.ps};
             cnt += __popc(tm);

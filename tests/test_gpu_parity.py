@@ -3,8 +3,9 @@
 Bar (BASELINE.json north_star): neighbour indices and order bit-exact under the (distance,
 index) tie rule; DK distances bit-exact; DTW distances bit-exact (allowed: 1e-12 relative,
 asserted exactly here because the suffix-order recursion is reproduced).
-LB_Box is summed in a different order, so it is compared with rel. tolerance 1e-12.
-All calls go through the C ABI (libtswarp_b200.so).
+The pipeline's LB_Box is an fp32 directed-rounding LOWER bound of the reference's value (checked
+lb <= oracle, and within rel. 2e-5 of it); the fp64 restatement tsw_lb_box_exact_all is compared
+with the reference bit for bit.  All calls go through the C ABI (libtswarp_b200.so).
 """
 import numpy as np
 import pytest
