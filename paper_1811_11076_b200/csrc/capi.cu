@@ -394,8 +394,11 @@ std::unique_ptr<tsw_plan> make_plan(tsw_store* s, uint64_t nq_max, uint64_t qlen
         const bool want_lb2 = lb2e ? std::atoi(lb2e) != 0 : r >= 32;
         // the candidate envelopes also feed the DP's reverse cumulative abandon bound; for
         // narrow bands (no reverse LB pass) only with TSW_CENV_DP=1 (measurements)
+        // the large-d path (d >= 5, r <= 31: dtwt) pays for it: per-cell work is 3d + 2 FP64
+        // operations, the per-pair setup L * d terms
         const char* cde = std::getenv("TSW_CENV_DP");
-        const bool want_cenv = want_lb2 || (cde && std::atoi(cde) != 0);
+        const bool big_d = s->d >= 5 && std::min<uint64_t>(r, qlen - 1) <= 31;
+        const bool want_cenv = want_lb2 || (cde ? std::atoi(cde) != 0 : big_d);
         p->lb2 = want_lb2;
         if (want_cenv) {
             const uint64_t bytes = 2 * (s->guard + n * s->ustride) * sizeof(float);

@@ -67,9 +67,14 @@ __global__ void __launch_bounds__(TPB, MINB) dtwt_kernel(DpArgs a, uint32_t pstr
     const int lane = threadIdx.x & 31;
     const int wib = threadIdx.x >> 5;
     double* ring = smem_t + (size_t)wib * (kRing * kRP);
-    float* pfx = (a.spill ? reinterpret_cast<float*>(a.spill + (size_t)blockIdx.x * a.spill_block)
-                          : reinterpret_cast<float*>(smem_t + (size_t)(TPB / 32) * (kRing * kRP))) +
-                 (size_t)wib * pstride;
+    float* pbig = a.spill ? reinterpret_cast<float*>(a.spill + (size_t)blockIdx.x * a.spill_block)
+                          : reinterpret_cast<float*>(smem_t + (size_t)(TPB / 32) * (kRing * kRP));
+    float* pfx = pbig + (size_t)wib * pstride;
+    // reverse cumulative bound (candidate envelopes present, dtw_common.cuh setup_pfq): the
+    // warp's pfq row after the pfx rows
+    const bool rev = a.cenv_m != nullptr;
+    float* pfq = rev ? pbig + (size_t)(TPB / 32) * pstride + (size_t)wib * pstride : pfx;
+    const float eq = rev ? __double2float_ru(__dmul_ru(*a.qabsmax, 0x1p-24)) : 0.0f;
     const int d = (int)a.store.d;
     const int s32d = 32 * d;
     const int L = (int)a.qlen;
@@ -115,6 +120,7 @@ __global__ void __launch_bounds__(TPB, MINB) dtwt_kernel(DpArgs a, uint32_t pstr
         const double* sq = a.queries + (uint64_t)pr.q * a.qstride;
         const double* tc = a.store.data + series_off(a.store, pr.c);
         setup_pfx<32>(a, pr, lane, kFull, pfx, L, d);
+        if (rev) setup_pfq<32>(a, pr, lane, kFull, pfq, L, d, eq);
         double v[2];
         v[0] = (lane == pstar && RPAR == 0) ? 0.0 : kInf;  // (0,0)'s diagonal predecessor
         v[1] = (lane == pstar && RPAR == 1) ? 0.0 : kInf;
@@ -247,7 +253,10 @@ __global__ void __launch_bounds__(TPB, MINB) dtwt_kernel(DpArgs a, uint32_t pstr
                 const int o = obase + e;
                 const int jp = itl - (o >> 1) + o;
                 const int tj = min(max(L - 1 - jp, 0), L - 1);
-                alive |= okm[e] && dadd(v[e], (double)pfx[tj >> plog]) <= Tm;
+                // the cell's query row (reversed index itl - (o >> 1)) in original order
+                const int si = min(max(L - 1 - (itl - (o >> 1)), 0), L - 1);
+                const float rb = rev ? fmaxf(pfx[tj >> plog], pfq[si]) : pfx[tj >> plog];
+                alive |= okm[e] && dadd(v[e], (double)rb) <= Tm;
             }
             if (!__any_sync(kFull, alive)) break;
             __syncwarp();  // the next cost phase overwrites ring rows this phase's DP read
@@ -291,7 +300,7 @@ void launch_dtwt(const DpArgs& a, uint32_t max_pairs, cudaStream_t st) {
     constexpr int TPB = 128, MINB = 4;
     const uint32_t pstride = (std::max<uint32_t>(a.qlen + 1, kPfxBlocks + 1) + 3) & ~3u;
     const size_t fixed = (size_t)(TPB / 32) * kRing * kRP * sizeof(double);
-    const size_t big = (size_t)(TPB / 32) * pstride * sizeof(float);
+    const size_t big = (size_t)(TPB / 32) * pstride * sizeof(float) * (a.cenv_m ? 2 : 1);
     const bool spill = fixed + big > smem_optin();
     const size_t smem = spill ? fixed : fixed + big;
     const uint32_t r = std::min(a.r, a.qlen - 1);
