@@ -449,7 +449,10 @@ template <int G, int D, int WL, int RPAR, bool IDLE, bool LONG>
 void run4(const DpArgs& a, uint32_t max_pairs, cudaStream_t st) {
     // 128-thread blocks: finer occupancy steps at ~100 registers per thread
     constexpr int TPB = 128;
-    constexpr int MINB = 4;
+#ifndef TSW_DTW4_MINB
+#define TSW_DTW4_MINB 4
+#endif
+    constexpr int MINB = TSW_DTW4_MINB;
     const uint32_t pstride = (std::max<uint32_t>(a.qlen + 1, kPfxBlocks + 1) + 3) & ~3u;
     const size_t fixed = (size_t)(TPB / WL) * sizeof(Stage) +
                          (a.state && a.nq <= kAbLocalMax ? ((a.nq + 3) & ~3u) * sizeof(unsigned) : 0);
