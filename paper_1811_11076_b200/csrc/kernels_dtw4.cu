@@ -173,7 +173,9 @@ __device__ __forceinline__ void iter(Lane<G, D>& s, const double* __restrict__ s
     }
 }
 
-template <int G, int D, int WL, int RPAR, bool IDLE, bool FIN>
+// TWO: two rotations of the point windows per body (2P iterations, one threshold read, one
+// staging step, one abandon check) -- long series, where a pair runs hundreds of iterations
+template <int G, int D, int WL, int RPAR, bool IDLE, bool FIN, bool TWO>
 __device__ __forceinline__ void body(Lane<G, D>& s, const double* __restrict__ sq,
                                      const double* __restrict__ tc, int gl, int edge, int it,
                                      int tb0, int sb0, unsigned okm, const float* __restrict__ pfx,
@@ -187,17 +189,24 @@ __device__ __forceinline__ void body(Lane<G, D>& s, const double* __restrict__ s
     if (st) T = ld_volatile(&st->T);
     // slot of offset 0: parity RPAR, +2 when ehi (G = 2)
     constexpr int E0 = RPAR, E1 = G == 2 ? RPAR + 2 : RPAR;
-#define TSW_ITER4(PH)                                                                          \
+#define TSW_ITER4(PH, OFF, CK)                                                                 \
     if constexpr (PH < P) {                                                                    \
-        iter<G, D, WL, RPAR, IDLE, PH == P - 1, PH>(s, sq, tc, gl, edge, tb0 - (it + PH),      \
-                                                    sb0 - (it + PH), okm, pfx, pfq, plog, L, T,\
-                                                    margin, alive);                            \
-        if (FIN && it + PH == L - 1) fin = ehi ? s.v[E1] : s.v[E0];                            \
+        iter<G, D, WL, RPAR, IDLE, CK && PH == P - 1, PH>(s, sq, tc, gl, edge,                 \
+                                                          tb0 - (it + OFF + PH),               \
+                                                          sb0 - (it + OFF + PH), okm, pfx, pfq,\
+                                                          plog, L, T, margin, alive);          \
+        if (FIN && it + OFF + PH == L - 1) fin = ehi ? s.v[E1] : s.v[E0];                      \
     }
-    TSW_ITER4(0)
-    TSW_ITER4(1)
-    TSW_ITER4(2)
-    TSW_ITER4(3)
+    TSW_ITER4(0, 0, !TWO)
+    TSW_ITER4(1, 0, !TWO)
+    TSW_ITER4(2, 0, !TWO)
+    TSW_ITER4(3, 0, !TWO)
+    if constexpr (TWO) {
+        TSW_ITER4(0, P, true)
+        TSW_ITER4(1, P, true)
+        TSW_ITER4(2, P, true)
+        TSW_ITER4(3, P, true)
+    }
 #undef TSW_ITER4
 }
 
@@ -410,13 +419,25 @@ __global__ void __launch_bounds__(TPB, MINB) dtw4_kernel(DpArgs a, uint32_t pstr
         if (!have) s.qo = s.co = 0;  // idle group: keep its (ignored) loads inside the guards
         // (the redundant `L <= 256` test in the LONG form is deliberate: that code generation
         // measured C5 DP 12.6 -> 11.1 ms against the plain `__any_sync` form, same registers)
-        if (!LONG || L <= 256 || __any_sync(kFull, have && it + P >= L))
-            body<G, D, WL, RPAR, IDLE, true>(s, sq, tc, gl, edge, it, tb0, sb0, okm, pfx, pfq,
-                                             plog, L, st, a.margin, T, alive, fin, estar >= 2);
-        else
-            body<G, D, WL, RPAR, IDLE, false>(s, sq, tc, gl, edge, it, tb0, sb0, okm, pfx, pfq,
-                                              plog, L, st, a.margin, T, alive, fin, estar >= 2);
-        it += P;
+#ifndef TSW_DTW4_TWO
+#define TSW_DTW4_TWO 1
+#endif
+        // LONG: 2P-iteration bodies while every group of the warp is more than 2P iterations
+        // from its pair's end; the final bodies are single-P ones with the final-cell capture,
+        // so a pair never runs more than P - 1 iterations past its last cell (the guard tiles
+        // cover that, dtw4_supported)
+        constexpr bool TWO = LONG && TSW_DTW4_TWO;
+        if (!LONG || L <= 256 || __any_sync(kFull, have && it + 2 * P >= L)) {
+            body<G, D, WL, RPAR, IDLE, true, false>(s, sq, tc, gl, edge, it, tb0, sb0, okm, pfx,
+                                                    pfq, plog, L, st, a.margin, T, alive, fin,
+                                                    estar >= 2);
+            it += P;
+        } else {
+            body<G, D, WL, RPAR, IDLE, false, TWO>(s, sq, tc, gl, edge, it, tb0, sb0, okm, pfx,
+                                                   pfq, plog, L, st, a.margin, T, alive, fin,
+                                                   estar >= 2);
+            it += TWO ? 2 * P : P;
+        }
         const unsigned bal = __ballot_sync(kFull, alive) & gmask;
         const bool completed = have && it >= L;
         const bool finished = completed || (have && bal == 0u);  // complete, or a dead cut
