@@ -173,9 +173,10 @@ __device__ __forceinline__ void iter(Lane<G, D>& s, const double* __restrict__ s
     }
 }
 
-// TWO: two rotations of the point windows per body (2P iterations, one threshold read, one
-// staging step, one abandon check) -- long series, where a pair runs hundreds of iterations
-template <int G, int D, int WL, int RPAR, bool IDLE, bool FIN, bool TWO>
+// ROT: rotations of the point windows per body (ROT * P iterations, one threshold read, one
+// staging step, one abandon check) -- > 1 for long series, where a pair runs hundreds of
+// iterations
+template <int G, int D, int WL, int RPAR, bool IDLE, bool FIN, int ROT>
 __device__ __forceinline__ void body(Lane<G, D>& s, const double* __restrict__ sq,
                                      const double* __restrict__ tc, int gl, int edge, int it,
                                      int tb0, int sb0, unsigned okm, const float* __restrict__ pfx,
@@ -197,15 +198,27 @@ __device__ __forceinline__ void body(Lane<G, D>& s, const double* __restrict__ s
                                                           plog, L, T, margin, alive);          \
         if (FIN && it + OFF + PH == L - 1) fin = ehi ? s.v[E1] : s.v[E0];                      \
     }
-    TSW_ITER4(0, 0, !TWO)
-    TSW_ITER4(1, 0, !TWO)
-    TSW_ITER4(2, 0, !TWO)
-    TSW_ITER4(3, 0, !TWO)
-    if constexpr (TWO) {
-        TSW_ITER4(0, P, true)
-        TSW_ITER4(1, P, true)
-        TSW_ITER4(2, P, true)
-        TSW_ITER4(3, P, true)
+    TSW_ITER4(0, 0, ROT == 1)
+    TSW_ITER4(1, 0, ROT == 1)
+    TSW_ITER4(2, 0, ROT == 1)
+    TSW_ITER4(3, 0, ROT == 1)
+    if constexpr (ROT >= 2) {
+        TSW_ITER4(0, P, ROT == 2)
+        TSW_ITER4(1, P, ROT == 2)
+        TSW_ITER4(2, P, ROT == 2)
+        TSW_ITER4(3, P, ROT == 2)
+    }
+    if constexpr (ROT >= 3) {
+        TSW_ITER4(0, 2 * P, ROT == 3)
+        TSW_ITER4(1, 2 * P, ROT == 3)
+        TSW_ITER4(2, 2 * P, ROT == 3)
+        TSW_ITER4(3, 2 * P, ROT == 3)
+    }
+    if constexpr (ROT >= 4) {
+        TSW_ITER4(0, 3 * P, true)
+        TSW_ITER4(1, 3 * P, true)
+        TSW_ITER4(2, 3 * P, true)
+        TSW_ITER4(3, 3 * P, true)
     }
 #undef TSW_ITER4
 }
@@ -419,24 +432,30 @@ __global__ void __launch_bounds__(TPB, MINB) dtw4_kernel(DpArgs a, uint32_t pstr
         if (!have) s.qo = s.co = 0;  // idle group: keep its (ignored) loads inside the guards
         // (the redundant `L <= 256` test in the LONG form is deliberate: that code generation
         // measured C5 DP 12.6 -> 11.1 ms against the plain `__any_sync` form, same registers)
-#ifndef TSW_DTW4_TWO
-#define TSW_DTW4_TWO 1
+#ifndef TSW_DTW4_ROT
+#define TSW_DTW4_ROT 3  // (C5 DP: 1 -> 11.07, 2 -> 10.09, 3 -> 10.02, 4 -> 10.25 ms)
 #endif
         // LONG: 2P-iteration bodies while every group of the warp is more than 2P iterations
         // from its pair's end; the final bodies are single-P ones with the final-cell capture,
         // so a pair never runs more than P - 1 iterations past its last cell (the guard tiles
         // cover that, dtw4_supported)
-        constexpr bool TWO = LONG && TSW_DTW4_TWO;
-        if (!LONG || L <= 256 || __any_sync(kFull, have && it + 2 * P >= L)) {
-            body<G, D, WL, RPAR, IDLE, true, false>(s, sq, tc, gl, edge, it, tb0, sb0, okm, pfx,
-                                                    pfq, plog, L, st, a.margin, T, alive, fin,
-                                                    estar >= 2);
+        // short series: 2 rotations per body for the wide groups (C3, r = 26: DP -6%), 1 for
+        // the 8-lane groups (C2, r = 13: pairs die after ~19 iterations, 2 rotations +12%)
+        constexpr int ROT = LONG ? TSW_DTW4_ROT : (WL >= 16 ? 2 : 1);
+#ifndef TSW_DTW4_LONGMIN
+#define TSW_DTW4_LONGMIN 256  // series longer than this use the LONG variant
+#endif
+        if (LONG ? (L <= TSW_DTW4_LONGMIN || __any_sync(kFull, have && it + ROT * P >= L))
+                 : (ROT == 1 || __any_sync(kFull, have && it + ROT * P >= L))) {
+            body<G, D, WL, RPAR, IDLE, true, 1>(s, sq, tc, gl, edge, it, tb0, sb0, okm, pfx,
+                                                pfq, plog, L, st, a.margin, T, alive, fin,
+                                                estar >= 2);
             it += P;
         } else {
-            body<G, D, WL, RPAR, IDLE, false, TWO>(s, sq, tc, gl, edge, it, tb0, sb0, okm, pfx,
+            body<G, D, WL, RPAR, IDLE, false, ROT>(s, sq, tc, gl, edge, it, tb0, sb0, okm, pfx,
                                                    pfq, plog, L, st, a.margin, T, alive, fin,
                                                    estar >= 2);
-            it += TWO ? 2 * P : P;
+            it += ROT * P;
         }
         const unsigned bal = __ballot_sync(kFull, alive) & gmask;
         const bool completed = have && it >= L;
@@ -510,7 +529,7 @@ void run4_dl(const DpArgs& a, uint32_t max_pairs, cudaStream_t st) {
 template <int G, int WL, int RPAR, bool IDLE>
 void run4_d(const DpArgs& a, uint32_t max_pairs, cudaStream_t st) {
     if constexpr (G == 2 && WL >= 16) {
-        if (a.qlen > 256 && std::getenv("TSW_DTW4_NOLONG") == nullptr) {
+        if (a.qlen > TSW_DTW4_LONGMIN && std::getenv("TSW_DTW4_NOLONG") == nullptr) {
             run4_dl<G, WL, RPAR, IDLE, true>(a, max_pairs, st);
             return;
         }
