@@ -452,7 +452,7 @@ __device__ __forceinline__ TileOut lb1_tile(const LbCompactArgs& a, PruneCount& 
                                             const float4* slo = nullptr, const float4* shi = nullptr) {
     static_assert(QB * CB == 32, "one pair per lane after the reduction");
     const unsigned lane = lane_id();
-    const uint32_t n = a.store.n;
+    const uint32_t n = a.c_hi;  // the pass's candidate range ends here (staged execution)
     // base pointers only (per-query / per-candidate offsets are recomputed: register budget)
     const float4* xb = reinterpret_cast<const float4*>(a.store.data32) + (uint64_t)c0 * (a.store.ustride / 4);
     const uint64_t xs = a.store.ustride / 4;
@@ -532,7 +532,7 @@ __device__ __forceinline__ TileOut lb1_tile(const LbCompactArgs& a, PruneCount& 
     const bool valid = t.q < a.nq && t.c < n;
     if (valid) {
         const double lb = (double)t.lb;
-        if (a.lb_out) a.lb_out[(uint64_t)t.q * n + t.c] = t.lb;
+        if (a.lb_out) a.lb_out[(uint64_t)t.q * a.store.n + t.c] = t.lb;
         if (a.state) {
             const double T = a.state[t.q].T;
             const bool probed = a.probed && a.probed[(uint64_t)t.c * a.nq + t.q];
@@ -585,7 +585,8 @@ __global__ void __launch_bounds__(256, 3) lb_few_kernel(LbCompactArgs a) {
     double T[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) T[q] = a.state ? a.state[q].T : kInf;
-    for (uint64_t c = w0; c < n; c += nw) {
+    (void)n;
+    for (uint64_t c = a.c_lo + w0; c < a.c_hi; c += nw) {
         const float4* xb = reinterpret_cast<const float4*>(a.store.data32) + c * (a.store.ustride / 4);
         float acc[NQ];
 #pragma unroll
@@ -650,8 +651,8 @@ __global__ void __launch_bounds__(256, 3) lb_few_kernel(LbCompactArgs a) {
 
 template <int QB, int CB>
 __global__ void __launch_bounds__(256, 2) lb_compact_kernel(LbCompactArgs a) {
-    const uint32_t n = a.store.n;
-    const uint64_t ngroups = (n + CB - 1) / CB;
+    const uint32_t g_lo = a.c_lo / CB;  // candidate groups of the pass's range (c_lo % CB == 0)
+    const uint64_t ngroups = (a.c_hi + CB - 1) / CB - g_lo;
     const uint32_t nqb = (a.nq + QB - 1) / QB;
     const uint64_t wid = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
@@ -669,7 +670,7 @@ __global__ void __launch_bounds__(256, 2) lb_compact_kernel(LbCompactArgs a) {
         // warps, so the group's bytes come from HBM once and are re-read from L1/L2
         const uint64_t cg = w / nqb;
         const uint32_t qbk = (uint32_t)(w - cg * nqb);
-        const TileOut t = lb1_tile<QB, CB>(a, pc, (uint32_t)cg * CB, qbk * QB, stash, total4);
+        const TileOut t = lb1_tile<QB, CB>(a, pc, (uint32_t)(g_lo + cg) * CB, qbk * QB, stash, total4);
         if (a.state) enqueue(sg, a.queue, t.take, t.near, t.q, t.c, t.lb, t.ps);
     }
     if (a.state) {
@@ -689,8 +690,8 @@ __global__ void __launch_bounds__(256, 2) lb_compact_kernel(LbCompactArgs a) {
 // running at the same time cover the same candidate chunks (their bytes come from L2).
 template <int QB, int CB>
 __global__ void __launch_bounds__(256, 2) lb_env_kernel(LbCompactArgs a, uint32_t chunk) {
-    const uint32_t n = a.store.n;
-    const uint32_t ngroups = (n + CB - 1) / CB;
+    const uint32_t g_lo = a.c_lo / CB;  // candidate groups of the pass's range (c_lo % CB == 0)
+    const uint32_t ngroups = (a.c_hi + CB - 1) / CB - g_lo;
     const uint32_t nqb = (a.nq + QB - 1) / QB;
     const uint32_t nchunks = (ngroups + chunk - 1) / chunk;
     const uint32_t total4 = (uint32_t)(a.store.tstride / 4);
@@ -723,7 +724,7 @@ __global__ void __launch_bounds__(256, 2) lb_env_kernel(LbCompactArgs a, uint32_
         }
         const uint32_t gend = min((ch + 1) * chunk, ngroups);
         for (uint32_t g = ch * chunk + warp; g < gend; g += 8) {
-            const TileOut t = lb1_tile<QB, CB, true>(a, pc, g * CB, qbk * QB, stash, total4, elo, ehi);
+            const TileOut t = lb1_tile<QB, CB, true>(a, pc, (g_lo + g) * CB, qbk * QB, stash, total4, elo, ehi);
             if (a.state) enqueue(sg, a.queue, t.take, t.near, t.q, t.c, t.lb, t.ps);
         }
     }
@@ -764,7 +765,7 @@ __device__ __forceinline__ void lb2_flush(const LbCompactArgs& a, uint32_t c0, Q
     const uint32_t qs4 = (uint32_t)(a.qstride / 4);
     for (int cb = 0; cb < CB; ++cb) {
         const uint32_t c = c0 + cb;
-        if (c >= a.store.n) break;
+        if (c >= a.c_hi) break;
         const uint64_t co = series_off(a.store, c) / 4;
         const float4* m4 = reinterpret_cast<const float4*>(a.cenv_m) + co;
         const float4* h4 = reinterpret_cast<const float4*>(a.cenv_h) + co;
@@ -879,8 +880,8 @@ __device__ __forceinline__ void lb2_flush(const LbCompactArgs& a, uint32_t c0, Q
 template <int QB, int CB, int FCH>
 __global__ void __launch_bounds__(256, 2) lb12_compact_kernel(LbCompactArgs a) {
     const unsigned lane = lane_id();
-    const uint32_t n = a.store.n;
-    const uint32_t ngroups = (n + CB - 1) / CB;
+    const uint32_t g_lo = a.c_lo / CB;  // candidate groups of the pass's range (c_lo % CB == 0)
+    const uint32_t ngroups = (a.c_hi + CB - 1) / CB - g_lo;
     const uint32_t nqb = (a.nq + QB - 1) / QB;
     const uint32_t total4 = (uint32_t)(a.store.tstride / 4);
     __shared__ QEntry stage_buf[8][2][kStage];
@@ -903,7 +904,7 @@ __global__ void __launch_bounds__(256, 2) lb12_compact_kernel(LbCompactArgs a) {
         if (lane == 0) cg = atomicAdd(a.task, 1u);  // dynamic: groups' reverse work varies
         cg = __shfl_sync(0xffffffffu, cg, 0);
         if (cg >= ngroups) break;
-        const uint32_t c0 = cg * CB;
+        const uint32_t c0 = (g_lo + cg) * CB;
         int cnt = 0;
         for (uint32_t qbk = 0; qbk < nqb; ++qbk) {
             const TileOut t = lb1_tile<QB, CB, false, TSW_LB12_PACK>(a, pc, c0, qbk * QB, stash, total4);
@@ -922,8 +923,13 @@ __global__ void __launch_bounds__(256, 2) lb12_compact_kernel(LbCompactArgs a) {
     pc.flush();
 }
 
-void launch_lb_compact(const LbCompactArgs& a, cudaStream_t st) {
+void launch_lb_compact(const LbCompactArgs& a_in, cudaStream_t st) {
     constexpr int QB = 8, CB = 4;
+    LbCompactArgs a = a_in;
+    if (a.c_hi == 0) {  // the whole store
+        a.c_lo = 0;
+        a.c_hi = a.store.n;
+    }
     const size_t smem = a.pfx_out ? (size_t)8 * 32 * 32 * sizeof(float) : 0;
     if (a.cenv_m && a.state) {
         // fused forward + reverse bound; envelope chunk = the whole series when it fits 4

@@ -334,6 +334,7 @@ struct LbCompactArgs {
     const float* q32;         // fp32 (round-to-nearest) queries, pitch qstride
     const double* qabsmax;    // max |query value|: the fp32 conversion error is <= it * 2^-24
     unsigned* task;           // candidate-group work counter (zeroed per execute)
+    uint32_t c_lo, c_hi;      // candidate range of this pass (staged execution; c_lo % 4 == 0)
 };
 void launch_lb_compact(const LbCompactArgs& a, cudaStream_t st);
 

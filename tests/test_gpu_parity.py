@@ -608,3 +608,27 @@ def test_lb_box_exact_and_pruning_power_match_reference(tsw, best_oracle):
         ods = oracle.Dataset(X)
         pruned = sum(int(best_oracle.knn(q, ods, 1, "dtw", r)[2][1]) for q in Q)
         assert pp == pruned / (len(Q) * n), (pp, pruned)
+
+
+@pytest.mark.parametrize("stages", ["1", "2"])
+def test_staged_dtw_execution(tsw, best_oracle, stages, monkeypatch):
+    """Staged DTW execution (the first quarter of the candidates bounded and DP'd first, the
+    rest against the stage-1 threshold; default for n >= 96k) gives the reference's neighbours
+    through every LB pass variant: shared-memory envelopes (short series), the L1 tile pass,
+    the fused reverse pass (r >= 32) and the 1-3 query pass."""
+    import oracle
+
+    monkeypatch.setenv("TSW_STAGES", stages)
+    rng = np.random.default_rng(404)
+    for n, L, d, r, k, nq in ((2001, 64, 3, 6, 3, 9), (1500, 300, 2, 40, 2, 6), (900, 96, 6, 9, 1, 5),
+                              (1203, 128, 3, 13, 4, 2), (640, 200, 3, 51, 10, 4)):
+        X = walks(rng, n, L, d)
+        Q = walks(rng, nq, L, d)
+        Q[0] = X[n - 7] + 1e-3 * rng.standard_normal((L, d))  # a neighbour in stage 2
+        Q[-1] = X[3] + 1e-3 * rng.standard_normal((L, d))     # ... and one in stage 1
+        gi, gd, gc = tsw.knn(tsw.Dataset(X), Q, k, "dtw", r)
+        ods = oracle.Dataset(X)
+        for q in range(nq):
+            oi, od, _ = best_oracle.knn(Q[q], ods, k, "dtw", r)
+            assert_knn_equal(gi[q], gd[q], oi, od, f"stages={stages} n={n} L={L} d={d} r={r} q{q}")
+            _check_counters(gc[q], n, "dtw")
