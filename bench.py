@@ -437,9 +437,11 @@ def gpu_leg(a, t, torch, store, db, cfg, metric, sh, qs, stream, flush, ws, rank
                 "frac": (lb_gbs / peaks["hbm_gbs"]) if lb_gbs else None,
                 "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json copy rate)",
                 "algorithmic_bytes_per_launch": ph["bound_bytes"] / max(1.0, ph["bound_passes"]),
-                "bytes_note": "padded fp32 shadow store (32-point tiles incl. guard tiles) + "
-                              "for r >= 32 the cached fp32 candidate envelopes; the SURVEY "
-                              "§8(d) fp64 view N*L*d*8 is fp64_store_bytes",
+                "bytes_note": "padded fp32 shadow store (32-point tiles incl. guard tiles; "
+                              "2.5 GB at C5, built at store creation) + for the fused reverse "
+                              "pass (r >= 32, >= 4 queries) the cached fp32 candidate envelopes "
+                              "(midpoint + half-width, 2x the shadow store); the SURVEY §8(d) "
+                              "fp64 view N*L*d*8 is fp64_store_bytes",
                 "fp64_store_bytes": fp64_store,
                 "fp64_view_gbs": fp64_store / (lb_ms * 1e-3) / 1e9 if lb_ms > 0 else None}
     lb_short = (L + 31) // 32 * 32 * d <= 768 and os.environ.get("TSW_LB_ENV", "1") != "0"

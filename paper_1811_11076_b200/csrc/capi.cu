@@ -1107,8 +1107,11 @@ int tsw_plan_stats(tsw_plan* p, tsw_stats* out) {
         // DTW: the fp32 copy of the store is streamed once per execute (query blocks of one
         // candidate tile are served from L1/L2);  DK: the candidates' first/last points (the
         // ends array, once per execute; each query re-reads them from L1/L2)
+        // (+ the fused reverse pass's cached fp32 candidate envelopes, midpoint and half-width,
+        // read once per execute)
+        const bool fused = !dk && p->cenv_m && p->lb2 && p->nq >= 4;
         out->bound_bytes = dk ? (uint64_t)p->store->n * 2 * p->store->d * sizeof(double)
-                              : p->store->bytes / 2;
+                              : p->store->bytes / 2 * (fused ? 3 : 1);
         out->kernel_launches = (uint64_t)p->launches;
         if (p->timing && p->executed) {
             float ms[6] = {0};
