@@ -193,8 +193,14 @@ struct tsw_store {
     struct CEnv {
         uint64_t r;
         DevBuf<float> m, h;
+        DevBuf<float> cm, ch;  // block means of the envelope (coarse LB pass), built on demand
     };
     std::vector<std::unique_ptr<CEnv>> cenv;
+    // coarse LB cascade: fp32 block means of every series (kPaa points per
+    // block, tiled, pitch cstride), built by the first plan that uses them
+    DevBuf<float> paa;
+    uint64_t clen = 0, cstride = 0;
+    float err_c = 0.0f;      // >= |coarse value - true block mean| (in-range values)
     StoreDev dev() const {
         StoreDev s{};
         s.data = data.p + guard;
@@ -235,6 +241,13 @@ struct tsw_plan {
     const float* cenv_m = nullptr;
     bool lb2 = false;  // the LB pass adds the reverse bound (else cenv feeds only the DP)
     const float* cenv_h = nullptr;
+    // coarse LB cascade: the LB pass runs on block means (store->paa, the candidate envelopes'
+    // block means, and these per-execution block means of the queries and their envelopes);
+    // the DP setup re-checks every pair with the full-resolution bounds
+    bool coarse = false;
+    const float* ccenv_m = nullptr;
+    const float* ccenv_h = nullptr;
+    DevBuf<float> cq_m, cq_h, cq32;
     uint32_t pfx_qn = 0, pfx_log = 0, pfx_cap = 0;
     DevBuf<uint32_t> sel_si, sel_i, top_i, fin_si;
     DevBuf<double> fin_sv;
@@ -446,6 +459,46 @@ std::unique_ptr<tsw_plan> make_plan(tsw_store* s, uint64_t nq_max, uint64_t qlen
             p->pfx_cap = (uint32_t)std::min<uint64_t>(nq_max * n, kPfxCapMax);
             p->pfx.alloc((uint64_t)p->pfx_cap * kPfxBlocks);
         }
+        // coarse LB cascade: with the reverse bound on and per-point prefixes in the DP setup
+        // (series > 256 points), the LB pass runs on block means of kPaa points -- 1/kPaa of the
+        // terms and bytes; measured on C5-shaped data the coarse forward + reverse bound admits
+        // only ~10% more pairs than the full-resolution one -- and the DP setup, which computes
+        // the full-resolution terms for its cumulative bounds anyway, drops those.
+        // TSW_COARSE=0/1 overrides.
+        const char* coe = std::getenv("TSW_COARSE");
+        const bool want_coarse = coe ? std::atoi(coe) != 0 : true;
+        if (want_coarse && p->cenv_m && p->lb2 && p->pfx_qn == 0 && s->ulen == qlen &&
+            qlen / kPaa >= 8) {
+            tsw_store::CEnv* ce = nullptr;
+            for (auto& c : s->cenv)
+                if (c->r == r) ce = c.get();
+            const uint64_t clen = qlen / kPaa, cst = stride_of(clen, s->d);
+            if (!s->paa.p) {
+                s->clen = clen;
+                s->cstride = cst;
+                s->paa.alloc(n * cst);
+                launch_paa_series(s->data.p + s->guard, n, (uint32_t)s->d, (uint32_t)clen, s->ustride,
+                                  cst, s->paa.p, p->own);
+                ck(cudaStreamSynchronize(p->own), "coarse store");
+            }
+            if (ce && !ce->cm.p) {
+                ce->cm.alloc(n * cst);
+                ce->ch.alloc(n * cst);
+                launch_paa_envelope(s->data.p + s->guard, n, (uint32_t)s->d, (uint32_t)s->ulen,
+                                    (uint32_t)clen, s->ustride, cst,
+                                    (uint32_t)std::min<uint64_t>(r, 0xffffffffu), 0.0f, ce->cm.p,
+                                    ce->ch.p, p->own);
+                ck(cudaStreamSynchronize(p->own), "coarse candidate envelope");
+            }
+            if (ce) {
+                p->coarse = true;
+                p->ccenv_m = ce->cm.p;
+                p->ccenv_h = ce->ch.p;
+                p->cq_m.alloc(nq_max * cst);
+                p->cq_h.alloc(nq_max * cst);
+                p->cq32.alloc(nq_max * cst);
+            }
+        }
     }
     p->ub.alloc(nq_max * p->S);
     // point-range splits of the sampled bounds when the (query, sample) tiles cannot fill the
@@ -582,6 +635,16 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
         launch_absmax(p->qg(), (uint64_t)nq * p->qstride, p->qabsmax.p, st);
         launches += 2;
     }
+    // coarse LB cascade: block means of the queries and of their envelopes
+    const bool coarse = !dk && p->coarse && nq >= 4;
+    if (coarse) {
+        launch_paa_envelope(p->qg(), nq, (uint32_t)s->d, (uint32_t)p->qlen, (uint32_t)s->clen,
+                            p->qstride, s->cstride, (uint32_t)std::min<uint64_t>(p->r, 0xffffffffu),
+                            s->err_c, p->cq_m.p, p->cq_h.p, st);
+        launch_paa_series(p->qg(), nq, (uint32_t)s->d, (uint32_t)s->clen, p->qstride, s->cstride,
+                          p->cq32.p, st);
+        launches += 2;
+    }
     DpArgs da{};
     da.store = s->dev();
     da.queries = p->qg();
@@ -607,6 +670,7 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
     da.pfx_blocks = p->pfx_qn ? p->pfx.p : nullptr;
     da.pfx_log = p->pfx_log;
     da.sub = sub ? 1 : 0;
+    da.coarse = coarse ? 1 : 0;
     auto run_dp = [&](const WorkQueue& w, uint32_t max_pairs, cudaStream_t on) {
         da.queue = w;
         da.probe = (p->probe && w.e == p->probe_wq().e) ? 1 : 0;
@@ -664,6 +728,23 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
             la.q32 = p->q32.p;
             la.qabsmax = p->qabsmax.p;
             la.task = p->counters.p + C_TASK;
+        }
+        if (coarse) {
+            // the same fused forward + reverse pass on the block means; keys scaled by kPaa
+            la.store.data = nullptr;
+            la.store.data32 = s->paa.p;
+            la.store.ulen = (uint32_t)s->clen;
+            la.store.ustride = la.store.tstride = s->cstride;
+            la.env_lo = p->cq_m.p;
+            la.env_hi = p->cq_h.p;
+            la.qstride = s->cstride;
+            la.cenv_m = p->ccenv_m;
+            la.cenv_h = p->ccenv_h;
+            la.q32 = p->cq32.p;
+            la.pfx_qn = 0;
+            la.pfx_out = nullptr;
+            la.lb_scale = (float)kPaa;
+            la.eq_scale = 0x1p-24 * (1.0 + 0x1p-20);
         }
         la.c_lo = 0;
         la.c_hi = p->n1 ? p->n1 : n;
@@ -967,6 +1048,7 @@ int tsw_store_create(const double* values, const uint64_t* lengths, uint64_t uni
         double xmax = 0.0;
         ck(cudaMemcpy(&xmax, mxb.p, sizeof(double), cudaMemcpyDeviceToHost), "store absmax");
         s->err32 = std::nextafter((float)(xmax * 0x1p-24), INFINITY);
+        s->err_c = std::nextafter((float)(xmax * 0x1p-24 * (1.0 + 0x1p-20)), INFINITY);
         if (!(s->err32 < INFINITY)) fail(TSW_EVALIDATION, "dataset values too large for the fp32 bound");
         ck(cudaDeviceSynchronize(), "store create");
         *out = s.release();
@@ -1110,8 +1192,11 @@ int tsw_plan_stats(tsw_plan* p, tsw_stats* out) {
         // (+ the fused reverse pass's cached fp32 candidate envelopes, midpoint and half-width,
         // read once per execute)
         const bool fused = !dk && p->cenv_m && p->lb2 && p->nq >= 4;
+        // coarse pass: the block means of the store and of the candidate envelopes instead
         out->bound_bytes = dk ? (uint64_t)p->store->n * 2 * p->store->d * sizeof(double)
-                              : p->store->bytes / 2 * (fused ? 3 : 1);
+                           : (fused && p->coarse)
+                               ? p->store->n * p->store->cstride * sizeof(float) * 3
+                               : p->store->bytes / 2 * (fused ? 3 : 1);
         out->kernel_launches = (uint64_t)p->launches;
         if (p->timing && p->executed) {
             float ms[6] = {0};

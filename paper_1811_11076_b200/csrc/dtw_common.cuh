@@ -57,10 +57,13 @@ __device__ __forceinline__ void scan_pfx_row(float (&bv)[kPfxBlocks / WL], int g
 // out[p] <= sum of the terms of points < p (all dimensions), p = 0..L.  Lanes own 4 consecutive
 // points (one float4 per dimension in the tiled layout); RD adds in any order keep every
 // prefix a lower bound.
+// `lim`: the pair is dropped (return false, group-uniform) as soon as the running total exceeds
+// it -- the total is the pair's full-resolution fp32 LB_Box bound (coarse mode, DESIGN.md §4.7;
+// +inf: never).
 template <int WL, bool HADD>
-__device__ __forceinline__ void prefix_terms(const float* x32, const float* em, const float* eh,
+__device__ __forceinline__ bool prefix_terms(const float* x32, const float* em, const float* eh,
                                              float hadd, int gl, unsigned gmask, float* out, int L,
-                                             int stride) {
+                                             int stride, float lim = kInfF) {
     float carry = 0.0f;
     if (gl == 0) out[0] = 0.0f;
     for (int j0 = 0; j0 < L; j0 += 4 * WL) {
@@ -102,24 +105,27 @@ __device__ __forceinline__ void prefix_terms(const float* x32, const float* em, 
         if (p0 + 3 <= L) out[p0 + 3] = __fadd_rd(base, t2);
         if (p0 + 4 <= L) out[p0 + 4] = __fadd_rd(base, t3);
         carry = __fadd_rd(carry, __shfl_sync(gmask, inc, WL - 1, WL));
+        if (carry > lim) return false;
     }
+    return true;
 }
 
 template <int WL>
-__device__ __forceinline__ void setup_pfx(const DpArgs& a, const QEntry& pr, int gl, unsigned gmask,
-                                          float* pfx, int L, int stride) {
+__device__ __forceinline__ bool setup_pfx(const DpArgs& a, const QEntry& pr, int gl, unsigned gmask,
+                                          float* pfx, int L, int stride, float lim = kInfF) {
     if (a.pfx_blocks) {
         float bv[kPfxBlocks / WL];
         load_pfx_row<WL>(a, pr.ps, gl, bv);
         scan_pfx_row<WL>(bv, gl, gmask, pfx);
     } else if (a.env_lo) {
-        prefix_terms<WL, false>(a.store.data32 + series_off(a.store, pr.c),
-                                a.env_lo + (uint64_t)pr.q * a.qstride,
-                                a.env_hi + (uint64_t)pr.q * a.qstride, 0.0f, gl, gmask, pfx, L,
-                                stride);
+        return prefix_terms<WL, false>(a.store.data32 + series_off(a.store, pr.c),
+                                       a.env_lo + (uint64_t)pr.q * a.qstride,
+                                       a.env_hi + (uint64_t)pr.q * a.qstride, 0.0f, gl, gmask, pfx,
+                                       L, stride, lim);
     } else {
         for (int j = gl; j <= L; j += WL) pfx[j] = 0.0f;
     }
+    return true;
 }
 
 // Reverse cumulative bound (LB_Keogh's other direction, the query points against the
@@ -129,11 +135,17 @@ __device__ __forceinline__ void setup_pfx(const DpArgs& a, const QEntry& pr, int
 // least v + max(pfx[j'], pfq[i']).  fp32 terms as in the reverse LB pass (kernels_bound.cu
 // lb2_flush): RN query copy, half-width + eq >= |q - fp32(q)|, rounded up.
 template <int WL>
-__device__ __forceinline__ void setup_pfq(const DpArgs& a, const QEntry& pr, int gl, unsigned gmask,
-                                          float* pfq, int L, int stride, float eq) {
+__device__ __forceinline__ bool setup_pfq(const DpArgs& a, const QEntry& pr, int gl, unsigned gmask,
+                                          float* pfq, int L, int stride, float eq, float lim = kInfF) {
     const uint64_t co = series_off(a.store, pr.c);
-    prefix_terms<WL, true>(a.q32 + (uint64_t)pr.q * a.qstride, a.cenv_m + co, a.cenv_h + co, eq,
-                           gl, gmask, pfq, L, stride);
+    return prefix_terms<WL, true>(a.q32 + (uint64_t)pr.q * a.qstride, a.cenv_m + co, a.cenv_h + co,
+                                  eq, gl, gmask, pfq, L, stride, lim);
+}
+
+// Coarse mode: the limit of the setup's full-resolution bounds.  total > RU32(T * M) implies
+// total > T * M (a threshold beyond the fp32 range gives +inf: never).
+__device__ __forceinline__ float setup_limit(const DpArgs& a, double Tm) {
+    return a.coarse ? __double2float_ru(Tm) : kInfF;
 }
 
 // The reference prunes on `lb >= eps` with its serially summed fp64 LB_Box (search.cpp:147,

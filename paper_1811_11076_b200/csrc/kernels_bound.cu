@@ -171,6 +171,151 @@ void launch_envelope64(const double* q, uint32_t nq, uint32_t d, uint32_t len, u
     envelope_kernel<double><<<std::max(blocks, 1), 256, 0, st>>>(q, nq, d, len, qstride, r, 0.0f, lo, hi);
 }
 
+// ---- coarse (piecewise-aggregate) series and envelopes for the LB cascade ----------------------
+// The coarse LB pass bounds LB_Box from below with block means over kPaa
+// consecutive points: f(x, lo, hi) = dist(x, [lo, hi])^2 is jointly convex, so by Jensen
+//   sum_{p in block} f(x_p, lo_p, hi_p)  >=  kPaa * f(mean x, mean lo, mean hi).
+// Coarse series are tiled like the fine ones (32 coarse points per tile, pitch = cstride
+// elements, no guard tiles); a tail of len % kPaa points is dropped (its terms are >= 0).
+// One thread per (series, coarse point, dim).
+//
+// Block mean of the values, fp32: the fp64 mean (7 additions, |error| <= 7 * 2^-53 * max|x|)
+// rounded to nearest, so |out - mean| <= max|x| * 2^-24 * (1 + 2^-20) over the in-range values;
+// a block holding a value beyond the fp32 range gets NaN: every term on it is
+// fmaxf(NaN, 0) = 0 (no bound from that block).
+__global__ void paa_series_kernel(const double* __restrict__ src, uint64_t nser, uint32_t d,
+                                  uint32_t clen, uint64_t pitch, uint64_t cstride,
+                                  float* __restrict__ dst) {
+    const uint64_t total = nser * cstride;
+    for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total;
+         g += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t ser = g / cstride;
+        const uint32_t f = (uint32_t)(g - ser * cstride);
+        const uint32_t tile = f / (kTile * d), rem = f - tile * (kTile * d);
+        const uint32_t k = rem / kTile, pc = tile * kTile + rem % kTile;
+        if (pc >= clen) {
+            dst[g] = 0.0f;
+            continue;
+        }
+        const double* row = src + ser * pitch;
+        double sum = 0.0;
+        bool ok = true;
+#pragma unroll
+        for (uint32_t j = 0; j < kPaa; ++j) {
+            const double v = row[tidx(pc * kPaa + j, k, d)];
+            ok = ok && fabs(v) <= (double)FLT_MAX;
+            sum = dadd(sum, v);
+        }
+        dst[g] = ok ? __double2float_rn(dmul(sum, 1.0 / kPaa)) : __int_as_float(0x7fc00000);
+    }
+}
+
+void launch_paa_series(const double* src, uint64_t nser, uint32_t d, uint32_t clen, uint64_t pitch,
+                       uint64_t cstride, float* dst, cudaStream_t st) {
+    const uint64_t total = nser * cstride;
+    const int blocks = (int)std::min<uint64_t>((total + 255) / 256, (uint64_t)sm_count() * 16);
+    paa_series_kernel<<<std::max(blocks, 1), 256, 0, st>>>(src, nser, d, clen, pitch, cstride, dst);
+}
+
+// Block means of a series' band envelope (window [p - r, p + r] clamped, envelope.cpp:25-59) in
+// the fp32 (midpoint, half-width) form: the means are summed with directed rounding (lo down,
+// hi up), the half-width covers [mean lo, mean hi] from the fp32 midpoint, rounded up, plus
+// `err` (the rounding bound of the coarse values it is compared with).  The eight windows of a
+// block share the core [p0 + 7 - r, p0 + r]; each adds a few points on either side.
+__global__ void paa_envelope_kernel(const double* __restrict__ src, uint64_t nser, uint32_t d,
+                                    uint32_t len, uint32_t clen, uint64_t pitch, uint64_t cstride,
+                                    uint32_t r, float err, float* __restrict__ om,
+                                    float* __restrict__ oh) {
+    const uint64_t total = nser * cstride;
+    for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total;
+         g += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t ser = g / cstride;
+        const uint32_t f = (uint32_t)(g - ser * cstride);
+        const uint32_t tile = f / (kTile * d), rem = f - tile * (kTile * d);
+        const uint32_t k = rem / kTile, pc = tile * kTile + rem % kTile;
+        if (pc >= clen) {
+            om[g] = 0.0f;
+            oh[g] = 0.0f;
+            continue;
+        }
+        const double* row = src + ser * pitch;
+        const int64_t p0 = (int64_t)pc * kPaa, last = (int64_t)len - 1, rr = (int64_t)r;
+        double slo = 0.0, shi = 0.0;
+        if (r >= kPaa) {
+            double cmn = kInf, cmx = -kInf;  // the shared core (non-empty: r >= kPaa)
+            for (int64_t w = max(p0 + (int64_t)kPaa - 1 - rr, (int64_t)0); w <= min(p0 + rr, last); ++w) {
+                const double v = row[tidx((uint32_t)w, k, d)];
+                cmn = v < cmn ? v : cmn;
+                cmx = v > cmx ? v : cmx;
+            }
+            // left extensions [p0 + j - r, p0 + kPaa - 2 - r], j = kPaa - 2 .. 0 (running)
+            double lmn[kPaa], lmx[kPaa];
+            double mn = kInf, mx = -kInf;
+            lmn[kPaa - 1] = kInf;
+            lmx[kPaa - 1] = -kInf;
+#pragma unroll
+            for (int j = (int)kPaa - 2; j >= 0; --j) {
+                const int64_t w = p0 + j - rr;
+                if (w >= 0 && w <= last) {
+                    const double v = row[tidx((uint32_t)w, k, d)];
+                    mn = v < mn ? v : mn;
+                    mx = v > mx ? v : mx;
+                }
+                lmn[j] = mn;
+                lmx[j] = mx;
+            }
+            // right extensions [p0 + r + 1, p0 + j + r], j = 1 .. kPaa - 1 (running)
+            mn = kInf;
+            mx = -kInf;
+#pragma unroll
+            for (int j = 0; j < (int)kPaa; ++j) {
+                if (j > 0) {
+                    const int64_t w = p0 + j + rr;
+                    if (w >= 0 && w <= last) {
+                        const double v = row[tidx((uint32_t)w, k, d)];
+                        mn = v < mn ? v : mn;
+                        mx = v > mx ? v : mx;
+                    }
+                }
+                const double lo = fmin(cmn, fmin(lmn[j], mn)), hi = fmax(cmx, fmax(lmx[j], mx));
+                slo = __dadd_rd(slo, lo);
+                shi = __dadd_ru(shi, hi);
+            }
+        } else {
+            for (uint32_t j = 0; j < kPaa; ++j) {
+                const int64_t p = p0 + j;
+                double mn = kInf, mx = -kInf;
+                for (int64_t w = max(p - rr, (int64_t)0); w <= min(p + rr, last); ++w) {
+                    const double v = row[tidx((uint32_t)w, k, d)];
+                    mn = v < mn ? v : mn;
+                    mx = v > mx ? v : mx;
+                }
+                slo = __dadd_rd(slo, mn);
+                shi = __dadd_ru(shi, mx);
+            }
+        }
+        const double mlo = __dmul_rd(slo, 1.0 / kPaa), mhi = __dmul_ru(shi, 1.0 / kPaa);
+        if (!(mlo >= -(double)FLT_MAX && mhi <= (double)FLT_MAX)) {
+            om[g] = 0.0f;  // the block's envelope leaves the fp32 range: terms of 0
+            oh[g] = INFINITY;
+            continue;
+        }
+        const float m32 = __double2float_rn(0.5 * (mlo + mhi));
+        const double hw = fmax(__dsub_ru((double)m32, mlo), __dsub_ru(mhi, (double)m32));
+        om[g] = m32;
+        oh[g] = __fadd_ru(__double2float_ru(hw), err);
+    }
+}
+
+void launch_paa_envelope(const double* src, uint64_t nser, uint32_t d, uint32_t len, uint32_t clen,
+                         uint64_t pitch, uint64_t cstride, uint32_t r, float err, float* om, float* oh,
+                         cudaStream_t st) {
+    const uint64_t total = nser * cstride;
+    const int blocks = (int)std::min<uint64_t>((total + 255) / 256, (uint64_t)sm_count() * 16);
+    paa_envelope_kernel<<<std::max(blocks, 1), 256, 0, st>>>(src, nser, d, len, clen, pitch, cstride,
+                                                             r, err, om, oh);
+}
+
 // ---- sampled seed upper bounds ----------------------------------------------------------------
 // One warp per (query, sampled candidate).  Per-point costs are exact detail::sq_dist.
 //  DTW: sum of c(i, i) along the diagonal (any order), scaled up by ub_scale so that it bounds
@@ -528,6 +673,8 @@ __device__ __forceinline__ TileOut lb1_tile(const LbCompactArgs& a, PruneCount& 
             v[i] = __fadd_rd(keep, __shfl_xor_sync(0xffffffffu, send, o));
         }
     }
+    // coarse pass: the block-mean terms count kPaa points each (RD: still a lower bound)
+    if (a.lb_scale != 0.0f) v[0] = __fmul_rd(v[0], a.lb_scale);
     TileOut t{v[0], q0 + lane / CB, c0 + lane % CB, kNoPfx, false, false};
     const bool valid = t.q < a.nq && t.c < n;
     if (valid) {
@@ -621,6 +768,7 @@ __global__ void __launch_bounds__(256, 3) lb_few_kernel(LbCompactArgs a) {
             float lb = acc[q];
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) lb = __fadd_rd(lb, __shfl_xor_sync(0xffffffffu, lb, o));
+            if (a.lb_scale != 0.0f) lb = __fmul_rd(lb, a.lb_scale);  // coarse pass
             bool take = false, near = false;
             if (a.lb_out && lane == 0) a.lb_out[(uint64_t)q * n + c] = lb;
             if (a.state) {
@@ -854,6 +1002,7 @@ __device__ __forceinline__ void lb2_flush(const LbCompactArgs& a, uint32_t c0, Q
             int em = -1;
 #pragma unroll
             for (int j = 0; j < NB; ++j) em = j == jm ? ej[j] : em;
+            if (a.lb_scale != 0.0f) acc[0] = __fmul_rd(acc[0], a.lb_scale);  // coarse pass
             if ((lane & 3) == 0 && em >= 0) l2[em] = acc[0];
             if (ej[NB - 1] < 0) break;
         }
@@ -898,7 +1047,7 @@ __global__ void __launch_bounds__(256, 2) lb12_compact_kernel(LbCompactArgs a) {
     float* l2 = reinterpret_cast<float*>(lb12_smem + 8 * kList * sizeof(QEntry)) + (size_t)wib * kList;
     float* stash = reinterpret_cast<float*>(lb12_smem + 8 * kList * (sizeof(QEntry) + sizeof(float))) +
                    (size_t)wib * 32 * 32;
-    const float eq = __double2float_ru(__dmul_ru(*a.qabsmax, 0x1p-24));
+    const float eq = __double2float_ru(__dmul_ru(*a.qabsmax, a.eq_scale != 0.0 ? a.eq_scale : 0x1p-24));
     for (;;) {
         unsigned cg = 0;
         if (lane == 0) cg = atomicAdd(a.task, 1u);  // dynamic: groups' reverse work varies

@@ -267,12 +267,16 @@ __global__ void __launch_bounds__(TPB, MINB) dtw_dp_kernel(DpArgs a, uint32_t ps
                     if (gl == 0 && st) atomicAdd(&st->lb_pruned, 1ull);
                     continue;
                 }
+                // (coarse mode: the prefix total is the full-resolution bound and drops the pair)
+                if (!setup_pfx<WL>(a, pr, gl, gmask, pfx, L, stride, setup_limit(a, Tm))) {
+                    if (gl == 0 && st) atomicAdd(&st->lb_pruned, 1ull);
+                    continue;
+                }
                 break;
             }
             if (!done) {
                 s = a.queries + (uint64_t)pr.q * a.qstride;
                 t = a.store.data + series_off(a.store, pr.c);
-                setup_pfx<WL>(a, pr, gl, gmask, pfx, L, stride);
                 __syncwarp(gmask);
                 // band registers; (0,0)'s diagonal predecessor is 0 so that v(0,0) = c + 0 = c
 #pragma unroll

@@ -401,13 +401,19 @@ __global__ void __launch_bounds__(TPB, MINB) dtw4_kernel(DpArgs a, uint32_t pstr
                     for (int i = 0; i < kPfxBlocks / WL; ++i) bv[i] = sg->row[cb][idx][gl * (kPfxBlocks / WL) + i];
                     scan_pfx_row<WL>(bv, gl, gmask, pfx);
                 }
+                // per-point prefixes; in coarse mode their totals are the pair's full-resolution
+                // LB_Box bounds (forward, then reverse) and drop it here
+                const float lim = setup_limit(a, Tm);
+                if ((!a.pfx_blocks && !setup_pfx<WL>(a, pr, gl, gmask, pfx, L, D, lim)) ||
+                    (rev && !setup_pfq<WL>(a, pr, gl, gmask, pfq, L, D, eq, lim))) {
+                    if (gl == 0 && st) atomicAdd(&st->lb_pruned, 1ull);
+                    continue;
+                }
                 break;
             }
             if (!done) {
                 sq = (IDLE && gl > edge) ? a.inf_query : a.queries + (uint64_t)pr.q * a.qstride;
                 tc = a.store.data + series_off(a.store, pr.c);
-                if (!a.pfx_blocks) setup_pfx<WL>(a, pr, gl, gmask, pfx, L, D);
-                if (rev) setup_pfq<WL>(a, pr, gl, gmask, pfq, L, D, eq);
                 __syncwarp(gmask);
 #pragma unroll
                 for (int e = 0; e < 2 * G; ++e) s.v[e] = (gl == pstar && e == estar) ? 0.0 : kInf;

@@ -119,8 +119,13 @@ __global__ void __launch_bounds__(TPB, MINB) dtwt_kernel(DpArgs a, uint32_t pstr
         }
         const double* sq = a.queries + (uint64_t)pr.q * a.qstride;
         const double* tc = a.store.data + series_off(a.store, pr.c);
-        setup_pfx<32>(a, pr, lane, kFull, pfx, L, d);
-        if (rev) setup_pfq<32>(a, pr, lane, kFull, pfq, L, d, eq);
+        // (coarse mode: the prefixes' totals are the full-resolution bounds and drop the pair)
+        const float lim = setup_limit(a, Tm);
+        if (!setup_pfx<32>(a, pr, lane, kFull, pfx, L, d, lim) ||
+            (rev && !setup_pfq<32>(a, pr, lane, kFull, pfq, L, d, eq, lim))) {
+            if (lane == 0 && st) atomicAdd(&st->lb_pruned, 1ull);
+            continue;
+        }
         double v[2];
         v[0] = (lane == pstar && RPAR == 0) ? 0.0 : kInf;  // (0,0)'s diagonal predecessor
         v[1] = (lane == pstar && RPAR == 1) ? 0.0 : kInf;
