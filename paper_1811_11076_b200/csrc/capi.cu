@@ -671,9 +671,29 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
     da.pfx_log = p->pfx_log;
     da.sub = sub ? 1 : 0;
     da.coarse = coarse ? 1 : 0;
+    bool csetup = false;
+    {
+        // coarse setup: the fast path's cumulative bounds from the block means (TSW_CSETUP=0:
+        // per-point prefixes with the full-resolution re-check)
+        const char* cse = std::getenv("TSW_CSETUP");
+        if (coarse && da.cenv_m && dtw4_supported(da) && (cse ? std::atoi(cse) != 0 : true)) {
+            csetup = true;
+            da.c_x32 = s->paa.p;
+            da.c_em = p->cq_m.p;
+            da.c_eh = p->cq_h.p;
+            da.c_q32 = p->cq32.p;
+            da.c_cm = p->ccenv_m;
+            da.c_ch = p->ccenv_h;
+            da.cstride = s->cstride;
+            da.clen = (uint32_t)s->clen;
+        }
+    }
     auto run_dp = [&](const WorkQueue& w, uint32_t max_pairs, cudaStream_t on) {
         da.queue = w;
         da.probe = (p->probe && w.e == p->probe_wq().e) ? 1 : 0;
+        // the few probe pairs keep the per-point (tighter) cumulative bounds: their launch is
+        // one pair's sequential sweep, and a looser bound abandons later (C5 probes +45%)
+        da.csetup = (csetup && !da.probe) ? 1 : 0;
         if (dk) launch_dk_dp(da, max_pairs, (uint32_t)s->max_len, on);
         else launch_dtw_dp(da, max_pairs, on);
         ++launches;

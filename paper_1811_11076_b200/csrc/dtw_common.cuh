@@ -60,10 +60,13 @@ __device__ __forceinline__ void scan_pfx_row(float (&bv)[kPfxBlocks / WL], int g
 // `lim`: the pair is dropped (return false, group-uniform) as soon as the running total exceeds
 // it -- the total is the pair's full-resolution fp32 LB_Box bound (coarse mode, DESIGN.md §4.7;
 // +inf: never).
-template <int WL, bool HADD>
+// PAA: the series are block means (kPaa points each): every prefix is scaled by
+// kPaa (RD), a lower bound of the full-resolution prefix at the block boundary.
+template <int WL, bool HADD, bool PAA = false>
 __device__ __forceinline__ bool prefix_terms(const float* x32, const float* em, const float* eh,
                                              float hadd, int gl, unsigned gmask, float* out, int L,
                                              int stride, float lim = kInfF) {
+    auto put = [&](float v) { return PAA ? __fmul_rd(v, (float)kPaa) : v; };
     float carry = 0.0f;
     if (gl == 0) out[0] = 0.0f;
     for (int j0 = 0; j0 < L; j0 += 4 * WL) {
@@ -100,12 +103,12 @@ __device__ __forceinline__ bool prefix_terms(const float* x32, const float* em, 
         float base = __shfl_up_sync(gmask, inc, 1, WL);
         if (gl == 0) base = 0.0f;
         base = __fadd_rd(base, carry);
-        if (p0 + 1 <= L) out[p0 + 1] = __fadd_rd(base, t0);
-        if (p0 + 2 <= L) out[p0 + 2] = __fadd_rd(base, t1);
-        if (p0 + 3 <= L) out[p0 + 3] = __fadd_rd(base, t2);
-        if (p0 + 4 <= L) out[p0 + 4] = __fadd_rd(base, t3);
+        if (p0 + 1 <= L) out[p0 + 1] = put(__fadd_rd(base, t0));
+        if (p0 + 2 <= L) out[p0 + 2] = put(__fadd_rd(base, t1));
+        if (p0 + 3 <= L) out[p0 + 3] = put(__fadd_rd(base, t2));
+        if (p0 + 4 <= L) out[p0 + 4] = put(__fadd_rd(base, t3));
         carry = __fadd_rd(carry, __shfl_sync(gmask, inc, WL - 1, WL));
-        if (carry > lim) return false;
+        if (put(carry) > lim) return false;
     }
     return true;
 }
@@ -140,6 +143,21 @@ __device__ __forceinline__ bool setup_pfq(const DpArgs& a, const QEntry& pr, int
     const uint64_t co = series_off(a.store, pr.c);
     return prefix_terms<WL, true>(a.q32 + (uint64_t)pr.q * a.qstride, a.cenv_m + co, a.cenv_h + co,
                                   eq, gl, gmask, pfq, L, stride, lim);
+}
+
+// Coarse setup (a.csetup): both cumulative bounds from the block means the coarse LB pass runs
+// on -- 1/kPaa of the terms and bytes of the per-point prefixes; pfx[b] / pfq[b] bound the terms
+// of the points < b * kPaa (index shift kPaaLog in the DP's abandon test).
+template <int WL>
+__device__ __forceinline__ bool setup_coarse(const DpArgs& a, const QEntry& pr, int gl, unsigned gmask,
+                                             float* pfx, float* pfq, bool rev, int stride, float eqc,
+                                             float lim) {
+    const uint64_t co = (uint64_t)pr.c * a.cstride, qo = (uint64_t)pr.q * a.cstride;
+    if (!prefix_terms<WL, false, true>(a.c_x32 + co, a.c_em + qo, a.c_eh + qo, 0.0f, gl, gmask, pfx,
+                                       (int)a.clen, stride, lim))
+        return false;
+    return !rev || prefix_terms<WL, true, true>(a.c_q32 + qo, a.c_cm + co, a.c_ch + co, eqc, gl, gmask,
+                                                pfq, (int)a.clen, stride, lim);
 }
 
 // Coarse mode: the limit of the setup's full-resolution bounds.  total > RU32(T * M) implies

@@ -102,7 +102,7 @@ struct Lane {
 };
 
 // One iteration `it` (phase PH = it % P): anti-diagonals 2it (offsets of parity 0) and 2it+1.
-template <int G, int D, int WL, int RPAR, bool IDLE, bool CHECK, int PH>
+template <int G, int D, int WL, int RPAR, bool IDLE, bool CHECK, int PH, bool CS>
 __device__ __forceinline__ void iter(Lane<G, D>& s, const double* __restrict__ sq,
                                      const double* __restrict__ tc, int gl, int edge, int tjb,
                                      int sjb, unsigned okm, const float* __restrict__ pfx,
@@ -130,8 +130,9 @@ __device__ __forceinline__ void iter(Lane<G, D>& s, const double* __restrict__ s
         // forward (candidate columns ahead) and reverse (query rows ahead, pfq) cumulative
         // bounds at the lane's smallest candidate / query index: both lower-bound every slot's
         // own (pfq == pfx when the reverse bound is off: max of equal values)
-        const float rc = pfx[min(max(tjb - TTMAX, 0), L - 1) >> plog];
-        const float rq = pfq == pfx ? rc : pfq[min(max(sjb, 0), L - 1)];
+        // (CS, coarse setup: both prefixes at block-mean granularity, kPaa points per entry)
+        const float rc = pfx[min(max(tjb - TTMAX, 0), L - 1) >> (CS ? kPaaLog : plog)];
+        const float rq = pfq == pfx ? rc : pfq[min(max(sjb, 0), L - 1) >> (CS ? kPaaLog : 0)];
         const double Rmin = (double)fmaxf(rc, rq);
         Tlim = __dsub_ru(__dmul_ru(T, margin), Rmin);
     }
@@ -176,7 +177,7 @@ __device__ __forceinline__ void iter(Lane<G, D>& s, const double* __restrict__ s
 // ROT: rotations of the point windows per body (ROT * P iterations, one threshold read, one
 // staging step, one abandon check) -- > 1 for long series, where a pair runs hundreds of
 // iterations
-template <int G, int D, int WL, int RPAR, bool IDLE, bool FIN, int ROT>
+template <int G, int D, int WL, int RPAR, bool IDLE, bool FIN, int ROT, bool CS>
 __device__ __forceinline__ void body(Lane<G, D>& s, const double* __restrict__ sq,
                                      const double* __restrict__ tc, int gl, int edge, int it,
                                      int tb0, int sb0, unsigned okm, const float* __restrict__ pfx,
@@ -192,10 +193,10 @@ __device__ __forceinline__ void body(Lane<G, D>& s, const double* __restrict__ s
     constexpr int E0 = RPAR, E1 = G == 2 ? RPAR + 2 : RPAR;
 #define TSW_ITER4(PH, OFF, CK)                                                                 \
     if constexpr (PH < P) {                                                                    \
-        iter<G, D, WL, RPAR, IDLE, CK && PH == P - 1, PH>(s, sq, tc, gl, edge,                 \
-                                                          tb0 - (it + OFF + PH),               \
-                                                          sb0 - (it + OFF + PH), okm, pfx, pfq,\
-                                                          plog, L, T, margin, alive);          \
+        iter<G, D, WL, RPAR, IDLE, CK && PH == P - 1, PH, CS>(s, sq, tc, gl, edge,             \
+                                                              tb0 - (it + OFF + PH),           \
+                                                              sb0 - (it + OFF + PH), okm, pfx, \
+                                                              pfq, plog, L, T, margin, alive); \
         if (FIN && it + OFF + PH == L - 1) fin = ehi ? s.v[E1] : s.v[E0];                      \
     }
     TSW_ITER4(0, 0, ROT == 1)
@@ -228,7 +229,9 @@ __device__ __forceinline__ void body(Lane<G, D>& s, const double* __restrict__ s
 // LONG (series > 256 points): the final cell is captured only in a pair's last body, a
 // warp-uniform choice between two body copies (C5 DP -12%); short series keep one body with a
 // per-iteration capture (the vote and the second copy cost C2 8%)
-template <int G, int D, int WL, int RPAR, bool IDLE, bool LONG, int TPB, int MINB>
+// CS (LONG only): coarse setup -- the cumulative bounds come from the block means of the coarse LB
+// pass (dtw_common.cuh setup_coarse)
+template <int G, int D, int WL, int RPAR, bool IDLE, bool LONG, int TPB, int MINB, bool CS>
 __global__ void __launch_bounds__(TPB, MINB) dtw4_kernel(DpArgs a, uint32_t pstride) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int P = Geo<G, RPAR>::P;
@@ -269,6 +272,8 @@ __global__ void __launch_bounds__(TPB, MINB) dtw4_kernel(DpArgs a, uint32_t pstr
         for (uint32_t i = threadIdx.x; i < a.nq; i += blockDim.x) ab_local[i] = 0u;
     __syncthreads();
     const int plog = a.pfx_blocks ? (int)a.pfx_log : 0;
+    const float eqc = CS && rev ? __double2float_ru(__dmul_ru(*a.qabsmax, 0x1p-24 * (1.0 + 0x1p-20)))
+                                : 0.0f;
     // lane geometry: slot e holds offset obase + e; lanes past `edge` are idle (garbage) and
     // read `edge`'s points
     const int edge = (2 * r + S0) / (2 * G);
@@ -404,8 +409,14 @@ __global__ void __launch_bounds__(TPB, MINB) dtw4_kernel(DpArgs a, uint32_t pstr
                 // per-point prefixes; in coarse mode their totals are the pair's full-resolution
                 // LB_Box bounds (forward, then reverse) and drop it here
                 const float lim = setup_limit(a, Tm);
-                if ((!a.pfx_blocks && !setup_pfx<WL>(a, pr, gl, gmask, pfx, L, D, lim)) ||
-                    (rev && !setup_pfq<WL>(a, pr, gl, gmask, pfq, L, D, eq, lim))) {
+                bool ok;
+                if constexpr (CS) {
+                    ok = setup_coarse<WL>(a, pr, gl, gmask, pfx, pfq, rev, D, eqc, lim);
+                } else {
+                    ok = (a.pfx_blocks || setup_pfx<WL>(a, pr, gl, gmask, pfx, L, D, lim)) &&
+                         (!rev || setup_pfq<WL>(a, pr, gl, gmask, pfq, L, D, eq, lim));
+                }
+                if (!ok) {
                     if (gl == 0 && st) atomicAdd(&st->lb_pruned, 1ull);
                     continue;
                 }
@@ -453,14 +464,14 @@ __global__ void __launch_bounds__(TPB, MINB) dtw4_kernel(DpArgs a, uint32_t pstr
 #endif
         if (LONG ? (L <= TSW_DTW4_LONGMIN || __any_sync(kFull, have && it + ROT * P >= L))
                  : (ROT == 1 || __any_sync(kFull, have && it + ROT * P >= L))) {
-            body<G, D, WL, RPAR, IDLE, true, 1>(s, sq, tc, gl, edge, it, tb0, sb0, okm, pfx,
-                                                pfq, plog, L, st, a.margin, T, alive, fin,
-                                                estar >= 2);
+            body<G, D, WL, RPAR, IDLE, true, 1, CS>(s, sq, tc, gl, edge, it, tb0, sb0, okm, pfx,
+                                                    pfq, plog, L, st, a.margin, T, alive, fin,
+                                                    estar >= 2);
             it += P;
         } else {
-            body<G, D, WL, RPAR, IDLE, false, ROT>(s, sq, tc, gl, edge, it, tb0, sb0, okm, pfx,
-                                                   pfq, plog, L, st, a.margin, T, alive, fin,
-                                                   estar >= 2);
+            body<G, D, WL, RPAR, IDLE, false, ROT, CS>(s, sq, tc, gl, edge, it, tb0, sb0, okm, pfx,
+                                                       pfq, plog, L, st, a.margin, T, alive, fin,
+                                                       estar >= 2);
             it += ROT * P;
         }
         const unsigned bal = __ballot_sync(kFull, alive) & gmask;
@@ -491,7 +502,7 @@ __global__ void __launch_bounds__(TPB, MINB) dtw4_kernel(DpArgs a, uint32_t pstr
     }
 }
 
-template <int G, int D, int WL, int RPAR, bool IDLE, bool LONG>
+template <int G, int D, int WL, int RPAR, bool IDLE, bool LONG, bool CS = false>
 void run4(const DpArgs& a, uint32_t max_pairs, cudaStream_t st) {
     // 128-thread blocks: finer occupancy steps at ~100 registers per thread
     constexpr int TPB = 128;
@@ -506,7 +517,7 @@ void run4(const DpArgs& a, uint32_t max_pairs, cudaStream_t st) {
                        ((a.qlen + 1 + 3) & ~3u) * sizeof(uint32_t);
     const bool spill = fixed + big > smem_optin();
     const size_t smem = spill ? fixed : fixed + big;
-    auto kern = dtw4_kernel<G, D, WL, RPAR, IDLE, LONG, TPB, MINB>;
+    auto kern = dtw4_kernel<G, D, WL, RPAR, IDLE, LONG, TPB, MINB, CS>;
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
@@ -523,6 +534,17 @@ void run4(const DpArgs& a, uint32_t max_pairs, cudaStream_t st) {
 
 template <int G, int WL, int RPAR, bool IDLE, bool LONG>
 void run4_dl(const DpArgs& a, uint32_t max_pairs, cudaStream_t st) {
+    if constexpr (LONG) {
+        if (a.csetup) {
+            switch (a.store.d) {
+                case 1: run4<G, 1, WL, RPAR, IDLE, LONG, true>(a, max_pairs, st); break;
+                case 2: run4<G, 2, WL, RPAR, IDLE, LONG, true>(a, max_pairs, st); break;
+                case 3: run4<G, 3, WL, RPAR, IDLE, LONG, true>(a, max_pairs, st); break;
+                default: run4<G, 4, WL, RPAR, IDLE, LONG, true>(a, max_pairs, st); break;
+            }
+            return;
+        }
+    }
     switch (a.store.d) {
         case 1: run4<G, 1, WL, RPAR, IDLE, LONG>(a, max_pairs, st); break;
         case 2: run4<G, 2, WL, RPAR, IDLE, LONG>(a, max_pairs, st); break;

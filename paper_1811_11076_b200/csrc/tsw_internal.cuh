@@ -30,6 +30,7 @@ constexpr double kInf = __builtin_huge_val();
 constexpr float kInfF = __builtin_huge_valf();
 constexpr uint32_t kTile = 32;  // points per layout tile
 constexpr uint32_t kPaa = 8;    // points per block mean of the coarse LB pass
+constexpr int kPaaLog = 3;
 
 // element offset of (point p, dim k) in a tiled series of dimension d
 __host__ __device__ __forceinline__ uint64_t tidx(uint32_t p, uint32_t k, uint32_t d) {
@@ -409,6 +410,17 @@ struct DpArgs {
     // DTW: the queue keys are COARSE bounds (block-mean LB pass); the per-pair setup's
     // full-resolution prefix totals are the pair's fp32 LB_Box bounds and prune it there
     int coarse;
+    // coarse setup (fast path): the DP's cumulative bounds come from the block means too (the
+    // coarse store / candidate-envelope means at pitch cstride, the queries' per execution)
+    int csetup;
+    const float* c_x32;
+    const float* c_em;
+    const float* c_eh;
+    const float* c_q32;
+    const float* c_cm;
+    const float* c_ch;
+    uint64_t cstride;
+    uint32_t clen;
 };
 
 // Host: the per-block opt-in shared-memory limit, and a stream-ordered global scratch for the
