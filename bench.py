@@ -475,7 +475,13 @@ def gpu_leg(a, t, torch, store, db, cfg, metric, sh, qs, stream, flush, ws, rank
     # the reference's own call shape, one query per pass: the LB pass streams the fp32 store
     # once (lb_few_kernel) and is HBM-bound -- achieved GB/s against the measured copy peak
     if metric == "dtw":
-        p1 = t.Plan(store, 1, L, metric, r, k)
+        # (the plain fp32 pass: the coarse cascade, which reads 1/8 of these bytes, is switched
+        # off for this plan only)
+        os.environ["TSW_COARSE"] = "0"
+        try:
+            p1 = t.Plan(store, 1, L, metric, r, k)
+        finally:
+            del os.environ["TSW_COARSE"]
         p1.set_timing(True)
         s1 = []
         for i in range(6):

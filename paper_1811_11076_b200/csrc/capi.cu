@@ -636,7 +636,10 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
         launches += 2;
     }
     // coarse LB cascade: block means of the queries and of their envelopes
-    const bool coarse = !dk && p->coarse && nq >= 4;
+    // (1-3 queries too: the fused pass on block means costs a fraction of streaming the fp32
+    // store; TSW_COARSE_FEW=0: the HBM-streaming forward pass lb_few_kernel, A/B and tests)
+    static const bool coarse_few = !(std::getenv("TSW_COARSE_FEW") && std::atoi(std::getenv("TSW_COARSE_FEW")) == 0);
+    const bool coarse = !dk && p->coarse && (nq >= 4 || coarse_few);
     if (coarse) {
         launch_paa_envelope(p->qg(), nq, (uint32_t)s->d, (uint32_t)p->qlen, (uint32_t)s->clen,
                             p->qstride, s->cstride, (uint32_t)std::min<uint64_t>(p->r, 0xffffffffu),
@@ -742,7 +745,7 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
         // fused reverse bound (queries in fp32 + their max |value| first); 1-3 queries stream
         // the store with the forward bound only (measured: the reverse pass costs more than
         // the DP pairs it removes there)
-        if (p->cenv_m && p->lb2 && nq >= 4) {
+        if (p->cenv_m && p->lb2 && (nq >= 4 || coarse)) {
             la.cenv_m = p->cenv_m;
             la.cenv_h = p->cenv_h;
             la.q32 = p->q32.p;
@@ -1211,7 +1214,8 @@ int tsw_plan_stats(tsw_plan* p, tsw_stats* out) {
         // ends array, once per execute; each query re-reads them from L1/L2)
         // (+ the fused reverse pass's cached fp32 candidate envelopes, midpoint and half-width,
         // read once per execute)
-        const bool fused = !dk && p->cenv_m && p->lb2 && p->nq >= 4;
+        static const bool coarse_few = !(std::getenv("TSW_COARSE_FEW") && std::atoi(std::getenv("TSW_COARSE_FEW")) == 0);
+        const bool fused = !dk && p->cenv_m && p->lb2 && (p->nq >= 4 || (p->coarse && coarse_few));
         // coarse pass: the block means of the store and of the candidate envelopes instead
         out->bound_bytes = dk ? (uint64_t)p->store->n * 2 * p->store->d * sizeof(double)
                            : (fused && p->coarse)
