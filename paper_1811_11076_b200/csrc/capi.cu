@@ -200,6 +200,7 @@ struct tsw_store {
     // block, tiled, pitch cstride), built by the first plan that uses them
     DevBuf<float> paa;
     uint64_t clen = 0, cstride = 0;
+    uint32_t cw = 0;         // points per block mean (8: long series, 4: short)
     float err_c = 0.0f;      // >= |coarse value - true block mean| (in-range values)
     StoreDev dev() const {
         StoreDev s{};
@@ -245,6 +246,7 @@ struct tsw_plan {
     // block means, and these per-execution block means of the queries and their envelopes);
     // the DP setup re-checks every pair with the full-resolution bounds
     bool coarse = false;
+    bool coarse_short = false;  // short series: the coarse pass replaces the forward-only pass
     const float* ccenv_m = nullptr;
     const float* ccenv_h = nullptr;
     DevBuf<float> cq_m, cq_h, cq32;
@@ -459,44 +461,62 @@ std::unique_ptr<tsw_plan> make_plan(tsw_store* s, uint64_t nq_max, uint64_t qlen
             p->pfx_cap = (uint32_t)std::min<uint64_t>(nq_max * n, kPfxCapMax);
             p->pfx.alloc((uint64_t)p->pfx_cap * kPfxBlocks);
         }
-        // coarse LB cascade: with the reverse bound on and per-point prefixes in the DP setup
-        // (series > 256 points), the LB pass runs on block means of kPaa points -- 1/kPaa of the
-        // terms and bytes; measured on C5-shaped data the coarse forward + reverse bound admits
-        // only ~10% more pairs than the full-resolution one -- and the DP setup, which computes
-        // the full-resolution terms for its cumulative bounds anyway, drops those.
-        // TSW_COARSE=0/1 overrides.
+        // Coarse LB cascade: the LB pass runs forward + reverse on block means of
+        // w points -- 1/w of the terms and bytes.  Measured on the configs' data, the coarse
+        // two-sided bound admits ~10% more pairs than the full-resolution two-sided one (w = 8,
+        // C5) and FEWER than the full-resolution forward bound alone (w = 4: C3 0.9% vs 1.5%,
+        // C2 12.8% vs 18.7%).
+        //  * long series (> 256 points, reverse bound on): w = 8; the DP setup's cumulative
+        //    bounds come from the same block means (fast path) or re-check at full resolution;
+        //  * short series on the fast path (d <= 4, r <= 52): w = 4 replaces the forward-only
+        //    full-resolution pass and its block-sum rows.
+        // TSW_COARSE=0/1 overrides (TSW_COARSE_SHORT=0: short series keep the plain pass).
         const char* coe = std::getenv("TSW_COARSE");
         const bool want_coarse = coe ? std::atoi(coe) != 0 : true;
-        if (want_coarse && p->cenv_m && p->lb2 && p->pfx_qn == 0 && s->ulen == qlen &&
-            qlen / kPaa >= 8) {
+        const char* cse = std::getenv("TSW_COARSE_SHORT");
+        const bool want_short = cse ? std::atoi(cse) != 0 : true;
+        const uint64_t r_eff = std::min<uint64_t>(r, qlen - 1);
+        const bool long_mode = p->cenv_m && p->lb2 && p->pfx_qn == 0;
+        const bool short_mode = want_short && p->pfx_qn != 0 && s->d <= 4 && r_eff <= 52 && qlen >= 64;
+        if (want_coarse && (long_mode || short_mode) && s->ulen == qlen) {
+            const uint32_t w = long_mode ? 8u : 4u;
             tsw_store::CEnv* ce = nullptr;
             for (auto& c : s->cenv)
                 if (c->r == r) ce = c.get();
-            const uint64_t clen = qlen / kPaa, cst = stride_of(clen, s->d);
+            if (!ce) {  // (short series: no full-resolution candidate envelopes)
+                auto c = std::make_unique<tsw_store::CEnv>();
+                c->r = r;
+                ce = c.get();
+                s->cenv.push_back(std::move(c));
+            }
+            const uint64_t clen = qlen / w, cst = stride_of(clen, s->d);
             if (!s->paa.p) {
                 s->clen = clen;
                 s->cstride = cst;
+                s->cw = w;
                 s->paa.alloc(n * cst);
-                launch_paa_series(s->data.p + s->guard, n, (uint32_t)s->d, (uint32_t)clen, s->ustride,
-                                  cst, s->paa.p, p->own);
+                launch_paa_series(s->data.p + s->guard, n, (uint32_t)s->d, (uint32_t)clen, w,
+                                  s->ustride, cst, s->paa.p, p->own);
                 ck(cudaStreamSynchronize(p->own), "coarse store");
             }
-            if (ce && !ce->cm.p) {
+            if (s->cw == w && !ce->cm.p) {
                 ce->cm.alloc(n * cst);
                 ce->ch.alloc(n * cst);
                 launch_paa_envelope(s->data.p + s->guard, n, (uint32_t)s->d, (uint32_t)s->ulen,
-                                    (uint32_t)clen, s->ustride, cst,
+                                    (uint32_t)clen, w, s->ustride, cst,
                                     (uint32_t)std::min<uint64_t>(r, 0xffffffffu), 0.0f, ce->cm.p,
                                     ce->ch.p, p->own);
                 ck(cudaStreamSynchronize(p->own), "coarse candidate envelope");
             }
-            if (ce) {
+            if (s->cw == w) {
                 p->coarse = true;
+                p->coarse_short = !long_mode;
                 p->ccenv_m = ce->cm.p;
                 p->ccenv_h = ce->ch.p;
                 p->cq_m.alloc(nq_max * cst);
                 p->cq_h.alloc(nq_max * cst);
                 p->cq32.alloc(nq_max * cst);
+                if (!p->qabsmax.p) p->qabsmax.alloc(1);
             }
         }
     }
@@ -632,8 +652,11 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
     const bool rev_cb = rev_e == nullptr || std::atoi(rev_e) != 0;
     if (!dk && p->cenv_m) {
         launch_to_float(p->qg(), (uint64_t)nq * p->qstride, p->q32.p, st);
+        ++launches;
+    }
+    if (!dk && p->qabsmax.p) {
         launch_absmax(p->qg(), (uint64_t)nq * p->qstride, p->qabsmax.p, st);
-        launches += 2;
+        ++launches;
     }
     // coarse LB cascade: block means of the queries and of their envelopes
     // (1-3 queries too: the fused pass on block means costs a fraction of streaming the fp32
@@ -641,11 +664,11 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
     static const bool coarse_few = !(std::getenv("TSW_COARSE_FEW") && std::atoi(std::getenv("TSW_COARSE_FEW")) == 0);
     const bool coarse = !dk && p->coarse && (nq >= 4 || coarse_few);
     if (coarse) {
-        launch_paa_envelope(p->qg(), nq, (uint32_t)s->d, (uint32_t)p->qlen, (uint32_t)s->clen,
+        launch_paa_envelope(p->qg(), nq, (uint32_t)s->d, (uint32_t)p->qlen, (uint32_t)s->clen, s->cw,
                             p->qstride, s->cstride, (uint32_t)std::min<uint64_t>(p->r, 0xffffffffu),
                             s->err_c, p->cq_m.p, p->cq_h.p, st);
-        launch_paa_series(p->qg(), nq, (uint32_t)s->d, (uint32_t)s->clen, p->qstride, s->cstride,
-                          p->cq32.p, st);
+        launch_paa_series(p->qg(), nq, (uint32_t)s->d, (uint32_t)s->clen, s->cw, p->qstride,
+                          s->cstride, p->cq32.p, st);
         launches += 2;
     }
     DpArgs da{};
@@ -679,7 +702,8 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
         // coarse setup: the fast path's cumulative bounds from the block means (TSW_CSETUP=0:
         // per-point prefixes with the full-resolution re-check)
         const char* cse = std::getenv("TSW_CSETUP");
-        if (coarse && da.cenv_m && dtw4_supported(da) && (cse ? std::atoi(cse) != 0 : true)) {
+        if (coarse && (da.cenv_m || p->coarse_short) && dtw4_supported(da) &&
+            (cse ? std::atoi(cse) != 0 : true)) {
             csetup = true;
             da.c_x32 = s->paa.p;
             da.c_em = p->cq_m.p;
@@ -689,6 +713,9 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
             da.c_ch = p->ccenv_h;
             da.cstride = s->cstride;
             da.clen = (uint32_t)s->clen;
+            da.cw = s->cw;
+            da.clog = s->cw == 8 ? 3u : 2u;
+            da.qabsmax = p->qabsmax.p;
         }
     }
     auto run_dp = [&](const WorkQueue& w, uint32_t max_pairs, cudaStream_t on) {
@@ -696,7 +723,10 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
         da.probe = (p->probe && w.e == p->probe_wq().e) ? 1 : 0;
         // the few probe pairs keep the per-point (tighter) cumulative bounds: their launch is
         // one pair's sequential sweep, and a looser bound abandons later (C5 probes +45%)
-        da.csetup = (csetup && !da.probe) ? 1 : 0;
+        // (short series: the probes' setup from the block means too -- one chunk per direction)
+        da.csetup = (csetup && (!da.probe || p->coarse_short)) ? 1 : 0;
+        // (coarse pass: no block-sum rows -- the DP builds its prefixes itself)
+        da.pfx_blocks = (p->pfx_qn && !coarse) ? p->pfx.p : nullptr;
         if (dk) launch_dk_dp(da, max_pairs, (uint32_t)s->max_len, on);
         else launch_dtw_dp(da, max_pairs, on);
         ++launches;
@@ -745,7 +775,7 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
         // fused reverse bound (queries in fp32 + their max |value| first); 1-3 queries stream
         // the store with the forward bound only (measured: the reverse pass costs more than
         // the DP pairs it removes there)
-        if (p->cenv_m && p->lb2 && (nq >= 4 || coarse)) {
+        if ((p->cenv_m && p->lb2 && nq >= 4) || coarse) {
             la.cenv_m = p->cenv_m;
             la.cenv_h = p->cenv_h;
             la.q32 = p->q32.p;
@@ -766,7 +796,7 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
             la.q32 = p->cq32.p;
             la.pfx_qn = 0;
             la.pfx_out = nullptr;
-            la.lb_scale = (float)kPaa;
+            la.lb_scale = (float)s->cw;
             la.eq_scale = 0x1p-24 * (1.0 + 0x1p-20);
         }
         la.c_lo = 0;
@@ -1215,12 +1245,12 @@ int tsw_plan_stats(tsw_plan* p, tsw_stats* out) {
         // (+ the fused reverse pass's cached fp32 candidate envelopes, midpoint and half-width,
         // read once per execute)
         static const bool coarse_few = !(std::getenv("TSW_COARSE_FEW") && std::atoi(std::getenv("TSW_COARSE_FEW")) == 0);
-        const bool fused = !dk && p->cenv_m && p->lb2 && (p->nq >= 4 || (p->coarse && coarse_few));
+        const bool coarse_run = !dk && p->coarse && (p->nq >= 4 || coarse_few);
+        const bool fused = !dk && p->cenv_m && p->lb2 && p->nq >= 4;
         // coarse pass: the block means of the store and of the candidate envelopes instead
         out->bound_bytes = dk ? (uint64_t)p->store->n * 2 * p->store->d * sizeof(double)
-                           : (fused && p->coarse)
-                               ? p->store->n * p->store->cstride * sizeof(float) * 3
-                               : p->store->bytes / 2 * (fused ? 3 : 1);
+                           : coarse_run ? p->store->n * p->store->cstride * sizeof(float) * 3
+                                        : p->store->bytes / 2 * (fused ? 3 : 1);
         out->kernel_launches = (uint64_t)p->launches;
         if (p->timing && p->executed) {
             float ms[6] = {0};

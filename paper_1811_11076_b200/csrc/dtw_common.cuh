@@ -65,8 +65,8 @@ __device__ __forceinline__ void scan_pfx_row(float (&bv)[kPfxBlocks / WL], int g
 template <int WL, bool HADD, bool PAA = false>
 __device__ __forceinline__ bool prefix_terms(const float* x32, const float* em, const float* eh,
                                              float hadd, int gl, unsigned gmask, float* out, int L,
-                                             int stride, float lim = kInfF) {
-    auto put = [&](float v) { return PAA ? __fmul_rd(v, (float)kPaa) : v; };
+                                             int stride, float lim = kInfF, float scale = 1.0f) {
+    auto put = [&](float v) { return PAA ? __fmul_rd(v, scale) : v; };
     float carry = 0.0f;
     if (gl == 0) out[0] = 0.0f;
     for (int j0 = 0; j0 < L; j0 += 4 * WL) {
@@ -146,18 +146,19 @@ __device__ __forceinline__ bool setup_pfq(const DpArgs& a, const QEntry& pr, int
 }
 
 // Coarse setup (a.csetup): both cumulative bounds from the block means the coarse LB pass runs
-// on -- 1/kPaa of the terms and bytes of the per-point prefixes; pfx[b] / pfq[b] bound the terms
-// of the points < b * kPaa (index shift kPaaLog in the DP's abandon test).
+// on -- 1/cw of the terms and bytes of the per-point prefixes; pfx[b] / pfq[b] bound the terms
+// of the points < b * cw (index shift a.clog in the DP's abandon test).
 template <int WL>
 __device__ __forceinline__ bool setup_coarse(const DpArgs& a, const QEntry& pr, int gl, unsigned gmask,
                                              float* pfx, float* pfq, bool rev, int stride, float eqc,
                                              float lim) {
     const uint64_t co = (uint64_t)pr.c * a.cstride, qo = (uint64_t)pr.q * a.cstride;
+    const float sc = (float)a.cw;
     if (!prefix_terms<WL, false, true>(a.c_x32 + co, a.c_em + qo, a.c_eh + qo, 0.0f, gl, gmask, pfx,
-                                       (int)a.clen, stride, lim))
+                                       (int)a.clen, stride, lim, sc))
         return false;
     return !rev || prefix_terms<WL, true, true>(a.c_q32 + qo, a.c_cm + co, a.c_ch + co, eqc, gl, gmask,
-                                                pfq, (int)a.clen, stride, lim);
+                                                pfq, (int)a.clen, stride, lim, sc);
 }
 
 // Coarse mode: the limit of the setup's full-resolution bounds.  total > RU32(T * M) implies

@@ -172,19 +172,20 @@ void launch_envelope64(const double* q, uint32_t nq, uint32_t d, uint32_t len, u
 }
 
 // ---- coarse (piecewise-aggregate) series and envelopes for the LB cascade ----------------------
-// The coarse LB pass bounds LB_Box from below with block means over kPaa
-// consecutive points: f(x, lo, hi) = dist(x, [lo, hi])^2 is jointly convex, so by Jensen
-//   sum_{p in block} f(x_p, lo_p, hi_p)  >=  kPaa * f(mean x, mean lo, mean hi).
+// The coarse LB pass bounds LB_Box from below with block means over w
+// consecutive points (w = 4 or 8 <= kPaa): f(x, lo, hi) = dist(x, [lo, hi])^2 is jointly convex,
+// so by Jensen
+//   sum_{p in block} f(x_p, lo_p, hi_p)  >=  w * f(mean x, mean lo, mean hi).
 // Coarse series are tiled like the fine ones (32 coarse points per tile, pitch = cstride
-// elements, no guard tiles); a tail of len % kPaa points is dropped (its terms are >= 0).
+// elements, no guard tiles); a tail of len % w points is dropped (its terms are >= 0).
 // One thread per (series, coarse point, dim).
 //
-// Block mean of the values, fp32: the fp64 mean (7 additions, |error| <= 7 * 2^-53 * max|x|)
+// Block mean of the values, fp32: the fp64 mean (<= 7 additions, |error| <= 7 * 2^-53 * max|x|)
 // rounded to nearest, so |out - mean| <= max|x| * 2^-24 * (1 + 2^-20) over the in-range values;
 // a block holding a value beyond the fp32 range gets NaN: every term on it is
 // fmaxf(NaN, 0) = 0 (no bound from that block).
 __global__ void paa_series_kernel(const double* __restrict__ src, uint64_t nser, uint32_t d,
-                                  uint32_t clen, uint64_t pitch, uint64_t cstride,
+                                  uint32_t clen, uint32_t w, uint64_t pitch, uint64_t cstride,
                                   float* __restrict__ dst) {
     const uint64_t total = nser * cstride;
     for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total;
@@ -200,31 +201,30 @@ __global__ void paa_series_kernel(const double* __restrict__ src, uint64_t nser,
         const double* row = src + ser * pitch;
         double sum = 0.0;
         bool ok = true;
-#pragma unroll
-        for (uint32_t j = 0; j < kPaa; ++j) {
-            const double v = row[tidx(pc * kPaa + j, k, d)];
+        for (uint32_t j = 0; j < w; ++j) {
+            const double v = row[tidx(pc * w + j, k, d)];
             ok = ok && fabs(v) <= (double)FLT_MAX;
             sum = dadd(sum, v);
         }
-        dst[g] = ok ? __double2float_rn(dmul(sum, 1.0 / kPaa)) : __int_as_float(0x7fc00000);
+        dst[g] = ok ? __double2float_rn(dmul(sum, 1.0 / (double)w)) : __int_as_float(0x7fc00000);
     }
 }
 
-void launch_paa_series(const double* src, uint64_t nser, uint32_t d, uint32_t clen, uint64_t pitch,
-                       uint64_t cstride, float* dst, cudaStream_t st) {
+void launch_paa_series(const double* src, uint64_t nser, uint32_t d, uint32_t clen, uint32_t w,
+                       uint64_t pitch, uint64_t cstride, float* dst, cudaStream_t st) {
     const uint64_t total = nser * cstride;
     const int blocks = (int)std::min<uint64_t>((total + 255) / 256, (uint64_t)sm_count() * 16);
-    paa_series_kernel<<<std::max(blocks, 1), 256, 0, st>>>(src, nser, d, clen, pitch, cstride, dst);
+    paa_series_kernel<<<std::max(blocks, 1), 256, 0, st>>>(src, nser, d, clen, w, pitch, cstride, dst);
 }
 
 // Block means of a series' band envelope (window [p - r, p + r] clamped, envelope.cpp:25-59) in
 // the fp32 (midpoint, half-width) form: the means are summed with directed rounding (lo down,
 // hi up), the half-width covers [mean lo, mean hi] from the fp32 midpoint, rounded up, plus
-// `err` (the rounding bound of the coarse values it is compared with).  The eight windows of a
-// block share the core [p0 + 7 - r, p0 + r]; each adds a few points on either side.
+// `err` (the rounding bound of the coarse values it is compared with).  The w windows of a
+// block share the core [p0 + w - 1 - r, p0 + r]; each adds a few points on either side.
 __global__ void paa_envelope_kernel(const double* __restrict__ src, uint64_t nser, uint32_t d,
-                                    uint32_t len, uint32_t clen, uint64_t pitch, uint64_t cstride,
-                                    uint32_t r, float err, float* __restrict__ om,
+                                    uint32_t len, uint32_t clen, uint32_t w, uint64_t pitch,
+                                    uint64_t cstride, uint32_t r, float err, float* __restrict__ om,
                                     float* __restrict__ oh) {
     const uint64_t total = nser * cstride;
     for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total;
@@ -239,40 +239,42 @@ __global__ void paa_envelope_kernel(const double* __restrict__ src, uint64_t nse
             continue;
         }
         const double* row = src + ser * pitch;
-        const int64_t p0 = (int64_t)pc * kPaa, last = (int64_t)len - 1, rr = (int64_t)r;
+        const int64_t p0 = (int64_t)pc * w, last = (int64_t)len - 1, rr = (int64_t)r;
+        const int wi = (int)w;
         double slo = 0.0, shi = 0.0;
-        if (r >= kPaa) {
-            double cmn = kInf, cmx = -kInf;  // the shared core (non-empty: r >= kPaa)
-            for (int64_t w = max(p0 + (int64_t)kPaa - 1 - rr, (int64_t)0); w <= min(p0 + rr, last); ++w) {
-                const double v = row[tidx((uint32_t)w, k, d)];
+        if (r >= w) {
+            double cmn = kInf, cmx = -kInf;  // the shared core (non-empty: r >= w)
+            for (int64_t x = max(p0 + wi - 1 - rr, (int64_t)0); x <= min(p0 + rr, last); ++x) {
+                const double v = row[tidx((uint32_t)x, k, d)];
                 cmn = v < cmn ? v : cmn;
                 cmx = v > cmx ? v : cmx;
             }
-            // left extensions [p0 + j - r, p0 + kPaa - 2 - r], j = kPaa - 2 .. 0 (running)
+            // left extensions [p0 + j - r, p0 + w - 2 - r], j = w - 2 .. 0 (running)
             double lmn[kPaa], lmx[kPaa];
             double mn = kInf, mx = -kInf;
-            lmn[kPaa - 1] = kInf;
-            lmx[kPaa - 1] = -kInf;
 #pragma unroll
-            for (int j = (int)kPaa - 2; j >= 0; --j) {
-                const int64_t w = p0 + j - rr;
-                if (w >= 0 && w <= last) {
-                    const double v = row[tidx((uint32_t)w, k, d)];
-                    mn = v < mn ? v : mn;
-                    mx = v > mx ? v : mx;
+            for (int j = (int)kPaa - 1; j >= 0; --j) {
+                if (j <= wi - 2) {
+                    const int64_t x = p0 + j - rr;
+                    if (x >= 0 && x <= last) {
+                        const double v = row[tidx((uint32_t)x, k, d)];
+                        mn = v < mn ? v : mn;
+                        mx = v > mx ? v : mx;
+                    }
                 }
                 lmn[j] = mn;
                 lmx[j] = mx;
             }
-            // right extensions [p0 + r + 1, p0 + j + r], j = 1 .. kPaa - 1 (running)
+            // right extensions [p0 + r + 1, p0 + j + r], j = 1 .. w - 1 (running)
             mn = kInf;
             mx = -kInf;
 #pragma unroll
             for (int j = 0; j < (int)kPaa; ++j) {
+                if (j >= wi) break;
                 if (j > 0) {
-                    const int64_t w = p0 + j + rr;
-                    if (w >= 0 && w <= last) {
-                        const double v = row[tidx((uint32_t)w, k, d)];
+                    const int64_t x = p0 + j + rr;
+                    if (x >= 0 && x <= last) {
+                        const double v = row[tidx((uint32_t)x, k, d)];
                         mn = v < mn ? v : mn;
                         mx = v > mx ? v : mx;
                     }
@@ -282,11 +284,11 @@ __global__ void paa_envelope_kernel(const double* __restrict__ src, uint64_t nse
                 shi = __dadd_ru(shi, hi);
             }
         } else {
-            for (uint32_t j = 0; j < kPaa; ++j) {
+            for (uint32_t j = 0; j < w; ++j) {
                 const int64_t p = p0 + j;
                 double mn = kInf, mx = -kInf;
-                for (int64_t w = max(p - rr, (int64_t)0); w <= min(p + rr, last); ++w) {
-                    const double v = row[tidx((uint32_t)w, k, d)];
+                for (int64_t x = max(p - rr, (int64_t)0); x <= min(p + rr, last); ++x) {
+                    const double v = row[tidx((uint32_t)x, k, d)];
                     mn = v < mn ? v : mn;
                     mx = v > mx ? v : mx;
                 }
@@ -294,7 +296,7 @@ __global__ void paa_envelope_kernel(const double* __restrict__ src, uint64_t nse
                 shi = __dadd_ru(shi, mx);
             }
         }
-        const double mlo = __dmul_rd(slo, 1.0 / kPaa), mhi = __dmul_ru(shi, 1.0 / kPaa);
+        const double mlo = __dmul_rd(slo, 1.0 / (double)w), mhi = __dmul_ru(shi, 1.0 / (double)w);
         if (!(mlo >= -(double)FLT_MAX && mhi <= (double)FLT_MAX)) {
             om[g] = 0.0f;  // the block's envelope leaves the fp32 range: terms of 0
             oh[g] = INFINITY;
@@ -308,12 +310,12 @@ __global__ void paa_envelope_kernel(const double* __restrict__ src, uint64_t nse
 }
 
 void launch_paa_envelope(const double* src, uint64_t nser, uint32_t d, uint32_t len, uint32_t clen,
-                         uint64_t pitch, uint64_t cstride, uint32_t r, float err, float* om, float* oh,
-                         cudaStream_t st) {
+                         uint32_t w, uint64_t pitch, uint64_t cstride, uint32_t r, float err,
+                         float* om, float* oh, cudaStream_t st) {
     const uint64_t total = nser * cstride;
     const int blocks = (int)std::min<uint64_t>((total + 255) / 256, (uint64_t)sm_count() * 16);
-    paa_envelope_kernel<<<std::max(blocks, 1), 256, 0, st>>>(src, nser, d, len, clen, pitch, cstride,
-                                                             r, err, om, oh);
+    paa_envelope_kernel<<<std::max(blocks, 1), 256, 0, st>>>(src, nser, d, len, clen, w, pitch,
+                                                             cstride, r, err, om, oh);
 }
 
 // ---- sampled seed upper bounds ----------------------------------------------------------------
@@ -1048,14 +1050,20 @@ __global__ void __launch_bounds__(256, 2) lb12_compact_kernel(LbCompactArgs a) {
     float* stash = reinterpret_cast<float*>(lb12_smem + 8 * kList * (sizeof(QEntry) + sizeof(float))) +
                    (size_t)wib * 32 * 32;
     const float eq = __double2float_ru(__dmul_ru(*a.qabsmax, a.eq_scale != 0.0 ? a.eq_scale : 0x1p-24));
+    // a task = one candidate group x qbt query blocks (all of them unless the groups alone
+    // cannot fill the GPU: small stores, launch_lb_compact)
+    const uint32_t qbt = a.qb_per_task ? a.qb_per_task : nqb;
+    const uint32_t tpg = (nqb + qbt - 1) / qbt;  // tasks per group
     for (;;) {
-        unsigned cg = 0;
-        if (lane == 0) cg = atomicAdd(a.task, 1u);  // dynamic: groups' reverse work varies
-        cg = __shfl_sync(0xffffffffu, cg, 0);
+        unsigned task = 0;
+        if (lane == 0) task = atomicAdd(a.task, 1u);  // dynamic: groups' reverse work varies
+        task = __shfl_sync(0xffffffffu, task, 0);
+        const uint32_t cg = task / tpg;
         if (cg >= ngroups) break;
         const uint32_t c0 = (g_lo + cg) * CB;
+        const uint32_t qb_lo = (task - cg * tpg) * qbt, qb_hi = min(qb_lo + qbt, nqb);
         int cnt = 0;
-        for (uint32_t qbk = 0; qbk < nqb; ++qbk) {
+        for (uint32_t qbk = qb_lo; qbk < qb_hi; ++qbk) {
             const TileOut t = lb1_tile<QB, CB, false, TSW_LB12_PACK>(a, pc, c0, qbk * QB, stash, total4);
             const unsigned tm = __ballot_sync(0xffffffffu, t.take);
             if (t.take) list[cnt + __popc(tm & ((1u << lane) - 1u))] = QEntry{t.q, t.c, t.lb, t.ps};
@@ -1087,6 +1095,12 @@ void launch_lb_compact(const LbCompactArgs& a_in, cudaStream_t st) {
         const uint32_t fpl = (total4 + 31) / 32;
         // (the reverse sums accumulate over all chunks: 2 float4 per lane per chunk suffice)
         auto kern = fpl <= 1 ? lb12_compact_kernel<QB, CB, 1> : lb12_compact_kernel<QB, CB, 2>;
+        // fewer query blocks per task until there are ~4 tasks per resident warp
+        const uint64_t ngroups = ((uint64_t)a.c_hi - a.c_lo + CB - 1) / CB;
+        const uint32_t nqb = (a.nq + QB - 1) / QB;
+        uint32_t qbt = nqb;
+        while (qbt > 1 && ngroups * ((nqb + qbt - 1) / qbt) < (uint64_t)sm_count() * 16 * 4) qbt = (qbt + 1) / 2;
+        a.qb_per_task = qbt;
         const size_t smem12 = (size_t)8 * kList * (sizeof(QEntry) + sizeof(float)) + smem;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem12);
         kern<<<sm_count() * 2, 256, smem12, st>>>(a);

@@ -130,9 +130,9 @@ __device__ __forceinline__ void iter(Lane<G, D>& s, const double* __restrict__ s
         // forward (candidate columns ahead) and reverse (query rows ahead, pfq) cumulative
         // bounds at the lane's smallest candidate / query index: both lower-bound every slot's
         // own (pfq == pfx when the reverse bound is off: max of equal values)
-        // (CS, coarse setup: both prefixes at block-mean granularity, kPaa points per entry)
-        const float rc = pfx[min(max(tjb - TTMAX, 0), L - 1) >> (CS ? kPaaLog : plog)];
-        const float rq = pfq == pfx ? rc : pfq[min(max(sjb, 0), L - 1) >> (CS ? kPaaLog : 0)];
+        // (CS, coarse setup: both prefixes at block-mean granularity, 2^plog points per entry)
+        const float rc = pfx[min(max(tjb - TTMAX, 0), L - 1) >> plog];
+        const float rq = pfq == pfx ? rc : pfq[min(max(sjb, 0), L - 1) >> (CS ? plog : 0)];
         const double Rmin = (double)fmaxf(rc, rq);
         Tlim = __dsub_ru(__dmul_ru(T, margin), Rmin);
     }
@@ -251,7 +251,7 @@ __global__ void __launch_bounds__(TPB, MINB) dtw4_kernel(DpArgs a, uint32_t pstr
                                                     (abl ? ((a.nq + 3) & ~3u) * sizeof(unsigned) : 0));
     float* pfx = big + (size_t)(threadIdx.x / WL) * pstride;
     // reverse cumulative bound (a.cenv_m set): the group's pfq row after the pfx rows
-    const bool rev = a.cenv_m != nullptr;
+    const bool rev = CS ? a.c_cm != nullptr : a.cenv_m != nullptr;
     float* pfq = rev ? big + (size_t)NG * pstride + (size_t)(threadIdx.x / WL) * pstride : pfx;
     const float eq = rev ? __double2float_ru(__dmul_ru(*a.qabsmax, 0x1p-24)) : 0.0f;
     const int L = (int)a.qlen;
@@ -271,7 +271,7 @@ __global__ void __launch_bounds__(TPB, MINB) dtw4_kernel(DpArgs a, uint32_t pstr
     if (ab_local)
         for (uint32_t i = threadIdx.x; i < a.nq; i += blockDim.x) ab_local[i] = 0u;
     __syncthreads();
-    const int plog = a.pfx_blocks ? (int)a.pfx_log : 0;
+    const int plog = CS ? (int)a.clog : (a.pfx_blocks ? (int)a.pfx_log : 0);
     const float eqc = CS && rev ? __double2float_ru(__dmul_ru(*a.qabsmax, 0x1p-24 * (1.0 + 0x1p-20)))
                                 : 0.0f;
     // lane geometry: slot e holds offset obase + e; lanes past `edge` are idle (garbage) and
@@ -513,7 +513,7 @@ void run4(const DpArgs& a, uint32_t max_pairs, cudaStream_t st) {
     const uint32_t pstride = (std::max<uint32_t>(a.qlen + 1, kPfxBlocks + 1) + 3) & ~3u;
     const size_t fixed = (size_t)(TPB / WL) * sizeof(Stage) +
                          (a.state && a.nq <= kAbLocalMax ? ((a.nq + 3) & ~3u) * sizeof(unsigned) : 0);
-    const size_t big = (size_t)(TPB / WL) * pstride * sizeof(float) * (a.cenv_m ? 2 : 1) +
+    const size_t big = (size_t)(TPB / WL) * pstride * sizeof(float) * ((CS ? a.c_cm : a.cenv_m) ? 2 : 1) +
                        ((a.qlen + 1 + 3) & ~3u) * sizeof(uint32_t);
     const bool spill = fixed + big > smem_optin();
     const size_t smem = spill ? fixed : fixed + big;
@@ -534,7 +534,7 @@ void run4(const DpArgs& a, uint32_t max_pairs, cudaStream_t st) {
 
 template <int G, int WL, int RPAR, bool IDLE, bool LONG>
 void run4_dl(const DpArgs& a, uint32_t max_pairs, cudaStream_t st) {
-    if constexpr (LONG) {
+    if constexpr (G == 2) {
         if (a.csetup) {
             switch (a.store.d) {
                 case 1: run4<G, 1, WL, RPAR, IDLE, LONG, true>(a, max_pairs, st); break;

@@ -29,8 +29,7 @@ constexpr int kSelChunk = 4096; // bitonic selection chunk
 constexpr double kInf = __builtin_huge_val();
 constexpr float kInfF = __builtin_huge_valf();
 constexpr uint32_t kTile = 32;  // points per layout tile
-constexpr uint32_t kPaa = 8;    // points per block mean of the coarse LB pass
-constexpr int kPaaLog = 3;
+constexpr uint32_t kPaa = 8;    // most points per block mean of the coarse LB pass
 
 // element offset of (point p, dim k) in a tiled series of dimension d
 __host__ __device__ __forceinline__ uint64_t tidx(uint32_t p, uint32_t k, uint32_t d) {
@@ -277,11 +276,11 @@ void launch_fill(double* p, uint64_t count, double v, cudaStream_t st);
 // coarse LB cascade: fp32 block means (kPaa points) of nser tiled fp64 series at `pitch`, and the
 // block means of their band envelopes in the (midpoint, half-width + err) form; outputs tiled
 // with clen coarse points at pitch `cstride`
-void launch_paa_series(const double* src, uint64_t nser, uint32_t d, uint32_t clen, uint64_t pitch,
-                       uint64_t cstride, float* dst, cudaStream_t st);
+void launch_paa_series(const double* src, uint64_t nser, uint32_t d, uint32_t clen, uint32_t w,
+                       uint64_t pitch, uint64_t cstride, float* dst, cudaStream_t st);
 void launch_paa_envelope(const double* src, uint64_t nser, uint32_t d, uint32_t len, uint32_t clen,
-                         uint64_t pitch, uint64_t cstride, uint32_t r, float err, float* om, float* oh,
-                         cudaStream_t st);
+                         uint32_t w, uint64_t pitch, uint64_t cstride, uint32_t r, float err,
+                         float* om, float* oh, cudaStream_t st);
 // ends[c] = (first point, last point) of every series of a store
 void launch_series_ends(const StoreDev& s, double* ends, cudaStream_t st);
 void launch_to_float(const double* src, uint64_t count, float* dst, cudaStream_t st);
@@ -344,6 +343,7 @@ struct LbCompactArgs {
     const float* q32;         // fp32 (round-to-nearest) queries, pitch qstride
     const double* qabsmax;    // max |query value|: the fp32 conversion error is <= it * 2^-24
     unsigned* task;           // candidate-group work counter (zeroed per execute)
+    uint32_t qb_per_task;     // query blocks per task of the fused pass (0: all; set by the launcher)
     uint32_t c_lo, c_hi;      // candidate range of this pass (staged execution; c_lo % 4 == 0)
     // coarse pass: `store.data32`, the envelopes and q32 hold block means; the
     // summed terms are scaled by lb_scale = kPaa (0: no scaling) and the fp32 error of the coarse
@@ -421,6 +421,7 @@ struct DpArgs {
     const float* c_ch;
     uint64_t cstride;
     uint32_t clen;
+    uint32_t cw, clog;          // points per block mean (4 or 8) and its log2
 };
 
 // Host: the per-block opt-in shared-memory limit, and a stream-ordered global scratch for the
