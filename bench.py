@@ -430,22 +430,30 @@ def gpu_leg(a, t, torch, store, db, cfg, metric, sh, qs, stream, flush, ws, rank
     sm_clk = clocks.get("sm_mhz") or 1965.0
     nsm = torch.cuda.get_device_properties(dev).multi_processor_count
     fp32_peak = nsm * 128 * sm_clk * 1e6 / 1e12  # T instr/s (1 FP32 lane-op per lane-cycle)
-    lb_terms = float(nq) * sh["count"] * sh["len"] * d if metric == "dtw" else 0.0
+    # coarse cascade: the pass runs on block means of `blk` points (forward terms counted; the
+    # reverse terms of the forward survivors are extra work, not counted)
+    blk = int(ph.get("bound_block") or 1)
+    lb_terms = float(nq) * sh["count"] * (sh["len"] // blk) * d if metric == "dtw" else 0.0
     lb_tips = lb_terms * 4 / (lb_ms * 1e-3) / 1e12 if (lb_ms > 0 and lb_terms) else None
     fp64_store = float(sh["count"]) * sh["len"] * d * 8
     hbm_view = {"achieved": lb_gbs, "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
                 "frac": (lb_gbs / peaks["hbm_gbs"]) if lb_gbs else None,
                 "peak_source": f"{peak_kind} hbm_gbs (MEASURED_PEAKS.json copy rate)",
                 "algorithmic_bytes_per_launch": ph["bound_bytes"] / max(1.0, ph["bound_passes"]),
-                "bytes_note": "padded fp32 shadow store (32-point tiles incl. guard tiles; "
-                              "2.5 GB at C5, built at store creation) + for the fused reverse "
-                              "pass (r >= 32, >= 4 queries) the cached fp32 candidate envelopes "
-                              "(midpoint + half-width, 2x the shadow store); the SURVEY §8(d) "
-                              "fp64 view N*L*d*8 is fp64_store_bytes",
+                "bytes_note": ("coarse cascade: fp32 block means (%d points) of the store and of "
+                               "the candidate envelopes (midpoint + half-width), 3 x N*(L/%d)*d*4 "
+                               "bytes, built once per store / band radius; the full-resolution "
+                               "terms are not read by the pass (the SURVEY §8(d) fp64 view "
+                               "N*L*d*8 is fp64_store_bytes)" % (blk, blk)) if blk > 1 else
+                              ("padded fp32 shadow store (32-point tiles incl. guard tiles, built "
+                               "at store creation) + for the fused reverse pass the cached fp32 "
+                               "candidate envelopes (2x the shadow store); the SURVEY §8(d) "
+                               "fp64 view N*L*d*8 is fp64_store_bytes"),
+                "block_mean_points": blk,
                 "fp64_store_bytes": fp64_store,
                 "fp64_view_gbs": fp64_store / (lb_ms * 1e-3) / 1e9 if lb_ms > 0 else None}
     lb_short = (L + 31) // 32 * 32 * d <= 768 and os.environ.get("TSW_LB_ENV", "1") != "0"
-    lb_kernel = ("lb12_compact_kernel" if (r >= 32) else
+    lb_kernel = ("lb12_compact_kernel" if (r >= 32 or blk > 1) else
                  "lb_env_kernel" if lb_short else "lb_compact_kernel") if metric == "dtw" \
         else "dk_compact_kernel"
     traffic = load_traffic(cfg, metric) or {}
@@ -587,8 +595,12 @@ def main():
                           "points + max|x| (tsw_store_create: H2D + tiling kernels)",
         "plan_build_s": {metric: main_leg["plan_build_s"],
                          **{m: extra[m]["plan_build_s"] for m in extra}},
-        "plan_contents": "scratch for nq_max queries; for DTW with r >= 32 also the per-radius "
-                         "fp32 candidate envelopes (N*L*d*8 bytes, built once per store and r)",
+        "plan_contents": "scratch for nq_max queries; for DTW, built once per store by the first "
+                         "plan: the coarse cascade's fp32 block means of the store (N*(L/w)*d*4 "
+                         "bytes, w = 8 above 256 points else 4) and, per band radius, of the "
+                         "candidate envelopes (2x that); with r >= 32 also the full-resolution "
+                         "fp32 candidate envelopes (N*L*d*8 bytes: the 1-query plans' and the "
+                         "probes' reverse cumulative bound)",
         "synth_s": synth_s}
     if extra:
         line["legs"] = {}

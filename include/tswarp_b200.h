@@ -76,6 +76,8 @@ typedef struct tsw_stats {
     uint64_t dp_pairs;    /* (query, candidate) pairs that entered a DP kernel                */
     uint64_t dp_cells;    /* DP cells evaluated (counted by the kernels)                      */
     uint64_t kernel_launches;
+    uint64_t bound_block; /* DTW: points per block mean of the bound pass (coarse cascade: 4 / 8;
+                             1 = full resolution)                                              */
 } tsw_stats;
 
 typedef struct tsw_store tsw_store; /* device-resident candidate store (read-only)      */

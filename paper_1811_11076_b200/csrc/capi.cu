@@ -1252,6 +1252,7 @@ int tsw_plan_stats(tsw_plan* p, tsw_stats* out) {
                            : coarse_run ? p->store->n * p->store->cstride * sizeof(float) * 3
                                         : p->store->bytes / 2 * (fused ? 3 : 1);
         out->kernel_launches = (uint64_t)p->launches;
+        out->bound_block = coarse_run ? p->store->cw : 1;
         if (p->timing && p->executed) {
             float ms[6] = {0};
             for (int i = 1; i <= 5; ++i) cudaEventElapsedTime(&ms[i], p->ev[i - 1], p->ev[i]);

@@ -51,12 +51,31 @@ __device__ __forceinline__ void prefetch_l1(const double* p) {
 template <bool VEC>
 __device__ __forceinline__ void ld4(double (&v)[4], const double* __restrict__ base, int o0, int k) {
     if constexpr (VEC) {
-        const double2 a = __ldg(reinterpret_cast<const double2*>(base + o0 + 32 * k));
-        const double2 b = __ldg(reinterpret_cast<const double2*>(base + o0 + 32 * k + 2));
-        v[0] = b.y;
-        v[1] = b.x;
-        v[2] = a.y;
-        v[3] = a.x;
+        // (TSW_DTWT_LD256=1: one 256-bit load, LDG.E.256 on sm_100 -- the lanes of a tile
+        // anti-diagonal read 32-byte runs 32 bytes apart, so one request covers whole cache
+        // lines, half the L1 data-pipe wavefronts of two 128-bit loads.  Measured at C4: DP
+        // 93.6 -> 105.9 ms, same-box -- the 8-register destination constrains the schedule
+        // more than the wavefronts cost; off)
+#ifndef TSW_DTWT_LD256
+#define TSW_DTWT_LD256 0
+#endif
+        if constexpr (TSW_DTWT_LD256) {
+            double a0, a1, a2, a3;
+            asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+                         : "=d"(a0), "=d"(a1), "=d"(a2), "=d"(a3)
+                         : "l"(base + o0 + 32 * k));
+            v[0] = a3;
+            v[1] = a2;
+            v[2] = a1;
+            v[3] = a0;
+        } else {
+            const double2 a = __ldg(reinterpret_cast<const double2*>(base + o0 + 32 * k));
+            const double2 b = __ldg(reinterpret_cast<const double2*>(base + o0 + 32 * k + 2));
+            v[0] = b.y;
+            v[1] = b.x;
+            v[2] = a.y;
+            v[3] = a.x;
+        }
     }
 }
 

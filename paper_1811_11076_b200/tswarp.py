@@ -83,7 +83,7 @@ class Stats_t(C.Structure):
                 ("ms_compact", C.c_double), ("ms_dp", C.c_double),
                 ("bound_bytes", C.c_uint64), ("bound_passes", C.c_uint64),
                 ("dp_pairs", C.c_uint64), ("dp_cells", C.c_uint64),
-                ("kernel_launches", C.c_uint64)]
+                ("kernel_launches", C.c_uint64), ("bound_block", C.c_uint64)]
 
 
 _lib = None
