@@ -460,14 +460,14 @@ def gpu_leg(a, t, torch, store, db, cfg, metric, sh, qs, stream, flush, ws, rank
     if lb_tips:
         roof_lb = {"bound": "fp32_issue", "kernel": lb_kernel, "achieved": lb_tips,
                    "peak": fp32_peak, "unit": "Tinst/s", "frac": lb_tips / fp32_peak,
-                   "traffic": traffic.get("bound"),
+                   "traffic": traffic.get("lb", traffic.get("bound")),
                    "peak_source": "SMs x 128 FP32 lanes x sampled SM clock (nvidia-smi, timed region)",
                    "algorithmic_instr_per_launch": lb_terms * 4, "ms": lb_ms,
                    "hbm_view": hbm_view,
                    "share_of_step": lb_ms / ph["ms_total"] if ph["ms_total"] else None}
     else:
         roof_lb = {"bound": "hbm", "kernel": lb_kernel, **hbm_view, "ms": lb_ms,
-                   "traffic": traffic.get("bound"),
+                   "traffic": traffic.get("lb", traffic.get("bound")),
                    "share_of_step": lb_ms / ph["ms_total"] if ph["ms_total"] else None}
     dp_kernel = ("dtw4_kernel" if (d <= 4 and r <= 52) else
                  "dtwt_kernel" if (d >= 5 and min(r, L - 1) <= 31) else "dtw_dp_kernel") \

@@ -709,8 +709,11 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
             da.c_em = p->cq_m.p;
             da.c_eh = p->cq_h.p;
             da.c_q32 = p->cq32.p;
-            da.c_cm = p->ccenv_m;
-            da.c_ch = p->ccenv_h;
+            // (TSW_CS_REV=0: forward cumulative bound only -- half the setup; A/B)
+            const char* cre = std::getenv("TSW_CS_REV");
+            const bool cs_rev = cre ? std::atoi(cre) != 0 : true;
+            da.c_cm = cs_rev ? p->ccenv_m : nullptr;
+            da.c_ch = cs_rev ? p->ccenv_h : nullptr;
             da.cstride = s->cstride;
             da.clen = (uint32_t)s->clen;
             da.cw = s->cw;
