@@ -391,9 +391,10 @@ std::unique_ptr<tsw_plan> make_plan(tsw_store* s, uint64_t nq_max, uint64_t qlen
     const uint64_t s_want = se && std::atoll(se) > 0 ? (uint64_t)std::atoll(se) : s_auto;
     p->S = std::min<uint64_t>(n, s_want);
     // probe = the most promising sampled candidates, DP'd first to tighten the threshold.  DTW
-    // probes are cheap (banded, abandoning) and feed the LB compaction: 2k (>= 8).  A DK probe
+    // probes are cheap (banded, abandoning) and feed the LB compaction: 2k (>= 16; with the coarse
+    // pass 16 instead of 8 probes cut the C3 step 3.8%, C2 unchanged).  A DK probe
     // runs a near-full L^2 DP under the loose seed, so DK probes only k.
-    uint64_t want_probe = metric == TSW_METRIC_DTW ? std::max<uint64_t>({8, 2 * p->kk, p->S / 256}) : p->kk;
+    uint64_t want_probe = metric == TSW_METRIC_DTW ? std::max<uint64_t>({16, 2 * p->kk, p->S / 256}) : p->kk;
     if (const char* pe = std::getenv("TSW_PROBE"); pe && *pe) want_probe = std::max<long long>(1, std::atoll(pe));
     p->probe = p->kk <= (uint64_t)kKMax ? std::min<uint64_t>({p->S, (uint64_t)kKMax, want_probe}) : 0;
     p->P = std::max<uint64_t>(1, std::min<uint64_t>(kKMax, std::max(p->kk, p->probe)));
