@@ -201,6 +201,11 @@ struct tsw_store {
     DevBuf<float> paa;
     uint64_t clen = 0, cstride = 0;
     uint32_t cw = 0;         // points per block mean (8: long series, 4: short)
+    // guided seed sample: a second, coarser level of block means (cw2 points)
+    // for the all-pairs distance estimate that picks the sampled candidates
+    DevBuf<float> paa2;
+    uint64_t clen2 = 0, cstride2 = 0;
+    uint32_t cw2 = 0;
     float err_c = 0.0f;      // >= |coarse value - true block mean| (in-range values)
     StoreDev dev() const {
         StoreDev s{};
@@ -250,6 +255,11 @@ struct tsw_plan {
     const float* ccenv_m = nullptr;
     const float* ccenv_h = nullptr;
     DevBuf<float> cq_m, cq_h, cq32;
+    // guided seed sample: the G candidates with the smallest coarse diagonal distance per query
+    uint32_t G = 0;            // 0: strided sample
+    DevBuf<float> cq2, zero2;  // query block means at the second level; zero half-widths
+    DevBuf<double> g_sv, g_val;
+    DevBuf<uint32_t> g_si, g_idx;
     uint32_t pfx_qn = 0, pfx_log = 0, pfx_cap = 0;
     DevBuf<uint32_t> sel_si, sel_i, top_i, fin_si;
     DevBuf<double> fin_sv;
@@ -518,6 +528,37 @@ std::unique_ptr<tsw_plan> make_plan(tsw_store* s, uint64_t nq_max, uint64_t qlen
                 p->cq_h.alloc(nq_max * cst);
                 p->cq32.alloc(nq_max * cst);
                 if (!p->qabsmax.p) p->qabsmax.alloc(1);
+                // guided seed sample (long series): estimate every pair's diagonal distance on
+                // block means of 32 points, take the G smallest per query as the sample.
+                // TSW_GUIDED=0 / G overrides.
+                const char* ge = std::getenv("TSW_GUIDED");
+                const uint64_t gw = ge ? (uint64_t)std::atoll(ge) : 32;
+                const uint32_t w2 = 32;
+                if (long_mode && gw > 0 && gw <= (uint64_t)kKMax && n >= 16 * gw && qlen / w2 >= 8 &&
+                    p->kk <= gw) {
+                    const uint64_t clen2 = qlen / w2, cst2 = stride_of(clen2, s->d);
+                    if (!s->paa2.p) {
+                        s->clen2 = clen2;
+                        s->cstride2 = cst2;
+                        s->cw2 = w2;
+                        s->paa2.alloc(n * cst2);
+                        launch_paa_series(s->data.p + s->guard, n, (uint32_t)s->d, (uint32_t)clen2, w2,
+                                          s->ustride, cst2, s->paa2.p, p->own);
+                        ck(cudaStreamSynchronize(p->own), "coarse store (level 2)");
+                    }
+                    p->G = (uint32_t)gw;
+                    p->cq2.alloc(nq_max * cst2);
+                    p->zero2.alloc(nq_max * cst2);
+                    ck(cudaMemset(p->zero2.p, 0, nq_max * cst2 * sizeof(float)), "memset");
+                    const uint64_t fch = (n + kSelChunk - 1) / kSelChunk;
+                    p->g_sv.alloc(2 * nq_max * fch * gw);
+                    p->g_si.alloc(2 * nq_max * fch * gw);
+                    p->g_val.alloc(nq_max * gw);
+                    p->g_idx.alloc(nq_max * gw);
+                    // the probes come from the guided sample
+                    p->probe = std::min<uint64_t>(p->probe, gw);
+                    p->P = std::max<uint64_t>(1, std::min<uint64_t>(kKMax, std::max(p->kk, p->probe)));
+                }
             }
         }
     }
@@ -609,20 +650,47 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
         ++launches;
     }
     mark(1);
+    // guided seed sample: the coarse diagonal distance of every (query, candidate) pair (the
+    // forward tile pass on second-level block means with zero half-widths: terms (x - q)^2),
+    // its G smallest per query become the sample -- instead of a strided 4% of the store
+    const uint32_t S_eff = (!dk && p->G) ? p->G : (uint32_t)p->S;
+    if (!dk && p->G) {
+        launch_paa_series(p->qg(), nq, (uint32_t)s->d, (uint32_t)s->clen2, s->cw2, p->qstride,
+                          s->cstride2, p->cq2.p, st);
+        LbCompactArgs ea{};
+        ea.store = s->dev();
+        ea.store.data = nullptr;
+        ea.store.data32 = s->paa2.p;
+        ea.store.ulen = (uint32_t)s->clen2;
+        ea.store.ustride = ea.store.tstride = s->cstride2;
+        ea.env_lo = p->cq2.p;
+        ea.env_hi = p->zero2.p;
+        ea.nq = nq;
+        ea.qstride = s->cstride2;
+        ea.margin = 1.0;
+        ea.lb_out = reinterpret_cast<float*>(p->res_i.p);  // scratch: the result buffers are idle here
+        launch_lb_compact(ea, st);
+        launch_widen(reinterpret_cast<const float*>(p->res_i.p), (uint64_t)nq * n, p->res_d.p, st);
+        launches += 3;
+        // (approximate: 4 values per warp of 256 in the chunked levels -- a sample, not a top-k)
+        launch_select_smallest(p->res_d.p, nullptr, nullptr, nq, n, p->G, p->g_sv.p, p->g_si.p,
+                               p->g_val.p, p->g_idx.p, st, &launches, 4u);
+    }
     SampleArgs sa{};
     sa.store = s->dev();
     sa.queries = p->qg();
     sa.nq = nq;
     sa.qlen = (uint32_t)p->qlen;
     sa.qstride = p->qstride;
-    sa.S = (uint32_t)p->S;
+    sa.S = S_eff;
+    sa.cand = (!dk && p->G) ? p->g_idx.p : nullptr;
     sa.ub_scale = p->ub_scale;
     sa.dk = dk;
     sa.out_ub = p->ub.p;
     sa.part = p->ub_part.p;
     sa.part_cap = p->ub_part.n;
     launches += launch_sample_ub(sa, st);
-    launch_select_smallest(p->ub.p, nullptr, nullptr, nq, (uint32_t)p->S, (uint32_t)p->P,
+    launch_select_smallest(p->ub.p, nullptr, nullptr, nq, S_eff, (uint32_t)p->P,
                            p->sel_sv.p, p->sel_si.p, p->sel_v.p, p->sel_i.p, st, &launches);
     SeedArgs se{};
     se.sel_v = p->sel_v.p;
@@ -632,7 +700,8 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
     se.P = (uint32_t)p->P;
     se.k = (uint32_t)std::min<uint64_t>(p->k, 0xffffffffu);
     se.probe = (uint32_t)p->probe;
-    se.S = (uint32_t)p->S;
+    se.S = S_eff;
+    se.cand = sa.cand;
     se.dk = dk;
     se.state = p->state.p;
     se.slots = p->slots.p;

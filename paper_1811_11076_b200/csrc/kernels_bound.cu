@@ -64,6 +64,17 @@ __global__ void to_float_kernel(const double* __restrict__ src, uint64_t n, floa
         dst[i] = isinf(src[i]) ? 0.0f : fminf(fmaxf(__double2float_rn(src[i]), -FLT_MAX), FLT_MAX);
 }
 
+__global__ void widen_kernel(const float* __restrict__ src, uint64_t n, double* __restrict__ dst) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        dst[i] = (double)src[i];
+}
+
+void launch_widen(const float* src, uint64_t count, double* dst, cudaStream_t st) {
+    const int blocks = (int)std::min<uint64_t>((count + 255) / 256, (uint64_t)sm_count() * 16);
+    widen_kernel<<<std::max(blocks, 1), 256, 0, st>>>(src, count, dst);
+}
+
 void launch_to_float(const double* src, uint64_t count, float* dst, cudaStream_t st) {
     const int blocks = (int)std::min<uint64_t>((count + 255) / 256, (uint64_t)sm_count() * 16);
     to_float_kernel<<<std::max(blocks, 1), 256, 0, st>>>(src, count, dst);
@@ -332,7 +343,8 @@ __global__ void __launch_bounds__(256) sample_ub_kernel(SampleArgs a) {
     const uint32_t d = a.store.d, m = a.qlen;
     for (uint64_t w = wid; w < (uint64_t)a.nq * a.S; w += nw) {
         const uint32_t q = (uint32_t)(w / a.S), j = (uint32_t)(w - (uint64_t)q * a.S);
-        const uint32_t c = (uint32_t)((uint64_t)j * a.store.n / a.S);
+        const uint32_t c = a.cand ? min(a.cand[(uint64_t)q * a.S + j], a.store.n - 1)
+                                  : (uint32_t)((uint64_t)j * a.store.n / a.S);
         const double* s = a.queries + (uint64_t)q * a.qstride;
         const double* t = a.store.data + series_off(a.store, c);
         const uint32_t n = series_len(a.store, c);
@@ -502,7 +514,9 @@ __global__ void sample_ub_combine_kernel(SampleArgs a, uint32_t nsplit) {
 }
 
 int launch_sample_ub(const SampleArgs& a, cudaStream_t st) {
-    if (a.store.ulen == a.qlen && (kUQ + kUC) * a.store.d * ub_chunk(a.store.d) <= kUElem * 128 * kUSub) {
+    // (a guided sample has its own candidates per query: the warp-per-pair kernel)
+    if (!a.cand && a.store.ulen == a.qlen &&
+        (kUQ + kUC) * a.store.d * ub_chunk(a.store.d) <= kUElem * 128 * kUSub) {
         dim3 grid((a.S + kUC - 1) / kUC, (a.nq + kUQ - 1) / kUQ);
         // few queries: split the point range so that the grid fills the resident slots (2
         // blocks per SM)

@@ -86,10 +86,13 @@ __device__ __forceinline__ int warp_argmin(double& v, uint32_t& i) {
     return l;
 }
 
+// wcap (approximate mode, the guided seed sample only): a warp hands over at most wcap of its
+// 256 values, so the chunk's P are drawn from 16 * wcap -- any P distinct candidates serve as a
+// sample, and P rounds of warp argmins per warp were most of the selection's time.  0: exact.
 __global__ void __launch_bounds__(512) select_small_kernel(const double* __restrict__ in_v,
                                                            const uint32_t* __restrict__ in_i,
                                                            const unsigned* __restrict__ counts,
-                                                           uint32_t n_in, uint32_t P,
+                                                           uint32_t n_in, uint32_t P, uint32_t wcap,
                                                            double* __restrict__ out_v,
                                                            uint32_t* __restrict__ out_i) {
     __shared__ double wv[16][kKMax];
@@ -121,7 +124,7 @@ __global__ void __launch_bounds__(512) select_small_kernel(const double* __restr
 #pragma unroll
             for (int b = a; b > 0; --b) cswap(v[b - 1], ix[b - 1], v[b], ix[b]);
     }
-    const uint32_t wp = min(P, wcount);
+    const uint32_t wp = wcap ? min(min(P, wcount), wcap) : min(P, wcount);
     for (uint32_t r = 0; r < wp; ++r) {
         double bv = v[0];
         uint32_t bi = ix[0];
@@ -168,7 +171,7 @@ __global__ void __launch_bounds__(512) select_small_kernel(const double* __restr
 void launch_select_smallest(const double* vals, const uint32_t* idx, const unsigned* counts,
                             uint32_t nq, uint32_t n, uint32_t P,
                             double* scratch_v, uint32_t* scratch_i, double* out_v,
-                            uint32_t* out_i, cudaStream_t st, int* launches) {
+                            uint32_t* out_i, cudaStream_t st, int* launches, uint32_t wcap) {
     const double* cur_v = vals;
     const uint32_t* cur_i = idx;
     const unsigned* cur_c = counts;
@@ -187,7 +190,8 @@ void launch_select_smallest(const double* vals, const uint32_t* idx, const unsig
             di = scratch_i + ping * half;
         }
         if (P <= (uint32_t)kKMax)
-            select_small_kernel<<<dim3(nchunks, nq), 512, 0, st>>>(cur_v, cur_i, cur_c, cur_n, P, dv, di);
+            select_small_kernel<<<dim3(nchunks, nq), 512, 0, st>>>(cur_v, cur_i, cur_c, cur_n, P,
+                                                                   nchunks > 1 ? wcap : 0u, dv, di);
         else
             select_chunk_kernel<<<dim3(nchunks, nq), 512, 0, st>>>(cur_v, cur_i, cur_c, cur_n, P, dv, di);
         if (launches) ++*launches;
@@ -222,7 +226,8 @@ __global__ void seed_kernel(SeedArgs a) {
     }
     for (uint32_t j = threadIdx.x; j < (uint32_t)kKMax; j += blockDim.x) a.slots[(size_t)q * kKMax + j] = kInf;
     for (uint32_t j = threadIdx.x; j < a.probe; j += blockDim.x) {
-        const uint32_t c = (uint32_t)((uint64_t)ix[j] * a.n / a.S);
+        const uint32_t c = a.cand ? min(a.cand[(uint64_t)q * a.S + ix[j]], a.n - 1)
+                                  : (uint32_t)((uint64_t)ix[j] * a.n / a.S);
         a.probe_q.e[(size_t)q * a.probe + j] = QEntry{q, c, 0.0f, kNoPfx};
         a.probed[(size_t)c * a.nq + q] = 1;  // candidate-major [n][nq]
     }

@@ -284,6 +284,7 @@ void launch_paa_envelope(const double* src, uint64_t nser, uint32_t d, uint32_t 
 // ends[c] = (first point, last point) of every series of a store
 void launch_series_ends(const StoreDev& s, double* ends, cudaStream_t st);
 void launch_to_float(const double* src, uint64_t count, float* dst, cudaStream_t st);
+void launch_widen(const float* src, uint64_t count, double* dst, cudaStream_t st);
 void launch_absmax(const double* src, uint64_t count, double* out, cudaStream_t st);
 
 struct SampleArgs {
@@ -292,6 +293,7 @@ struct SampleArgs {
     uint32_t nq, qlen;
     uint64_t qstride;
     uint32_t S;           // sample size (candidates c = j * n / S)
+    const uint32_t* cand; // guided sample (nullable): candidate of slot j of query q at [q * S + j]
     double ub_scale;      // DTW: diagonal-sum inflation factor (rounded up)
     int dk;
     double* out_ub;       // [nq][S]  DTW: diagonal upper bound; DK: diagonal-path max sq
@@ -304,7 +306,8 @@ int launch_sample_ub(const SampleArgs& a, cudaStream_t st);  // returns the kern
 // counts: optional per-query number of valid values (the rest count as +inf).
 void launch_select_smallest(const double* vals, const uint32_t* idx, const unsigned* counts,
                             uint32_t nq, uint32_t n, uint32_t P, double* scratch_v, uint32_t* scratch_i,
-                            double* out_v, uint32_t* out_i, cudaStream_t st, int* launches);
+                            double* out_v, uint32_t* out_i, cudaStream_t st, int* launches,
+                            uint32_t wcap = 0);  // wcap: approximate first levels (guided sample only)
 
 struct SeedArgs {
     const double* sel_v;  // [nq][P] sorted smallest sampled upper bounds (DTW value / DK sq)
@@ -315,6 +318,7 @@ struct SeedArgs {
     double* slots;
     WorkQueue probe_q;
     uint8_t* probed;      // [n][nq] (candidate-major)
+    const uint32_t* cand; // guided sample (nullable): see SampleArgs
 };
 void launch_seed(const SeedArgs& a, cudaStream_t st);
 
