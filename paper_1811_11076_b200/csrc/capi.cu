@@ -257,9 +257,9 @@ struct tsw_plan {
     DevBuf<float> cq_m, cq_h, cq32;
     // guided seed sample: the G candidates with the smallest coarse diagonal distance per query
     uint32_t G = 0;            // 0: strided sample
-    DevBuf<float> cq2, zero2;  // query block means at the second level; zero half-widths
-    DevBuf<double> g_sv, g_val;
-    DevBuf<uint32_t> g_si, g_idx;
+    DevBuf<float> cq2;         // query block means at the second level (empty: the first level's)
+    DevBuf<double> g_v, g_sv, g_val;    // group minima [nq][n / 32], selection scratch, the G estimates
+    DevBuf<uint32_t> g_i, g_si, g_idx;  // ... and their candidate indices
     uint32_t pfx_qn = 0, pfx_log = 0, pfx_cap = 0;
     DevBuf<uint32_t> sel_si, sel_i, top_i, fin_si;
     DevBuf<double> fin_sv;
@@ -528,31 +528,33 @@ std::unique_ptr<tsw_plan> make_plan(tsw_store* s, uint64_t nq_max, uint64_t qlen
                 p->cq_h.alloc(nq_max * cst);
                 p->cq32.alloc(nq_max * cst);
                 if (!p->qabsmax.p) p->qabsmax.alloc(1);
-                // guided seed sample (long series): estimate every pair's diagonal distance on
-                // block means of 32 points, take the G smallest per query as the sample.
-                // TSW_GUIDED=0 / G overrides.
+                // guided seed sample: estimate every pair's diagonal distance on block means
+                // (~32 per series: the first level's when they are that coarse, else a second
+                // level), take the G smallest per query as the sample.  TSW_GUIDED=0 / G overrides.
                 const char* ge = std::getenv("TSW_GUIDED");
                 const uint64_t gw = ge ? (uint64_t)std::atoll(ge) : 32;
-                const uint32_t w2 = 32;
-                if (long_mode && gw > 0 && gw <= (uint64_t)kKMax && n >= 16 * gw && qlen / w2 >= 8 &&
-                    p->kk <= gw) {
-                    const uint64_t clen2 = qlen / w2, cst2 = stride_of(clen2, s->d);
-                    if (!s->paa2.p) {
-                        s->clen2 = clen2;
-                        s->cstride2 = cst2;
-                        s->cw2 = w2;
-                        s->paa2.alloc(n * cst2);
-                        launch_paa_series(s->data.p + s->guard, n, (uint32_t)s->d, (uint32_t)clen2, w2,
-                                          s->ustride, cst2, s->paa2.p, p->own);
-                        ck(cudaStreamSynchronize(p->own), "coarse store (level 2)");
+                uint32_t w2 = 1;
+                while ((uint64_t)w2 * 2 * 24 <= qlen) w2 *= 2;
+                if (gw > 0 && gw <= (uint64_t)kKMax && n >= 64 * gw && p->kk <= gw) {
+                    if (w2 > w) {
+                        const uint64_t clen2 = qlen / w2, cst2 = stride_of(clen2, s->d);
+                        if (!s->paa2.p) {
+                            s->clen2 = clen2;
+                            s->cstride2 = cst2;
+                            s->cw2 = w2;
+                            s->paa2.alloc(n * cst2);
+                            launch_paa_series(s->data.p + s->guard, n, (uint32_t)s->d, (uint32_t)clen2,
+                                              w2, s->ustride, cst2, s->paa2.p, p->own);
+                            ck(cudaStreamSynchronize(p->own), "coarse store (level 2)");
+                        }
+                        p->cq2.alloc(nq_max * cst2);
                     }
                     p->G = (uint32_t)gw;
-                    p->cq2.alloc(nq_max * cst2);
-                    p->zero2.alloc(nq_max * cst2);
-                    ck(cudaMemset(p->zero2.p, 0, nq_max * cst2 * sizeof(float)), "memset");
-                    const uint64_t fch = (n + kSelChunk - 1) / kSelChunk;
-                    p->g_sv.alloc(2 * nq_max * fch * gw);
-                    p->g_si.alloc(2 * nq_max * fch * gw);
+                    const uint64_t ng = (n + 31) / 32, gch = (ng + kSelChunk - 1) / kSelChunk;
+                    p->g_v.alloc(nq_max * ng);
+                    p->g_i.alloc(nq_max * ng);
+                    p->g_sv.alloc(2 * nq_max * gch * gw);
+                    p->g_si.alloc(2 * nq_max * gch * gw);
                     p->g_val.alloc(nq_max * gw);
                     p->g_idx.alloc(nq_max * gw);
                     // the probes come from the guided sample
@@ -650,32 +652,34 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
         ++launches;
     }
     mark(1);
-    // guided seed sample: the coarse diagonal distance of every (query, candidate) pair (the
-    // forward tile pass on second-level block means with zero half-widths: terms (x - q)^2),
-    // its G smallest per query become the sample -- instead of a strided 4% of the store
-    const uint32_t S_eff = (!dk && p->G) ? p->G : (uint32_t)p->S;
+    // guided seed sample: the coarse diagonal distance of every (query, candidate) pair
+    // (coarse_est_kernel); its G smallest per query become the sample -- instead of a strided
+    // 4% of the store
+    bool guided = false;
     if (!dk && p->G) {
-        launch_paa_series(p->qg(), nq, (uint32_t)s->d, (uint32_t)s->clen2, s->cw2, p->qstride,
-                          s->cstride2, p->cq2.p, st);
-        LbCompactArgs ea{};
-        ea.store = s->dev();
-        ea.store.data = nullptr;
-        ea.store.data32 = s->paa2.p;
-        ea.store.ulen = (uint32_t)s->clen2;
-        ea.store.ustride = ea.store.tstride = s->cstride2;
-        ea.env_lo = p->cq2.p;
-        ea.env_hi = p->zero2.p;
-        ea.nq = nq;
-        ea.qstride = s->cstride2;
-        ea.margin = 1.0;
-        ea.lb_out = reinterpret_cast<float*>(p->res_i.p);  // scratch: the result buffers are idle here
-        launch_lb_compact(ea, st);
-        launch_widen(reinterpret_cast<const float*>(p->res_i.p), (uint64_t)nq * n, p->res_d.p, st);
-        launches += 3;
-        // (approximate: 4 values per warp of 256 in the chunked levels -- a sample, not a top-k)
-        launch_select_smallest(p->res_d.p, nullptr, nullptr, nq, n, p->G, p->g_sv.p, p->g_si.p,
-                               p->g_val.p, p->g_idx.p, st, &launches, 4u);
+        const float* xs = s->paa.p;
+        const float* qm = p->cq32.p;
+        uint64_t E = s->cstride;
+        if (p->cq2.p) {  // second level
+            launch_paa_series(p->qg(), nq, (uint32_t)s->d, (uint32_t)s->clen2, s->cw2, p->qstride,
+                              s->cstride2, p->cq2.p, st);
+            ++launches;
+            xs = s->paa2.p;
+            qm = p->cq2.p;
+            E = s->cstride2;
+        } else {  // first level: the queries' block means are needed before their usual place
+            launch_paa_series(p->qg(), nq, (uint32_t)s->d, (uint32_t)s->clen, s->cw, p->qstride,
+                              s->cstride, p->cq32.p, st);
+            ++launches;
+        }
+        guided = launch_coarse_est(xs, qm, n, nq, (uint32_t)E, p->g_v.p, p->g_i.p, st);
+        if (guided) {
+            ++launches;
+            launch_select_smallest(p->g_v.p, p->g_i.p, nullptr, nq, (n + 31) / 32, p->G, p->g_sv.p,
+                                   p->g_si.p, p->g_val.p, p->g_idx.p, st, &launches);
+        }
     }
+    const uint32_t S_eff = guided ? p->G : (uint32_t)p->S;
     SampleArgs sa{};
     sa.store = s->dev();
     sa.queries = p->qg();
@@ -683,7 +687,7 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
     sa.qlen = (uint32_t)p->qlen;
     sa.qstride = p->qstride;
     sa.S = S_eff;
-    sa.cand = (!dk && p->G) ? p->g_idx.p : nullptr;
+    sa.cand = guided ? p->g_idx.p : nullptr;
     sa.ub_scale = p->ub_scale;
     sa.dk = dk;
     sa.out_ub = p->ub.p;

@@ -64,6 +64,86 @@ __global__ void to_float_kernel(const double* __restrict__ src, uint64_t n, floa
         dst[i] = isinf(src[i]) ? 0.0f : fminf(fmaxf(__double2float_rn(src[i]), -FLT_MAX), FLT_MAX);
 }
 
+// ---- guided seed sample: coarse diagonal distance of every (query, candidate) pair -------------
+// est(q, c) = sum over the block means (second level, E floats per series incl. zero padding) of
+// (x - q)^2 in plain fp32 -- a ranking heuristic only (the sample it picks gets exact upper
+// bounds).  A block owns kEC = 32 consecutive candidates (staged transposed in shared memory,
+// NaN means of out-of-range blocks as 0) against chunks of kEQ = 64 queries; thread (c, wq)
+// accumulates 8 queries, then the warp reduces each query's 32 candidates to their minimum:
+// the output is the best candidate of every group of 32 per query, [nq][ngroups] (value, index)
+// -- a 32x smaller selection problem (two sample members in one group cost one of them).
+constexpr int kEC = 32, kEQ = 64, kECP = 33, kEQP = 68;
+
+__global__ void __launch_bounds__(256) coarse_est_kernel(const float* __restrict__ x,
+                                                         const float* __restrict__ q, uint32_t n,
+                                                         uint32_t nq, uint32_t E,
+                                                         double* __restrict__ out_v,
+                                                         uint32_t* __restrict__ out_i) {
+    extern __shared__ __align__(16) float esm[];  // cs[E][kECP], qs[E][kEQP]
+    float* cs = esm;
+    float* qs = esm + (size_t)E * kECP;
+    const uint32_t c0 = blockIdx.x * kEC, ng = gridDim.x;
+    const uint32_t c = threadIdx.x & 31, wq = threadIdx.x >> 5;
+    for (uint32_t i = threadIdx.x; i < kEC * E; i += blockDim.x) {
+        const uint32_t cc = i / E, e = i - cc * E;
+        const float v = c0 + cc < n ? x[(uint64_t)(c0 + cc) * E + e] : 0.0f;
+        cs[e * kECP + cc] = v == v ? v : 0.0f;
+    }
+    for (uint32_t q0 = 0; q0 < nq; q0 += kEQ) {
+        __syncthreads();
+        for (uint32_t i = threadIdx.x; i < kEQ * E; i += blockDim.x) {
+            const uint32_t qq = i / E, e = i - qq * E;
+            const float v = q0 + qq < nq ? q[(uint64_t)(q0 + qq) * E + e] : 0.0f;
+            qs[e * kEQP + qq] = v == v ? v : 0.0f;
+        }
+        __syncthreads();
+        if (q0 + 8 * wq >= nq) continue;  // warp-uniform (the barriers above are passed first)
+        float acc[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[i] = 0.0f;
+        for (uint32_t e = 0; e < E; ++e) {
+            const float xv = cs[e * kECP + c];
+            const float4 a = *reinterpret_cast<const float4*>(qs + e * kEQP + 8 * wq);
+            const float4 b = *reinterpret_cast<const float4*>(qs + e * kEQP + 8 * wq + 4);
+            const float qv[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const float dd = xv - qv[i];
+                acc[i] = fmaf(dd, dd, acc[i]);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            float v = c0 + c < n ? acc[i] : kInfF;
+            uint32_t ix = c0 + c;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const float ov = __shfl_xor_sync(0xffffffffu, v, o);
+                const uint32_t oi = __shfl_xor_sync(0xffffffffu, ix, o);
+                if (ov < v || (ov == v && oi < ix)) {
+                    v = ov;
+                    ix = oi;
+                }
+            }
+            const uint32_t qi = q0 + 8 * wq + i;
+            if (c == 0 && qi < nq) {
+                out_v[(uint64_t)qi * ng + blockIdx.x] = (double)v;
+                out_i[(uint64_t)qi * ng + blockIdx.x] = ix;
+            }
+        }
+    }
+}
+
+bool launch_coarse_est(const float* x, const float* q, uint32_t n, uint32_t nq, uint32_t E,
+                       double* out_v, uint32_t* out_i, cudaStream_t st) {
+    const size_t smem = (size_t)E * (kECP + kEQP) * sizeof(float);
+    if (smem > smem_optin()) return false;
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(coarse_est_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    coarse_est_kernel<<<(n + kEC - 1) / kEC, 256, smem, st>>>(x, q, n, nq, E, out_v, out_i);
+    return true;
+}
+
 __global__ void widen_kernel(const float* __restrict__ src, uint64_t n, double* __restrict__ dst) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
          i += (uint64_t)gridDim.x * blockDim.x)

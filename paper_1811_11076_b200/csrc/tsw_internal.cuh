@@ -285,6 +285,11 @@ void launch_paa_envelope(const double* src, uint64_t nser, uint32_t d, uint32_t 
 void launch_series_ends(const StoreDev& s, double* ends, cudaStream_t st);
 void launch_to_float(const double* src, uint64_t count, float* dst, cudaStream_t st);
 void launch_widen(const float* src, uint64_t count, double* dst, cudaStream_t st);
+// guided seed sample: per query the best candidate (smallest coarse diagonal distance on E
+// floats of block means per series) of every group of 32 candidates, [nq][ceil(n / 32)];
+// false when the shared-memory tile does not fit
+bool launch_coarse_est(const float* x, const float* q, uint32_t n, uint32_t nq, uint32_t E,
+                       double* out_v, uint32_t* out_i, cudaStream_t st);
 void launch_absmax(const double* src, uint64_t count, double* out, cudaStream_t st);
 
 struct SampleArgs {
