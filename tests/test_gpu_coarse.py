@@ -5,7 +5,7 @@ reverse bound on, w = 4 for shorter series on the fast path) and the DP's cumula
 bounds come from the same block means.  Every switch of the cascade must give the reference's
 neighbours (indices, order, distances bit for bit) and conserved device counters
 (search.hpp:10-12): cascade off, short series on the plain pass, per-point DP setup, the
-1-3 query plans, lengths that are not a multiple of the block, values beyond the fp32 range
+guided seed sample on / off, the 1-3 query plans, lengths that are not a multiple of the block, values beyond the fp32 range
 inside some blocks (NaN block means: no bound from those blocks).  All calls go through the
 C ABI (libtswarp_b200.so); the checker is oracle/_ref (the reference's own sources) or the C port.
 """
@@ -29,10 +29,14 @@ def assert_knn_equal(gi, gd, oi, od, msg=""):
 # (n, L, d, r, k): short series (w = 4) with and without a ragged tail, clen = 16 (the smallest
 # coarse length), long series (w = 8) with a tail of 3 and the C5 shape, a band wider than the
 # block and one narrower
+# ... and two stores large enough for the guided seed sample (n >= 2048: the candidates with the
+# smallest coarse diagonal distance instead of a strided sample), short and long series
 CASES = [(400, 203, 3, 20, 3), (300, 67, 2, 9, 2), (500, 128, 3, 13, 5), (350, 256, 2, 26, 4),
-         (200, 515, 2, 40, 2), (150, 1024, 3, 51, 3), (250, 96, 4, 2, 3), (300, 64, 1, 52, 1)]
+         (200, 515, 2, 40, 2), (150, 1024, 3, 51, 3), (250, 96, 4, 2, 3), (300, 64, 1, 52, 1),
+         (2600, 128, 3, 13, 4), (2200, 300, 2, 33, 3)]
 MODES = {"default": {}, "off": {"TSW_COARSE": "0"}, "short_off": {"TSW_COARSE_SHORT": "0"},
-         "per_point_setup": {"TSW_CSETUP": "0"}}
+         "per_point_setup": {"TSW_CSETUP": "0"}, "strided_sample": {"TSW_GUIDED": "0"},
+         "guided_64": {"TSW_GUIDED": "64"}}
 
 
 @pytest.mark.parametrize("mode", sorted(MODES))
