@@ -257,6 +257,7 @@ struct tsw_plan {
     DevBuf<float> cq_m, cq_h, cq32;
     // guided seed sample: the G candidates with the smallest coarse diagonal distance per query
     uint32_t G = 0;            // 0: strided sample
+    uint64_t seed_bounds = 0;  // seed upper bounds per query of the last execute (DK: gdk_calls)
     DevBuf<float> cq2;         // query block means at the second level (empty: the first level's)
     DevBuf<double> g_v, g_sv, g_val;    // group minima [nq][n / 32], selection scratch, the G estimates
     DevBuf<uint32_t> g_i, g_si, g_idx;  // ... and their candidate indices
@@ -564,6 +565,39 @@ std::unique_ptr<tsw_plan> make_plan(tsw_store* s, uint64_t nq_max, uint64_t qlen
             }
         }
     }
+    // DK (whole match, uniform store of the query's length): the guided seed sample too -- the
+    // same estimate on second-level block means ranks the candidates, the G best get the exact
+    // diagonal-path maxima that seed the threshold.  TSW_GUIDED_DK=0 / G overrides.
+    if (metric == TSW_METRIC_DK && s->ulen == qlen && s->ulen != 0) {
+        const char* ge = std::getenv("TSW_GUIDED_DK");
+        const uint64_t gw = ge ? (uint64_t)std::atoll(ge) : 32;
+        uint32_t w2 = 1;
+        while ((uint64_t)w2 * 2 * 24 <= qlen) w2 *= 2;
+        const uint64_t clen2 = qlen / w2, cst2 = stride_of(clen2, s->d);
+        if (gw > 0 && gw <= (uint64_t)kKMax && n >= 64 * gw && p->kk <= gw && clen2 >= 8 &&
+            cst2 * 101 * sizeof(float) <= 96 * 1024 && (!s->paa2.p || s->cw2 == w2)) {
+            if (!s->paa2.p) {
+                s->clen2 = clen2;
+                s->cstride2 = cst2;
+                s->cw2 = w2;
+                s->paa2.alloc(n * cst2);
+                launch_paa_series(s->data.p + s->guard, n, (uint32_t)s->d, (uint32_t)clen2, w2,
+                                  s->ustride, cst2, s->paa2.p, p->own);
+                ck(cudaStreamSynchronize(p->own), "coarse store (level 2)");
+            }
+            p->cq2.alloc(nq_max * cst2);
+            p->G = (uint32_t)gw;
+            const uint64_t ng = (n + 31) / 32, gch = (ng + kSelChunk - 1) / kSelChunk;
+            p->g_v.alloc(nq_max * ng);
+            p->g_i.alloc(nq_max * ng);
+            p->g_sv.alloc(2 * nq_max * gch * gw);
+            p->g_si.alloc(2 * nq_max * gch * gw);
+            p->g_val.alloc(nq_max * gw);
+            p->g_idx.alloc(nq_max * gw);
+            p->probe = std::min<uint64_t>(p->probe, gw);
+            p->P = std::max<uint64_t>(1, std::min<uint64_t>(kKMax, std::max(p->kk, p->probe)));
+        }
+    }
     p->ub.alloc(nq_max * p->S);
     // point-range splits of the sampled bounds when the (query, sample) tiles cannot fill the
     // GPU (few queries): up to 8 partial rows per pair
@@ -656,7 +690,7 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
     // (coarse_est_kernel); its G smallest per query become the sample -- instead of a strided
     // 4% of the store
     bool guided = false;
-    if (!dk && p->G) {
+    if (p->G) {
         const float* xs = s->paa.p;
         const float* qm = p->cq32.p;
         uint64_t E = s->cstride;
@@ -680,6 +714,7 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
         }
     }
     const uint32_t S_eff = guided ? p->G : (uint32_t)p->S;
+    p->seed_bounds = S_eff;
     SampleArgs sa{};
     sa.store = s->dev();
     sa.queries = p->qg();
@@ -1029,7 +1064,7 @@ void fetch_impl(tsw_plan* p, tsw_neighbor* out, tsw_counters* counters, cudaStre
                 c.lb_computed = 0;
                 c.lb_pruned = 0;
                 c.early_abandoned = h.bound_pruned + h.lb_pruned + h.early_abandoned;
-                c.gdk_calls = p->S;
+                c.gdk_calls = p->seed_bounds;
             }
         }
     }

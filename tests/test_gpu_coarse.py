@@ -5,9 +5,10 @@ reverse bound on, w = 4 for shorter series on the fast path) and the DP's cumula
 bounds come from the same block means.  Every switch of the cascade must give the reference's
 neighbours (indices, order, distances bit for bit) and conserved device counters
 (search.hpp:10-12): cascade off, short series on the plain pass, per-point DP setup, the
-guided seed sample on / off, the 1-3 query plans, lengths that are not a multiple of the block, values beyond the fp32 range
-inside some blocks (NaN block means: no bound from those blocks).  All calls go through the
-C ABI (libtswarp_b200.so); the checker is oracle/_ref (the reference's own sources) or the C port.
+guided seed sample on / off, the 1-3 query plans, lengths that are not a multiple of the
+block, values beyond the fp32 range inside some blocks (NaN block means: no bound from those
+blocks).  All calls go through the C ABI (libtswarp_b200.so); the checker is oracle/_ref (the
+reference's own sources) or the C port.
 """
 import numpy as np
 import pytest
