@@ -689,8 +689,10 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
     // guided seed sample: the coarse diagonal distance of every (query, candidate) pair
     // (coarse_est_kernel); its G smallest per query become the sample -- instead of a strided
     // 4% of the store
+    // (1-3 queries on a small store: the extra launches cost more than the tighter seed saves
+    // -- C2 / C3 single-query calls +15% -- so those keep the strided sample)
     bool guided = false;
-    if (p->G) {
+    if (p->G && (nq >= 4 || n >= 98304)) {
         const float* xs = s->paa.p;
         const float* qm = p->cq32.p;
         uint64_t E = s->cstride;

@@ -16,12 +16,12 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-def seed_sample(n, L=None, d=1, k=1):
+def seed_sample(n, L=None, d=1, k=1, nq=4):
     """Seed bounds the engine computes per query (capi.cu make_plan).  Strided sample: 2048,
     ~n/24 for n >= 96k.  Guided sample (whole-match DK on a uniform store of the query's length
-    L, n >= 2048, k <= 32, the estimate's shared-memory tile fits): the 32 best-ranked
-    candidates."""
-    if L is not None and n >= 2048 and k <= 32:
+    L, n >= 2048, k <= 32, >= 4 queries or n >= 98304, the estimate's shared-memory tile fits):
+    the 32 best-ranked candidates."""
+    if L is not None and n >= 2048 and k <= 32 and (nq >= 4 or n >= 98304):
         w2 = 1
         while w2 * 2 * 24 <= L:
             w2 *= 2
@@ -63,7 +63,7 @@ def test_config_parity(tsw, best_oracle, cfg, metric, nref):
         if metric == "dtw":
             assert c[0] == n and c[1] + c[2] + c[3] == n, c
         else:
-            assert c[4] == seed_sample(n, sh["len"], sh["d"], k) and c[2] + c[3] == n, c
+            assert c[4] == seed_sample(n, sh["len"], sh["d"], k, len(qs)) and c[2] + c[3] == n, c
         keys = list(zip(dist[q].tolist(), idx[q].tolist()))
         assert keys == sorted(keys), f"query {q} not sorted by (distance, index)"
     # returned distances == unpruned brute force values (first 4 queries)

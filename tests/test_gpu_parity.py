@@ -13,12 +13,12 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-def seed_sample(n, L=None, d=1, k=1):
+def seed_sample(n, L=None, d=1, k=1, nq=4):
     """Seed bounds the engine computes per query (capi.cu make_plan).  Strided sample: 2048,
     ~n/24 for n >= 96k.  Guided sample (whole-match DK on a uniform store of the query's length
-    L, n >= 2048, k <= 32, the estimate's shared-memory tile fits): the 32 best-ranked
-    candidates."""
-    if L is not None and n >= 2048 and k <= 32:
+    L, n >= 2048, k <= 32, >= 4 queries or n >= 98304, the estimate's shared-memory tile fits):
+    the 32 best-ranked candidates."""
+    if L is not None and n >= 2048 and k <= 32 and (nq >= 4 or n >= 98304):
         w2 = 1
         while w2 * 2 * 24 <= L:
             w2 *= 2
@@ -268,7 +268,7 @@ def test_counters_prune_and_abandon(tsw):
     assert c[0] == 3000 and c[1] + c[2] + c[3] == 3000 and c[1] > 2000 and c[2] >= 1, c
     _, _, c = tsw.knn(ds, q[None], 1, "dk", 0)
     c = c[0]
-    assert c[2] + c[3] == 3000 and c[2] >= 1 and c[3] > 2000 and c[4] == seed_sample(3000, 64, 3, 1), c
+    assert c[2] + c[3] == 3000 and c[2] >= 1 and c[3] > 2000 and c[4] == seed_sample(3000, 64, 3, 1, nq=1), c
 
 
 def test_knn_random_datasets(tsw, best_oracle):
