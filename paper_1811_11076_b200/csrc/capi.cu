@@ -194,6 +194,7 @@ struct tsw_store {
         uint64_t r;
         DevBuf<float> m, h;
         DevBuf<float> cm, ch;  // block means of the envelope (coarse LB pass), built on demand
+        DevBuf<float> cm_s, ch_s;  // ... at the DP setup's finer level (long series)
     };
     std::vector<std::unique_ptr<CEnv>> cenv;
     // coarse LB cascade: fp32 block means of every series (kPaa points per
@@ -201,6 +202,11 @@ struct tsw_store {
     DevBuf<float> paa;
     uint64_t clen = 0, cstride = 0;
     uint32_t cw = 0;         // points per block mean (8: long series, 4: short)
+    // long series: the DP setup's cumulative bounds use a finer level (4 points per mean):
+    // tighter prefixes (-6% cells at C5) for one more 128-point chunk per direction
+    DevBuf<float> paa_s;
+    uint64_t clen_s = 0, cstride_s = 0;
+    uint32_t cw_s = 0;
     // guided seed sample: a second, coarser level of block means (cw2 points)
     // for the all-pairs distance estimate that picks the sampled candidates
     DevBuf<float> paa2;
@@ -255,6 +261,9 @@ struct tsw_plan {
     const float* ccenv_m = nullptr;
     const float* ccenv_h = nullptr;
     DevBuf<float> cq_m, cq_h, cq32;
+    DevBuf<float> cq_m_s, cq_h_s, cq32_s;  // the DP setup's finer level (long series)
+    const float* ccenv_m_s = nullptr;
+    const float* ccenv_h_s = nullptr;
     // guided seed sample: the G candidates with the smallest coarse diagonal distance per query
     uint32_t G = 0;            // 0: strided sample
     uint64_t seed_bounds = 0;  // seed upper bounds per query of the last execute (DK: gdk_calls)
@@ -529,6 +538,34 @@ std::unique_ptr<tsw_plan> make_plan(tsw_store* s, uint64_t nq_max, uint64_t qlen
                 p->cq_h.alloc(nq_max * cst);
                 p->cq32.alloc(nq_max * cst);
                 if (!p->qabsmax.p) p->qabsmax.alloc(1);
+                // long series: a finer level for the DP setup (TSW_CSETUP_W=8: the pass's level)
+                const char* swe = std::getenv("TSW_CSETUP_W");
+                const uint32_t ws = swe ? (uint32_t)std::atoi(swe) : 4u;
+                if (long_mode && ws == 4 && s->d <= 4 && (!s->paa_s.p || s->cw_s == ws)) {
+                    const uint64_t clen_s = qlen / ws, cst_s = stride_of(clen_s, s->d);
+                    if (!s->paa_s.p) {
+                        s->clen_s = clen_s;
+                        s->cstride_s = cst_s;
+                        s->cw_s = ws;
+                        s->paa_s.alloc(n * cst_s);
+                        launch_paa_series(s->data.p + s->guard, n, (uint32_t)s->d, (uint32_t)clen_s, ws,
+                                          s->ustride, cst_s, s->paa_s.p, p->own);
+                    }
+                    if (!ce->cm_s.p) {
+                        ce->cm_s.alloc(n * cst_s);
+                        ce->ch_s.alloc(n * cst_s);
+                        launch_paa_envelope(s->data.p + s->guard, n, (uint32_t)s->d, (uint32_t)s->ulen,
+                                            (uint32_t)clen_s, ws, s->ustride, cst_s,
+                                            (uint32_t)std::min<uint64_t>(r, 0xffffffffu), 0.0f,
+                                            ce->cm_s.p, ce->ch_s.p, p->own);
+                    }
+                    ck(cudaStreamSynchronize(p->own), "coarse store (setup level)");
+                    p->ccenv_m_s = ce->cm_s.p;
+                    p->ccenv_h_s = ce->ch_s.p;
+                    p->cq_m_s.alloc(nq_max * cst_s);
+                    p->cq_h_s.alloc(nq_max * cst_s);
+                    p->cq32_s.alloc(nq_max * cst_s);
+                }
                 // guided seed sample: estimate every pair's diagonal distance on block means
                 // (~32 per series: the first level's when they are that coarse, else a second
                 // level), take the G smallest per query as the sample.  TSW_GUIDED=0 / G overrides.
@@ -691,7 +728,7 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
     // 4% of the store
     // (1-3 queries on a small store: the extra launches cost more than the tighter seed saves
     // -- C2 / C3 single-query calls +15% -- so those keep the strided sample)
-    bool guided = false;
+    bool guided = false, cq32_done = false;
     if (p->G && (nq >= 4 || n >= 98304)) {
         const float* xs = s->paa.p;
         const float* qm = p->cq32.p;
@@ -707,6 +744,7 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
             launch_paa_series(p->qg(), nq, (uint32_t)s->d, (uint32_t)s->clen, s->cw, p->qstride,
                               s->cstride, p->cq32.p, st);
             ++launches;
+            cq32_done = true;
         }
         guided = launch_coarse_est(xs, qm, n, nq, (uint32_t)E, p->g_v.p, p->g_i.p, st);
         if (guided) {
@@ -778,9 +816,10 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
         launch_paa_envelope(p->qg(), nq, (uint32_t)s->d, (uint32_t)p->qlen, (uint32_t)s->clen, s->cw,
                             p->qstride, s->cstride, (uint32_t)std::min<uint64_t>(p->r, 0xffffffffu),
                             s->err_c, p->cq_m.p, p->cq_h.p, st);
-        launch_paa_series(p->qg(), nq, (uint32_t)s->d, (uint32_t)s->clen, s->cw, p->qstride,
-                          s->cstride, p->cq32.p, st);
-        launches += 2;
+        if (!cq32_done)
+            launch_paa_series(p->qg(), nq, (uint32_t)s->d, (uint32_t)s->clen, s->cw, p->qstride,
+                              s->cstride, p->cq32.p, st);
+        launches += cq32_done ? 1 : 2;
     }
     DpArgs da{};
     da.store = s->dev();
@@ -816,19 +855,38 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
         if (coarse && (da.cenv_m || p->coarse_short) && dtw4_supported(da) &&
             (cse ? std::atoi(cse) != 0 : true)) {
             csetup = true;
-            da.c_x32 = s->paa.p;
-            da.c_em = p->cq_m.p;
-            da.c_eh = p->cq_h.p;
-            da.c_q32 = p->cq32.p;
             // (TSW_CS_REV=0: forward cumulative bound only -- half the setup; A/B)
             const char* cre = std::getenv("TSW_CS_REV");
             const bool cs_rev = cre ? std::atoi(cre) != 0 : true;
-            da.c_cm = cs_rev ? p->ccenv_m : nullptr;
-            da.c_ch = cs_rev ? p->ccenv_h : nullptr;
-            da.cstride = s->cstride;
-            da.clen = (uint32_t)s->clen;
-            da.cw = s->cw;
-            da.clog = s->cw == 8 ? 3u : 2u;
+            if (p->cq32_s.p) {  // long series: the finer setup level
+                launch_paa_envelope(p->qg(), nq, (uint32_t)s->d, (uint32_t)p->qlen, (uint32_t)s->clen_s,
+                                    s->cw_s, p->qstride, s->cstride_s,
+                                    (uint32_t)std::min<uint64_t>(p->r, 0xffffffffu), s->err_c,
+                                    p->cq_m_s.p, p->cq_h_s.p, st);
+                launch_paa_series(p->qg(), nq, (uint32_t)s->d, (uint32_t)s->clen_s, s->cw_s, p->qstride,
+                                  s->cstride_s, p->cq32_s.p, st);
+                launches += 2;
+                da.c_x32 = s->paa_s.p;
+                da.c_em = p->cq_m_s.p;
+                da.c_eh = p->cq_h_s.p;
+                da.c_q32 = p->cq32_s.p;
+                da.c_cm = cs_rev ? p->ccenv_m_s : nullptr;
+                da.c_ch = cs_rev ? p->ccenv_h_s : nullptr;
+                da.cstride = s->cstride_s;
+                da.clen = (uint32_t)s->clen_s;
+                da.cw = s->cw_s;
+            } else {
+                da.c_x32 = s->paa.p;
+                da.c_em = p->cq_m.p;
+                da.c_eh = p->cq_h.p;
+                da.c_q32 = p->cq32.p;
+                da.c_cm = cs_rev ? p->ccenv_m : nullptr;
+                da.c_ch = cs_rev ? p->ccenv_h : nullptr;
+                da.cstride = s->cstride;
+                da.clen = (uint32_t)s->clen;
+                da.cw = s->cw;
+            }
+            da.clog = da.cw == 8 ? 3u : 2u;
             da.qabsmax = p->qabsmax.p;
         }
     }
@@ -1245,6 +1303,8 @@ int tsw_plan_create(tsw_store* store, uint64_t nq_max, uint64_t qlen, int metric
     return guard([&] {
         if (!store || !out) fail(TSW_EINVAL, "null argument");
         DeviceGuard dg(store->device);
+        // the store's caches (candidate envelopes, block means) are built under its mutex
+        std::lock_guard<std::mutex> lk(store->mu);
         *out = make_plan(store, nq_max, qlen, metric, r, k).release();
     });
 }
