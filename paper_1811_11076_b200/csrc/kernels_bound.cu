@@ -84,17 +84,27 @@ __global__ void __launch_bounds__(256) coarse_est_kernel(const float* __restrict
     float* qs = esm + (size_t)E * kECP;
     const uint32_t c0 = blockIdx.x * kEC, ng = gridDim.x;
     const uint32_t c = threadIdx.x & 31, wq = threadIdx.x >> 5;
-    for (uint32_t i = threadIdx.x; i < kEC * E; i += blockDim.x) {
-        const uint32_t cc = i / E, e = i - cc * E;
-        const float v = c0 + cc < n ? x[(uint64_t)(c0 + cc) * E + e] : 0.0f;
-        cs[e * kECP + cc] = v == v ? v : 0.0f;
+    // staging by float4 (E % 4 == 0: whole 32-point tile rows), 4x fewer dependent L2 loads
+    const uint32_t E4 = E / 4;
+    auto put4 = [](float* dst, uint32_t pitch, uint32_t e, uint32_t col, float4 v) {
+        dst[(e + 0) * pitch + col] = v.x == v.x ? v.x : 0.0f;
+        dst[(e + 1) * pitch + col] = v.y == v.y ? v.y : 0.0f;
+        dst[(e + 2) * pitch + col] = v.z == v.z ? v.z : 0.0f;
+        dst[(e + 3) * pitch + col] = v.w == v.w ? v.w : 0.0f;
+    };
+    for (uint32_t i = threadIdx.x; i < kEC * E4; i += blockDim.x) {
+        const uint32_t cc = i / E4, e4 = i - cc * E4;
+        const float4 v = c0 + cc < n ? __ldg(reinterpret_cast<const float4*>(x + (uint64_t)(c0 + cc) * E) + e4)
+                                     : make_float4(0.f, 0.f, 0.f, 0.f);
+        put4(cs, kECP, 4 * e4, cc, v);
     }
     for (uint32_t q0 = 0; q0 < nq; q0 += kEQ) {
         __syncthreads();
-        for (uint32_t i = threadIdx.x; i < kEQ * E; i += blockDim.x) {
-            const uint32_t qq = i / E, e = i - qq * E;
-            const float v = q0 + qq < nq ? q[(uint64_t)(q0 + qq) * E + e] : 0.0f;
-            qs[e * kEQP + qq] = v == v ? v : 0.0f;
+        for (uint32_t i = threadIdx.x; i < kEQ * E4; i += blockDim.x) {
+            const uint32_t qq = i / E4, e4 = i - qq * E4;
+            const float4 v = q0 + qq < nq ? __ldg(reinterpret_cast<const float4*>(q + (uint64_t)(q0 + qq) * E) + e4)
+                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+            put4(qs, kEQP, 4 * e4, qq, v);
         }
         __syncthreads();
         if (q0 + 8 * wq >= nq) continue;  // warp-uniform (the barriers above are passed first)
@@ -137,7 +147,7 @@ __global__ void __launch_bounds__(256) coarse_est_kernel(const float* __restrict
 bool launch_coarse_est(const float* x, const float* q, uint32_t n, uint32_t nq, uint32_t E,
                        double* out_v, uint32_t* out_i, cudaStream_t st) {
     const size_t smem = (size_t)E * (kECP + kEQP) * sizeof(float);
-    if (smem > smem_optin()) return false;
+    if (smem > smem_optin() || E % 4 != 0) return false;
     if (smem > 48 * 1024)
         cudaFuncSetAttribute(coarse_est_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     coarse_est_kernel<<<(n + kEC - 1) / kEC, 256, smem, st>>>(x, q, n, nq, E, out_v, out_i);
