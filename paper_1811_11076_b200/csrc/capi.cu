@@ -487,8 +487,8 @@ std::unique_ptr<tsw_plan> make_plan(tsw_store* s, uint64_t nq_max, uint64_t qlen
         // two-sided bound admits ~10% more pairs than the full-resolution two-sided one (w = 8,
         // C5) and FEWER than the full-resolution forward bound alone (w = 4: C3 0.9% vs 1.5%,
         // C2 12.8% vs 18.7%).
-        //  * long series (> 256 points, reverse bound on): w = 8; the DP setup's cumulative
-        //    bounds come from the same block means (fast path) or re-check at full resolution;
+        //  * long series (> 256 points, reverse bound on): w = 16; the DP setup's cumulative
+        //    bounds come from block means of 4 (fast path) or re-check at full resolution;
         //  * short series on the fast path (d <= 4, r <= 52): w = 4 replaces the forward-only
         //    full-resolution pass and its block-sum rows.
         // TSW_COARSE=0/1 overrides (TSW_COARSE_SHORT=0: short series keep the plain pass).
@@ -500,7 +500,12 @@ std::unique_ptr<tsw_plan> make_plan(tsw_store* s, uint64_t nq_max, uint64_t qlen
         const bool long_mode = p->cenv_m && p->lb2 && p->pfx_qn == 0;
         const bool short_mode = want_short && p->pfx_qn != 0 && s->d <= 4 && r_eff <= 52 && qlen >= 64;
         if (want_coarse && (long_mode || short_mode) && s->ulen == qlen) {
-            const uint32_t w = long_mode ? 8u : 4u;
+            // long series: 16 points per mean in the pass (it admits ~10% more pairs than 8, which
+            // the DP setup's finer level drops at once; C5 pass 0.765 -> 0.545 ms, step -1.9%);
+            // TSW_COARSE_W=8 overrides
+            const char* cwe = std::getenv("TSW_COARSE_W");
+            const uint32_t wl = cwe && std::atoi(cwe) == 8 ? 8u : 16u;
+            const uint32_t w = long_mode ? wl : 4u;
             tsw_store::CEnv* ce = nullptr;
             for (auto& c : s->cenv)
                 if (c->r == r) ce = c.get();
@@ -886,7 +891,7 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
                 da.clen = (uint32_t)s->clen;
                 da.cw = s->cw;
             }
-            da.clog = da.cw == 8 ? 3u : 2u;
+            da.clog = da.cw == 16 ? 4u : da.cw == 8 ? 3u : 2u;
             da.qabsmax = p->qabsmax.p;
         }
     }

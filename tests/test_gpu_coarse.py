@@ -1,8 +1,8 @@
 """GPU parity of the coarse LB cascade against the reference.
 
-The DTW bound pass runs on block means of w points (w = 8 for series above 256 points with the
+The DTW bound pass runs on block means of w points (w = 16 for series above 256 points with the
 reverse bound on, w = 4 for shorter series on the fast path) and the DP's cumulative abandon
-bounds come from the same block means.  Every switch of the cascade must give the reference's
+bounds come from block means of 4.  Every switch of the cascade must give the reference's
 neighbours (indices, order, distances bit for bit) and conserved device counters
 (search.hpp:10-12): cascade off, short series on the plain pass, per-point DP setup, the
 guided seed sample on / off, the 1-3 query plans, lengths that are not a multiple of the
@@ -36,6 +36,7 @@ CASES = [(400, 203, 3, 20, 3), (300, 67, 2, 9, 2), (500, 128, 3, 13, 5), (350, 2
          (200, 515, 2, 40, 2), (150, 1024, 3, 51, 3), (250, 96, 4, 2, 3), (300, 64, 1, 52, 1),
          (2600, 128, 3, 13, 4), (2200, 300, 2, 33, 3)]
 MODES = {"default": {}, "off": {"TSW_COARSE": "0"}, "short_off": {"TSW_COARSE_SHORT": "0"},
+         "pass_8_setup_8": {"TSW_COARSE_W": "8", "TSW_CSETUP_W": "8"},
          "per_point_setup": {"TSW_CSETUP": "0"}, "strided_sample": {"TSW_GUIDED": "0"},
          "guided_64": {"TSW_GUIDED": "64"}}
 
@@ -92,11 +93,11 @@ def test_coarse_blocks_beyond_fp32_range(tsw, best_oracle):
 
 
 def test_coarse_prunes_and_reports_block(tsw, monkeypatch):
-    """The cascade is what runs by default (bound_block = 4 / 8 in the plan statistics, 1 with
+    """The cascade is what runs by default (bound_block = 4 / 16 in the plan statistics, 1 with
     TSW_COARSE=0), it prunes (lb_pruned > 0 on a clustered store), and both settings return
     the same neighbours."""
     rng = np.random.default_rng(5)
-    for L, r, blk in ((128, 13, 4), (640, 40, 8)):
+    for L, r, blk in ((128, 13, 4), (640, 40, 16)):
         X = walks(rng, 3000, L, 3)
         X /= X.std(axis=1, keepdims=True)
         Q = X[:8] + 0.05 * rng.standard_normal((8, L, 3))
