@@ -504,7 +504,7 @@ std::unique_ptr<tsw_plan> make_plan(tsw_store* s, uint64_t nq_max, uint64_t qlen
             // the DP setup's finer level drops at once; C5 pass 0.765 -> 0.545 ms, step -1.9%);
             // TSW_COARSE_W=8 overrides
             const char* cwe = std::getenv("TSW_COARSE_W");
-            const uint32_t wl = cwe && std::atoi(cwe) == 8 ? 8u : 16u;
+            const uint32_t wl = cwe && (std::atoi(cwe) == 8 || std::atoi(cwe) == 32) ? (uint32_t)std::atoi(cwe) : 16u;
             const uint32_t w = long_mode ? wl : 4u;
             tsw_store::CEnv* ce = nullptr;
             for (auto& c : s->cenv)
@@ -891,7 +891,7 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
                 da.clen = (uint32_t)s->clen;
                 da.cw = s->cw;
             }
-            da.clog = da.cw == 16 ? 4u : da.cw == 8 ? 3u : 2u;
+            da.clog = da.cw == 32 ? 5u : da.cw == 16 ? 4u : da.cw == 8 ? 3u : 2u;
             da.qabsmax = p->qabsmax.p;
         }
     }
