@@ -597,7 +597,7 @@ def main():
                          **{m: extra[m]["plan_build_s"] for m in extra}},
         "plan_contents": "scratch for nq_max queries; for DTW, built once per store by the first "
                          "plan: the coarse cascade's fp32 block means of the store (N*(L/w)*d*4 "
-                         "bytes, w = 8 above 256 points else 4) and, per band radius, of the "
+                         "bytes, w = 16 above 256 points else 4; long series also a level of 4 for the DP setup and of 32 for the guided sample) and, per band radius, of the "
                          "candidate envelopes (2x that); with r >= 32 also the full-resolution "
                          "fp32 candidate envelopes (N*L*d*8 bytes: the 1-query plans' and the "
                          "probes' reverse cumulative bound)",

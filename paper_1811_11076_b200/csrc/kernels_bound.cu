@@ -274,14 +274,14 @@ void launch_envelope64(const double* q, uint32_t nq, uint32_t d, uint32_t len, u
 
 // ---- coarse (piecewise-aggregate) series and envelopes for the LB cascade ----------------------
 // The coarse LB pass bounds LB_Box from below with block means over w
-// consecutive points (w = 4 or 8 <= kPaa): f(x, lo, hi) = dist(x, [lo, hi])^2 is jointly convex,
+// consecutive points (w = 4 ... 32 <= kPaa): f(x, lo, hi) = dist(x, [lo, hi])^2 is jointly convex,
 // so by Jensen
 //   sum_{p in block} f(x_p, lo_p, hi_p)  >=  w * f(mean x, mean lo, mean hi).
 // Coarse series are tiled like the fine ones (32 coarse points per tile, pitch = cstride
 // elements, no guard tiles); a tail of len % w points is dropped (its terms are >= 0).
 // One thread per (series, coarse point, dim).
 //
-// Block mean of the values, fp32: the fp64 mean (<= 7 additions, |error| <= 7 * 2^-53 * max|x|)
+// Block mean of the values, fp32: the fp64 mean (<= 31 additions, |error| <= 31 * 2^-53 * max|x|)
 // rounded to nearest, so |out - mean| <= max|x| * 2^-24 * (1 + 2^-20) over the in-range values;
 // a block holding a value beyond the fp32 range gets NaN: every term on it is
 // fmaxf(NaN, 0) = 0 (no bound from that block).
