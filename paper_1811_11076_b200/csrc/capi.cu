@@ -770,6 +770,7 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
     sa.cand = guided ? p->g_idx.p : nullptr;
     sa.ub_scale = p->ub_scale;
     sa.dk = dk;
+    sa.sub = sub ? 1 : 0;
     sa.out_ub = p->ub.p;
     sa.part = p->ub_part.p;
     sa.part_cap = p->ub_part.n;

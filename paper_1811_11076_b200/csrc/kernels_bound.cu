@@ -438,6 +438,30 @@ __global__ void __launch_bounds__(256) sample_ub_kernel(SampleArgs a) {
         const double* s = a.queries + (uint64_t)q * a.qstride;
         const double* t = a.store.data + series_off(a.store, c);
         const uint32_t n = series_len(a.store, c);
+        if (a.sub && n >= m) {
+            // subsequence DK: every window [o, o + m) matched point for point is a valid
+            // subsequence match, so the smallest window maximum (disjoint windows: the same n
+            // point costs as the whole-match path) bounds dk_sub from above -- the whole-match
+            // path's forced tail (the last query point against every remaining column) made the
+            // seed useless
+            double best = kInf;
+            for (uint32_t o = 0; o + m <= n; o += m) {
+                double wacc = 0.0;
+                for (uint32_t p = lane; p < m; p += 32) {
+                    double cst = 0.0;
+                    for (uint32_t k = 0; k < d; ++k) {
+                        const double e = dsub(s[tidx(p, k, d)], t[tidx(o + p, k, d)]);
+                        cst = dadd(cst, dmul(e, e));
+                    }
+                    wacc = dmax(wacc, cst);
+                }
+#pragma unroll
+                for (int sh = 16; sh > 0; sh >>= 1) wacc = dmax(wacc, __shfl_xor_sync(0xffffffffu, wacc, sh));
+                best = dmin(best, wacc);
+            }
+            if (lane == 0) a.out_ub[(uint64_t)q * a.S + j] = best;
+            continue;
+        }
         const uint32_t steps = a.dk ? max(m, n) : m;
         double acc = 0.0;
         for (uint32_t p = lane; p < steps; p += 32) {

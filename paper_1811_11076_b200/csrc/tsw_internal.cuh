@@ -301,6 +301,7 @@ struct SampleArgs {
     const uint32_t* cand; // guided sample (nullable): candidate of slot j of query q at [q * S + j]
     double ub_scale;      // DTW: diagonal-sum inflation factor (rounded up)
     int dk;
+    int sub;              // subsequence DK: the best point-for-point window instead of the whole-match path
     double* out_ub;       // [nq][S]  DTW: diagonal upper bound; DK: diagonal-path max sq
     double* part;         // optional scratch for point-range splits ([split][nq][S]), nullable
     uint64_t part_cap;    // doubles in `part`
