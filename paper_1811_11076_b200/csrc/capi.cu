@@ -407,7 +407,11 @@ std::unique_ptr<tsw_plan> make_plan(tsw_store* s, uint64_t nq_max, uint64_t qlen
     // probes find tighter thresholds); at C2/C3 larger samples cost more than they save.
     // TSW_SAMPLE overrides.
     const char* se = std::getenv("TSW_SAMPLE");
-    const uint64_t s_auto = n < 98304 ? 2048 : std::min<uint64_t>(8192, n / 24);
+    // (subsequence DK: every pair is queued whatever the seed and the threshold converges within
+    // the first pairs, so a small sample does: S = 512 instead of 2048 / 8192 -3% / -4% per step)
+    const uint64_t s_auto = metric == TSW_METRIC_DK_SUB ? 512
+                            : n < 98304               ? 2048
+                                                      : std::min<uint64_t>(8192, n / 24);
     const uint64_t s_want = se && std::atoll(se) > 0 ? (uint64_t)std::atoll(se) : s_auto;
     p->S = std::min<uint64_t>(n, s_want);
     // probe = the most promising sampled candidates, DP'd first to tighten the threshold.  DTW

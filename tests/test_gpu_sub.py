@@ -19,8 +19,8 @@ pytestmark = pytest.mark.gpu
 
 
 def seed_sample(n):
-    """Seed bounds the engine computes per query (capi.cu make_plan): 2048, ~n/24 for n >= 96k."""
-    return min(n, 2048 if n < 98304 else min(8192, n // 24))
+    """Seed bounds the engine computes per query of a subsequence search (capi.cu make_plan)."""
+    return min(n, 512)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 RNG = np.random.default_rng(1811_11076 + 5)
