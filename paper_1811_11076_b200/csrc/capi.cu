@@ -209,6 +209,8 @@ struct tsw_store {
     uint32_t cw_s = 0;
     // guided seed sample: a second, coarser level of block means (cw2 points)
     // for the all-pairs distance estimate that picks the sampled candidates
+    // subsequence DK: per-tile bounding boxes of every series (built by the first knn_dk_sub plan)
+    DevBuf<float> box_lo, box_hi;
     DevBuf<float> paa2;
     uint64_t clen2 = 0, cstride2 = 0;
     uint32_t cw2 = 0;
@@ -644,6 +646,17 @@ std::unique_ptr<tsw_plan> make_plan(tsw_store* s, uint64_t nq_max, uint64_t qlen
             p->P = std::max<uint64_t>(1, std::min<uint64_t>(kKMax, std::max(p->kk, p->probe)));
         }
     }
+    // Subsequence DK: the box bound of the query's end points (dk_compact_kernel) needs the
+    // store's per-tile bounding boxes.  TSW_SUB_BOX=0: every pair queued with key 0.
+    if (metric == TSW_METRIC_DK_SUB && !s->box_lo.p) {
+        const char* be = std::getenv("TSW_SUB_BOX");
+        if (!be || std::atoi(be) != 0) {
+            s->box_lo.alloc(s->data.n / kTile);
+            s->box_hi.alloc(s->data.n / kTile);
+            launch_series_boxes(s->dev(), (uint32_t)s->max_len, s->box_lo.p, s->box_hi.p, p->own);
+            ck(cudaStreamSynchronize(p->own), "series boxes");
+        }
+    }
     p->ub.alloc(nq_max * p->S);
     // point-range splits of the sampled bounds when the (query, sample) tiles cannot fill the
     // GPU (few queries): up to 8 partial rows per pair
@@ -997,6 +1010,10 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
         ka.probed = p->probed.p;
         ka.queue = p->main_wq();
         ka.sub = sub ? 1 : 0;
+        if (sub && s->box_lo.p) {
+            ka.box_lo = s->box_lo.p;
+            ka.box_hi = s->box_hi.p;
+        }
         launch_dk_compact(ka, st);
     }
     ++launches;

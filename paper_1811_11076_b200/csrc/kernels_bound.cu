@@ -1305,6 +1305,40 @@ void launch_lb64_serial(const StoreDev& s, const double* lo, const double* hi, u
 // Both cells lie on every warping path, so max(c(0,0), c(m-1,n-1)) > Tsq  =>  dk > T (exact).
 // Subsequence mode: a match may start and end at any column, so the key is 0 (every pair that
 // was not probed enters the queue; the DP's own frontier test prunes it).
+// ---- subsequence DK: per-tile bounding boxes ----------------------------------------------------
+// One thread per (series, tile, dim): min / max over the tile's points of that series (padding
+// and guard points excluded), rounded outward to fp32.
+__global__ void series_boxes_kernel(StoreDev s, uint32_t tmax, float* __restrict__ lo,
+                                    float* __restrict__ hi) {
+    const uint64_t total = (uint64_t)s.n * tmax * s.d;
+    for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total;
+         g += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t c = (uint32_t)(g / ((uint64_t)tmax * s.d));
+        const uint32_t rem = (uint32_t)(g - (uint64_t)c * tmax * s.d);
+        const uint32_t ti = rem / s.d, k = rem - ti * s.d;
+        const uint32_t len = series_len(s, c);
+        if (ti * kTile >= len) continue;
+        const uint64_t off = series_off(s, c);
+        const double* x = s.data + off;
+        double mn = kInf, mx = -kInf;
+        for (uint32_t j = 0; j < kTile && ti * kTile + j < len; ++j) {
+            const double v = x[tidx(ti * kTile + j, k, s.d)];
+            mn = v < mn ? v : mn;
+            mx = v > mx ? v : mx;
+        }
+        const uint64_t o = (off / (kTile * s.d) + ti) * s.d + k;
+        lo[o] = __double2float_rd(mn);
+        hi[o] = __double2float_ru(mx);
+    }
+}
+
+void launch_series_boxes(const StoreDev& s, uint32_t max_len, float* lo, float* hi, cudaStream_t st) {
+    const uint32_t tmax = (max_len + kTile - 1) / kTile;
+    const uint64_t total = (uint64_t)s.n * tmax * s.d;
+    const int blocks = (int)std::min<uint64_t>((total + 255) / 256, (uint64_t)sm_count() * 16);
+    series_boxes_kernel<<<std::max(blocks, 1), 256, 0, st>>>(s, tmax, lo, hi);
+}
+
 __global__ void __launch_bounds__(256) dk_compact_kernel(DkCompactArgs a) {
     const uint32_t n = a.store.n, d = a.store.d;
     const uint64_t total = (uint64_t)a.nq * n;
@@ -1336,6 +1370,33 @@ __global__ void __launch_bounds__(256) dk_compact_kernel(DkCompactArgs a) {
                     c1 = dadd(c1, dmul(e1, e1));
                 }
                 key = dmax(c0, c1);
+                if (a.sub && a.box_lo) {
+                    // Subsequence box bound: the query's first and last points are each matched
+                    // to SOME point of the series, so dk_sub^2 >= max over those two points of
+                    // the smallest squared distance to a tile's bounding box.  Round-down
+                    // arithmetic on outward-rounded boxes, then (1 - 2^-40): below every fl
+                    // point cost the DP can compute for these points (relative error of
+                    // sq_dist <= (d + 2) 2^-53).
+                    const uint32_t nt = (series_len(a.store, c) + kTile - 1) / kTile;
+                    const uint64_t bt = series_off(a.store, c) / (kTile * d);
+                    double m0 = kInf, m1 = kInf;
+                    for (uint32_t ti = 0; ti < nt; ++ti) {
+                        double a0 = 0.0, a1 = 0.0;
+                        for (uint32_t k = 0; k < d; ++k) {
+                            const double l = (double)a.box_lo[(bt + ti) * d + k];
+                            const double h = (double)a.box_hi[(bt + ti) * d + k];
+                            const double q0 = a.qends[(uint64_t)k * a.nq + q];
+                            const double q1 = a.qends[(uint64_t)(d + k) * a.nq + q];
+                            const double e0 = fmax(fmax(__dsub_rd(l, q0), __dsub_rd(q0, h)), 0.0);
+                            const double e1 = fmax(fmax(__dsub_rd(l, q1), __dsub_rd(q1, h)), 0.0);
+                            a0 = __dadd_rd(a0, __dmul_rd(e0, e0));
+                            a1 = __dadd_rd(a1, __dmul_rd(e1, e1));
+                        }
+                        m0 = fmin(m0, a0);
+                        m1 = fmin(m1, a1);
+                    }
+                    key = __dmul_rd(dmax(m0, m1), 1.0 - 0x1p-40);
+                }
                 const double Tsq = a.state ? a.state[q].Tsq : a.fixed_eps_sq;
                 take = key <= Tsq;
                 near = key <= a.near_frac * Tsq;

@@ -118,6 +118,9 @@ __device__ bool sub_claim_masks(const DpArgs& a, int cnt, bool ok, uint32_t eq, 
     // lane i < cnt holds claimed entry i (ok, eq, ec) and its threshold tsq
     const unsigned c0 = __shfl_sync(kFull, ec, 0);
     if (!__all_sync(kFull, lane >= cnt || (ok && ec == c0))) return false;
+    // (tsq < 0: the entry's bound already exceeds its threshold -- it is dropped at dequeue and
+    // needs no bits; a claim of such entries only skips the series altogether)
+    if (!__any_sync(kFull, lane < cnt && tsq >= 0.0)) return true;
     Pt<D> p0;  // lane i < cnt: point 0 of query i
     if (lane < cnt) p0 = sp0_of<D>(a.queries + (uint64_t)eq * a.qstride, stride);
     const double* t = a.store.data + series_off(a.store, c0);
@@ -133,6 +136,7 @@ __device__ bool sub_claim_masks(const DpArgs& a, int cnt, bool ok, uint32_t eq, 
 #pragma unroll
             for (int kk = 0; kk < D; ++kk) pi.x[kk] = __shfl_sync(kFull, p0.x[kk], i);
             const double ti = __shfl_sync(kFull, tsq, i);
+            if (ti < 0.0) continue;  // warp-uniform
             const unsigned bm = __ballot_sync(kFull, j < n && cost<D>(pi, tj) <= ti);
             if (lane == 0) r0m[i * wmax + w] = bm;
         }
@@ -263,7 +267,9 @@ __global__ void __launch_bounds__(128) dk_dp_kernel(DpArgs a, uint32_t max_len) 
                 if (cok && a.state) ctsq = ld_volatile(&a.state[e.q].Tsq);
                 if constexpr (D > 0) {
                     if (cnt > 1)
-                        premask = sub_claim_masks<D>(a, cnt, cok, cq, cc, ctsq, r0m, wmax, lane, stride);
+                        premask = sub_claim_masks<D>(a, cnt, cok, cq, cc,
+                                                     cok && (double)ckey <= ctsq ? ctsq : -1.0, r0m,
+                                                     wmax, lane, stride);
                 }
             }
         }

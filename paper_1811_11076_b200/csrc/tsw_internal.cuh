@@ -377,8 +377,15 @@ struct DkCompactArgs {
     const uint8_t* probed;
     WorkQueue queue;
     int sub;                  // subsequence DK: no endpoint bound (every column may start/end a match)
+    // subsequence DK: per-tile bounding boxes of the store (32 points, per dimension, fp32
+    // rounded outward; index (series_off / (32 d) + tile) * d + k) for the box bound of the
+    // query's first and last points (nullable: every pair is queued with key 0)
+    const float* box_lo;
+    const float* box_hi;
 };
 void launch_dk_compact(const DkCompactArgs& a, cudaStream_t st);
+// per-tile bounding boxes of every series (padding points excluded); lo / hi: data elements / 32 floats
+void launch_series_boxes(const StoreDev& s, uint32_t max_len, float* lo, float* hi, cudaStream_t st);
 
 struct DpArgs {
     StoreDev store;
