@@ -244,7 +244,7 @@ struct tsw_plan {
     cudaStream_t own = nullptr;
     cudaStream_t aux = nullptr;  // DTW probe DP, overlapped with the LB pass
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
-    DevBuf<double> qends;  // DK compaction scratch [2d][nq_max]
+    DevBuf<double> qends;  // DK compaction scratch [kQPts * d][nq_max]
     DevBuf<double> q, q_rm, ub, ub_part, sel_sv, sel_v, slots, top_d;
     DevBuf<double> qinf;  // DTW: one all-+inf guarded query (the fast path's idle lanes)
     DevBuf<float> env_lo, env_hi;
@@ -433,7 +433,7 @@ std::unique_ptr<tsw_plan> make_plan(tsw_store* s, uint64_t nq_max, uint64_t qlen
     launch_fill(p->q.p, kTile * s->d, INFINITY, p->own);  // leading guard of query 0
     ck(cudaStreamSynchronize(p->own), "plan init");
     p->q_rm.alloc(nq_max * qlen * s->d);
-    p->qends.alloc(2 * s->d * nq_max);
+    p->qends.alloc((uint64_t)kQPts * s->d * nq_max);
     if (metric == TSW_METRIC_DTW) {
         p->qinf.alloc(kTile * s->d + p->qstride);
         launch_fill(p->qinf.p, kTile * s->d + p->qstride, INFINITY, p->own);
@@ -1531,7 +1531,7 @@ int tsw_epsnn_dk(tsw_store* s, const double* query, uint64_t qlen, double eps,
         DeviceGuard dg(s->device);
         const uint64_t n = s->n, d = s->d, qs = stride_of(qlen, d);
         cudaStream_t st = 0;
-        DevBuf<double> q(qs), rd(n), qe(2 * d);
+        DevBuf<double> q(qs), rd(n), qe((uint64_t)kQPts * d);
         DevBuf<uint32_t> ri(n);
         DevBuf<unsigned> rn(1), ctr(4);
         DevBuf<unsigned long long> pruned(2);  // [0] compaction, [1] dequeue drops + abandoned

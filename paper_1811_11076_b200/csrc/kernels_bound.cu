@@ -1377,25 +1377,62 @@ __global__ void __launch_bounds__(256) dk_compact_kernel(DkCompactArgs a) {
                     // arithmetic on outward-rounded boxes, then (1 - 2^-40): below every fl
                     // point cost the DP can compute for these points (relative error of
                     // sq_dist <= (d + 2) 2^-53).
+                    // (kQPts query points: first, last and two interior ones -- every query point
+                    // is matched to some point of the series)
                     const uint32_t nt = (series_len(a.store, c) + kTile - 1) / kTile;
                     const uint64_t bt = series_off(a.store, c) / (kTile * d);
-                    double m0 = kInf, m1 = kInf;
-                    for (uint32_t ti = 0; ti < nt; ++ti) {
-                        double a0 = 0.0, a1 = 0.0;
-                        for (uint32_t k = 0; k < d; ++k) {
-                            const double l = (double)a.box_lo[(bt + ti) * d + k];
-                            const double h = (double)a.box_hi[(bt + ti) * d + k];
-                            const double q0 = a.qends[(uint64_t)k * a.nq + q];
-                            const double q1 = a.qends[(uint64_t)(d + k) * a.nq + q];
-                            const double e0 = fmax(fmax(__dsub_rd(l, q0), __dsub_rd(q0, h)), 0.0);
-                            const double e1 = fmax(fmax(__dsub_rd(l, q1), __dsub_rd(q1, h)), 0.0);
-                            a0 = __dadd_rd(a0, __dmul_rd(e0, e0));
-                            a1 = __dadd_rd(a1, __dmul_rd(e1, e1));
+                    double mn[kQPts];
+#pragma unroll
+                    for (int w = 0; w < kQPts; ++w) mn[w] = kInf;
+                    if (d <= 4) {  // the query points in registers
+                        double qp[kQPts][4];
+#pragma unroll
+                        for (int w = 0; w < kQPts; ++w)
+#pragma unroll
+                            for (uint32_t k = 0; k < 4; ++k)
+                                qp[w][k] = k < d ? a.qends[(uint64_t)(w * d + k) * a.nq + q] : 0.0;
+                        for (uint32_t ti = 0; ti < nt; ++ti) {
+                            double acc[kQPts];
+#pragma unroll
+                            for (int w = 0; w < kQPts; ++w) acc[w] = 0.0;
+#pragma unroll
+                            for (uint32_t k = 0; k < 4; ++k) {
+                                if (k < d) {
+                                    const double l = (double)__ldg(a.box_lo + (bt + ti) * d + k);
+                                    const double h = (double)__ldg(a.box_hi + (bt + ti) * d + k);
+#pragma unroll
+                                    for (int w = 0; w < kQPts; ++w) {
+                                        const double e = fmax(fmax(__dsub_rd(l, qp[w][k]), __dsub_rd(qp[w][k], h)), 0.0);
+                                        acc[w] = __dadd_rd(acc[w], __dmul_rd(e, e));
+                                    }
+                                }
+                            }
+#pragma unroll
+                            for (int w = 0; w < kQPts; ++w) mn[w] = fmin(mn[w], acc[w]);
                         }
-                        m0 = fmin(m0, a0);
-                        m1 = fmin(m1, a1);
+                    } else {
+                        for (uint32_t ti = 0; ti < nt; ++ti) {
+                            double acc[kQPts];
+#pragma unroll
+                            for (int w = 0; w < kQPts; ++w) acc[w] = 0.0;
+                            for (uint32_t k = 0; k < d; ++k) {
+                                const double l = (double)a.box_lo[(bt + ti) * d + k];
+                                const double h = (double)a.box_hi[(bt + ti) * d + k];
+#pragma unroll
+                                for (int w = 0; w < kQPts; ++w) {
+                                    const double qv = a.qends[(uint64_t)(w * d + k) * a.nq + q];
+                                    const double e = fmax(fmax(__dsub_rd(l, qv), __dsub_rd(qv, h)), 0.0);
+                                    acc[w] = __dadd_rd(acc[w], __dmul_rd(e, e));
+                                }
+                            }
+#pragma unroll
+                            for (int w = 0; w < kQPts; ++w) mn[w] = fmin(mn[w], acc[w]);
+                        }
                     }
-                    key = __dmul_rd(dmax(m0, m1), 1.0 - 0x1p-40);
+                    double mx = mn[0];
+#pragma unroll
+                    for (int w = 1; w < kQPts; ++w) mx = dmax(mx, mn[w]);
+                    key = __dmul_rd(mx, 1.0 - 0x1p-40);
                 }
                 const double Tsq = a.state ? a.state[q].Tsq : a.fixed_eps_sq;
                 take = key <= Tsq;
@@ -1410,18 +1447,21 @@ __global__ void __launch_bounds__(256) dk_compact_kernel(DkCompactArgs a) {
     pc.flush();
 }
 
+// query points of the compaction bounds, query-minor [kQPts * d][nq]: first, last (the
+// whole-match cell bound), then the points at 1/3 and 2/3 (subsequence box bound)
 __global__ void query_ends_kernel(const double* __restrict__ q, uint32_t nq, uint32_t m, uint32_t d,
                                   uint64_t qstride, double* __restrict__ out) {
-    const uint32_t total = 2 * d * nq;
+    const uint32_t total = kQPts * d * nq;
     for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < total; g += gridDim.x * blockDim.x) {
         const uint32_t qi = g % nq, wk = g / nq;          // wk = which * d + k
         const uint32_t which = wk / d, k = wk - which * d;
-        out[g] = q[(uint64_t)qi * qstride + tidx(which ? m - 1 : 0, k, d)];
+        const uint32_t p = which == 0 ? 0u : which == 1 ? m - 1 : (uint32_t)(((uint64_t)(m - 1) * (which - 1)) / 3);
+        out[g] = q[(uint64_t)qi * qstride + tidx(p, k, d)];
     }
 }
 
 void launch_dk_compact(const DkCompactArgs& a, cudaStream_t st) {
-    query_ends_kernel<<<std::max(1u, std::min(64u, (2 * a.store.d * a.nq + 255) / 256)), 256, 0, st>>>(
+    query_ends_kernel<<<std::max(1u, std::min(64u, (kQPts * a.store.d * a.nq + 255) / 256)), 256, 0, st>>>(
         a.queries, a.nq, a.qlen, a.store.d, a.qstride, a.qends);
     const uint64_t total = (uint64_t)a.nq * a.store.n;
     const int blocks = (int)std::min<uint64_t>((total + 255) / 256, (uint64_t)sm_count() * 8);

@@ -29,6 +29,7 @@ constexpr int kSelChunk = 4096; // bitonic selection chunk
 constexpr double kInf = __builtin_huge_val();
 constexpr float kInfF = __builtin_huge_valf();
 constexpr uint32_t kTile = 32;  // points per layout tile
+constexpr int kQPts = 4;        // query points of the DK compaction bounds (first, last, 1/3, 2/3)
 constexpr uint32_t kPaa = 32;   // most points per block mean of the coarse LB pass
 
 // element offset of (point p, dim k) in a tiled series of dimension d
@@ -367,7 +368,7 @@ void launch_lb_compact(const LbCompactArgs& a, cudaStream_t st);
 struct DkCompactArgs {
     StoreDev store;
     const double* queries;
-    double* qends;            // scratch [2d][nq]: query first/last points, query-minor
+    double* qends;            // scratch [kQPts * d][nq]: query first / last / interior points, query-minor
     uint32_t nq, qlen;
     uint64_t qstride;
     double near_frac;
