@@ -1384,32 +1384,42 @@ __global__ void __launch_bounds__(256) dk_compact_kernel(DkCompactArgs a) {
                     double mn[kQPts];
 #pragma unroll
                     for (int w = 0; w < kQPts; ++w) mn[w] = kInf;
-                    if (d <= 4) {  // the query points in registers
-                        double qp[kQPts][4];
+                    if (d <= 4) {
+                        // fp32, round-down: the query point as the interval [RD32(q), RU32(q)],
+                        // so l - q_hi <= l - q and q_lo - h <= q - h hold without an error term
+                        // (the key is stored as a float anyway); sums saturate, never +inf
+                        float ql[kQPts][4], qh[kQPts][4], mnf[kQPts];
 #pragma unroll
-                        for (int w = 0; w < kQPts; ++w)
+                        for (int w = 0; w < kQPts; ++w) {
+                            mnf[w] = kInfF;
 #pragma unroll
-                            for (uint32_t k = 0; k < 4; ++k)
-                                qp[w][k] = k < d ? a.qends[(uint64_t)(w * d + k) * a.nq + q] : 0.0;
+                            for (uint32_t k = 0; k < 4; ++k) {
+                                const double qv = k < d ? a.qends[(uint64_t)(w * d + k) * a.nq + q] : 0.0;
+                                ql[w][k] = __double2float_rd(qv);
+                                qh[w][k] = __double2float_ru(qv);
+                            }
+                        }
                         for (uint32_t ti = 0; ti < nt; ++ti) {
-                            double acc[kQPts];
+                            float acc[kQPts];
 #pragma unroll
-                            for (int w = 0; w < kQPts; ++w) acc[w] = 0.0;
+                            for (int w = 0; w < kQPts; ++w) acc[w] = 0.0f;
 #pragma unroll
                             for (uint32_t k = 0; k < 4; ++k) {
                                 if (k < d) {
-                                    const double l = (double)__ldg(a.box_lo + (bt + ti) * d + k);
-                                    const double h = (double)__ldg(a.box_hi + (bt + ti) * d + k);
+                                    const float l = __ldg(a.box_lo + (bt + ti) * d + k);
+                                    const float h = __ldg(a.box_hi + (bt + ti) * d + k);
 #pragma unroll
                                     for (int w = 0; w < kQPts; ++w) {
-                                        const double e = fmax(fmax(__dsub_rd(l, qp[w][k]), __dsub_rd(qp[w][k], h)), 0.0);
-                                        acc[w] = __dadd_rd(acc[w], __dmul_rd(e, e));
+                                        const float e = fmaxf(fmaxf(__fsub_rd(l, qh[w][k]), __fsub_rd(ql[w][k], h)), 0.0f);
+                                        acc[w] = __fmaf_rd(e, e, acc[w]);
                                     }
                                 }
                             }
 #pragma unroll
-                            for (int w = 0; w < kQPts; ++w) mn[w] = fmin(mn[w], acc[w]);
+                            for (int w = 0; w < kQPts; ++w) mnf[w] = fminf(mnf[w], acc[w]);
                         }
+#pragma unroll
+                        for (int w = 0; w < kQPts; ++w) mn[w] = (double)__fmul_rd(mnf[w], 1.0f - 0x1p-20f);
                     } else {
                         for (uint32_t ti = 0; ti < nt; ++ti) {
                             double acc[kQPts];
@@ -1455,7 +1465,8 @@ __global__ void query_ends_kernel(const double* __restrict__ q, uint32_t nq, uin
     for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < total; g += gridDim.x * blockDim.x) {
         const uint32_t qi = g % nq, wk = g / nq;          // wk = which * d + k
         const uint32_t which = wk / d, k = wk - which * d;
-        const uint32_t p = which == 0 ? 0u : which == 1 ? m - 1 : (uint32_t)(((uint64_t)(m - 1) * (which - 1)) / 3);
+        const uint32_t p = which == 0 ? 0u : which == 1 ? m - 1
+                                           : (uint32_t)(((uint64_t)(m - 1) * (which - 1)) / (kQPts - 1));
         out[g] = q[(uint64_t)qi * qstride + tidx(p, k, d)];
     }
 }

@@ -29,7 +29,7 @@ constexpr int kSelChunk = 4096; // bitonic selection chunk
 constexpr double kInf = __builtin_huge_val();
 constexpr float kInfF = __builtin_huge_valf();
 constexpr uint32_t kTile = 32;  // points per layout tile
-constexpr int kQPts = 4;        // query points of the DK compaction bounds (first, last, 1/3, 2/3)
+constexpr int kQPts = 8;        // query points of the DK compaction bounds (first, last, interior i/7)
 constexpr uint32_t kPaa = 32;   // most points per block mean of the coarse LB pass
 
 // element offset of (point p, dim k) in a tiled series of dimension d
