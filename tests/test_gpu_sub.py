@@ -105,6 +105,41 @@ def test_knn_dk_sub_random(tsw, best_oracle):
             assert gc[q][4] == seed_sample(n) and gc[q][2] + gc[q][3] == n
 
 
+def test_knn_dk_sub_box_bound_cases(tsw, best_oracle, monkeypatch):
+    """The subsequence box bound (per-tile bounding boxes of the store against eight query
+    points, fp32 interval arithmetic) only prunes: with it on and off the neighbours equal the
+    reference's, on ragged stores, d = 1..5 (d >= 5: the fp64 form), query subsequences cut out
+    of stored series (distance 0 and near 0: the tightest thresholds), series shorter than the
+    query, and values beyond the fp32 range."""
+    import oracle
+
+    rng = np.random.default_rng(1234)
+    for trial in range(12):
+        d = 1 + trial % 5
+        n = int(rng.integers(60, 400))
+        X = [rng.standard_normal((int(rng.integers(3, 300)), d)).cumsum(0) for _ in range(n)]
+        if trial % 4 == 3:
+            for c in range(0, n, 7):
+                X[c] = X[c] * 1e39  # beyond the fp32 range: boxes with infinite sides
+        m = int(rng.integers(8, 90))
+        Q = rng.standard_normal((4, m, d)).cumsum(1)
+        src = [x for x in X if len(x) >= m + 5]
+        if src:
+            Q[0] = src[0][3:3 + m]                                       # an exact subsequence
+            Q[1] = src[-1][2:2 + m] + 1e-4 * rng.standard_normal((m, d))  # a near one
+        k = int(rng.integers(1, 8))
+        ods = oracle.Dataset(X)
+        want = [best_oracle.knn(Q[q], ods, k, "dk_sub") for q in range(len(Q))]
+        for box in ("1", "0"):
+            monkeypatch.setenv("TSW_SUB_BOX", box)
+            gi, gd, gc = tsw.knn(tsw.Dataset(X), Q, k, "dk_sub")
+            for q in range(len(Q)):
+                oi, od, _ = want[q]
+                assert np.array_equal(gi[q], oi), (trial, box, q, gi[q], oi)
+                assert np.array_equal(_bits(gd[q]), _bits(od)), (trial, box, q, gd[q], od)
+                assert gc[q][2] + gc[q][3] == n
+
+
 def test_knn_dk_sub_large_k_and_dupes(tsw, best_oracle):
     import oracle
 
