@@ -1339,6 +1339,9 @@ void launch_series_boxes(const StoreDev& s, uint32_t max_len, float* lo, float* 
     series_boxes_kernel<<<std::max(blocks, 1), 256, 0, st>>>(s, tmax, lo, hi);
 }
 
+// SUB: subsequence mode (its box bound lives in this instantiation only: the whole-match kernel
+// keeps its registers -- sharing one kernel cost the whole-match compaction 50%)
+template <bool SUB>
 __global__ void __launch_bounds__(256) dk_compact_kernel(DkCompactArgs a) {
     const uint32_t n = a.store.n, d = a.store.d;
     const uint64_t total = (uint64_t)a.nq * n;
@@ -1363,14 +1366,14 @@ __global__ void __launch_bounds__(256) dk_compact_kernel(DkCompactArgs a) {
                 // queries), candidate endpoints broadcast from the store's ends array
                 const double* e = a.store.ends + (uint64_t)c * 2 * d;  // first, last point
                 double c0 = 0.0, c1 = 0.0;
-                for (uint32_t k = 0; k < (a.sub ? 0u : d); ++k) {
+                for (uint32_t k = 0; k < (SUB ? 0u : d); ++k) {
                     const double e0 = dsub(a.qends[(uint64_t)k * a.nq + q], e[k]);
                     c0 = dadd(c0, dmul(e0, e0));
                     const double e1 = dsub(a.qends[(uint64_t)(d + k) * a.nq + q], e[d + k]);
                     c1 = dadd(c1, dmul(e1, e1));
                 }
                 key = dmax(c0, c1);
-                if (a.sub && a.box_lo) {
+                if (SUB && a.box_lo) {
                     // Subsequence box bound: the query's first and last points are each matched
                     // to SOME point of the series, so dk_sub^2 >= max over those two points of
                     // the smallest squared distance to a tile's bounding box.  Round-down
@@ -1476,7 +1479,8 @@ void launch_dk_compact(const DkCompactArgs& a, cudaStream_t st) {
         a.queries, a.nq, a.qlen, a.store.d, a.qstride, a.qends);
     const uint64_t total = (uint64_t)a.nq * a.store.n;
     const int blocks = (int)std::min<uint64_t>((total + 255) / 256, (uint64_t)sm_count() * 8);
-    dk_compact_kernel<<<std::max(blocks, 1), 256, 0, st>>>(a);
+    if (a.sub) dk_compact_kernel<true><<<std::max(blocks, 1), 256, 0, st>>>(a);
+    else dk_compact_kernel<false><<<std::max(blocks, 1), 256, 0, st>>>(a);
 }
 
 }  // namespace tswb
