@@ -62,3 +62,36 @@ for q in range(nq):
     tot["improved_fwd"] += p_f / nq
     tot["improved_both"] += p_b / nq
 print("mean", {a: round(float(b), 4) for a, b in tot.items()})
+
+
+# ---- a block-level relaxation: everything from per-block means / minima / maxima ----------------
+def blk(x, w, f):
+    s_ = x.shape
+    return f(x.reshape(s_[:-2] + (s_[-2] // w, w, s_[-1])), axis=-2)
+
+
+def coarse_improved(w):
+    L = sub.shape[1]
+    nb = L // w
+    cmean, cmn, cmx = blk(sub, w, np.mean), blk(sub, w, np.min), blk(sub, w, np.max)
+    res = 0.0
+    rb = (r + w - 1) // w  # blocks a window of radius r can reach on either side
+    for q in range(nq):
+        lq_mean, uq_mean = blk(qlo[q], w, np.mean), blk(qhi[q], w, np.mean)
+        lq_mn, lq_mx = blk(qlo[q], w, np.min), blk(qlo[q], w, np.max)
+        uq_mn, uq_mx = blk(qhi[q], w, np.min), blk(qhi[q], w, np.max)
+        qmean = blk(qs[q], w, np.mean)
+        f1 = w * lb(cmean, lq_mean, uq_mean)                      # Jensen on the first term
+        hlo = np.maximum(lq_mn, np.minimum(cmn, uq_mn))           # H_j >= hlo_B on block B
+        hhi = np.minimum(uq_mx, np.maximum(cmx, lq_mx))           # H_j <= hhi_B
+        elo = minimum_filter1d(hlo, 2 * rb + 1, axis=-2, mode="nearest")
+        ehi = maximum_filter1d(hhi, 2 * rb + 1, axis=-2, mode="nearest")
+        f2 = w * lb(qmean, elo, ehi)                              # Jensen in q, block-constant interval
+        rev = w * lb(qmean, blk(clo, w, np.mean), blk(chi, w, np.mean))
+        key = np.maximum(f1 + f2, rev)
+        res += (key <= T[q]).mean() / nq
+    return res
+
+
+for w in (4, 8):
+    print("block-level improved, w =", w, "pass", round(float(coarse_improved(w)), 4))
