@@ -209,6 +209,10 @@ struct tsw_store {
     uint32_t cw_s = 0;
     // guided seed sample: a second, coarser level of block means (cw2 points)
     // for the all-pairs distance estimate that picks the sampled candidates
+    // block-level improved bound (long series): block means / minima / maxima
+    // of every series at 8 points per block
+    DevBuf<float> lbi_xm, lbi_xmn, lbi_xmx;
+    uint64_t lbi_clen = 0, lbi_cstride = 0;
     // subsequence DK: per-tile bounding boxes of every series (built by the first knn_dk_sub plan)
     DevBuf<float> box_lo, box_hi;
     DevBuf<float> paa2;
@@ -264,6 +268,10 @@ struct tsw_plan {
     const float* ccenv_h = nullptr;
     DevBuf<float> cq_m, cq_h, cq32;
     DevBuf<float> cq_m_s, cq_h_s, cq32_s;  // the DP setup's finer level (long series)
+    // block-level improved bound: the queries' block means, envelope means and the block minima
+    // / maxima of their lower / upper envelopes (per execute)
+    bool lbi = false;
+    DevBuf<float> lbi_qm, lbi_qem, lbi_qeh, lbi_lqmn, lbi_lqmx, lbi_uqmn, lbi_uqmx;
     const float* ccenv_m_s = nullptr;
     const float* ccenv_h_s = nullptr;
     // guided seed sample: the G candidates with the smallest coarse diagonal distance per query
@@ -549,6 +557,30 @@ std::unique_ptr<tsw_plan> make_plan(tsw_store* s, uint64_t nq_max, uint64_t qlen
                 p->cq_h.alloc(nq_max * cst);
                 p->cq32.alloc(nq_max * cst);
                 if (!p->qabsmax.p) p->qabsmax.alloc(1);
+                // long series: the block-level improved bound on the queued pairs.  Off by default
+                // (TSW_LBI=1): measured at C5 it takes 37% of the pairs' DPs away but those are
+                // the cheap ones (DP 7.45 -> 6.68 ms) and the filter costs 1.3 ms
+                const char* lie = std::getenv("TSW_LBI");
+                const uint64_t clen8 = qlen / 8, cst8 = stride_of(clen8, s->d);
+                if (long_mode && s->d <= 4 && lie && std::atoi(lie) != 0 && clen8 >= 8 &&
+                    ((clen8 + 31) / 32 * 32) * s->d * 2 * 8 * sizeof(float) <= 96 * 1024) {
+                    if (!s->lbi_xm.p) {
+                        s->lbi_clen = clen8;
+                        s->lbi_cstride = cst8;
+                        s->lbi_xm.alloc(n * cst8);
+                        s->lbi_xmn.alloc(n * cst8);
+                        s->lbi_xmx.alloc(n * cst8);
+                        launch_paa_series(s->data.p + s->guard, n, (uint32_t)s->d, (uint32_t)clen8, 8,
+                                          s->ustride, cst8, s->lbi_xm.p, p->own);
+                        launch_paa_minmax(s->data.p + s->guard, n, (uint32_t)s->d, (uint32_t)clen8, 8,
+                                          s->ustride, cst8, s->lbi_xmn.p, s->lbi_xmx.p, p->own);
+                        ck(cudaStreamSynchronize(p->own), "improved-bound store level");
+                    }
+                    p->lbi = true;
+                    for (DevBuf<float>* b : {&p->lbi_qm, &p->lbi_qem, &p->lbi_qeh, &p->lbi_lqmn,
+                                             &p->lbi_lqmx, &p->lbi_uqmn, &p->lbi_uqmx})
+                        b->alloc(nq_max * cst8);
+                }
                 // long series: a finer level for the DP setup (TSW_CSETUP_W=8: the pass's level)
                 const char* swe = std::getenv("TSW_CSETUP_W");
                 const uint32_t ws = swe ? (uint32_t)std::atoi(swe) : 4u;
@@ -997,6 +1029,39 @@ void execute_impl(tsw_plan* p, cudaStream_t st) {
         la.c_lo = 0;
         la.c_hi = p->n1 ? p->n1 : n;
         launch_lb_compact(la, st);
+        if (coarse && p->lbi && !p->n1) {
+            // block-level improved bound on the queued pairs (their keys grow; the DP drops the
+            // dead ones at dequeue)
+            launch_paa_series(p->qg(), nq, (uint32_t)s->d, (uint32_t)s->lbi_clen, 8, p->qstride,
+                              s->lbi_cstride, p->lbi_qm.p, st);
+            launch_paa_envelope(p->qg(), nq, (uint32_t)s->d, (uint32_t)p->qlen, (uint32_t)s->lbi_clen, 8,
+                                p->qstride, s->lbi_cstride, (uint32_t)std::min<uint64_t>(p->r, 0xffffffffu),
+                                s->err_c, p->lbi_qem.p, p->lbi_qeh.p, st, p->lbi_lqmn.p, p->lbi_lqmx.p,
+                                p->lbi_uqmn.p, p->lbi_uqmx.p);
+            LbiArgs li{};
+            li.queue = p->main_wq();
+            li.state = p->state.p;
+            li.margin = p->margin;
+            li.d = (uint32_t)s->d;
+            li.clen = (uint32_t)s->lbi_clen;
+            li.rb = (uint32_t)((std::min<uint64_t>(p->r, p->qlen - 1) + 7) / 8);
+            li.cstride = s->lbi_cstride;
+            li.w = 8.0f;
+            li.xm = s->lbi_xm.p;
+            li.xmn = s->lbi_xmn.p;
+            li.xmx = s->lbi_xmx.p;
+            li.qm = p->lbi_qm.p;
+            li.qem = p->lbi_qem.p;
+            li.qeh = p->lbi_qeh.p;
+            li.lqmn = p->lbi_lqmn.p;
+            li.lqmx = p->lbi_lqmx.p;
+            li.uqmn = p->lbi_uqmn.p;
+            li.uqmx = p->lbi_uqmx.p;
+            li.qabsmax = p->qabsmax.p;
+            li.eq_scale = 0x1p-24 * (1.0 + 0x1p-20);
+            launch_lbi_filter(li, st);
+            launches += 3;
+        }
     } else {
         DkCompactArgs ka{};
         ka.store = s->dev();

@@ -326,7 +326,10 @@ void launch_paa_series(const double* src, uint64_t nser, uint32_t d, uint32_t cl
 __global__ void paa_envelope_kernel(const double* __restrict__ src, uint64_t nser, uint32_t d,
                                     uint32_t len, uint32_t clen, uint32_t w, uint64_t pitch,
                                     uint64_t cstride, uint32_t r, float err, float* __restrict__ om,
-                                    float* __restrict__ oh) {
+                                    float* __restrict__ oh, float* __restrict__ xlo_mn = nullptr,
+                                    float* __restrict__ xlo_mx = nullptr,
+                                    float* __restrict__ xhi_mn = nullptr,
+                                    float* __restrict__ xhi_mx = nullptr) {
     const uint64_t total = nser * cstride;
     for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total;
          g += (uint64_t)gridDim.x * blockDim.x) {
@@ -337,12 +340,17 @@ __global__ void paa_envelope_kernel(const double* __restrict__ src, uint64_t nse
         if (pc >= clen) {
             om[g] = 0.0f;
             oh[g] = 0.0f;
+            if (xlo_mn) {
+                xlo_mn[g] = xlo_mx[g] = xhi_mn[g] = xhi_mx[g] = 0.0f;
+            }
             continue;
         }
         const double* row = src + ser * pitch;
         const int64_t p0 = (int64_t)pc * w, last = (int64_t)len - 1, rr = (int64_t)r;
         const int wi = (int)w;
         double slo = 0.0, shi = 0.0;
+        // (block minima / maxima of the per-point envelope bounds: the improved bound, §4.8)
+        double lomn = kInf, lomx = -kInf, himn = kInf, himx = -kInf;
         if (r >= w) {
             double cmn = kInf, cmx = -kInf;  // the shared core (non-empty: r >= w)
             for (int64_t x = max(p0 + wi - 1 - rr, (int64_t)0); x <= min(p0 + rr, last); ++x) {
@@ -383,6 +391,10 @@ __global__ void paa_envelope_kernel(const double* __restrict__ src, uint64_t nse
                 const double lo = fmin(cmn, fmin(lmn[j], mn)), hi = fmax(cmx, fmax(lmx[j], mx));
                 slo = __dadd_rd(slo, lo);
                 shi = __dadd_ru(shi, hi);
+                lomn = fmin(lomn, lo);
+                lomx = fmax(lomx, lo);
+                himn = fmin(himn, hi);
+                himx = fmax(himx, hi);
             }
         } else {
             for (uint32_t j = 0; j < w; ++j) {
@@ -395,7 +407,17 @@ __global__ void paa_envelope_kernel(const double* __restrict__ src, uint64_t nse
                 }
                 slo = __dadd_rd(slo, mn);
                 shi = __dadd_ru(shi, mx);
+                lomn = fmin(lomn, mn);
+                lomx = fmax(lomx, mn);
+                himn = fmin(himn, mx);
+                himx = fmax(himx, mx);
             }
+        }
+        if (xlo_mn) {
+            xlo_mn[g] = __double2float_rd(lomn);
+            xlo_mx[g] = __double2float_ru(lomx);
+            xhi_mn[g] = __double2float_rd(himn);
+            xhi_mx[g] = __double2float_ru(himx);
         }
         const double mlo = __dmul_rd(slo, 1.0 / (double)w), mhi = __dmul_ru(shi, 1.0 / (double)w);
         if (!(mlo >= -(double)FLT_MAX && mhi <= (double)FLT_MAX)) {
@@ -412,11 +434,126 @@ __global__ void paa_envelope_kernel(const double* __restrict__ src, uint64_t nse
 
 void launch_paa_envelope(const double* src, uint64_t nser, uint32_t d, uint32_t len, uint32_t clen,
                          uint32_t w, uint64_t pitch, uint64_t cstride, uint32_t r, float err,
-                         float* om, float* oh, cudaStream_t st) {
+                         float* om, float* oh, cudaStream_t st, float* lo_mn, float* lo_mx,
+                         float* hi_mn, float* hi_mx) {
     const uint64_t total = nser * cstride;
     const int blocks = (int)std::min<uint64_t>((total + 255) / 256, (uint64_t)sm_count() * 16);
     paa_envelope_kernel<<<std::max(blocks, 1), 256, 0, st>>>(src, nser, d, len, clen, w, pitch,
-                                                             cstride, r, err, om, oh);
+                                                             cstride, r, err, om, oh, lo_mn, lo_mx,
+                                                             hi_mn, hi_mx);
+}
+
+// block minima / maxima of the values (fp32, rounded outward), same layout as paa_series_kernel
+__global__ void paa_minmax_kernel(const double* __restrict__ src, uint64_t nser, uint32_t d,
+                                  uint32_t clen, uint32_t w, uint64_t pitch, uint64_t cstride,
+                                  float* __restrict__ omn, float* __restrict__ omx) {
+    const uint64_t total = nser * cstride;
+    for (uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; g < total;
+         g += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t ser = g / cstride;
+        const uint32_t f = (uint32_t)(g - ser * cstride);
+        const uint32_t tile = f / (kTile * d), rem = f - tile * (kTile * d);
+        const uint32_t k = rem / kTile, pc = tile * kTile + rem % kTile;
+        if (pc >= clen) {
+            omn[g] = omx[g] = 0.0f;
+            continue;
+        }
+        const double* row = src + ser * pitch;
+        double mn = kInf, mx = -kInf;
+        for (uint32_t j = 0; j < w; ++j) {
+            const double v = row[tidx(pc * w + j, k, d)];
+            mn = v < mn ? v : mn;
+            mx = v > mx ? v : mx;
+        }
+        omn[g] = __double2float_rd(mn);
+        omx[g] = __double2float_ru(mx);
+    }
+}
+
+void launch_paa_minmax(const double* src, uint64_t nser, uint32_t d, uint32_t clen, uint32_t w,
+                       uint64_t pitch, uint64_t cstride, float* omn, float* omx, cudaStream_t st) {
+    const uint64_t total = nser * cstride;
+    const int blocks = (int)std::min<uint64_t>((total + 255) / 256, (uint64_t)sm_count() * 16);
+    paa_minmax_kernel<<<std::max(blocks, 1), 256, 0, st>>>(src, nser, d, clen, w, pitch, cstride, omn, omx);
+}
+
+// ---- block-level improved bound on the queued pairs ---------------------------
+// LB_Improved (Lemire 2009), per dimension on the box envelopes: with H_j = clip(c_j, Lq_j, Uq_j),
+//   DTW^2 >= sum_j (c_j - H_j)^2 + sum_i dist(q_i, [min_{|j-i|<=r} H_j, max_{|j-i|<=r} H_j])^2
+// (each matched cell splits as (q_i - c_j)^2 >= (c_j - H_j)^2 + (H_j - q_i)^2 because H_j lies
+// between them; every column and every row is matched at least once).  Block level: the first
+// sum by Jensen on the block means (the coarse forward bound); on a block, H_j lies in
+// [max(min Lq, min(min c, min Uq)), min(max Uq, max(max c, max Lq))]; the window over blocks
+// widens that interval; Jensen on the query's block mean gives the second sum.  All fp32 with
+// outward-rounded inputs and round-down accumulation.  One warp per queue entry; a pair whose
+// improved key exceeds T * margin gets the key, so the DP drops it at dequeue (counted there).
+__global__ void __launch_bounds__(256) lbi_filter_kernel(LbiArgs a) {
+    extern __shared__ float lsm[];  // per warp: lo[d][CP], hi[d][CP]
+    const unsigned lane = lane_id();
+    const uint32_t d = a.d, clen = a.clen, CP = (clen + 31u) & ~31u;
+    float* lo = lsm + (size_t)(threadIdx.x >> 5) * 2 * d * CP;
+    float* hi = lo + (size_t)d * CP;
+    const unsigned nf = *a.queue.front, nb = *a.queue.back, total = nf + nb;
+    const float eq = __double2float_ru(__dmul_ru(*a.qabsmax, a.eq_scale));
+    const uint64_t w0 = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t slot = w0; slot < total; slot += nw) {
+        QEntry* en = slot < nf ? a.queue.e + slot : a.queue.e + (a.queue.cap - 1 - (slot - nf));
+        const uint32_t q = en->q, c = en->c;
+        const float key = en->key;
+        const double Tm = __dmul_ru(a.state[q].T, a.margin);
+        if (!((double)key <= Tm)) continue;  // warp-uniform: dead already
+        const float* xm = a.xm + (uint64_t)c * a.cstride;
+        const float* xmn = a.xmn + (uint64_t)c * a.cstride;
+        const float* xmx = a.xmx + (uint64_t)c * a.cstride;
+        const uint64_t qo = (uint64_t)q * a.cstride;
+        float f1 = 0.0f, f2 = 0.0f;
+        for (uint32_t k = 0; k < d; ++k)
+            for (uint32_t b = lane; b < CP; b += 32) {
+                const uint32_t idx = (b >> 5) * kTile * d + kTile * k + (b & 31u);
+                float hl = kInfF, hh = -kInfF;
+                if (b < clen) {
+                    f1 = lb_term_rd(f1, __ldg(xm + idx), __ldg(a.qem + qo + idx), __ldg(a.qeh + qo + idx));
+                    hl = fmaxf(__ldg(a.lqmn + qo + idx), fminf(__ldg(xmn + idx), __ldg(a.uqmn + qo + idx)));
+                    hh = fminf(__ldg(a.uqmx + qo + idx), fmaxf(__ldg(xmx + idx), __ldg(a.lqmx + qo + idx)));
+                }
+                lo[k * CP + b] = hl;
+                hi[k * CP + b] = hh;
+            }
+        __syncwarp();
+        const int rb = (int)a.rb;
+        for (uint32_t k = 0; k < d; ++k)
+            for (uint32_t b = lane; b < clen; b += 32) {
+                float el = kInfF, eh = -kInfF;
+                const int b0 = max((int)b - rb, 0), b1 = min((int)b + rb, (int)clen - 1);
+                for (int bb = b0; bb <= b1; ++bb) {
+                    el = fminf(el, lo[k * CP + bb]);
+                    eh = fmaxf(eh, hi[k * CP + bb]);
+                }
+                const uint32_t idx = (b >> 5) * kTile * d + kTile * k + (b & 31u);
+                const float qb = __ldg(a.qm + qo + idx);
+                const float t = fmaxf(fmaxf(__fsub_rd(__fsub_rd(el, qb), eq), __fsub_rd(__fsub_rd(qb, eh), eq)), 0.0f);
+                f2 = __fmaf_rd(t, t, f2);
+            }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            f1 = __fadd_rd(f1, __shfl_xor_sync(0xffffffffu, f1, o));
+            f2 = __fadd_rd(f2, __shfl_xor_sync(0xffffffffu, f2, o));
+        }
+        if (lane == 0) {
+            const float k2 = __fmul_rd(__fadd_rd(f1, f2), a.w);
+            if (k2 > key) en->key = k2;
+        }
+        __syncwarp();
+    }
+}
+
+void launch_lbi_filter(const LbiArgs& a, cudaStream_t st) {
+    const uint32_t CP = (a.clen + 31u) & ~31u;
+    const size_t smem = (size_t)8 * 2 * a.d * CP * sizeof(float);
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(lbi_filter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    lbi_filter_kernel<<<sm_count() * 6, 256, smem, st>>>(a);
 }
 
 // ---- sampled seed upper bounds ----------------------------------------------------------------

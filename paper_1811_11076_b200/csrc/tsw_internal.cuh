@@ -281,7 +281,11 @@ void launch_paa_series(const double* src, uint64_t nser, uint32_t d, uint32_t cl
                        uint64_t pitch, uint64_t cstride, float* dst, cudaStream_t st);
 void launch_paa_envelope(const double* src, uint64_t nser, uint32_t d, uint32_t len, uint32_t clen,
                          uint32_t w, uint64_t pitch, uint64_t cstride, uint32_t r, float err,
-                         float* om, float* oh, cudaStream_t st);
+                         float* om, float* oh, cudaStream_t st, float* lo_mn = nullptr,
+                         float* lo_mx = nullptr, float* hi_mn = nullptr, float* hi_mx = nullptr);
+// block minima / maxima of the values (fp32, rounded outward), layout of launch_paa_series
+void launch_paa_minmax(const double* src, uint64_t nser, uint32_t d, uint32_t clen, uint32_t w,
+                       uint64_t pitch, uint64_t cstride, float* omn, float* omx, cudaStream_t st);
 // ends[c] = (first point, last point) of every series of a store
 void launch_series_ends(const StoreDev& s, double* ends, cudaStream_t st);
 void launch_to_float(const double* src, uint64_t count, float* dst, cudaStream_t st);
@@ -363,6 +367,31 @@ struct LbCompactArgs {
     double eq_scale;
 };
 void launch_lb_compact(const LbCompactArgs& a, cudaStream_t st);
+
+// Block-level improved bound (LB_Improved relaxation) on the queued pairs:
+// rewrites the key of every entry whose improved bound is larger (the DP re-checks keys at
+// dequeue).  All arrays: block values of `w` points, clen blocks, tiled, pitch cstride.
+struct LbiArgs {
+    WorkQueue queue;
+    const QState* state;
+    double margin;
+    uint32_t d, clen, rb;     // rb: blocks a window of the band radius reaches on either side
+    uint64_t cstride;
+    float w;
+    const float* xm;          // candidates: block means, minima, maxima
+    const float* xmn;
+    const float* xmx;
+    const float* qm;          // queries: block means; envelope means (midpoint, half-width + err);
+    const float* qem;         // block minima / maxima of the lower and upper envelope
+    const float* qeh;
+    const float* lqmn;
+    const float* lqmx;
+    const float* uqmn;
+    const float* uqmx;
+    const double* qabsmax;
+    double eq_scale;
+};
+void launch_lbi_filter(const LbiArgs& a, cudaStream_t st);
 
 // DK: first/last cell bound of every pair fused with compaction (exact, squared domain).
 struct DkCompactArgs {

@@ -37,6 +37,7 @@ CASES = [(400, 203, 3, 20, 3), (300, 67, 2, 9, 2), (500, 128, 3, 13, 5), (350, 2
          (2600, 128, 3, 13, 4), (2200, 300, 2, 33, 3)]
 MODES = {"default": {}, "off": {"TSW_COARSE": "0"}, "short_off": {"TSW_COARSE_SHORT": "0"},
          "pass_8_setup_8": {"TSW_COARSE_W": "8", "TSW_CSETUP_W": "8"},
+         "improved_bound": {"TSW_LBI": "1"},
          "per_point_setup": {"TSW_CSETUP": "0"}, "strided_sample": {"TSW_GUIDED": "0"},
          "guided_64": {"TSW_GUIDED": "64"}}
 
